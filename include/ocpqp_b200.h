@@ -1,0 +1,222 @@
+/*
+ * ocpqp_b200.h -- C ABI of the B200-native batched OCP-QP interior-point solver.
+ *
+ * This is the drop-in boundary for the reference's OCP-QP solve path
+ * (/root/reference/pkg/src/mpcqp).  The reference is a pure-Python package, so
+ * it has no FFI of its own; every entry point below names the Python call it
+ * replaces (file:line), and INTEGRATION.md shows the ctypes stub a maintainer
+ * adds to the reference to route `solve_ocp_qp` through this library.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch / C++ types cross the boundary;
+ *   - all arithmetic is fp64; integers are int32 (indices) / int64 (strides);
+ *   - a "plan" is created once per (dims, idxb, idxs, batch) and owns the device
+ *     workspace (no allocation inside a solve);
+ *   - functions return 0 on success and a negative OCPQP_E_* code on misuse or
+ *     CUDA error (ocpqp_last_error() gives the message).  Numerical trouble is
+ *     never an error: it is a per-QP status word, as in the reference
+ *     (solver.py:18-20, ipm_core.py:56-63).
+ *
+ * Data layout ("packed batch"): each stage-data field of the reference catalog
+ * (qp_data.py:248-270 plus A, B, b of :329-336) is one fp64 array holding, per
+ * QP, all stages back to back in canonical order (stage 0..N; matrices
+ * row-major; dynamics fields only for stages 0..N-1).  QP i's copy starts at
+ * ptr[f] + i * batch_stride[f]; batch_stride 0 broadcasts one copy to the whole
+ * batch (e.g. the shared plant of the mass-spring benchmarks).  Per-stage sizes:
+ *   A nx[n+1]*nx[n]   B nx[n+1]*nu[n]   b nx[n+1]      (n < N only)
+ *   Q nx*nx  S nu*nx  R nu*nu  q nx  r nu
+ *   lb ub nb   C ng*nx  D ng*nu  lg ug ng
+ *   Zl Zu zl zu sl_lb su_lb ns   maskl masku nb+ng
+ * idxb/idxs are structural and shared by the whole batch (they are part of the
+ * plan).  A NULL field pointer means "all zeros" for matrices and vectors,
+ * "all ones" for masks and "-inf / +inf" for lower / upper bounds, i.e. the
+ * reference's zero-initialised stage (qp_data.py:221-245).
+ *
+ * Iterate / solution layout: exactly the reference's flat vectors
+ * (view.py:3-13): y = [v | sl | su] with v = (u_0, x_0, u_1, x_1, ...),
+ * pi = (pi_0 .. pi_{N-1}), lam/t per stage [lower m | upper m | slack-lower ns |
+ * slack-upper ns] with m = nb + ng.  Batched as [B, ny], [B, ne], [B, nc], [B, nc].
+ */
+#ifndef OCPQP_B200_H
+#define OCPQP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OCPQP_ABI_VERSION 1
+
+/* error codes */
+#define OCPQP_OK 0
+#define OCPQP_E_INVALID_DIM (-1)      /* maps to mpcqp InvalidDim (errors.py:18) */
+#define OCPQP_E_DIMENSION (-2)        /* DimensionMismatch (errors.py:14) */
+#define OCPQP_E_UNSUPPORTED (-3)      /* option outside the implemented modes */
+#define OCPQP_E_CUDA (-4)             /* CUDA runtime error */
+#define OCPQP_E_ARG (-5)              /* bad argument / NULL pointer */
+
+/* per-QP status words; values 0..4 mirror ipm_core.Status (ipm_core.py:56-63) */
+#define OCPQP_STATUS_SUCCESS 0
+#define OCPQP_STATUS_MAXITER 1
+#define OCPQP_STATUS_MINSTEP 2
+#define OCPQP_STATUS_NAN 3
+#define OCPQP_STATUS_FAILURE 4
+/* reference raises NonPositiveIterate (kkt_common.py:70-71) / SingularSlackBlock
+ * (kkt_common.py:84-87) out of the solve; the library reports them per QP */
+#define OCPQP_STATUS_NONPOSITIVE_ITERATE 5
+#define OCPQP_STATUS_SINGULAR_SLACK 6
+
+/* stage-data field ids (reference catalog qp_data.py:248-270, :329-336) */
+enum OcpQpField {
+    OCPQP_F_A = 0,
+    OCPQP_F_B,
+    OCPQP_F_b,
+    OCPQP_F_Q,
+    OCPQP_F_S,
+    OCPQP_F_R,
+    OCPQP_F_q,
+    OCPQP_F_r,
+    OCPQP_F_lb,
+    OCPQP_F_ub,
+    OCPQP_F_C,
+    OCPQP_F_D,
+    OCPQP_F_lg,
+    OCPQP_F_ug,
+    OCPQP_F_Zl,
+    OCPQP_F_Zu,
+    OCPQP_F_zl,
+    OCPQP_F_zu,
+    OCPQP_F_sl_lb,
+    OCPQP_F_su_lb,
+    OCPQP_F_maskl,
+    OCPQP_F_masku,
+    OCPQP_NUM_FIELDS
+};
+
+/* Stage dimensions; replaces OcpQpDim (qp_data.py:65-111) plus the structural
+ * index sets idxb / idxs of every stage (qp_data.py:254, :261).  All arrays are
+ * host memory; nx..ns have N+1 entries, idxb has sum(nb), idxs sum(ns). */
+typedef struct OcpQpDimC {
+    int32_t N;
+    const int32_t* nx;
+    const int32_t* nu;
+    const int32_t* nb;
+    const int32_t* ng;
+    const int32_t* ns;
+    const int32_t* idxb;
+    const int32_t* idxs;
+} OcpQpDimC;
+
+/* Packed batch of QP data (see layout above). */
+typedef struct OcpQpDataC {
+    const double* ptr[OCPQP_NUM_FIELDS];
+    int64_t batch_stride[OCPQP_NUM_FIELDS];
+} OcpQpDataC;
+
+/* IpmArg (ipm_core.py:66-128) restricted to what the speed-mode loop reads.
+ * ocpqp_solve rejects (OCPQP_E_UNSUPPORTED) the settings of other modes. */
+typedef struct OcpIpmArgC {
+    int32_t iter_max;
+    int32_t pred_corr;       /* bool */
+    int32_t cond_pred_corr;  /* bool */
+    int32_t warm_start;      /* 0 none, 1 primal, 2 primal_dual */
+    double alpha_min;
+    double mu0;
+    double tol_stat;
+    double tol_eq;
+    double tol_ineq;
+    double tol_comp;
+    double reg_prim;
+    double lam_min;
+    double t_min;
+    double t0;
+    double corr_ratio;
+    double ftb;
+} OcpIpmArgC;
+
+/* Primal-dual point, batched: y [B,ny], pi [B,ne], lam [B,nc], t [B,nc].
+ * Replaces QpSolution (view.py:568-672). */
+typedef struct OcpIterC {
+    double* y;
+    double* pi;
+    double* lam;
+    double* t;
+} OcpIterC;
+
+/* Per-QP outcome; replaces SolverStats (ipm_core.py:186-198) and the final
+ * QpResiduals norms (view.py:675-695).  trace may be NULL; otherwise it is
+ * [B, iter_max, 8] = (alpha_aff, alpha, mu, sigma, res_g, res_b, res_d, res_m)
+ * per iteration, the IterRecord fields (ipm_core.py:171-184). */
+typedef struct OcpStatsC {
+    int32_t* status;      /* [B] OCPQP_STATUS_* */
+    int32_t* iterations;  /* [B] */
+    double* res;          /* [B,5] res_g, res_b, res_d, res_m, mu */
+    int64_t* flops;       /* [B] nominal flops, linalg.py:41-78 counting rules */
+    double* trace;        /* [B, iter_max, 8] or NULL */
+} OcpStatsC;
+
+/* Layout sizes of one QP: out[0..5] = ny, ne, nc, nv, ns_tot, n_act_max (=nc),
+ * out[6 + f] = per-QP element count of field f (OCPQP_NUM_FIELDS entries).
+ * Mirrors make_view / OcpView._build (view.py:337-366, :551-565). */
+int ocpqp_layout(const OcpQpDimC* dim, int64_t* out, int32_t out_len);
+
+typedef struct OcpPlan OcpPlan;
+
+/* Create a plan for `batch` QPs of identical structure.  Validates the dims
+ * like OcpQpDim.__init__ (qp_data.py:82-111) and the index sets like
+ * validate() (qp_data.py:528-533). */
+int ocpqp_plan_create(const OcpQpDimC* dim, int32_t batch, OcpPlan** out);
+int ocpqp_plan_destroy(OcpPlan* plan);
+
+/* Batched `solve_ocp_qp(qp, arg, guess)` (solver.py:103-105, loop
+ * solver.py:180-308) over device-resident data.  `iter` holds the warm-start
+ * guess on entry when arg->warm_start != 0 and the solution on exit.
+ * Stream-ordered on `stream` (a cudaStream_t; NULL = legacy default stream). */
+int ocpqp_solve(OcpPlan* plan, const OcpQpDataC* data, const OcpIpmArgC* arg,
+                OcpIterC* iter, OcpStatsC* stats, void* stream);
+
+/* Same as ocpqp_solve with HOST buffers: copies data in, solves and copies the
+ * solution and stats out, then synchronizes `stream`.  This is the call an FFI
+ * binding of the reference makes with numpy arrays. */
+int ocpqp_solve_host(OcpPlan* plan, const OcpQpDataC* host_data,
+                     const OcpIpmArgC* arg, OcpIterC* host_iter,
+                     OcpStatsC* host_stats, void* stream);
+
+/* Residuals of a batch of points; replaces compute_residuals / residuals
+ * (view.py:698-706, :272-288).  r_* may be NULL (norms only); norms is
+ * [B,5] = res_g, res_b, res_d, res_m, mu.  Device pointers. */
+int ocpqp_residuals(OcpPlan* plan, const OcpQpDataC* data, const OcpIterC* point,
+                    double* r_g, double* r_b, double* r_d, double* r_m,
+                    double* norms, void* stream);
+
+/* Newton step: classical riccati_factor(qp, iterate, arg) followed by
+ * RiccatiFactor.solve(r_g, r_b, r_d, r_m) (kkt_ocp.py:142-201, :254-320).
+ * reg is the primal regularisation (IpmArg.reg_prim).  fail_stage[B] receives
+ * -1 on success or the FactorizationFailed.stage of the reference
+ * (kkt_ocp.py:180-200); the step of a failed QP is left as zeros.
+ * Device pointers. */
+int ocpqp_newton_step(OcpPlan* plan, const OcpQpDataC* data, double reg,
+                      const OcpIterC* iterate, const double* r_g,
+                      const double* r_b, const double* r_d, const double* r_m,
+                      OcpIterC* step, int32_t* fail_stage, void* stream);
+
+/* Cost-to-go matrices P[n] and gains K[n] of the last classical factor of
+ * ocpqp_newton_step for QP `qp` (RiccatiFactor.p_matrix / feedback_gains,
+ * kkt_ocp.py:122-125, :323-330).  P_out: sum nx[n]^2, K_out: sum nu[n]*nx[n],
+ * stage-major row-major, host memory. */
+int ocpqp_factor_export(OcpPlan* plan, int32_t qp, double* P_out, double* K_out);
+
+/* Plan introspection: out[0..4] = threads per CTA, resident CTA slots,
+ * dynamic shared memory bytes per CTA, shared-memory buffer mask, workspace
+ * doubles per slot. */
+int ocpqp_plan_info(const OcpPlan* plan, int64_t* out, int32_t out_len);
+
+/* Library identity. */
+int ocpqp_abi_version(void);
+const char* ocpqp_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OCPQP_B200_H */

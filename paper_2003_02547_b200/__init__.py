@@ -1,0 +1,52 @@
+"""B200-native batched OCP-QP interior-point solver (HPIPM-paper path).
+
+Drop-in for the reference package's optimal-control QP solve
+(mpcqp.solve_ocp_qp, solver.py:103-105): the same ``OcpQpDim`` / ``OcpQp`` /
+``IpmArg`` / ``QpSolution`` / ``SolveReport`` objects, solved by a fused
+sm_100a fp64 kernel (residuals, Riccati factor/solve and the IPM vector
+steps of every QP in one launch).  See DESIGN.md.
+"""
+
+from .batch import OcpQpBatch
+from .errors import (
+    CondenseError,
+    DimensionMismatch,
+    FactorizationFailed,
+    IndexOutOfRange,
+    InvalidBlockSize,
+    InvalidConfig,
+    InvalidDim,
+    MpcQpError,
+    NativeLibraryError,
+    NonPositiveIterate,
+    NotPositiveDefinite,
+    RankDeficient,
+    SingularFactor,
+    SingularSlackBlock,
+    UnknownField,
+)
+from .ipm import IpmArg, IterRecord, SolverStats, Status, mode_preset
+from .layout import OcpLayout, QpResiduals, QpSolution
+from .qp_data import OcpQp, OcpQpDim, Violation, validate
+from .solver import (
+    BatchReport,
+    SolveReport,
+    compute_residuals,
+    newton_step,
+    solve_ocp_qp,
+    solve_ocp_qp_batch,
+    solve_ocp_qp_host,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "OcpQpBatch", "CondenseError", "DimensionMismatch", "FactorizationFailed",
+    "IndexOutOfRange", "InvalidBlockSize", "InvalidConfig", "InvalidDim", "MpcQpError",
+    "NativeLibraryError", "NonPositiveIterate", "NotPositiveDefinite", "RankDeficient",
+    "SingularFactor", "SingularSlackBlock", "UnknownField", "IpmArg", "IterRecord",
+    "SolverStats", "Status", "mode_preset", "OcpLayout", "QpResiduals", "QpSolution",
+    "OcpQp", "OcpQpDim", "Violation", "validate", "BatchReport", "SolveReport",
+    "compute_residuals", "newton_step", "solve_ocp_qp", "solve_ocp_qp_batch",
+    "solve_ocp_qp_host", "__version__",
+]

@@ -1,0 +1,525 @@
+// C ABI of the batched OCP-QP solver (include/ocpqp_b200.h): plan creation,
+// layout tables, workspace placement (shared memory vs per-slot global), and
+// the device- and host-buffer solve entry points.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "ocpqp_internal.h"
+
+using namespace ocpqp;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(OCPQP_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(expr)                                   \
+    do {                                                 \
+        cudaError_t _e = (expr);                         \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+    } while (0)
+
+// Host copy of the structure; everything derived from OcpQpDimC.
+struct Layout {
+    int N = 0;
+    std::vector<int> nx, nu, nb, ng, ns, idxb, idxs;
+    std::vector<StageInfo> st;
+    int ny = 0, ne = 0, nc = 0, nv = 0, ns_tot = 0, msum = 0;
+    int nw_max = 0, nx_max = 0, nu_max = 0, m_max = 0, nc_max = 0, ns_max = 0;
+    long long flen[OCPQP_NUM_FIELDS] = {0};
+    std::vector<int> var_box, row_slack;
+    long long ws_size[WS_NUM] = {0};
+};
+
+long long field_stage_size(int f, const Layout& L, int n) {
+    const int nx = L.nx[n], nu = L.nu[n], nb = L.nb[n], ng = L.ng[n], ns = L.ns[n];
+    const int nxn = n < L.N ? L.nx[n + 1] : 0;
+    switch (f) {
+        case OCPQP_F_A: return n < L.N ? (long long)nxn * nx : 0;
+        case OCPQP_F_B: return n < L.N ? (long long)nxn * nu : 0;
+        case OCPQP_F_b: return n < L.N ? nxn : 0;
+        case OCPQP_F_Q: return (long long)nx * nx;
+        case OCPQP_F_S: return (long long)nu * nx;
+        case OCPQP_F_R: return (long long)nu * nu;
+        case OCPQP_F_q: return nx;
+        case OCPQP_F_r: return nu;
+        case OCPQP_F_lb: case OCPQP_F_ub: return nb;
+        case OCPQP_F_C: return (long long)ng * nx;
+        case OCPQP_F_D: return (long long)ng * nu;
+        case OCPQP_F_lg: case OCPQP_F_ug: return ng;
+        case OCPQP_F_Zl: case OCPQP_F_Zu: case OCPQP_F_zl: case OCPQP_F_zu:
+        case OCPQP_F_sl_lb: case OCPQP_F_su_lb: return ns;
+        case OCPQP_F_maskl: case OCPQP_F_masku: return nb + ng;
+    }
+    return 0;
+}
+
+// Validation mirrors OcpQpDim.__init__ (qp_data.py:82-111) and the index-set
+// checks of validate() (qp_data.py:528-533).
+int build_layout(const OcpQpDimC* d, Layout& L) {
+    if (!d) return fail(OCPQP_E_ARG, "dim is NULL");
+    if (d->N < 0) return fail(OCPQP_E_INVALID_DIM, "horizon N must be >= 0");
+    if (!d->nx || !d->nu || !d->nb || !d->ng || !d->ns)
+        return fail(OCPQP_E_ARG, "dimension arrays must not be NULL");
+    L.N = d->N;
+    const int S = d->N + 1;
+    L.nx.assign(d->nx, d->nx + S);
+    L.nu.assign(d->nu, d->nu + S);
+    L.nb.assign(d->nb, d->nb + S);
+    L.ng.assign(d->ng, d->ng + S);
+    L.ns.assign(d->ns, d->ns + S);
+    long long sum_nb = 0, sum_ns = 0;
+    for (int n = 0; n < S; ++n) {
+        if (L.nx[n] < 0 || L.nu[n] < 0 || L.nb[n] < 0 || L.ng[n] < 0 || L.ns[n] < 0)
+            return fail(OCPQP_E_INVALID_DIM, "stage %d: dimensions must be nonnegative", n);
+        if (L.nb[n] > L.nu[n] + L.nx[n])
+            return fail(OCPQP_E_INVALID_DIM, "stage %d: nb = %d exceeds nu + nx = %d", n, L.nb[n],
+                        L.nu[n] + L.nx[n]);
+        if (L.ns[n] > L.nb[n] + L.ng[n])
+            return fail(OCPQP_E_INVALID_DIM, "stage %d: ns = %d exceeds nb + ng = %d", n, L.ns[n],
+                        L.nb[n] + L.ng[n]);
+        sum_nb += L.nb[n];
+        sum_ns += L.ns[n];
+    }
+    if (sum_nb && !d->idxb) return fail(OCPQP_E_ARG, "idxb is NULL");
+    if (sum_ns && !d->idxs) return fail(OCPQP_E_ARG, "idxs is NULL");
+    L.idxb.assign(d->idxb ? d->idxb : nullptr, d->idxb ? d->idxb + sum_nb : nullptr);
+    L.idxs.assign(d->idxs ? d->idxs : nullptr, d->idxs ? d->idxs + sum_ns : nullptr);
+    L.st.resize(S);
+    int v = 0, s = 0, c = 0, p = 0, ib = 0, is = 0, mo = 0;
+    int Po = 0, Ko = 0, Lo = 0, pvo = 0, kfo = 0;
+    long long foff[OCPQP_NUM_FIELDS] = {0};
+    long long t1 = 0;
+    for (int n = 0; n < S; ++n) {
+        StageInfo& si = L.st[n];
+        memset(&si, 0, sizeof(si));
+        si.nx = L.nx[n]; si.nu = L.nu[n]; si.nb = L.nb[n]; si.ng = L.ng[n]; si.ns = L.ns[n];
+        si.nxn = n < L.N ? L.nx[n + 1] : 0;
+        si.nw = si.nu + si.nx;
+        si.m = si.nb + si.ng;
+        si.nc = 2 * si.m + 2 * si.ns;
+        si.u_off = v; si.x_off = v + si.nu;
+        si.pi_off = p;
+        si.c_off = c; si.s_off = s; si.ib_off = ib; si.is_off = is; si.m_off = mo;
+        for (int i = 0; i < si.nb; ++i) {
+            const int k = L.idxb[ib + i];
+            if (k < 0 || k >= si.nw)
+                return fail(OCPQP_E_DIMENSION, "stage %d: idxb entries must lie in [0, %d)", n, si.nw);
+            if (i > 0 && k <= L.idxb[ib + i - 1])
+                return fail(OCPQP_E_DIMENSION, "stage %d: idxb entries must be strictly increasing", n);
+        }
+        for (int j = 0; j < si.ns; ++j) {
+            const int k = L.idxs[is + j];
+            if (k < 0 || k >= si.m)
+                return fail(OCPQP_E_DIMENSION, "stage %d: idxs entries must lie in [0, %d)", n, si.m);
+            if (j > 0 && k <= L.idxs[is + j - 1])
+                return fail(OCPQP_E_DIMENSION, "stage %d: idxs entries must be strictly increasing", n);
+        }
+        for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) {
+            si.foff[f] = (int)foff[f];
+            foff[f] += field_stage_size(f, L, n);
+        }
+        si.P_off = Po; Po += si.nx * si.nx;
+        si.K_off = Ko; Ko += si.nu * si.nx;
+        si.L_off = Lo; Lo += si.nu * si.nu;
+        si.pv_off = pvo; pvo += si.nx;
+        si.kff_off = kfo; kfo += si.nu;
+        v += si.nw; s += si.ns; c += si.nc; ib += si.nb; is += si.ns; mo += si.m;
+        if (n < L.N) p += si.nxn;
+        L.nw_max = std::max(L.nw_max, si.nw);
+        L.nx_max = std::max(L.nx_max, si.nx);
+        L.nu_max = std::max(L.nu_max, si.nu);
+        L.m_max = std::max(L.m_max, si.m);
+        L.nc_max = std::max(L.nc_max, si.nc);
+        L.ns_max = std::max(L.ns_max, si.ns);
+        t1 = std::max(t1, std::max((long long)si.nxn * si.nw, (long long)si.nx * si.nx));
+    }
+    L.nv = v; L.ns_tot = s; L.ny = v + 2 * s; L.ne = p; L.nc = c; L.msum = mo;
+    for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) L.flen[f] = foff[f];
+    L.var_box.assign(std::max(1, L.nv), -1);
+    L.row_slack.assign(std::max(1, L.msum), -1);
+    for (int n = 0; n < S; ++n) {
+        const StageInfo& si = L.st[n];
+        for (int i = 0; i < si.nb; ++i) L.var_box[si.u_off + L.idxb[si.ib_off + i]] = i;
+        for (int j = 0; j < si.ns; ++j) L.row_slack[si.m_off + L.idxs[si.is_off + j]] = j;
+    }
+    long long* w = L.ws_size;
+    w[WS_RG] = L.ny; w[WS_RB] = L.ne; w[WS_RD] = L.nc; w[WS_DVEC] = L.nc; w[WS_ACT] = L.nc;
+    w[WS_AFF_Y] = w[WS_DIR_Y] = L.ny;
+    w[WS_AFF_PI] = w[WS_DIR_PI] = L.ne;
+    w[WS_AFF_LAM] = w[WS_AFF_T] = w[WS_DIR_LAM] = w[WS_DIR_T] = L.nc;
+    w[WS_GAM] = L.nc; w[WS_COEF] = L.msum; w[WS_DL] = w[WS_DU] = L.ns_tot;
+    w[WS_WALL] = L.nc; w[WS_RTSL] = w[WS_RTSU] = L.ns_tot;
+    w[WS_CROW] = L.msum; w[WS_ROWV] = L.msum; w[WS_RHAT] = L.nv;
+    w[WS_P] = Po; w[WS_K] = Ko; w[WS_L] = Lo; w[WS_LP0] = (long long)L.nx[0] * L.nx[0];
+    w[WS_PV] = pvo; w[WS_KFF] = kfo;
+    w[WS_G] = (long long)L.nw_max * L.nw_max;
+    w[WS_T1] = t1;
+    w[WS_VEC] = L.nw_max + L.nx_max + std::max(L.nu_max, L.nx_max);
+    return OCPQP_OK;
+}
+
+inline long long align2(long long x) { return (x + 1) & ~1ll; }
+
+}  // namespace
+
+struct OcpPlan {
+    Layout L;
+    int B = 0;
+    int device = 0;
+    int num_sms = 0;
+    int threads = 32;
+    int slots = 1;
+    size_t smem_bytes = 0;
+    unsigned smem_mask = 0;
+    int smem_off[WS_NUM] = {0};
+    int ws_off[WS_NUM] = {0};
+    long long ws_slot = 0;
+    // device structure tables
+    StageInfo* d_st = nullptr;
+    int* d_idxb = nullptr;
+    int* d_idxs = nullptr;
+    int* d_var_box = nullptr;
+    int* d_row_slack = nullptr;
+    int* d_counter = nullptr;
+    double* d_ws = nullptr;
+    // host-path device buffers (allocated on first use)
+    double* h_field[OCPQP_NUM_FIELDS] = {nullptr};
+    long long h_field_len[OCPQP_NUM_FIELDS] = {0};
+    double *hy = nullptr, *hpi = nullptr, *hlam = nullptr, *ht = nullptr;
+    int32_t *hstatus = nullptr, *hiters = nullptr;
+    double* hres = nullptr;
+    long long* hflops = nullptr;
+    double* htrace = nullptr;
+    int htrace_iters = 0;
+};
+
+namespace {
+
+// Workspace placement: the hottest buffers go to shared memory up to a
+// per-CTA budget chosen so that enough CTAs stay resident per SM.
+void place_workspace(OcpPlan* P) {
+    const Layout& L = P->L;
+    const char* env = getenv("OCPQP_THREADS");
+    int threads;
+    if (env && atoi(env) > 0) {
+        threads = atoi(env);
+    } else if (L.nw_max <= 12) {
+        threads = 32;
+    } else if (L.nw_max <= 24) {
+        threads = 64;
+    } else if (L.nw_max <= 48) {
+        threads = 128;
+    } else {
+        threads = 256;
+    }
+    threads = std::min(512, std::max(32, (threads + 31) / 32 * 32));
+    P->threads = threads;
+    long long off = 0;
+    for (int b = 0; b < WS_NUM; ++b) {
+        P->ws_off[b] = (int)off;
+        off += align2(L.ws_size[b]);
+    }
+    P->ws_slot = std::max(2ll, off);
+
+    int tgt = std::max(1, 768 / threads);
+    const int per_sm_need = (P->B + P->num_sms - 1) / std::max(1, P->num_sms);
+    tgt = std::max(1, std::min(tgt, per_sm_need));
+    const char* envs = getenv("OCPQP_SMEM_KB");
+    long long budget;
+    if (envs) {
+        budget = (long long)atoi(envs) * 1024;
+    } else {
+        budget = (228ll * 1024) / tgt - 2048;
+        budget = std::min(budget, 227ll * 1024 - 1024);
+    }
+    const int prio[] = {WS_G, WS_T1, WS_VEC, WS_ACT, WS_DVEC, WS_GAM, WS_WALL, WS_COEF,
+                        WS_CROW, WS_ROWV, WS_RHAT, WS_P, WS_K, WS_L, WS_LP0, WS_PV, WS_KFF,
+                        WS_RG, WS_RB, WS_RD, WS_DIR_LAM, WS_DIR_T, WS_AFF_LAM, WS_AFF_T,
+                        WS_DIR_Y, WS_DIR_PI, WS_AFF_Y, WS_AFF_PI, WS_DL, WS_DU, WS_RTSL, WS_RTSU};
+    long long used = 0;
+    P->smem_mask = 0;
+    for (int b : prio) {
+        const long long sz = align2(L.ws_size[b]) * 8;
+        if (sz == 0) continue;
+        if (used + sz <= budget) {
+            P->smem_mask |= 1u << b;
+            P->smem_off[b] = (int)(used / 8);
+            used += sz;
+        }
+    }
+    P->smem_bytes = (size_t)used;
+}
+
+void fill_kparams(const OcpPlan* P, KParams& k, const OcpQpDataC* data, bool use_smem) {
+    const Layout& L = P->L;
+    memset(&k, 0, sizeof(k));
+    k.N = L.N; k.B = P->B;
+    k.ny = L.ny; k.ne = L.ne; k.nc = L.nc; k.nv = L.nv; k.ns_tot = L.ns_tot; k.msum = L.msum;
+    k.nw_max = L.nw_max; k.nx_max = L.nx_max; k.nu_max = L.nu_max; k.m_max = L.m_max;
+    k.nc_max = L.nc_max; k.ns_max = L.ns_max;
+    k.st = P->d_st; k.idxb = P->d_idxb; k.idxs = P->d_idxs;
+    k.var_box = P->d_var_box; k.row_slack = P->d_row_slack;
+    for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) {
+        const bool present = data && data->ptr[f] && L.flen[f] > 0;
+        k.f[f] = present ? data->ptr[f] : nullptr;
+        k.bs[f] = present ? data->batch_stride[f] : 0;
+    }
+    k.ws = P->d_ws; k.ws_slot = P->ws_slot;
+    for (int b = 0; b < WS_NUM; ++b) { k.ws_off[b] = P->ws_off[b]; k.smem_off[b] = P->smem_off[b]; }
+    k.smem_mask = use_smem ? P->smem_mask : 0u;
+    k.counter = P->d_counter;
+}
+
+int check_arg(const OcpIpmArgC* a) {
+    if (!a) return fail(OCPQP_E_ARG, "arg is NULL");
+    if (!(a->tol_stat > 0) || !(a->tol_eq > 0) || !(a->tol_ineq > 0) || !(a->tol_comp > 0))
+        return fail(OCPQP_E_ARG, "tolerances must be > 0");
+    if (!(a->alpha_min > 0.0 && a->alpha_min < 1.0))
+        return fail(OCPQP_E_ARG, "alpha_min must lie in (0, 1)");
+    if (a->lam_min < 0.0 || a->t_min < 0.0) return fail(OCPQP_E_ARG, "lam_min and t_min must be >= 0");
+    if (a->warm_start < 0 || a->warm_start > 2) return fail(OCPQP_E_ARG, "unknown warm_start");
+    if (a->iter_max < 0) return fail(OCPQP_E_ARG, "iter_max must be >= 0");
+    return OCPQP_OK;
+}
+
+template <typename T>
+int ensure(T** p, long long n) {
+    if (*p) return OCPQP_OK;
+    CUDA_TRY(cudaMalloc((void**)p, sizeof(T) * (size_t)std::max(1ll, n)));
+    return OCPQP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ocpqp_abi_version(void) { return OCPQP_ABI_VERSION; }
+
+const char* ocpqp_last_error(void) { return g_last_error.c_str(); }
+
+int ocpqp_layout(const OcpQpDimC* dim, int64_t* out, int32_t out_len) {
+    Layout L;
+    int rc = build_layout(dim, L);
+    if (rc) return rc;
+    if (!out || out_len < 6 + OCPQP_NUM_FIELDS) return fail(OCPQP_E_ARG, "out too short");
+    out[0] = L.ny; out[1] = L.ne; out[2] = L.nc; out[3] = L.nv; out[4] = L.ns_tot; out[5] = L.nc;
+    for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) out[6 + f] = L.flen[f];
+    return OCPQP_OK;
+}
+
+int ocpqp_plan_create(const OcpQpDimC* dim, int32_t batch, OcpPlan** out) {
+    if (!out) return fail(OCPQP_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (batch < 0) return fail(OCPQP_E_ARG, "batch must be >= 0");
+    OcpPlan* P = new OcpPlan();
+    int rc = build_layout(dim, P->L);
+    if (rc) { delete P; return rc; }
+    P->B = batch;
+    cudaError_t e = cudaGetDevice(&P->device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device);
+    if (e != cudaSuccess) { delete P; return cuda_fail(e, "no CUDA device"); }
+    place_workspace(P);
+    int occ = ipm_occupancy(P->threads, P->smem_bytes);
+    while (occ == 0 && P->smem_bytes > 0) {
+        // shrink the shared-memory share until one CTA fits
+        P->smem_mask = 0; P->smem_bytes = 0;
+        occ = ipm_occupancy(P->threads, 0);
+    }
+    if (occ == 0) { delete P; return fail(OCPQP_E_CUDA, "kernel does not fit on an SM"); }
+    P->slots = std::max(1, std::min(std::max(1, batch), occ * P->num_sms));
+    const Layout& L = P->L;
+    const size_t S = L.st.size();
+    e = cudaMalloc(&P->d_st, sizeof(StageInfo) * S);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_idxb, sizeof(int) * std::max<size_t>(1, L.idxb.size()));
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_idxs, sizeof(int) * std::max<size_t>(1, L.idxs.size()));
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_var_box, sizeof(int) * L.var_box.size());
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_row_slack, sizeof(int) * L.row_slack.size());
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_counter, sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_ws, sizeof(double) * (size_t)P->ws_slot * P->slots);
+    if (e == cudaSuccess) e = cudaMemcpy(P->d_st, L.st.data(), sizeof(StageInfo) * S, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !L.idxb.empty())
+        e = cudaMemcpy(P->d_idxb, L.idxb.data(), sizeof(int) * L.idxb.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !L.idxs.empty())
+        e = cudaMemcpy(P->d_idxs, L.idxs.data(), sizeof(int) * L.idxs.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(P->d_var_box, L.var_box.data(), sizeof(int) * L.var_box.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(P->d_row_slack, L.row_slack.data(), sizeof(int) * L.row_slack.size(),
+                       cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        ocpqp_plan_destroy(P);
+        return cuda_fail(e, "plan allocation");
+    }
+    *out = P;
+    return OCPQP_OK;
+}
+
+int ocpqp_plan_destroy(OcpPlan* P) {
+    if (!P) return OCPQP_OK;
+    cudaFree(P->d_st); cudaFree(P->d_idxb); cudaFree(P->d_idxs); cudaFree(P->d_var_box);
+    cudaFree(P->d_row_slack); cudaFree(P->d_counter); cudaFree(P->d_ws);
+    for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) cudaFree(P->h_field[f]);
+    cudaFree(P->hy); cudaFree(P->hpi); cudaFree(P->hlam); cudaFree(P->ht);
+    cudaFree(P->hstatus); cudaFree(P->hiters); cudaFree(P->hres); cudaFree(P->hflops);
+    cudaFree(P->htrace);
+    delete P;
+    return OCPQP_OK;
+}
+
+// Plan introspection for the host bindings: threads, slots, smem bytes,
+// smem mask, workspace doubles per slot.
+int ocpqp_plan_info(const OcpPlan* P, int64_t* out, int32_t out_len) {
+    if (!P || !out || out_len < 5) return fail(OCPQP_E_ARG, "bad arguments");
+    out[0] = P->threads; out[1] = P->slots; out[2] = (int64_t)P->smem_bytes;
+    out[3] = P->smem_mask; out[4] = P->ws_slot;
+    return OCPQP_OK;
+}
+
+int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIterC* iter,
+                OcpStatsC* stats, void* stream) {
+    if (!P) return fail(OCPQP_E_ARG, "plan is NULL");
+    int rc = check_arg(arg);
+    if (rc) return rc;
+    if (!iter || !stats || !iter->y || !iter->pi || !iter->lam || !iter->t || !stats->status ||
+        !stats->iterations || !stats->res || !stats->flops)
+        return fail(OCPQP_E_ARG, "iterate / stats buffers must not be NULL");
+    if (P->B == 0) return OCPQP_OK;
+    KParams k;
+    fill_kparams(P, k, data, true);
+    SolveParams sp;
+    memset(&sp, 0, sizeof(sp));
+    sp.arg = *arg;
+    sp.y = iter->y; sp.pi = iter->pi; sp.lam = iter->lam; sp.t = iter->t;
+    sp.status = stats->status; sp.iters = stats->iterations; sp.res = stats->res;
+    sp.flops = (long long*)stats->flops; sp.trace = stats->trace;
+    cudaError_t e = launch_ipm_solve(k, sp, P->slots, P->threads, P->smem_bytes, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "k_ipm_solve launch");
+    return OCPQP_OK;
+}
+
+int ocpqp_solve_host(OcpPlan* P, const OcpQpDataC* hd, const OcpIpmArgC* arg, OcpIterC* hit,
+                     OcpStatsC* hst, void* stream_) {
+    if (!P || !hd || !hit || !hst) return fail(OCPQP_E_ARG, "NULL argument");
+    int rc = check_arg(arg);
+    if (rc) return rc;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const Layout& L = P->L;
+    const long long B = P->B;
+    OcpQpDataC dd;
+    memset(&dd, 0, sizeof(dd));
+    for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) {
+        if (!hd->ptr[f] || L.flen[f] == 0) continue;
+        const long long copies = hd->batch_stride[f] == 0 ? 1 : B;
+        if (hd->batch_stride[f] != 0 && hd->batch_stride[f] != L.flen[f])
+            return fail(OCPQP_E_DIMENSION, "host field %d: batch stride must be 0 or %lld", f, L.flen[f]);
+        const long long n = copies * L.flen[f];
+        if (P->h_field_len[f] < n) {
+            cudaFree(P->h_field[f]);
+            P->h_field[f] = nullptr;
+            CUDA_TRY(cudaMalloc(&P->h_field[f], sizeof(double) * n));
+            P->h_field_len[f] = n;
+        }
+        CUDA_TRY(cudaMemcpyAsync(P->h_field[f], hd->ptr[f], sizeof(double) * n, cudaMemcpyHostToDevice, stream));
+        dd.ptr[f] = P->h_field[f];
+        dd.batch_stride[f] = hd->batch_stride[f];
+    }
+    if ((rc = ensure(&P->hy, B * L.ny)) || (rc = ensure(&P->hpi, B * L.ne)) ||
+        (rc = ensure(&P->hlam, B * L.nc)) || (rc = ensure(&P->ht, B * L.nc)) ||
+        (rc = ensure(&P->hstatus, B)) || (rc = ensure(&P->hiters, B)) ||
+        (rc = ensure(&P->hres, B * 5)) || (rc = ensure(&P->hflops, B)))
+        return rc;
+    if (hst->trace) {
+        if (P->htrace_iters < arg->iter_max) {
+            cudaFree(P->htrace);
+            P->htrace = nullptr;
+            CUDA_TRY(cudaMalloc(&P->htrace, sizeof(double) * std::max(1ll, B * arg->iter_max * 8)));
+            P->htrace_iters = arg->iter_max;
+        }
+    }
+    if (arg->warm_start != 0) {
+        CUDA_TRY(cudaMemcpyAsync(P->hy, hit->y, sizeof(double) * B * L.ny, cudaMemcpyHostToDevice, stream));
+        if (arg->warm_start == 2) {
+            CUDA_TRY(cudaMemcpyAsync(P->hpi, hit->pi, sizeof(double) * B * L.ne, cudaMemcpyHostToDevice, stream));
+            CUDA_TRY(cudaMemcpyAsync(P->hlam, hit->lam, sizeof(double) * B * L.nc, cudaMemcpyHostToDevice, stream));
+        }
+    }
+    OcpIterC di{P->hy, P->hpi, P->hlam, P->ht};
+    OcpStatsC ds{P->hstatus, P->hiters, P->hres, (int64_t*)P->hflops, hst->trace ? P->htrace : nullptr};
+    rc = ocpqp_solve(P, &dd, arg, &di, &ds, stream);
+    if (rc) return rc;
+    if (hit->y) CUDA_TRY(cudaMemcpyAsync(hit->y, P->hy, sizeof(double) * B * L.ny, cudaMemcpyDeviceToHost, stream));
+    if (hit->pi) CUDA_TRY(cudaMemcpyAsync(hit->pi, P->hpi, sizeof(double) * B * L.ne, cudaMemcpyDeviceToHost, stream));
+    if (hit->lam) CUDA_TRY(cudaMemcpyAsync(hit->lam, P->hlam, sizeof(double) * B * L.nc, cudaMemcpyDeviceToHost, stream));
+    if (hit->t) CUDA_TRY(cudaMemcpyAsync(hit->t, P->ht, sizeof(double) * B * L.nc, cudaMemcpyDeviceToHost, stream));
+    if (hst->status) CUDA_TRY(cudaMemcpyAsync(hst->status, P->hstatus, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, stream));
+    if (hst->iterations) CUDA_TRY(cudaMemcpyAsync(hst->iterations, P->hiters, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, stream));
+    if (hst->res) CUDA_TRY(cudaMemcpyAsync(hst->res, P->hres, sizeof(double) * B * 5, cudaMemcpyDeviceToHost, stream));
+    if (hst->flops) CUDA_TRY(cudaMemcpyAsync(hst->flops, P->hflops, sizeof(int64_t) * B, cudaMemcpyDeviceToHost, stream));
+    if (hst->trace) CUDA_TRY(cudaMemcpyAsync(hst->trace, P->htrace, sizeof(double) * B * arg->iter_max * 8, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    return OCPQP_OK;
+}
+
+int ocpqp_residuals(OcpPlan* P, const OcpQpDataC* data, const OcpIterC* pt, double* r_g,
+                    double* r_b, double* r_d, double* r_m, double* norms, void* stream) {
+    if (!P || !pt || !norms) return fail(OCPQP_E_ARG, "NULL argument");
+    if (P->B == 0) return OCPQP_OK;
+    KParams k;
+    fill_kparams(P, k, data, false);
+    cudaError_t e = launch_residuals(k, pt->y, pt->pi, pt->lam, pt->t, r_g, r_b, r_d, r_m, norms,
+                                     P->slots, P->threads, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "k_residuals launch");
+    return OCPQP_OK;
+}
+
+int ocpqp_newton_step(OcpPlan* P, const OcpQpDataC* data, double reg, const OcpIterC* it,
+                      const double* r_g, const double* r_b, const double* r_d, const double* r_m,
+                      OcpIterC* step, int32_t* fail_stage, void* stream) {
+    if (!P || !it || !step || !r_g || !r_b || !r_d || !r_m || !fail_stage)
+        return fail(OCPQP_E_ARG, "NULL argument");
+    if (P->B == 0) return OCPQP_OK;
+    KParams k;
+    fill_kparams(P, k, data, false);
+    cudaError_t e = launch_newton_step(k, reg, it->lam, it->t, r_g, r_b, r_d, r_m, step->y,
+                                       step->pi, step->lam, step->t, fail_stage, P->slots,
+                                       P->threads, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "k_newton_step launch");
+    return OCPQP_OK;
+}
+
+int ocpqp_factor_export(OcpPlan* P, int32_t qp, double* P_out, double* K_out) {
+    if (!P || qp < 0 || qp >= P->B) return fail(OCPQP_E_ARG, "bad plan or qp index");
+    if (P->B > P->slots)
+        return fail(OCPQP_E_UNSUPPORTED, "factor export needs batch <= slots (%d)", P->slots);
+    const double* slot = P->d_ws + (long long)qp * P->ws_slot;
+    if (P_out)
+        CUDA_TRY(cudaMemcpy(P_out, slot + P->ws_off[WS_P], sizeof(double) * P->L.ws_size[WS_P],
+                            cudaMemcpyDeviceToHost));
+    if (K_out)
+        CUDA_TRY(cudaMemcpy(K_out, slot + P->ws_off[WS_K], sizeof(double) * P->L.ws_size[WS_K],
+                            cudaMemcpyDeviceToHost));
+    return OCPQP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// Internal plan / kernel-parameter structures shared by the C ABI layer and
+// the sm_100a kernels.  Not part of the public ABI (include/ocpqp_b200.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ocpqp_b200.h"
+
+namespace ocpqp {
+
+// Per-stage layout record, computed once per plan on the host.  The offsets
+// reproduce the reference's flat layout (view.py:337-366 OcpView._build,
+// view.py:108-129 ConBlock) so that kernel outputs are the reference vectors.
+struct StageInfo {
+    int nx, nu, nb, ng, ns;
+    int nxn;      // nx[n+1] (0 at n == N)
+    int nw, m, nc;
+    int u_off, x_off;   // into v / y
+    int pi_off;         // into pi (n < N)
+    int c_off;          // into lam / t
+    int s_off;          // into the flat slack vectors (sl part at nv + s_off)
+    int ib_off;         // into the concatenated idxb
+    int is_off;         // into the concatenated idxs
+    int m_off;          // into per-row (box+general) work vectors, sum of m
+    int foff[OCPQP_NUM_FIELDS];  // per-QP element offsets of each field
+    // factor workspace offsets (doubles, per slot)
+    int P_off, K_off, L_off;     // P[n] (nx^2), K[n] (nu*nx), L_uu[n] (nu^2)
+    int pv_off, kff_off;         // pv[n] (nx), kff[n] (nu)
+};
+
+// Workspace buffers of one slot (one CTA solving one QP at a time).
+enum WsBuf {
+    WS_RG = 0, WS_RB, WS_RD,                 // residuals r_g (ny), r_b (ne), r_d (nc)
+    WS_DVEC,                                 // d vector (nc), view.py:156-157, 184
+    WS_ACT,                                  // activity as 0/1 doubles (nc)
+    WS_AFF_Y, WS_AFF_PI, WS_AFF_LAM, WS_AFF_T,   // affine step
+    WS_DIR_Y, WS_DIR_PI, WS_DIR_LAM, WS_DIR_T,   // combined step
+    WS_GAM,                                  // raw gamma = lam/t (nc)
+    WS_COEF,                                 // ge_lo + ge_up per row (sum m)
+    WS_DL, WS_DU,                            // soft-slack augmented diagonals (ns_tot)
+    WS_WALL,                                 // fold_rhs w_all (nc)
+    WS_RTSL, WS_RTSU,                        // fold_rhs rt_sl / rt_su (ns_tot)
+    WS_CROW,                                 // per-row fold coefficient (sum m)
+    WS_ROWV,                                 // per-row values Jc w (sum m)
+    WS_RHAT,                                 // reduced window rhs (nv)
+    WS_P, WS_K, WS_L, WS_LP0,                // Riccati factor
+    WS_PV, WS_KFF,                           // backward-sweep vectors
+    WS_G,                                    // stage matrix G (nw_max^2)
+    WS_T1,                                   // stage temp (max(nx' * nw, nx^2))
+    WS_VEC,                                  // small stage vectors (4 * nw_max)
+    WS_NUM
+};
+
+struct KParams {
+    // structure
+    int N, B;
+    int ny, ne, nc, nv, ns_tot, msum;
+    int nw_max, nx_max, nu_max, m_max, nc_max, ns_max;
+    const StageInfo* st;      // [N+1] device
+    const int* idxb;          // concatenated, device
+    const int* idxs;          // concatenated, device
+    const int* var_box;       // [nv] box row (within stage) targeting variable, or -1
+    const int* row_slack;     // [msum] soft slack index (within stage) of a row, or -1
+    // data
+    const double* f[OCPQP_NUM_FIELDS];
+    long long bs[OCPQP_NUM_FIELDS];
+    // workspace
+    double* ws;               // slots * ws_slot doubles
+    long long ws_slot;        // doubles per slot
+    int ws_off[WS_NUM];       // offsets within a slot
+    unsigned smem_mask;       // bit b set: buffer b lives in shared memory
+    int smem_off[WS_NUM];     // offsets within dynamic smem (doubles)
+    int* counter;             // dynamic QP scheduler
+};
+
+struct SolveParams {
+    OcpIpmArgC arg;
+    double* y; double* pi; double* lam; double* t;
+    int32_t* status; int32_t* iters; double* res; long long* flops; double* trace;
+};
+
+// launchers (ocpqp_ipm.cu)
+cudaError_t launch_ipm_solve(const KParams& p, const SolveParams& sp, int grid, int threads,
+                             size_t smem, cudaStream_t stream);
+cudaError_t launch_newton_step(const KParams& p, double reg, const double* lam, const double* t,
+                               const double* rg, const double* rb, const double* rd,
+                               const double* rm, double* sy, double* spi, double* slam,
+                               double* st, int* fail, int grid, int threads, cudaStream_t stream);
+cudaError_t launch_residuals(const KParams& p, const double* y, const double* pi,
+                             const double* lam, const double* t, double* rg, double* rb,
+                             double* rd, double* rm, double* norms, int grid, int threads,
+                             cudaStream_t stream);
+int ipm_occupancy(int threads, size_t smem);
+
+}  // namespace ocpqp
