@@ -212,6 +212,10 @@ int ocpqp_factor_export(OcpPlan* plan, int32_t qp, double* P_out, double* K_out)
  * doubles per slot. */
 int ocpqp_plan_info(const OcpPlan* plan, int64_t* out, int32_t out_len);
 
+/* fp64 peak microbenchmarks (roofline denominators): DFMA and DMMA
+ * (mma.sync.m8n8k4.f64) throughput of the current device in TFLOP/s. */
+int ocpqp_fp64_peak(double* dfma_tflops, double* dmma_tflops);
+
 /* Library identity. */
 int ocpqp_abi_version(void);
 const char* ocpqp_last_error(void);

@@ -29,7 +29,7 @@ NF = len(FIELD_ORDER)
 EXPORTED_SYMBOLS = (
     "ocpqp_layout", "ocpqp_plan_create", "ocpqp_plan_destroy", "ocpqp_solve",
     "ocpqp_solve_host", "ocpqp_residuals", "ocpqp_newton_step", "ocpqp_factor_export",
-    "ocpqp_plan_info", "ocpqp_abi_version", "ocpqp_last_error",
+    "ocpqp_plan_info", "ocpqp_fp64_peak", "ocpqp_abi_version", "ocpqp_last_error",
 )
 
 _i32p = ctypes.POINTER(ctypes.c_int32)
@@ -180,10 +180,10 @@ class Plan:
         self.handle = h
 
     def info(self):
-        out = (ctypes.c_int64 * 5)()
-        check(lib().ocpqp_plan_info(self.handle, out, 5))
+        out = (ctypes.c_int64 * 6)()
+        check(lib().ocpqp_plan_info(self.handle, out, 6))
         return dict(threads=out[0], slots=out[1], smem_bytes=out[2], smem_mask=out[3],
-                    ws_doubles_per_slot=out[4])
+                    ws_doubles_per_slot=out[4], shaped_kernel=bool(out[5]))
 
     def close(self):
         if getattr(self, "handle", None):

@@ -2,6 +2,7 @@
 // layout tables, workspace placement (shared memory vs per-slot global), and
 // the device- and host-buffer solve entry points.
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -176,6 +177,7 @@ int build_layout(const OcpQpDimC* d, Layout& L) {
     w[WS_G] = (long long)L.nw_max * L.nw_max;
     w[WS_T1] = t1;
     w[WS_VEC] = L.nw_max + L.nx_max + std::max(L.nu_max, L.nx_max);
+    w[WS_IY] = L.ny; w[WS_IPI] = L.ne; w[WS_ILAM] = L.nc; w[WS_IT] = L.nc;
     return OCPQP_OK;
 }
 
@@ -191,8 +193,15 @@ struct OcpPlan {
     int threads = 32;
     int slots = 1;
     size_t smem_bytes = 0;
-    unsigned smem_mask = 0;
+    unsigned long long smem_mask = 0;
     int smem_off[WS_NUM] = {0};
+    // shaped fast path (ocpqp_fast.cu)
+    bool fast = false;
+    FastShape shape{0, 0, 0, 0};
+    int NB = 0, NBN = 0, NGN = 0;
+    int stage_smem = 0;          // offset (doubles) of the per-stage scratch
+    double* d_defaults = nullptr;  // zeros | ones | -inf | +inf, each max_flen long
+    long long max_flen = 1;
     int ws_off[WS_NUM] = {0};
     long long ws_slot = 0;
     // device structure tables
@@ -263,7 +272,7 @@ void place_workspace(OcpPlan* P) {
         const long long sz = align2(L.ws_size[b]) * 8;
         if (sz == 0) continue;
         if (used + sz <= budget) {
-            P->smem_mask |= 1u << b;
+            P->smem_mask |= 1ull << b;
             P->smem_off[b] = (int)(used / 8);
             used += sz;
         }
@@ -287,8 +296,98 @@ void fill_kparams(const OcpPlan* P, KParams& k, const OcpQpDataC* data, bool use
     }
     k.ws = P->d_ws; k.ws_slot = P->ws_slot;
     for (int b = 0; b < WS_NUM; ++b) { k.ws_off[b] = P->ws_off[b]; k.smem_off[b] = P->smem_off[b]; }
-    k.smem_mask = use_smem ? P->smem_mask : 0u;
+    k.smem_mask = use_smem ? P->smem_mask : 0ull;
     k.counter = P->d_counter;
+    k.NB = P->NB; k.NBN = P->NBN; k.NGN = P->NGN;
+    k.stage_smem = P->stage_smem;
+}
+
+// The shaped kernel reads every field unconditionally: absent fields point at
+// the plan's default rows (zeros, ones for masks, -inf / +inf for bounds).
+void fill_defaults(const OcpPlan* P, KParams& k) {
+    const long long L = P->max_flen;
+    for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) {
+        if (k.f[f]) continue;
+        int which = 0;
+        if (f == OCPQP_F_maskl || f == OCPQP_F_masku) which = 1;
+        else if (f == OCPQP_F_lb || f == OCPQP_F_lg) which = 2;
+        else if (f == OCPQP_F_ub || f == OCPQP_F_ug) which = 3;
+        k.f[f] = P->d_defaults + which * L;
+        k.bs[f] = 0;
+    }
+}
+
+// Shaped-kernel eligibility: uniform stages 0..N-1 (nx, nu >= 1, nb, ng),
+// terminal stage with nu = 0, nx equal, nb <= nx, ng <= NG; no soft rows.
+bool detect_fast(OcpPlan* P) {
+    const Layout& L = P->L;
+    const char* gen = getenv("OCPQP_GENERIC");
+    if (gen && atoi(gen)) return false;
+    const int N = L.N;
+    if (N < 1 || L.ns_tot != 0) return false;
+    const int NX = L.nx[0], NU = L.nu[0], NB = L.nb[0], NG = L.ng[0];
+    if (NU < 1 || NX < 1) return false;
+    for (int n = 0; n < N; ++n)
+        if (L.nx[n] != NX || L.nu[n] != NU || L.nb[n] != NB || L.ng[n] != NG) return false;
+    if (L.nx[N] != NX || L.nu[N] != 0 || L.ng[N] > NG || L.nb[N] > NX) return false;
+    int team = 0;
+    const char* envt = getenv("OCPQP_TEAM");
+    if (envt && atoi(envt) > 0) {
+        team = atoi(envt);
+        if (!fast_supported(FastShape{NX, NU, NG, team})) return false;
+    } else {
+        const int cands[] = {32, 64, 128, 256};
+        int pref = NX + NU <= 12 ? 32 : NX + NU <= 32 ? 64 : NX + NU <= 48 ? 128 : 256;
+        if (fast_supported(FastShape{NX, NU, NG, pref})) team = pref;
+        for (int c : cands)
+            if (!team && fast_supported(FastShape{NX, NU, NG, c})) team = c;
+        if (!team) return false;
+    }
+    P->fast = true;
+    P->shape = FastShape{NX, NU, NG, team};
+    P->NB = NB; P->NBN = L.nb[N]; P->NGN = L.ng[N];
+    return true;
+}
+
+// Placement for the shaped kernel: per-stage scratch first, then the hottest
+// per-QP buffers while they fit.
+void place_fast(OcpPlan* P) {
+    const Layout& L = P->L;
+    long long sz[WS_NUM];
+    for (int b = 0; b < WS_NUM; ++b) sz[b] = L.ws_size[b];
+    P->threads = P->shape.team;
+    long long off = 0;
+    for (int b = 0; b < WS_NUM; ++b) {
+        P->ws_off[b] = (int)off;
+        off += align2(sz[b]);
+    }
+    P->ws_slot = std::max(2ll, off);
+    const long long stage = align2(fast_stage_smem_doubles(P->shape)) * 8;
+    int tgt = std::max(1, 1024 / P->threads);
+    const int per_sm_need = (P->B + P->num_sms - 1) / std::max(1, P->num_sms);
+    tgt = std::max(1, std::min(tgt, per_sm_need));
+    const char* envs = getenv("OCPQP_SMEM_KB");
+    long long budget;
+    if (envs) budget = (long long)atoi(envs) * 1024;
+    else budget = std::min((228ll * 1024) / tgt - 2048, 227ll * 1024 - 2048);
+    budget -= stage;
+    const int prio[] = {WS_ILAM, WS_IT, WS_ACT, WS_DVEC, WS_IY, WS_IPI, WS_GAM, WS_RD, WS_WALL,
+                        WS_DIR_LAM, WS_DIR_T, WS_AFF_LAM, WS_AFF_T, WS_CROW, WS_ROWV, WS_COEF,
+                        WS_PV, WS_KFF, WS_L, WS_LP0, WS_K, WS_P, WS_RG, WS_RB, WS_RHAT, WS_DIR_Y,
+                        WS_DIR_PI, WS_AFF_Y, WS_AFF_PI};
+    long long used = 0;
+    P->smem_mask = 0;
+    for (int b : prio) {
+        const long long bytes = align2(sz[b]) * 8;
+        if (bytes == 0) continue;
+        if (used + bytes <= budget) {
+            P->smem_mask |= 1ull << b;
+            P->smem_off[b] = (int)(used / 8);
+            used += bytes;
+        }
+    }
+    P->stage_smem = (int)(used / 8);
+    P->smem_bytes = (size_t)(used + stage);
 }
 
 int check_arg(const OcpIpmArgC* a) {
@@ -339,12 +438,26 @@ int ocpqp_plan_create(const OcpQpDimC* dim, int32_t batch, OcpPlan** out) {
     cudaError_t e = cudaGetDevice(&P->device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device);
     if (e != cudaSuccess) { delete P; return cuda_fail(e, "no CUDA device"); }
-    place_workspace(P);
-    int occ = ipm_occupancy(P->threads, P->smem_bytes);
-    while (occ == 0 && P->smem_bytes > 0) {
-        // shrink the shared-memory share until one CTA fits
-        P->smem_mask = 0; P->smem_bytes = 0;
-        occ = ipm_occupancy(P->threads, 0);
+    int occ = 0;
+    if (detect_fast(P)) {
+        place_fast(P);
+        occ = fast_occupancy(P->shape, P->smem_bytes);
+        if (occ == 0) {  // placement too greedy: scratch only
+            P->smem_mask = 0;
+            P->stage_smem = 0;
+            P->smem_bytes = align2(fast_stage_smem_doubles(P->shape)) * 8;
+            occ = fast_occupancy(P->shape, P->smem_bytes);
+        }
+        if (occ == 0) P->fast = false;
+    }
+    if (!P->fast) {
+        place_workspace(P);
+        occ = ipm_occupancy(P->threads, P->smem_bytes);
+        while (occ == 0 && P->smem_bytes > 0) {
+            // shrink the shared-memory share until one CTA fits
+            P->smem_mask = 0; P->smem_bytes = 0;
+            occ = ipm_occupancy(P->threads, 0);
+        }
     }
     if (occ == 0) { delete P; return fail(OCPQP_E_CUDA, "kernel does not fit on an SM"); }
     P->slots = std::max(1, std::min(std::max(1, batch), occ * P->num_sms));
@@ -356,6 +469,18 @@ int ocpqp_plan_create(const OcpQpDimC* dim, int32_t batch, OcpPlan** out) {
     if (e == cudaSuccess) e = cudaMalloc(&P->d_var_box, sizeof(int) * L.var_box.size());
     if (e == cudaSuccess) e = cudaMalloc(&P->d_row_slack, sizeof(int) * L.row_slack.size());
     if (e == cudaSuccess) e = cudaMalloc(&P->d_counter, sizeof(int));
+    for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) P->max_flen = std::max(P->max_flen, L.flen[f]);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_defaults, sizeof(double) * 4 * P->max_flen);
+    if (e == cudaSuccess) {
+        std::vector<double> dflt(4 * P->max_flen);
+        for (long long i = 0; i < P->max_flen; ++i) {
+            dflt[i] = 0.0;
+            dflt[P->max_flen + i] = 1.0;
+            dflt[2 * P->max_flen + i] = -INFINITY;
+            dflt[3 * P->max_flen + i] = INFINITY;
+        }
+        e = cudaMemcpy(P->d_defaults, dflt.data(), sizeof(double) * dflt.size(), cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess) e = cudaMalloc(&P->d_ws, sizeof(double) * (size_t)P->ws_slot * P->slots);
     if (e == cudaSuccess) e = cudaMemcpy(P->d_st, L.st.data(), sizeof(StageInfo) * S, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !L.idxb.empty())
@@ -378,7 +503,7 @@ int ocpqp_plan_create(const OcpQpDimC* dim, int32_t batch, OcpPlan** out) {
 int ocpqp_plan_destroy(OcpPlan* P) {
     if (!P) return OCPQP_OK;
     cudaFree(P->d_st); cudaFree(P->d_idxb); cudaFree(P->d_idxs); cudaFree(P->d_var_box);
-    cudaFree(P->d_row_slack); cudaFree(P->d_counter); cudaFree(P->d_ws);
+    cudaFree(P->d_row_slack); cudaFree(P->d_counter); cudaFree(P->d_ws); cudaFree(P->d_defaults);
     for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) cudaFree(P->h_field[f]);
     cudaFree(P->hy); cudaFree(P->hpi); cudaFree(P->hlam); cudaFree(P->ht);
     cudaFree(P->hstatus); cudaFree(P->hiters); cudaFree(P->hres); cudaFree(P->hflops);
@@ -390,9 +515,9 @@ int ocpqp_plan_destroy(OcpPlan* P) {
 // Plan introspection for the host bindings: threads, slots, smem bytes,
 // smem mask, workspace doubles per slot.
 int ocpqp_plan_info(const OcpPlan* P, int64_t* out, int32_t out_len) {
-    if (!P || !out || out_len < 5) return fail(OCPQP_E_ARG, "bad arguments");
+    if (!P || !out || out_len < 6) return fail(OCPQP_E_ARG, "bad arguments");
     out[0] = P->threads; out[1] = P->slots; out[2] = (int64_t)P->smem_bytes;
-    out[3] = P->smem_mask; out[4] = P->ws_slot;
+    out[3] = (int64_t)P->smem_mask; out[4] = P->ws_slot; out[5] = P->fast ? 1 : 0;
     return OCPQP_OK;
 }
 
@@ -413,8 +538,15 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     sp.y = iter->y; sp.pi = iter->pi; sp.lam = iter->lam; sp.t = iter->t;
     sp.status = stats->status; sp.iters = stats->iterations; sp.res = stats->res;
     sp.flops = (long long*)stats->flops; sp.trace = stats->trace;
-    cudaError_t e = launch_ipm_solve(k, sp, P->slots, P->threads, P->smem_bytes, (cudaStream_t)stream);
-    if (e != cudaSuccess) return cuda_fail(e, "k_ipm_solve launch");
+    cudaError_t e;
+    if (P->fast) {
+        fill_defaults(P, k);
+        e = launch_fast_solve(P->shape, k, sp, P->slots, P->smem_bytes, (cudaStream_t)stream);
+        if (e != cudaSuccess) return cuda_fail(e, "k_fast_solve launch");
+    } else {
+        e = launch_ipm_solve(k, sp, P->slots, P->threads, P->smem_bytes, (cudaStream_t)stream);
+        if (e != cudaSuccess) return cuda_fail(e, "k_ipm_solve launch");
+    }
     return OCPQP_OK;
 }
 

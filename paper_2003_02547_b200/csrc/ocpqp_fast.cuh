@@ -1,0 +1,1076 @@
+// Shaped fused OCP-QP IPM kernel for sm_100a (fp64).
+//
+// Same algorithm as ocpqp_ipm.cu (the speed-mode loop of the reference,
+// solver.py:180-308, with the classical Riccati factor/solve of
+// kkt_ocp.py:142-320), specialised at compile time on the stage shape
+// (NX states, NU inputs, NG general rows on stages 0..N-1; terminal stage N
+// with nu = 0, nb <= NX, ng <= NG) and on the team size.  Compile-time shapes
+// turn every stage offset into a formula, keep the dense stage algebra in
+// unrolled register/shared-memory loops, and let the small factorizations run
+// as warp-synchronous register code:
+//   * per stage, the recursion works on shared-memory tiles P_{n+1}, T1 =
+//     P_{n+1}[B A] and the input rows of G; P_n, K_n and L_uu,n are written to
+//     the factor store (shared memory when it fits, else the slot's global
+//     workspace, which stays L2-resident);
+//   * chol(G_uu) for NU <= 32 runs in warp 0 with lane i owning row i;
+//   * mat-vecs of the solve sweeps split each dot product over a lane group
+//     and reduce with warp shuffles.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#pragma once
+#include "ocpqp_internal.h"
+
+namespace ocpqp {
+namespace fastk {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <int TEAM>
+__device__ __forceinline__ void bar() {
+    if constexpr (TEAM == 32) __syncwarp();
+    else __syncthreads();
+}
+
+template <int TEAM>
+__device__ __forceinline__ int any_of(int v) {
+    if constexpr (TEAM == 32) return __any_sync(FULL, v);
+    else return __syncthreads_or(v);
+}
+
+template <int TEAM>
+__device__ __forceinline__ double tsum(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    if constexpr (TEAM == 32) {
+        return v;
+    } else {
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < TEAM / 32; ++i) s += red[i];
+        return s;
+    }
+}
+
+template <int TEAM>
+__device__ __forceinline__ double tmax(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
+    if constexpr (TEAM == 32) {
+        return v;
+    } else {
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        double s = red[0];
+#pragma unroll
+        for (int i = 1; i < TEAM / 32; ++i) s = fmax(s, red[i]);
+        return s;
+    }
+}
+
+template <int TEAM>
+__device__ __forceinline__ double tmin(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
+    if constexpr (TEAM == 32) {
+        return v;
+    } else {
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        double s = red[0];
+#pragma unroll
+        for (int i = 1; i < TEAM / 32; ++i) s = fmin(s, red[i]);
+        return s;
+    }
+}
+
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
+
+struct AbsMax {
+    double m = 0.0;
+    int nan = 0;
+    __device__ __forceinline__ void add(double x) {
+        if (isnan(x)) nan = 1;
+        else m = fmax(m, fabs(x));
+    }
+};
+
+template <int TEAM>
+__device__ __forceinline__ double tabsmax(const AbsMax& a, double* red) {
+    const int nan = any_of<TEAM>(a.nan);
+    const double m = tmax<TEAM>(a.m, red);
+    return nan ? qnan() : m;
+}
+
+// lane-group split mat-vec: out(i, sum_k a(i,k) x(k)) for i < R.  GS lanes
+// per row reduce with butterflies; all lanes take part in the shuffles.
+template <int R, int KD, int TEAM>
+struct MV {
+    static constexpr int cap = TEAM / (R > 0 ? R : 1);
+    static constexpr int GS0 = cap >= 8 ? 8 : cap >= 4 ? 4 : cap >= 2 ? 2 : 1;
+    static constexpr int GS = (KD >= 8 ? GS0 : (KD >= 4 ? (GS0 < 4 ? GS0 : 4) : (KD >= 2 ? (GS0 < 2 ? GS0 : 2) : 1)));
+    static constexpr int RPP = TEAM / GS;  // rows per pass
+    template <class FA, class FX, class FO>
+    __device__ __forceinline__ static void run(FA a, FX x, FO out) {
+        const int tid = threadIdx.x;
+        const int g = tid % GS;
+        const int r0 = tid / GS;
+#pragma unroll
+        for (int i0 = 0; i0 < R; i0 += RPP) {
+            const int i = i0 + r0;
+            double acc = 0.0;
+            if (i < R) {
+#pragma unroll 4
+                for (int k = g; k < KD; k += GS) acc = fma(a(i, k), x(k), acc);
+            }
+#pragma unroll
+            for (int o = GS / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+            if (i < R && g == 0) out(i, acc);
+        }
+    }
+};
+
+// Cholesky of an NN x NN (NN <= 32) matrix held row-wise by the lanes of one
+// warp (lane i: row[j] = A[i][j], j <= i).  Pivot test as LAPACK potrf: a
+// pivot that is not > 0 (or NaN) fails (linalg.py:81-118).
+template <int NN>
+__device__ __forceinline__ bool warp_chol(double (&row)[NN], int lane) {
+#pragma unroll
+    for (int k = 0; k < NN; ++k) {
+        const double piv = __shfl_sync(FULL, row[k], k);
+        if (!(piv > 0.0)) return false;
+        const double dkk = sqrt(piv);
+        const double inv = 1.0 / dkk;
+        const double lik = lane == k ? dkk : row[k] * inv;
+        if (lane >= k) row[k] = lik;
+#pragma unroll
+        for (int j = k + 1; j < NN; ++j) {
+            const double ljk = __shfl_sync(FULL, lik, j);
+            if (lane >= j) row[j] = fma(-lik, ljk, row[j]);
+        }
+    }
+    return true;
+}
+
+// Team Cholesky of an n x n matrix in place (lower; upper zeroed), any n.
+template <int TEAM>
+__device__ bool team_chol(double* L, int n, int* flag) {
+    const int tid = threadIdx.x;
+    for (int k = 0; k < n; ++k) {
+        if (tid == 0) {
+            const double d = L[k * n + k];
+            const int ok = d > 0.0;
+            if (ok) L[k * n + k] = sqrt(d);
+            *flag = ok;
+        }
+        bar<TEAM>();
+        if (!*flag) return false;
+        const double inv = 1.0 / L[k * n + k];
+        for (int i = k + 1 + tid; i < n; i += TEAM) L[i * n + k] *= inv;
+        bar<TEAM>();
+        const int rem = n - k - 1;
+        for (int idx = tid; idx < rem * rem; idx += TEAM) {
+            const int i = k + 1 + idx / rem, j = k + 1 + idx % rem;
+            if (j <= i) L[i * n + j] = fma(-L[i * n + k], L[j * n + k], L[i * n + j]);
+        }
+        bar<TEAM>();
+    }
+    for (int idx = tid; idx < n * n; idx += TEAM) {
+        const int i = idx / n, j = idx - i * n;
+        if (j > i) L[idx] = 0.0;
+    }
+    bar<TEAM>();
+    return true;
+}
+
+// per-CTA context in shared memory
+struct FCtx {
+    const double* f[OCPQP_NUM_FIELDS];
+    double* w[WS_NUM];
+    double red[32];
+    int flag;
+    int q;
+    double n_act;
+};
+
+// runtime structure (uniform stages)
+struct RD {
+    int N, NB, M, NBN, NGN, MN, nc, nv, ne, msum;
+    __device__ __forceinline__ int slot_stage(int k) const {
+        if (M == 0) return N;
+        const int n = k / (2 * M);
+        return n < N ? n : N;
+    }
+    __device__ __forceinline__ int row_stage(int r) const {
+        if (M == 0) return N;
+        const int n = r / M;
+        return n < N ? n : N;
+    }
+};
+
+template <int NX_, int NU_, int NG_, int TEAM_>
+struct Shape {
+    static constexpr int NX = NX_, NU = NU_, NG = NG_, TEAM = TEAM_, NW = NU_ + NX_;
+    static constexpr int T1N = NX * (NW > NX ? NW : NX);
+    static constexpr int VEC = 2 * NW + 3 * NX + 2 * NU + 16;
+    static constexpr int STAGE = NX * NX + T1N + NU * NW + VEC;
+};
+
+template <class S>
+struct Kern {
+    static constexpr int NX = S::NX, NU = S::NU, NG = S::NG, NW = S::NW, TEAM = S::TEAM;
+
+    // ---- field access (uniform-stage formula offsets) ----
+    __device__ static __forceinline__ const double* A(const FCtx& c, int n) { return c.f[OCPQP_F_A] + n * NX * NX; }
+    __device__ static __forceinline__ const double* Bm(const FCtx& c, int n) { return c.f[OCPQP_F_B] + n * NX * NU; }
+    __device__ static __forceinline__ const double* bv(const FCtx& c, int n) { return c.f[OCPQP_F_b] + n * NX; }
+    __device__ static __forceinline__ const double* Q(const FCtx& c, int n) { return c.f[OCPQP_F_Q] + n * NX * NX; }
+    __device__ static __forceinline__ const double* Sm(const FCtx& c, int n) { return c.f[OCPQP_F_S] + n * NU * NX; }
+    __device__ static __forceinline__ const double* R(const FCtx& c, int n) { return c.f[OCPQP_F_R] + n * NU * NU; }
+    __device__ static __forceinline__ const double* qv(const FCtx& c, int n) { return c.f[OCPQP_F_q] + n * NX; }
+    __device__ static __forceinline__ const double* rv(const FCtx& c, int n) { return c.f[OCPQP_F_r] + n * NU; }
+    __device__ static __forceinline__ const double* Cm(const FCtx& c, int n) { return c.f[OCPQP_F_C] + n * NG * NX; }
+    __device__ static __forceinline__ const double* Dm(const FCtx& c, int n) { return c.f[OCPQP_F_D] + n * NG * NU; }
+    // general-row entry Jg[g][j] = [D C] of stage n (nu_n = NU for n < N, 0 at N)
+    __device__ static __forceinline__ double Jg(const FCtx& c, int n, int nu_n, int g, int j) {
+        return j < nu_n ? Dm(c, n)[g * NU + j] : Cm(c, n)[g * NX + (j - nu_n)];
+    }
+
+    // ---------------- setup: d vector, activity (view.py:108-129, 156-184) ----------------
+    __device__ static void setup(FCtx& c, const RD& d) {
+        double* dvec = c.w[WS_DVEC];
+        double* act = c.w[WS_ACT];
+        double cnt = 0.0;
+        for (int k = threadIdx.x; k < d.nc; k += TEAM) {
+            const int n = d.slot_stage(k);
+            const int m = n < d.N ? d.M : d.MN;
+            const int nb = n < d.N ? d.NB : d.NBN;
+            const int kk = k - n * 2 * d.M;
+            const int lo = kk < m;
+            const int i = lo ? kk : kk - m;
+            double bound;
+            if (i < nb) bound = c.f[lo ? OCPQP_F_lb : OCPQP_F_ub][n * d.NB + i];
+            else bound = c.f[lo ? OCPQP_F_lg : OCPQP_F_ug][n * NG + (i - nb)];
+            const double mask = c.f[lo ? OCPQP_F_maskl : OCPQP_F_masku][n * d.M + i];
+            const bool a = (mask != 0.0) && isfinite(bound);
+            act[k] = a ? 1.0 : 0.0;
+            dvec[k] = a ? (lo ? bound : -bound) : 0.0;
+            cnt += a ? 1.0 : 0.0;
+        }
+        const double tot = tsum<TEAM>(cnt, c.red);
+        if (threadIdx.x == 0) c.n_act = tot;
+        bar<TEAM>();
+    }
+
+    // row values Jc w for all rows (ConBlock.rows_w, view.py:91-97)
+    __device__ static void rows_values(const FCtx& c, const RD& d, const int* idxb, const double* y,
+                                       double* rowv) {
+        for (int r = threadIdx.x; r < d.msum; r += TEAM) {
+            const int n = d.row_stage(r);
+            const int i = r - n * d.M;
+            const int nb = n < d.N ? d.NB : d.NBN;
+            const double* w = y + n * NW;
+            double v;
+            if (i < nb) {
+                v = w[idxb[n * d.NB + i]];
+            } else {
+                const int g = i - nb;
+                const int nu_n = n < d.N ? NU : 0;
+                v = 0.0;
+                if (n < d.N) {
+#pragma unroll 4
+                    for (int j = 0; j < NW; ++j) v = fma(Jg(c, n, NU, g, j), w[j], v);
+                } else {
+                    for (int j = 0; j < NX; ++j) v = fma(Jg(c, n, nu_n, g, j), w[j], v);
+                }
+            }
+            rowv[r] = v;
+        }
+    }
+
+    // Jc' coeff at window variable j of stage n
+    __device__ static __forceinline__ double rows_t(const FCtx& c, const RD& d, const int* var_box,
+                                                    int n, int jglob, int j, const double* coeff) {
+        const int kb = var_box[jglob];
+        double out = kb >= 0 ? coeff[n * d.M + kb] : 0.0;
+        const int ng = n < d.N ? NG : d.NGN;
+        if (NG > 0 && ng > 0) {
+            const int nb = n < d.N ? d.NB : d.NBN;
+            const int nu_n = n < d.N ? NU : 0;
+            double g = 0.0;
+            for (int r = 0; r < ng; ++r) g = fma(Jg(c, n, nu_n, r, j), coeff[n * d.M + nb + r], g);
+            out += g;
+        }
+        return out;
+    }
+
+    __device__ static __forceinline__ double slot_cy(const RD& d, int k, const double* rowv) {
+        const int n = d.slot_stage(k);
+        const int m = n < d.N ? d.M : d.MN;
+        const int kk = k - n * 2 * d.M;
+        return kk < m ? rowv[n * d.M + kk] : -rowv[n * d.M + kk - m];
+    }
+
+    struct Res {
+        double g, b, d, m, mu;
+    };
+
+    // ---------------- residuals (view.py:272-288) ----------------
+    __device__ static Res residuals(FCtx& c, const RD& d, const KParams& p, const double* y,
+                                    const double* pi, const double* lam, const double* t) {
+        const double* act = c.w[WS_ACT];
+        const double* dvec = c.w[WS_DVEC];
+        double* rowv = c.w[WS_ROWV];
+        double* crow = c.w[WS_CROW];
+        double* r_g = c.w[WS_RG];
+        double* r_b = c.w[WS_RB];
+        double* r_d = c.w[WS_RD];
+        rows_values(c, d, p.idxb, y, rowv);
+        for (int r = threadIdx.x; r < d.msum; r += TEAM) {
+            const int n = d.row_stage(r);
+            const int i = r - n * d.M;
+            const int m = n < d.N ? d.M : d.MN;
+            const int k = n * 2 * d.M + i;
+            const double ll = act[k] != 0.0 ? lam[k] : 0.0;
+            const double lu = act[k + m] != 0.0 ? lam[k + m] : 0.0;
+            crow[r] = ll - lu;
+        }
+        bar<TEAM>();
+        AbsMax ag, ab, ad, am;
+        double musum = 0.0;
+        for (int j = threadIdx.x; j < d.nv; j += TEAM) {
+            int n = j / NW;
+            if (n > d.N) n = d.N;
+            const int jj = j - n * NW;
+            const double* w = y + n * NW;
+            double r;
+            if (n < d.N) {
+                double h1 = 0.0, h2 = 0.0, g;
+                if (jj < NU) {
+                    const double* Rr = R(c, n) + jj * NU;
+                    const double* Sr = Sm(c, n) + jj * NX;
+#pragma unroll
+                    for (int k = 0; k < NU; ++k) h1 = fma(Rr[k], w[k], h1);
+#pragma unroll 8
+                    for (int k = 0; k < NX; ++k) h2 = fma(Sr[k], w[NU + k], h2);
+                    g = rv(c, n)[jj];
+                } else {
+                    const int jx = jj - NU;
+                    const double* Ss = Sm(c, n) + jx;
+                    const double* Qr = Q(c, n) + jx * NX;
+#pragma unroll
+                    for (int k = 0; k < NU; ++k) h1 = fma(Ss[k * NX], w[k], h1);
+#pragma unroll 8
+                    for (int k = 0; k < NX; ++k) h2 = fma(Qr[k], w[NU + k], h2);
+                    g = qv(c, n)[jx];
+                }
+                r = (h1 + h2) + g;
+                double atp = (jj >= NU && n > 0) ? pi[(n - 1) * NX + (jj - NU)] : 0.0;
+                double a = 0.0;
+                const double* pn = pi + n * NX;
+                if (jj < NU) {
+                    const double* Bc = Bm(c, n) + jj;
+#pragma unroll 8
+                    for (int k = 0; k < NX; ++k) a = fma(Bc[k * NU], pn[k], a);
+                } else {
+                    const double* Ac = A(c, n) + (jj - NU);
+#pragma unroll 8
+                    for (int k = 0; k < NX; ++k) a = fma(Ac[k * NX], pn[k], a);
+                }
+                atp -= a;
+                r -= atp;
+            } else {
+                const double* Qr = Q(c, n) + jj * NX;
+                double h2 = 0.0;
+#pragma unroll 8
+                for (int k = 0; k < NX; ++k) h2 = fma(Qr[k], w[k], h2);
+                r = (0.0 + h2) + qv(c, n)[jj];
+                const double atp = d.N > 0 ? pi[(n - 1) * NX + jj] : 0.0;
+                r -= atp;
+            }
+            r -= rows_t(c, d, p.var_box, n, j, jj, crow);
+            r_g[j] = r;
+            ag.add(r);
+        }
+        for (int e = threadIdx.x; e < d.ne; e += TEAM) {
+            const int n = e / NX;
+            const int i = e - n * NX;
+            const double* u = y + n * NW;
+            const double* x = u + NU;
+            const double xn = y[(n + 1) * NW + (n + 1 < d.N ? NU : 0) + i];
+            const double* Ar = A(c, n) + i * NX;
+            const double* Br = Bm(c, n) + i * NU;
+            double ax = 0.0, bu = 0.0;
+#pragma unroll 8
+            for (int k = 0; k < NX; ++k) ax = fma(Ar[k], x[k], ax);
+#pragma unroll
+            for (int k = 0; k < NU; ++k) bu = fma(Br[k], u[k], bu);
+            const double r = -((xn - ax) - bu) + bv(c, n)[i];
+            r_b[e] = r;
+            ab.add(r);
+        }
+        for (int k = threadIdx.x; k < d.nc; k += TEAM) {
+            double rd = 0.0, rm = 0.0;
+            if (act[k] != 0.0) {
+                rd = (-slot_cy(d, k, rowv) + dvec[k]) + t[k];
+                rm = lam[k] * t[k];
+                musum += rm;
+            }
+            r_d[k] = rd;
+            ad.add(rd);
+            am.add(rm);
+        }
+        Res o;
+        o.g = tabsmax<TEAM>(ag, c.red);
+        o.b = tabsmax<TEAM>(ab, c.red);
+        o.d = tabsmax<TEAM>(ad, c.red);
+        o.m = tabsmax<TEAM>(am, c.red);
+        const double tot = tsum<TEAM>(musum, c.red);
+        o.mu = c.n_act > 0.0 ? tot / c.n_act : 0.0;
+        return o;
+    }
+
+    // ---------------- classical Riccati factor ----------------
+    // returns -1 ok, failing stage, -2 non-positive iterate
+    __device__ static int factor(FCtx& c, const RD& d, const KParams& p, double* stg,
+                                 const double* lam, const double* t, double reg, long long& flops) {
+        const int tid = threadIdx.x;
+        const double* act = c.w[WS_ACT];
+        double* gam = c.w[WS_GAM];
+        double* coef = c.w[WS_COEF];
+        double* Pst = c.w[WS_P];
+        double* Kst = c.w[WS_K];
+        double* Lst = c.w[WS_L];
+        double* Pc = stg;                       // NX*NX: P_{n+1}, then G_xx / P_n
+        double* T1 = Pc + NX * NX;              // NX*NW
+        double* Gu = T1 + S::T1N;               // NU*NW
+        double* vec = Gu + NU * NW;
+        int bad = 0;
+        for (int k = tid; k < d.nc; k += TEAM) {
+            double g = 0.0;
+            if (act[k] != 0.0) {
+                if (lam[k] <= 0.0 || t[k] <= 0.0) bad = 1;
+                g = lam[k] / t[k];
+            }
+            gam[k] = g;
+        }
+        if (any_of<TEAM>(bad)) return -2;
+        bar<TEAM>();
+        for (int r = tid; r < d.msum; r += TEAM) {
+            const int n = d.row_stage(r);
+            const int i = r - n * d.M;
+            const int m = n < d.N ? d.M : d.MN;
+            const int k = n * 2 * d.M + i;
+            coef[r] = gam[k] + gam[k + m];
+        }
+        bar<TEAM>();
+        const int N = d.N;
+        // ---- terminal stage: P_N = sym(M~_N) ----
+        {
+            const int n = N;
+            const double* Qn = Q(c, n);
+            const double* cf = coef + n * d.M;
+            const int ng = d.NGN;
+            for (int idx = tid; idx < NX * NX; idx += TEAM) {
+                const int i = idx / NX, j = idx - i * NX;
+                double h = 0.5 * (Qn[i * NX + j] + Qn[j * NX + i]);
+                if (i == j) {
+                    const int kb = p.var_box[n * NW + i];
+                    if (kb >= 0) h += cf[kb];
+                }
+                if (NG > 0 && ng > 0) {
+                    const double* Cn = Cm(c, n);
+                    double a = 0.0;
+                    for (int r = 0; r < ng; ++r) a = fma(Cn[r * NX + i], cf[d.NBN + r] * Cn[r * NX + j], a);
+                    h = a + h;
+                }
+                if (i == j && reg != 0.0) h += reg;
+                T1[idx] = h;
+            }
+            if (NG > 0 && ng > 0) flops += 2ll * NX * NX * ng;
+            bar<TEAM>();
+            double* Pn = Pst + n * NX * NX;
+            for (int idx = tid; idx < NX * NX; idx += TEAM) {
+                const int i = idx / NX, j = idx - i * NX;
+                const double v = 0.5 * (T1[idx] + T1[j * NX + i]);
+                Pc[idx] = v;
+                Pn[idx] = v;
+            }
+            bar<TEAM>();
+        }
+        // ---- stages N-1 .. 0 ----
+        for (int n = N - 1; n >= 0; --n) {
+            const double* An = A(c, n);
+            const double* Bn = Bm(c, n);
+            // T1 = P_{n+1} [B A]   (kkt_ocp.py:232)
+            for (int idx = tid; idx < NX * NW; idx += TEAM) {
+                const int i = idx / NW, j = idx - i * NW;
+                const double* Pr = Pc + i * NX;
+                double a = 0.0;
+                if (j < NU) {
+#pragma unroll 8
+                    for (int k = 0; k < NX; ++k) a = fma(Pr[k], Bn[k * NU + j], a);
+                } else {
+                    const double* Ac = An + (j - NU);
+#pragma unroll 8
+                    for (int k = 0; k < NX; ++k) a = fma(Pr[k], Ac[k * NX], a);
+                }
+                T1[idx] = a;
+            }
+            bar<TEAM>();
+            // G = [B A]' T1 + M~ (kkt_ocp.py:233, 70-80): input rows -> Gu, G_xx -> Pc
+            const double* Qn = Q(c, n);
+            const double* Rn = R(c, n);
+            const double* Sn = Sm(c, n);
+            const double* cf = coef + n * d.M;
+            for (int idx = tid; idx < NU * NW + NX * NX; idx += TEAM) {
+                int i, j;
+                if (idx < NU * NW) { i = idx / NW; j = idx - i * NW; }
+                else { const int e = idx - NU * NW; i = NU + e / NX; j = NU + (e % NX); }
+                double a = 0.0;
+                if (i < NU) {
+#pragma unroll 8
+                    for (int k = 0; k < NX; ++k) a = fma(Bn[k * NU + i], T1[k * NW + j], a);
+                } else {
+                    const double* Ac = An + (i - NU);
+#pragma unroll 8
+                    for (int k = 0; k < NX; ++k) a = fma(Ac[k * NX], T1[k * NW + j], a);
+                }
+                double mij, mji;
+                if (i < NU && j < NU) { mij = Rn[i * NU + j]; mji = Rn[j * NU + i]; }
+                else if (i < NU) { mij = Sn[i * NX + (j - NU)]; mji = mij; }
+                else if (j < NU) { mij = Sn[j * NX + (i - NU)]; mji = mij; }
+                else { mij = Qn[(i - NU) * NX + (j - NU)]; mji = Qn[(j - NU) * NX + (i - NU)]; }
+                double h = 0.5 * (mij + mji);
+                if (i == j) {
+                    const int kb = p.var_box[n * NW + i];
+                    if (kb >= 0) h += cf[kb];
+                }
+                if (NG > 0) {
+                    double s = 0.0;
+#pragma unroll 4
+                    for (int r = 0; r < NG; ++r)
+                        s = fma(Jg(c, n, NU, r, i), cf[d.NB + r] * Jg(c, n, NU, r, j), s);
+                    h = s + h;
+                }
+                if (i == j && reg != 0.0) h += reg;
+                const double g = a + h;
+                if (i < NU) Gu[idx] = g;
+                else Pc[idx - NU * NW] = g;
+            }
+            if (NG > 0) flops += 2ll * NW * NW * NG;
+            flops += 2ll * NX * NW * NX + 2ll * NW * NW * NX;
+            bar<TEAM>();
+            // L_uu = chol(G_uu)
+            double* Ln = Lst + n * NU * NU;
+            double* rinv = vec;  // NU
+            flops += (long long)NU * NU * NU / 3;
+            if constexpr (NU <= 32) {
+                if (tid < 32) {
+                    double row[NU];
+#pragma unroll
+                    for (int j = 0; j < NU; ++j) row[j] = (tid < NU && j <= tid) ? Gu[tid * NW + j] : 0.0;
+                    const bool ok = warp_chol<NU>(row, tid);
+                    if (tid == 0) c.flag = ok;
+                    if (ok && tid < NU) {
+#pragma unroll
+                        for (int j = 0; j < NU; ++j) Ln[tid * NU + j] = j <= tid ? row[j] : 0.0;
+                    }
+                }
+                bar<TEAM>();
+                if (!c.flag) return n;
+                for (int i = tid; i < NU; i += TEAM) rinv[i] = 1.0 / Ln[i * NU + i];
+            } else {
+                for (int idx = tid; idx < NU * NU; idx += TEAM) {
+                    const int i = idx / NU, j = idx - i * NU;
+                    Ln[idx] = Gu[i * NW + j];
+                }
+                bar<TEAM>();
+                if (!team_chol<TEAM>(Ln, NU, &c.flag)) return n;
+                for (int i = tid; i < NU; i += TEAM) rinv[i] = 1.0 / Ln[i * NU + i];
+            }
+            bar<TEAM>();
+            // K = -L'^{-1} L^{-1} G_ux (kkt_ocp.py:240-243), one column per thread
+            double* Kn = Kst + n * NU * NX;
+            for (int j = tid; j < NX; j += TEAM) {
+                if constexpr (NU <= 32) {
+                    double z[NU];
+#pragma unroll
+                    for (int i = 0; i < NU; ++i) {
+                        double a = Gu[i * NW + NU + j];
+#pragma unroll
+                        for (int k = 0; k < i; ++k) a = fma(-Ln[i * NU + k], z[k], a);
+                        z[i] = a * rinv[i];
+                    }
+#pragma unroll
+                    for (int i = NU - 1; i >= 0; --i) {
+                        double a = z[i];
+#pragma unroll
+                        for (int k = i + 1; k < NU; ++k) a = fma(-Ln[k * NU + i], z[k], a);
+                        z[i] = a * rinv[i];
+                    }
+#pragma unroll
+                    for (int i = 0; i < NU; ++i) Kn[i * NX + j] = -z[i];
+                } else {
+                    for (int i = 0; i < NU; ++i) {
+                        double a = Gu[i * NW + NU + j];
+                        for (int k = 0; k < i; ++k) a = fma(-Ln[i * NU + k], Kn[k * NX + j], a);
+                        Kn[i * NX + j] = a * rinv[i];
+                    }
+                    for (int i = NU - 1; i >= 0; --i) {
+                        double a = Kn[i * NX + j];
+                        for (int k = i + 1; k < NU; ++k) a = fma(-Ln[k * NU + i], Kn[k * NX + j], a);
+                        Kn[i * NX + j] = a * rinv[i];
+                    }
+                    for (int i = 0; i < NU; ++i) Kn[i * NX + j] = -Kn[i * NX + j];
+                }
+            }
+            flops += 2ll * NU * NU * NX;
+            bar<TEAM>();
+            // P = G_xx + G_ux' K, symmetrised (kkt_ocp.py:244, 251)
+            for (int idx = tid; idx < NX * NX; idx += TEAM) {
+                const int i = idx / NX, j = idx - i * NX;
+                double a = 0.0;
+#pragma unroll
+                for (int k = 0; k < NU; ++k) a = fma(Gu[k * NW + NU + i], Kn[k * NX + j], a);
+                T1[idx] = a + Pc[idx];
+            }
+            flops += 2ll * NX * NX * NU;
+            bar<TEAM>();
+            double* Pn = Pst + n * NX * NX;
+            for (int idx = tid; idx < NX * NX; idx += TEAM) {
+                const int i = idx / NX, j = idx - i * NX;
+                const double v = 0.5 * (T1[idx] + T1[j * NX + i]);
+                Pc[idx] = v;
+                Pn[idx] = v;
+            }
+            bar<TEAM>();
+        }
+        // L_P0 = chol(P_0) (kkt_ocp.py:193-200)
+        double* LP0 = c.w[WS_LP0];
+        flops += (long long)NX * NX * NX / 3;
+        if constexpr (NX <= 32) {
+            if (tid < 32) {
+                double row[NX];
+#pragma unroll
+                for (int j = 0; j < NX; ++j) row[j] = (tid < NX && j <= tid) ? Pc[tid * NX + j] : 0.0;
+                const bool ok = warp_chol<NX>(row, tid);
+                if (tid == 0) c.flag = ok;
+                if (ok && tid < NX) {
+#pragma unroll
+                    for (int j = 0; j < NX; ++j) LP0[tid * NX + j] = j <= tid ? row[j] : 0.0;
+                }
+            }
+            bar<TEAM>();
+            if (!c.flag) return 0;
+        } else {
+            for (int idx = tid; idx < NX * NX; idx += TEAM) LP0[idx] = Pc[idx];
+            bar<TEAM>();
+            if (!team_chol<TEAM>(LP0, NX, &c.flag)) return 0;
+        }
+        return -1;
+    }
+
+    // warp-0 cho_solve of an n-vector: x <- (L L')^{-1} x, L row-major n x n.
+    // Right-looking: one broadcast per step.  Result written to out[] (scaled by sgn).
+    template <int NN>
+    __device__ static void warp_cho_solve(const double* L, const double* xin, double* out, double sgn) {
+        const int lane = threadIdx.x;
+        if constexpr (NN <= 32) {
+            double z = lane < NN ? xin[lane] : 0.0;
+            const double dii = lane < NN ? L[lane * NN + lane] : 1.0;
+#pragma unroll
+            for (int k = 0; k < NN; ++k) {
+                if (lane == k) z = z / dii;
+                const double zk = __shfl_sync(FULL, z, k);
+                if (lane > k && lane < NN) z = fma(-L[lane * NN + k], zk, z);
+            }
+#pragma unroll
+            for (int k = NN - 1; k >= 0; --k) {
+                if (lane == k) z = z / dii;
+                const double zk = __shfl_sync(FULL, z, k);
+                if (lane < k) z = fma(-L[k * NN + lane], zk, z);
+            }
+            if (lane < NN) out[lane] = sgn * z;
+        } else {
+            if (lane == 0) {
+                for (int i = 0; i < NN; ++i) out[i] = xin[i];
+                for (int i = 0; i < NN; ++i) {
+                    double a = out[i];
+                    for (int k = 0; k < i; ++k) a = fma(-L[i * NN + k], out[k], a);
+                    out[i] = a / L[i * NN + i];
+                }
+                for (int i = NN - 1; i >= 0; --i) {
+                    double a = out[i];
+                    for (int k = i + 1; k < NN; ++k) a = fma(-L[k * NN + i], out[k], a);
+                    out[i] = a / L[i * NN + i];
+                }
+                for (int i = 0; i < NN; ++i) out[i] *= sgn;
+            }
+        }
+    }
+
+    // ---------------- Riccati solve (kkt_ocp.py:254-320) ----------------
+    // r_m(k) = act ? (lam t - tau) + [dlam_a dt_a] : 0, or rm_ext (masked)
+    __device__ static int solve(FCtx& c, const RD& d, const KParams& p, double* stg,
+                                const double* lam, const double* t, const double* rm_ext,
+                                double tau, const double* dla, const double* dta, double* dy,
+                                double* dpi, double* dlam, double* dt, long long& flops) {
+        const int tid = threadIdx.x;
+        const double* act = c.w[WS_ACT];
+        const double* gam = c.w[WS_GAM];
+        const double* r_g = c.w[WS_RG];
+        const double* r_b = c.w[WS_RB];
+        const double* r_d = c.w[WS_RD];
+        double* wall = c.w[WS_WALL];
+        double* crow = c.w[WS_CROW];
+        double* rhat = c.w[WS_RHAT];
+        const double* Pst = c.w[WS_P];
+        const double* Kst = c.w[WS_K];
+        const double* Lst = c.w[WS_L];
+        double* pv = c.w[WS_PV];
+        double* kff = c.w[WS_KFF];
+        double* vec = stg + NX * NX + S::T1N + NU * NW;
+        double* win = vec;              // NW
+        double* e = vec + NW;           // NX
+        int nonfinite = 0;
+        // fold_rhs (kkt_common.py:118-137)
+        for (int k = tid; k < d.nc; k += TEAM) {
+            double w = 0.0;
+            if (act[k] != 0.0) {
+                double rmk;
+                if (rm_ext) {
+                    rmk = rm_ext[k];
+                } else {
+                    rmk = lam[k] * t[k] - tau;
+                    if (dla) rmk = rmk + dla[k] * dta[k];
+                }
+                w = (lam[k] * r_d[k] - rmk) / t[k];
+            }
+            wall[k] = w;
+        }
+        bar<TEAM>();
+        for (int r = tid; r < d.msum; r += TEAM) {
+            const int n = d.row_stage(r);
+            const int i = r - n * d.M;
+            const int m = n < d.N ? d.M : d.MN;
+            const int k = n * 2 * d.M + i;
+            crow[r] = wall[k] - wall[k + m];
+        }
+        bar<TEAM>();
+        for (int j = tid; j < d.nv; j += TEAM) {
+            int n = j / NW;
+            if (n > d.N) n = d.N;
+            rhat[j] = r_g[j] - rows_t(c, d, p.var_box, n, j, j - n * NW, crow);
+        }
+        bar<TEAM>();
+        const int N = d.N;
+        // backward sweep (kkt_ocp.py:276-289); terminal stage: nu = 0
+        for (int i = tid; i < NX; i += TEAM) pv[N * NX + i] = rhat[N * NW + i];
+        bar<TEAM>();
+        for (int n = N - 1; n >= 0; --n) {
+            const double* Pn = Pst + (n + 1) * NX * NX;
+            const double* rb = r_b + n * NX;
+            const double* pvn = pv + (n + 1) * NX;
+            MV<NX, NX, TEAM>::run([&](int i, int k) { return Pn[i * NX + k]; },
+                                  [&](int k) { return rb[k]; },
+                                  [&](int i, double v) { e[i] = v + pvn[i]; });
+            bar<TEAM>();
+            const double* An = A(c, n);
+            const double* Bn = Bm(c, n);
+            const double* rh = rhat + n * NW;
+            MV<NW, NX, TEAM>::run(
+                [&](int j, int k) { return j < NU ? Bn[k * NU + j] : An[k * NX + (j - NU)]; },
+                [&](int k) { return e[k]; },
+                [&](int j, double v) { win[j] = rh[j] + v; });
+            bar<TEAM>();
+            const double* Kn = Kst + n * NU * NX;
+            double* pvc = pv + n * NX;
+            MV<NX, NU, TEAM>::run([&](int i, int k) { return Kn[k * NX + i]; },
+                                  [&](int k) { return win[k]; },
+                                  [&](int i, double v) { pvc[i] = win[NU + i] + v; });
+            if (tid < 32) warp_cho_solve<NU>(Lst + n * NU * NU, win, kff + n * NU, -1.0);
+            flops += 2ll * NU * NU;
+            bar<TEAM>();
+        }
+        // x0 step
+        if (tid < 32) warp_cho_solve<NX>(c.w[WS_LP0], pv, dy + NU, -1.0);
+        flops += 2ll * NX * NX;
+        bar<TEAM>();
+        // forward rollout (kkt_ocp.py:293-305)
+        for (int n = 0; n < N; ++n) {
+            const double* xi = dy + n * NW + NU;
+            const double* Kn = Kst + n * NU * NX;
+            const double* kf = kff + n * NU;
+            double* du = dy + n * NW;
+            MV<NU, NX, TEAM>::run([&](int i, int k) { return Kn[i * NX + k]; },
+                                  [&](int k) { return xi[k]; },
+                                  [&](int i, double v) { du[i] = v + kf[i]; });
+            bar<TEAM>();
+            const double* An = A(c, n);
+            const double* Bn = Bm(c, n);
+            const double* rb = r_b + n * NX;
+            double* xn = dy + (n + 1) * NW + (n + 1 < N ? NU : 0);
+            MV<NX, NW, TEAM>::run(
+                [&](int i, int k) { return k < NX ? An[i * NX + k] : Bn[i * NU + (k - NX)]; },
+                [&](int k) { return k < NX ? xi[k] : du[k - NX]; },
+                [&](int i, double v) { xn[i] = v + rb[i]; });
+            bar<TEAM>();
+        }
+        // dpi_n = P_{n+1} x_{n+1} + pv_{n+1}, all stages in parallel
+        for (int e2 = tid; e2 < d.ne; e2 += TEAM) {
+            const int n = e2 / NX;
+            const int i = e2 - n * NX;
+            const double* Pn = Pst + (n + 1) * NX * NX + i * NX;
+            const double* xn = dy + (n + 1) * NW + (n + 1 < N ? NU : 0);
+            double a = 0.0;
+#pragma unroll 8
+            for (int k = 0; k < NX; ++k) a = fma(Pn[k], xn[k], a);
+            const double v = a + pv[(n + 1) * NX + i];
+            dpi[e2] = v;
+            if (!isfinite(v)) nonfinite = 1;
+        }
+        for (int j = tid; j < d.nv; j += TEAM)
+            if (!isfinite(dy[j])) nonfinite = 1;
+        // recover_block (kkt_common.py:140-163)
+        double* rowv = c.w[WS_ROWV];
+        rows_values(c, d, p.idxb, dy, rowv);
+        bar<TEAM>();
+        for (int k = tid; k < d.nc; k += TEAM) {
+            double dl = 0.0, dtt = 0.0;
+            if (act[k] != 0.0) {
+                const double cy = slot_cy(d, k, rowv);
+                dl = wall[k] - gam[k] * cy;
+                dtt = -r_d[k] + cy;
+            }
+            dlam[k] = dl;
+            dt[k] = dtt;
+            if (!isfinite(dl) || !isfinite(dtt)) nonfinite = 1;
+        }
+        return any_of<TEAM>(nonfinite);
+    }
+
+    __device__ static double max_step(FCtx& c, const RD& d, const double* lam, const double* t,
+                                      const double* dlam, const double* dt, double ftb) {
+        const double* act = c.w[WS_ACT];
+        double ratio = INFINITY;
+        for (int k = threadIdx.x; k < d.nc; k += TEAM) {
+            if (act[k] != 0.0) {
+                if (dlam[k] < 0.0) ratio = fmin(ratio, -lam[k] / dlam[k]);
+                if (dt[k] < 0.0) ratio = fmin(ratio, -t[k] / dt[k]);
+            }
+        }
+        ratio = tmin<TEAM>(ratio, c.red);
+        return fmin(1.0, ftb * ratio);
+    }
+
+    __device__ static double trial_mu(FCtx& c, const RD& d, const double* lam, const double* t,
+                                      const double* dlam, const double* dt, double alpha) {
+        const double* act = c.w[WS_ACT];
+        double s = 0.0;
+        for (int k = threadIdx.x; k < d.nc; k += TEAM)
+            if (act[k] != 0.0) s += (lam[k] + alpha * dlam[k]) * (t[k] + alpha * dt[k]);
+        s = tsum<TEAM>(s, c.red);
+        return c.n_act > 0.0 ? s / c.n_act : 0.0;
+    }
+
+    // ---------------- the IPM loop of one QP (solver.py:180-308) ----------------
+    __device__ static void ipm_one(FCtx& c, const RD& d, const KParams& p, const SolveParams& sp,
+                                   double* stg, int q) {
+        const OcpIpmArgC& arg = sp.arg;
+        const int tid = threadIdx.x;
+        double* gy = sp.y + (long long)q * d.nv;
+        double* gpi = sp.pi + (long long)q * d.ne;
+        double* glam = sp.lam + (long long)q * d.nc;
+        double* gt = sp.t + (long long)q * d.nc;
+        double* y = c.w[WS_IY];
+        double* pi = c.w[WS_IPI];
+        double* lam = c.w[WS_ILAM];
+        double* t = c.w[WS_IT];
+        double *ay = c.w[WS_AFF_Y], *api = c.w[WS_AFF_PI], *alam = c.w[WS_AFF_LAM], *at = c.w[WS_AFF_T];
+        double *dy = c.w[WS_DIR_Y], *dpi = c.w[WS_DIR_PI], *dlam = c.w[WS_DIR_LAM], *dt = c.w[WS_DIR_T];
+        setup(c, d);
+        // initial iterate (solver.py:113-142)
+        const int warm = arg.warm_start;
+        for (int i = tid; i < d.nv; i += TEAM) y[i] = warm ? gy[i] : 0.0;
+        for (int i = tid; i < d.ne; i += TEAM) pi[i] = warm == 2 ? gpi[i] : 0.0;
+        for (int k = tid; k < d.nc; k += TEAM) lam[k] = warm == 2 ? glam[k] : 0.0;
+        bar<TEAM>();
+        {
+            const double* act = c.w[WS_ACT];
+            const double* dvec = c.w[WS_DVEC];
+            double* rowv = c.w[WS_ROWV];
+            double floor = arg.t0;
+            if (warm) {
+                rows_values(c, d, p.idxb, y, rowv);
+                bar<TEAM>();
+            }
+            if (warm == 2) {
+                double gd = 0.0, gb = 0.0;
+                for (int k = tid; k < d.nc; k += TEAM)
+                    if (act[k] != 0.0) gd = fmax(gd, dvec[k] - slot_cy(d, k, rowv));
+                for (int e = tid; e < d.ne; e += TEAM) {
+                    const int n = e / NX, i = e - n * NX;
+                    const double* u = y + n * NW;
+                    const double* Ar = A(c, n) + i * NX;
+                    const double* Br = Bm(c, n) + i * NU;
+                    double ax = 0.0, bu = 0.0;
+                    for (int k = 0; k < NX; ++k) ax = fma(Ar[k], u[NU + k], ax);
+                    for (int k = 0; k < NU; ++k) bu = fma(Br[k], u[k], bu);
+                    const double xn = y[(n + 1) * NW + (n + 1 < d.N ? NU : 0) + i];
+                    gb = fmax(gb, fabs(-((xn - ax) - bu) + bv(c, n)[i]));
+                }
+                gd = tmax<TEAM>(gd, c.red);
+                gb = tmax<TEAM>(gb, c.red);
+                floor = fmax(fmax(1e-8, arg.t_min), fmin(1.0, fmax(gd, gb)));
+            }
+            const double lfloor = fmax(1e-8, arg.lam_min);
+            for (int k = tid; k < d.nc; k += TEAM) {
+                double tv = 0.0, lv = 0.0;
+                if (act[k] != 0.0) {
+                    const double cy = warm ? slot_cy(d, k, rowv) : 0.0;
+                    tv = fmax(cy - dvec[k], floor);
+                    lv = warm == 2 ? fmax(lam[k], lfloor) : arg.mu0 / tv;
+                }
+                t[k] = tv;
+                lam[k] = lv;
+            }
+            bar<TEAM>();
+        }
+        double* trace = sp.trace ? sp.trace + (long long)q * arg.iter_max * 8 : nullptr;
+        long long flops = 0;
+        double alpha_last = 1.0;
+        int it = 0, status = -1;
+        Res res;
+        const double reg2 = arg.reg_prim > 0.0 ? 2.0 * arg.reg_prim : 1e-8;
+        while (true) {
+            res = residuals(c, d, p, y, pi, lam, t);
+            const double mu = res.mu;
+            if (!isfinite(res.g) || !isfinite(res.b) || !isfinite(res.d) || !isfinite(res.m) || !isfinite(mu))
+                status = OCPQP_STATUS_NAN;
+            else if (alpha_last < arg.alpha_min)
+                status = OCPQP_STATUS_MINSTEP;
+            else if (mu <= arg.tol_comp && res.g <= arg.tol_stat && res.b <= arg.tol_eq &&
+                     res.d <= arg.tol_ineq && res.m <= arg.tol_comp)
+                status = OCPQP_STATUS_SUCCESS;
+            else if (it >= arg.iter_max)
+                status = OCPQP_STATUS_MAXITER;
+            if (status >= 0) break;
+            bar<TEAM>();
+            int fs = factor(c, d, p, stg, lam, t, arg.reg_prim, flops);
+            if (fs >= 0) { bar<TEAM>(); fs = factor(c, d, p, stg, lam, t, reg2, flops); }
+            if (fs == -2) { status = OCPQP_STATUS_NONPOSITIVE_ITERATE; break; }
+            if (fs >= 0) { status = OCPQP_STATUS_FAILURE; break; }
+            if (solve(c, d, p, stg, lam, t, nullptr, 0.0, nullptr, nullptr, ay, api, alam, at, flops)) {
+                status = OCPQP_STATUS_NAN;
+                break;
+            }
+            bar<TEAM>();
+            const double alpha_aff = max_step(c, d, lam, t, alam, at, 1.0);
+            const double mu_aff = trial_mu(c, d, lam, t, alam, at, alpha_aff);
+            double sigma = 0.0;
+            if (mu > 0.0) sigma = fmin(1.0, fmax(0.0, pow(mu_aff / mu, 3.0)));
+            const double tau = sigma * mu;
+            int nf = solve(c, d, p, stg, lam, t, nullptr, tau, arg.pred_corr ? alam : nullptr,
+                           arg.pred_corr ? at : nullptr, dy, dpi, dlam, dt, flops);
+            bar<TEAM>();
+            if (arg.pred_corr && arg.cond_pred_corr) {
+                const double a_t = max_step(c, d, lam, t, dlam, dt, 1.0);
+                const double mu_t = trial_mu(c, d, lam, t, dlam, dt, a_t);
+                if (!(mu_t <= arg.corr_ratio * mu_aff)) {
+                    nf = solve(c, d, p, stg, lam, t, nullptr, tau, nullptr, nullptr, dy, dpi, dlam, dt, flops);
+                    bar<TEAM>();
+                }
+            }
+            if (nf) { status = OCPQP_STATUS_NAN; break; }
+            const double alpha = max_step(c, d, lam, t, dlam, dt, arg.ftb);
+            const double* act = c.w[WS_ACT];
+            for (int i = tid; i < d.nv; i += TEAM) y[i] += alpha * dy[i];
+            for (int i = tid; i < d.ne; i += TEAM) pi[i] += alpha * dpi[i];
+            for (int k = tid; k < d.nc; k += TEAM) {
+                double lv = lam[k] + alpha * dlam[k];
+                double tv = t[k] + alpha * dt[k];
+                if (act[k] != 0.0) {
+                    lv = fmax(lv, arg.lam_min);
+                    tv = fmax(tv, arg.t_min);
+                }
+                lam[k] = lv;
+                t[k] = tv;
+            }
+            if (trace && tid == 0 && it < arg.iter_max) {
+                double* tr = trace + (long long)it * 8;
+                tr[0] = alpha_aff; tr[1] = alpha; tr[2] = mu; tr[3] = sigma;
+                tr[4] = res.g; tr[5] = res.b; tr[6] = res.d; tr[7] = res.m;
+            }
+            bar<TEAM>();
+            alpha_last = alpha;
+            ++it;
+        }
+        bar<TEAM>();
+        for (int i = tid; i < d.nv; i += TEAM) gy[i] = y[i];
+        for (int i = tid; i < d.ne; i += TEAM) gpi[i] = pi[i];
+        for (int k = tid; k < d.nc; k += TEAM) { glam[k] = lam[k]; gt[k] = t[k]; }
+        if (tid == 0) {
+            sp.status[q] = status;
+            sp.iters[q] = it;
+            double* r = sp.res + (long long)q * 5;
+            r[0] = res.g; r[1] = res.b; r[2] = res.d; r[3] = res.m; r[4] = res.mu;
+            sp.flops[q] = flops;
+        }
+    }
+};
+
+template <class S>
+__global__ void __launch_bounds__(S::TEAM) k_fast_solve(KParams p, SolveParams sp) {
+    extern __shared__ double smem[];
+    __shared__ FCtx c;
+    double* gslot = p.ws + (long long)blockIdx.x * p.ws_slot;
+    RD d;
+    d.N = p.N; d.NB = p.NB; d.M = p.NB + S::NG; d.NBN = p.NBN; d.NGN = p.NGN;
+    d.MN = p.NBN + p.NGN; d.nc = p.nc; d.nv = p.nv; d.ne = p.ne; d.msum = p.msum;
+    for (int b = threadIdx.x; b < WS_NUM; b += S::TEAM)
+        c.w[b] = ((p.smem_mask >> b) & 1u) ? smem + p.smem_off[b] : gslot + p.ws_off[b];
+    double* stg = smem + p.stage_smem;
+    while (true) {
+        if (threadIdx.x == 0) c.q = atomicAdd(p.counter, 1);
+        bar<S::TEAM>();
+        const int q = c.q;
+        if (q >= p.B) break;
+        for (int f = threadIdx.x; f < OCPQP_NUM_FIELDS; f += S::TEAM)
+            c.f[f] = p.f[f] + (long long)q * p.bs[f];
+        bar<S::TEAM>();
+        Kern<S>::ipm_one(c, d, p, sp, stg, q);
+        bar<S::TEAM>();
+    }
+}
+
+template <class S>
+int stage_doubles() { return S::STAGE; }
+
+template <class S>
+cudaError_t launch(const KParams& p, const SolveParams& sp, int grid, size_t smem, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(k_fast_solve<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(p.counter, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    k_fast_solve<S><<<grid, S::TEAM, smem, st>>>(p, sp);
+    return cudaGetLastError();
+}
+
+template <class S>
+int occupancy(size_t smem) {
+    int nb = 0;
+    cudaFuncSetAttribute(k_fast_solve<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fast_solve<S>, S::TEAM, smem) != cudaSuccess)
+        return 0;
+    return nb;
+}
+
+}  // namespace fastk
+}  // namespace ocpqp

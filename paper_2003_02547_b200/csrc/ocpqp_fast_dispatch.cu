@@ -1,0 +1,63 @@
+// Dispatch table of the shaped kernel instantiations (ocpqp_fast_*.cu).
+#include <cuda_runtime.h>
+
+#include "ocpqp_internal.h"
+
+namespace ocpqp {
+namespace fastk {
+template <int NX_, int NU_, int NG_, int TEAM_>
+struct Shape;
+template <class S>
+cudaError_t launch(const KParams& p, const SolveParams& sp, int grid, size_t smem, cudaStream_t st);
+template <class S>
+int occupancy(size_t smem);
+template <class S>
+int stage_doubles();
+}  // namespace fastk
+
+#define OCPQP_FAST_SHAPES(X) \
+    X(8, 3, 0, 32)           \
+    X(8, 3, 0, 64)           \
+    X(24, 4, 0, 64)          \
+    X(24, 4, 0, 128)         \
+    X(30, 10, 10, 128)       \
+    X(30, 10, 10, 64)        \
+    X(60, 20, 0, 256)        \
+    X(60, 20, 0, 128)        \
+    X(60, 100, 240, 256)
+
+
+#define OCPQP_MATCH(nx_, nu_, ng_, team_) \
+    (s.nx == (nx_) && s.nu == (nu_) && s.ng == (ng_) && s.team == (team_))
+
+bool fast_supported(const FastShape& s) {
+#define X(a, b, c_, t) if (OCPQP_MATCH(a, b, c_, t)) return true;
+    OCPQP_FAST_SHAPES(X)
+#undef X
+    return false;
+}
+
+int fast_stage_smem_doubles(const FastShape& s) {
+#define X(a, b, c_, t) if (OCPQP_MATCH(a, b, c_, t)) return fastk::stage_doubles<fastk::Shape<a, b, c_, t>>();
+    OCPQP_FAST_SHAPES(X)
+#undef X
+    return -1;
+}
+
+cudaError_t launch_fast_solve(const FastShape& s, const KParams& p, const SolveParams& sp, int grid,
+                              size_t smem, cudaStream_t stream) {
+#define X(a, b, c_, t) \
+    if (OCPQP_MATCH(a, b, c_, t)) return fastk::launch<fastk::Shape<a, b, c_, t>>(p, sp, grid, smem, stream);
+    OCPQP_FAST_SHAPES(X)
+#undef X
+    return cudaErrorNotSupported;
+}
+
+int fast_occupancy(const FastShape& s, size_t smem) {
+#define X(a, b, c_, t) if (OCPQP_MATCH(a, b, c_, t)) return fastk::occupancy<fastk::Shape<a, b, c_, t>>(smem);
+    OCPQP_FAST_SHAPES(X)
+#undef X
+    return 0;
+}
+
+}  // namespace ocpqp

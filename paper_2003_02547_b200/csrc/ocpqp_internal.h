@@ -48,6 +48,7 @@ enum WsBuf {
     WS_G,                                    // stage matrix G (nw_max^2)
     WS_T1,                                   // stage temp (max(nx' * nw, nx^2))
     WS_VEC,                                  // small stage vectors (4 * nw_max)
+    WS_IY, WS_IPI, WS_ILAM, WS_IT,           // working iterate (shaped kernel)
     WS_NUM
 };
 
@@ -68,9 +69,12 @@ struct KParams {
     double* ws;               // slots * ws_slot doubles
     long long ws_slot;        // doubles per slot
     int ws_off[WS_NUM];       // offsets within a slot
-    unsigned smem_mask;       // bit b set: buffer b lives in shared memory
+    unsigned long long smem_mask;  // bit b set: buffer b lives in shared memory
     int smem_off[WS_NUM];     // offsets within dynamic smem (doubles)
     int* counter;             // dynamic QP scheduler
+    // shaped-kernel structure (uniform stages 0..N-1, terminal stage N)
+    int NB, NBN, NGN;         // box rows (n < N), box / general rows at N
+    int stage_smem;           // doubles of per-stage scratch after the placement
 };
 
 struct SolveParams {
@@ -91,5 +95,16 @@ cudaError_t launch_residuals(const KParams& p, const double* y, const double* pi
                              double* rd, double* rm, double* norms, int grid, int threads,
                              cudaStream_t stream);
 int ipm_occupancy(int threads, size_t smem);
+
+// Shaped (compile-time NX, NU, NG, TEAM) fused kernel, ocpqp_fast.cu.  Returns
+// cudaErrorNotSupported when no instantiation matches.
+struct FastShape {
+    int nx, nu, ng, team;
+};
+bool fast_supported(const FastShape& s);
+int fast_stage_smem_doubles(const FastShape& s);
+cudaError_t launch_fast_solve(const FastShape& s, const KParams& p, const SolveParams& sp,
+                              int grid, size_t smem, cudaStream_t stream);
+int fast_occupancy(const FastShape& s, size_t smem);
 
 }  // namespace ocpqp
