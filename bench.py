@@ -286,7 +286,7 @@ def main():
     achieved = alg_flops / (t_step * 1e-3) / 1e12
     roof = {"bound": "fp64", "achieved": achieved, "peak": peak_dfma, "unit": "TFLOP/s",
             "frac": achieved / peak_dfma if peak_dfma else None, "traffic": None,
-            "kernel": "k_fast_solve" if plan_info.get("shaped_kernel") else "k_ipm_solve",
+            "kernel": {"row": "k_row_solve", "team": "k_fast_solve"}.get(plan_info.get("kernel"), "k_ipm_solve"),
             "work": f"sum over QPs of iterations x (F_fac + 2 F_sol) = {iters.sum()} x {ric} flops "
                     f"(SURVEY §8(d)); one launch per step",
             "peak_source": "measured live: DFMA microbenchmark (ocpqp_fp64_peak), "

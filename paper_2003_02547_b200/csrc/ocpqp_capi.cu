@@ -192,6 +192,8 @@ struct OcpPlan {
     int num_sms = 0;
     int threads = 32;
     int slots = 1;
+    int grid = 1;
+    int team_stride = 0;
     size_t smem_bytes = 0;
     unsigned long long smem_mask = 0;
     int smem_off[WS_NUM] = {0};
@@ -300,6 +302,7 @@ void fill_kparams(const OcpPlan* P, KParams& k, const OcpQpDataC* data, bool use
     k.counter = P->d_counter;
     k.NB = P->NB; k.NBN = P->NBN; k.NGN = P->NGN;
     k.stage_smem = P->stage_smem;
+    k.team_stride = P->team_stride;
 }
 
 // The shaped kernel reads every field unconditionally: absent fields point at
@@ -319,6 +322,8 @@ void fill_defaults(const OcpPlan* P, KParams& k) {
 
 // Shaped-kernel eligibility: uniform stages 0..N-1 (nx, nu >= 1, nb, ng),
 // terminal stage with nu = 0, nx equal, nb <= nx, ng <= NG; no soft rows.
+// Prefers the row kernel (NX <= 32, full box rows) over the team kernel.
+// Environment overrides: OCPQP_GENERIC=1, OCPQP_KIND=0|1, OCPQP_TEAM, OCPQP_WPB.
 bool detect_fast(OcpPlan* P) {
     const Layout& L = P->L;
     const char* gen = getenv("OCPQP_GENERIC");
@@ -330,55 +335,70 @@ bool detect_fast(OcpPlan* P) {
     for (int n = 0; n < N; ++n)
         if (L.nx[n] != NX || L.nu[n] != NU || L.nb[n] != NB || L.ng[n] != NG) return false;
     if (L.nx[N] != NX || L.nu[N] != 0 || L.ng[N] > NG || L.nb[N] > NX) return false;
-    int team = 0;
+    const char* envk = getenv("OCPQP_KIND");
     const char* envt = getenv("OCPQP_TEAM");
-    if (envt && atoi(envt) > 0) {
-        team = atoi(envt);
-        if (!fast_supported(FastShape{NX, NU, NG, team})) return false;
-    } else {
-        const int cands[] = {32, 64, 128, 256};
-        int pref = NX + NU <= 12 ? 32 : NX + NU <= 32 ? 64 : NX + NU <= 48 ? 128 : 256;
-        if (fast_supported(FastShape{NX, NU, NG, pref})) team = pref;
-        for (int c : cands)
-            if (!team && fast_supported(FastShape{NX, NU, NG, c})) team = c;
-        if (!team) return false;
+    const char* envw = getenv("OCPQP_WPB");
+    const int want_kind = envk ? atoi(envk) : -1;
+    FastShape pick{-1, 0, 0, 0, 0, 0, 0};
+    // row kernel
+    if (want_kind != 0) {
+        const int gdef = (NX <= 8 && NU <= 8) ? 8 : (NX <= 16 && NU <= 16) ? 16 : 32;
+        const int g = envt && want_kind == 1 ? atoi(envt) : gdef;
+        const int wpbs[] = {envw ? atoi(envw) : 1, 1, 2, 4};
+        for (int w : wpbs) {
+            FastShape s{1, NX, NU, NG, NB, g, w};
+            if (fast_supported(s)) { pick = s; break; }
+        }
     }
+    if (pick.kind < 0 && want_kind != 1) {
+        int team = 0;
+        if (envt && atoi(envt) > 0) {
+            team = atoi(envt);
+            if (!fast_supported(FastShape{0, NX, NU, NG, NB, team, 1})) team = 0;
+        } else {
+            const int cands[] = {32, 64, 128, 256};
+            int pref = NX + NU <= 12 ? 32 : NX + NU <= 32 ? 64 : NX + NU <= 48 ? 128 : 256;
+            if (fast_supported(FastShape{0, NX, NU, NG, NB, pref, 1})) team = pref;
+            for (int c : cands)
+                if (!team && fast_supported(FastShape{0, NX, NU, NG, NB, c, 1})) team = c;
+        }
+        if (team) pick = FastShape{0, NX, NU, NG, NB, team, 1};
+    }
+    if (pick.kind < 0) return false;
     P->fast = true;
-    P->shape = FastShape{NX, NU, NG, team};
+    P->shape = pick;
     P->NB = NB; P->NBN = L.nb[N]; P->NGN = L.ng[N];
     return true;
 }
 
-// Placement for the shaped kernel: per-stage scratch first, then the hottest
-// per-QP buffers while they fit.
-void place_fast(OcpPlan* P) {
+// Placement for the shaped kernels: each team (a CTA for kind 0) gets a
+// shared-memory region = [hottest per-QP buffers while they fit | stage tile].
+void place_fast(OcpPlan* P, long long budget_per_cta) {
     const Layout& L = P->L;
-    long long sz[WS_NUM];
-    for (int b = 0; b < WS_NUM; ++b) sz[b] = L.ws_size[b];
-    P->threads = P->shape.team;
+    const int teams = fast_teams_per_cta(P->shape);
+    P->threads = P->shape.kind == 1 ? 32 * P->shape.wpb : P->shape.team;
     long long off = 0;
     for (int b = 0; b < WS_NUM; ++b) {
         P->ws_off[b] = (int)off;
-        off += align2(sz[b]);
+        off += align2(L.ws_size[b]);
     }
     P->ws_slot = std::max(2ll, off);
-    const long long stage = align2(fast_stage_smem_doubles(P->shape)) * 8;
-    int tgt = std::max(1, 1024 / P->threads);
-    const int per_sm_need = (P->B + P->num_sms - 1) / std::max(1, P->num_sms);
-    tgt = std::max(1, std::min(tgt, per_sm_need));
-    const char* envs = getenv("OCPQP_SMEM_KB");
-    long long budget;
-    if (envs) budget = (long long)atoi(envs) * 1024;
-    else budget = std::min((228ll * 1024) / tgt - 2048, 227ll * 1024 - 2048);
-    budget -= stage;
-    const int prio[] = {WS_ILAM, WS_IT, WS_ACT, WS_DVEC, WS_IY, WS_IPI, WS_GAM, WS_RD, WS_WALL,
-                        WS_DIR_LAM, WS_DIR_T, WS_AFF_LAM, WS_AFF_T, WS_CROW, WS_ROWV, WS_COEF,
-                        WS_PV, WS_KFF, WS_L, WS_LP0, WS_K, WS_P, WS_RG, WS_RB, WS_RHAT, WS_DIR_Y,
-                        WS_DIR_PI, WS_AFF_Y, WS_AFF_PI};
+    const long long tile = align2(fast_stage_smem_doubles(P->shape)) * 8;
+    long long budget = budget_per_cta / teams - tile;
+    static const int prio0[] = {WS_ILAM, WS_IT, WS_ACT, WS_DVEC, WS_IY, WS_IPI, WS_GAM, WS_RD, WS_WALL,
+                                WS_DIR_LAM, WS_DIR_T, WS_AFF_LAM, WS_AFF_T, WS_CROW, WS_ROWV, WS_COEF,
+                                WS_PV, WS_KFF, WS_L, WS_LP0, WS_K, WS_P, WS_RG, WS_RB, WS_RHAT, WS_DIR_Y,
+                                WS_DIR_PI, WS_AFF_Y, WS_AFF_PI};
+    static const int prio1[] = {WS_DVEC, WS_ILAM, WS_IT, WS_GAM, WS_RD, WS_WALL, WS_DIR_LAM, WS_DIR_T,
+                                WS_AFF_LAM, WS_AFF_T, WS_IY, WS_DIR_Y, WS_RG, WS_IPI, WS_DIR_PI, WS_RB,
+                                WS_CROW, WS_COEF, WS_L, WS_K, WS_KFF, WS_PV, WS_LP0, WS_P};
+    const int* prio = P->shape.kind == 1 ? prio1 : prio0;
+    const int np = P->shape.kind == 1 ? (int)(sizeof(prio1) / sizeof(int)) : (int)(sizeof(prio0) / sizeof(int));
     long long used = 0;
     P->smem_mask = 0;
-    for (int b : prio) {
-        const long long bytes = align2(sz[b]) * 8;
+    for (int i = 0; i < np; ++i) {
+        const int b = prio[i];
+        const long long bytes = align2(L.ws_size[b]) * 8;
         if (bytes == 0) continue;
         if (used + bytes <= budget) {
             P->smem_mask |= 1ull << b;
@@ -387,7 +407,28 @@ void place_fast(OcpPlan* P) {
         }
     }
     P->stage_smem = (int)(used / 8);
-    P->smem_bytes = (size_t)(used + stage);
+    P->team_stride = (int)((used + tile) / 8);
+    P->smem_bytes = (size_t)(used + tile) * teams;
+}
+
+// Plan the shaped kernel: choose a shared-memory budget so that the CTAs the
+// batch needs can be resident, check occupancy, and size the slot count.
+bool plan_fast(OcpPlan* P, int* occ_out) {
+    const int teams = fast_teams_per_cta(P->shape);
+    const int ctas_needed = (P->B + teams - 1) / teams;
+    const int per_sm = std::max(1, (ctas_needed + P->num_sms - 1) / P->num_sms);
+    const char* envs = getenv("OCPQP_SMEM_KB");
+    long long budget;
+    if (envs) budget = (long long)atoi(envs) * 1024;
+    else budget = std::min((228ll * 1024) / std::min(per_sm, 32) - 2048, 227ll * 1024 - 2048);
+    budget = std::max(budget, 0ll);
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        place_fast(P, budget);
+        const int occ = fast_occupancy(P->shape, P->smem_bytes);
+        if (occ > 0) { *occ_out = occ; return true; }
+        budget /= 2;
+    }
+    return false;
 }
 
 int check_arg(const OcpIpmArgC* a) {
@@ -440,15 +481,7 @@ int ocpqp_plan_create(const OcpQpDimC* dim, int32_t batch, OcpPlan** out) {
     if (e != cudaSuccess) { delete P; return cuda_fail(e, "no CUDA device"); }
     int occ = 0;
     if (detect_fast(P)) {
-        place_fast(P);
-        occ = fast_occupancy(P->shape, P->smem_bytes);
-        if (occ == 0) {  // placement too greedy: scratch only
-            P->smem_mask = 0;
-            P->stage_smem = 0;
-            P->smem_bytes = align2(fast_stage_smem_doubles(P->shape)) * 8;
-            occ = fast_occupancy(P->shape, P->smem_bytes);
-        }
-        if (occ == 0) P->fast = false;
+        if (!plan_fast(P, &occ)) P->fast = false;
     }
     if (!P->fast) {
         place_workspace(P);
@@ -460,7 +493,15 @@ int ocpqp_plan_create(const OcpQpDimC* dim, int32_t batch, OcpPlan** out) {
         }
     }
     if (occ == 0) { delete P; return fail(OCPQP_E_CUDA, "kernel does not fit on an SM"); }
-    P->slots = std::max(1, std::min(std::max(1, batch), occ * P->num_sms));
+    if (P->fast) {
+        const int teams = fast_teams_per_cta(P->shape);
+        const int ctas = std::max(1, std::min((std::max(1, batch) + teams - 1) / teams, occ * P->num_sms));
+        P->grid = ctas;
+        P->slots = ctas * teams;
+    } else {
+        P->slots = std::max(1, std::min(std::max(1, batch), occ * P->num_sms));
+        P->grid = P->slots;
+    }
     const Layout& L = P->L;
     const size_t S = L.st.size();
     e = cudaMalloc(&P->d_st, sizeof(StageInfo) * S);
@@ -515,9 +556,12 @@ int ocpqp_plan_destroy(OcpPlan* P) {
 // Plan introspection for the host bindings: threads, slots, smem bytes,
 // smem mask, workspace doubles per slot.
 int ocpqp_plan_info(const OcpPlan* P, int64_t* out, int32_t out_len) {
-    if (!P || !out || out_len < 6) return fail(OCPQP_E_ARG, "bad arguments");
+    if (!P || !out || out_len < 8) return fail(OCPQP_E_ARG, "bad arguments");
     out[0] = P->threads; out[1] = P->slots; out[2] = (int64_t)P->smem_bytes;
-    out[3] = (int64_t)P->smem_mask; out[4] = P->ws_slot; out[5] = P->fast ? 1 : 0;
+    out[3] = (int64_t)P->smem_mask; out[4] = P->ws_slot;
+    out[5] = P->fast ? 1 + P->shape.kind : 0;   /* 0 generic, 1 team kernel, 2 row kernel */
+    out[6] = P->fast ? P->shape.team : P->threads;
+    out[7] = P->grid;
     return OCPQP_OK;
 }
 
@@ -541,7 +585,7 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     cudaError_t e;
     if (P->fast) {
         fill_defaults(P, k);
-        e = launch_fast_solve(P->shape, k, sp, P->slots, P->smem_bytes, (cudaStream_t)stream);
+        e = launch_fast_solve(P->shape, k, sp, P->grid, P->smem_bytes, (cudaStream_t)stream);
         if (e != cudaSuccess) return cuda_fail(e, "k_fast_solve launch");
     } else {
         e = launch_ipm_solve(k, sp, P->slots, P->threads, P->smem_bytes, (cudaStream_t)stream);

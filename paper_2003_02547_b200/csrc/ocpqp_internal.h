@@ -74,7 +74,8 @@ struct KParams {
     int* counter;             // dynamic QP scheduler
     // shaped-kernel structure (uniform stages 0..N-1, terminal stage N)
     int NB, NBN, NGN;         // box rows (n < N), box / general rows at N
-    int stage_smem;           // doubles of per-stage scratch after the placement
+    int stage_smem;           // doubles: offset of the per-stage scratch / per-team tile
+    int team_stride;          // doubles of shared memory per team (row kernel)
 };
 
 struct SolveParams {
@@ -98,9 +99,12 @@ int ipm_occupancy(int threads, size_t smem);
 
 // Shaped (compile-time NX, NU, NG, TEAM) fused kernel, ocpqp_fast.cu.  Returns
 // cudaErrorNotSupported when no instantiation matches.
+// kind 0: team kernel (ocpqp_fast.cuh), one CTA of `team` threads per QP;
+// kind 1: row kernel (ocpqp_row.cuh), `team` lanes per QP, `wpb` warps per CTA.
 struct FastShape {
-    int nx, nu, ng, team;
+    int kind, nx, nu, ng, nb, team, wpb;
 };
+int fast_teams_per_cta(const FastShape& s);
 bool fast_supported(const FastShape& s);
 int fast_stage_smem_doubles(const FastShape& s);
 cudaError_t launch_fast_solve(const FastShape& s, const KParams& p, const SolveParams& sp,
