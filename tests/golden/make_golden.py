@@ -1,0 +1,198 @@
+"""Generate golden vectors from the REAL reference package (run in the build container).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+The reference (/root/reference/pkg/src/mpcqp, pure Python) is imported here
+only; it does not exist on the GPU box, so tests read the committed .npz
+fixtures written by this script.  Inputs are NOT stored for the seeded
+generators -- they are regenerated bit-identically from
+paper_2003_02547_b200.generators (BASELINE configs) and tests/qpgen.py
+(random feasible instances) with the recorded parameters; only the
+reference's outputs are stored.
+
+Fixtures:
+  solve_cfg.npz      speed-mode solves (tol 1e-8) of the first QPs of configs 0-4
+  solve_random.npz   speed-mode solves of random instances with soft rows,
+                     masks, one-sided rows, general rows, fixed x0
+  newton.npz         riccati_factor + solve Newton steps at random iterates,
+                     with the cost-to-go matrices P[n] and gains K[n]
+  residuals.npz      compute_residuals at random points
+  known.npz          hand-derivable answers (scalar LQR) and failure statuses
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import mpcqp  # noqa: E402  (the reference)
+import mpcqp.kkt_ocp as ko  # noqa: E402
+from mpcqp.view import QpSolution as RefSol, make_view  # noqa: E402
+
+import qpgen  # noqa: E402
+from paper_2003_02547_b200.generators import make_batch  # noqa: E402
+
+STATUS = {"Success": 0, "MaxIter": 1, "MinStep": 2, "NaNDetected": 3, "Failure": 4}
+ARG = mpcqp.mode_preset("speed").with_tol(1e-8)
+
+# (cfg, indices, N) of the config fixtures
+CFG_CASES = [(0, [0], None), (1, list(range(12)), None), (2, [0, 1, 2], None),
+             (3, [0, 1, 2], None), (4, [0], None)]
+# random instances: (seed, kwargs)
+RANDOM_CASES = [
+    (11, dict(N=5, nx=4, nu=2, nb=3, ng=1, ns=1)),
+    (12, dict(N=6, nx=3, nu=2, nb=4, ng=2, ns=2, fix_x0=True)),
+    (13, dict(N=4, nx=5, nu=1, nb=2, ng=0, ns=0)),
+    (14, dict(N=7, nx=4, nu=3, nb=5, ng=2, ns=0, mask_last=False, inf_side=False)),
+    (15, dict(N=3, nx=2, nu=2, nb=4, ng=1, ns=3, fix_x0=True)),
+    (16, dict(N=8, nx=6, nu=2, nb=8, ng=0, ns=2)),
+]
+
+
+def to_ref(qp_local):
+    """Copy a package OcpQp into a reference OcpQp (same field catalog)."""
+    d = qp_local.dim
+    ref = mpcqp.OcpQp(mpcqp.OcpQpDim(d.N, d.nx, d.nu, d.nb, d.ng, d.ns))
+    for n in range(d.N + 1):
+        for k, v in qp_local._stages[n].items():
+            ref._stages[n][k] = np.array(v, copy=True)
+    for n in range(d.N):
+        for k, v in qp_local._dyn[n].items():
+            ref._dyn[n][k] = np.array(v, copy=True)
+    ref._rev += 1
+    return ref
+
+
+def pack_report(rep):
+    s = rep.solution
+    st = rep.stats
+    tr = np.array([[r.alpha_aff, r.alpha, r.mu, r.sigma, r.res_g, r.res_b, r.res_d, r.res_m]
+                   for r in st.trace]).reshape(-1, 8)
+    return dict(status=STATUS[st.status.value], iters=st.iterations, y=s.y, pi=s.pi, lam=s.lam,
+                t=s.t, res=np.array([st.res_g, st.res_b, st.res_d, st.res_m, st.mu]),
+                flops=st.flops, trace=tr)
+
+
+def solve_cfg():
+    out = {}
+    for cfg, idx, N in CFG_CASES:
+        for i in idx:
+            qp = to_ref(make_batch(cfg, batch=1, start=i, N=N).qp(0))
+            rep = mpcqp.solve_ocp_qp(qp, ARG)
+            for k, v in pack_report(rep).items():
+                out[f"c{cfg}_q{i}_{k}"] = v
+            print("cfg", cfg, "qp", i, rep.status.value, rep.iterations, flush=True)
+    out["cases"] = np.array([[c, i] for c, idx, _ in CFG_CASES for i in idx])
+    np.savez_compressed(HERE / "solve_cfg.npz", **out)
+
+
+def solve_random():
+    out = {}
+    for seed, kw in RANDOM_CASES:
+        qp = qpgen.build_qp(mpcqp, *qpgen.random_ocp_fields(seed, **kw))
+        rep = mpcqp.solve_ocp_qp(qp, ARG)
+        for k, v in pack_report(rep).items():
+            out[f"s{seed}_{k}"] = v
+        print("random", seed, rep.status.value, rep.iterations, flush=True)
+    np.savez_compressed(HERE / "solve_random.npz", **out)
+
+
+def random_iterate(rng, vw, spread=(0.1, 5.0)):
+    it = RefSol(vw)
+    it.y[:] = rng.standard_normal(vw.ny)
+    it.pi[:] = rng.standard_normal(vw.ne)
+    it.lam[:] = np.where(vw.act, rng.uniform(*spread, vw.nc), 0.0)
+    it.t[:] = np.where(vw.act, rng.uniform(*spread, vw.nc), 0.0)
+    return it
+
+
+def newton():
+    out = {}
+    rng = np.random.default_rng(2024)
+    for seed, kw in RANDOM_CASES:
+        qp = qpgen.build_qp(mpcqp, *qpgen.random_ocp_fields(seed, **kw))
+        vw = make_view(qp)
+        it = random_iterate(rng, vw)
+        res = mpcqp.compute_residuals(qp, it)
+        rm = np.where(vw.act, it.lam * it.t, 0.0)
+        fac = ko.riccati_factor(qp, it)
+        step = fac.solve(res.r_g, res.r_b, res.r_d, rm)
+        P = np.concatenate([fac.p_matrix(n).reshape(-1) for n in range(qp.dim.N + 1)])
+        K = np.concatenate([fac.K[n].reshape(-1) for n in range(qp.dim.N + 1)])
+        for k, v in dict(y=it.y, pi=it.pi, lam=it.lam, t=it.t, r_g=res.r_g, r_b=res.r_b,
+                         r_d=res.r_d, r_m=rm, dy=step.y, dpi=step.pi, dlam=step.lam,
+                         dt=step.t, P=P, K=K).items():
+            out[f"s{seed}_{k}"] = v
+    # the same at BASELINE config shapes
+    for cfg in (1, 2, 3):
+        qp = to_ref(make_batch(cfg, batch=1, start=7).qp(0))
+        vw = make_view(qp)
+        it = random_iterate(rng, vw)
+        res = mpcqp.compute_residuals(qp, it)
+        rm = np.where(vw.act, it.lam * it.t, 0.0)
+        fac = ko.riccati_factor(qp, it)
+        step = fac.solve(res.r_g, res.r_b, res.r_d, rm)
+        for k, v in dict(y=it.y, pi=it.pi, lam=it.lam, t=it.t, r_g=res.r_g, r_b=res.r_b,
+                         r_d=res.r_d, r_m=rm, dy=step.y, dpi=step.pi, dlam=step.lam,
+                         dt=step.t).items():
+            out[f"c{cfg}_{k}"] = v
+    np.savez_compressed(HERE / "newton.npz", **out)
+
+
+def residuals():
+    out = {}
+    rng = np.random.default_rng(77)
+    for seed, kw in RANDOM_CASES:
+        qp = qpgen.build_qp(mpcqp, *qpgen.random_ocp_fields(seed, **kw))
+        vw = make_view(qp)
+        it = random_iterate(rng, vw)
+        r = mpcqp.compute_residuals(qp, it)
+        for k, v in dict(y=it.y, pi=it.pi, lam=it.lam, t=it.t, r_g=r.r_g, r_b=r.r_b, r_d=r.r_d,
+                         r_m=r.r_m, norms=np.array([r.res_g, r.res_b, r.res_d, r.res_m, r.mu])).items():
+            out[f"s{seed}_{k}"] = v
+    np.savez_compressed(HERE / "residuals.npz", **out)
+
+
+def known():
+    out = {}
+    qp = qpgen.scalar_lqr(mpcqp)
+    fac = ko.riccati_factor(qp, RefSol(make_view(qp)))
+    out["lqr_P1"] = fac.p_matrix(1)[0, 0]
+    out["lqr_K0"] = fac.K[0][0, 0]
+    out["lqr_P0"] = fac.p_matrix(0)[0, 0]
+    rep = mpcqp.solve_ocp_qp(qpgen.scalar_lqr(mpcqp, bounds=True), ARG)
+    out["lqr_bounds_u0"] = rep.solution.u(0)[0]
+    out["lqr_bounds_status"] = STATUS[rep.status.value]
+    # indefinite input weight: Failure after the regularised retry
+    q = qpgen.scalar_lqr(mpcqp)
+    q.set_field("r", 0, [1.0])
+    q.set_field("R", 0, [[-1.0]])
+    q.set_field("Q", 0, [[-1.0]])
+    q.set_field("Q", 1, [[-1.0]])
+    rep = mpcqp.solve_ocp_qp(q, ARG)
+    out["indef_status"] = STATUS[rep.status.value]
+    out["indef_iters"] = rep.iterations
+    out["indef_flops"] = rep.stats.flops
+    # crossed bounds: never Success
+    q = qpgen.scalar_lqr(mpcqp, bounds=True)
+    q.set_field("lb", 1, [1.0])
+    q.set_field("ub", 1, [0.0])
+    rep = mpcqp.solve_ocp_qp(q, ARG)
+    out["infeas_status"] = STATUS[rep.status.value]
+    out["infeas_iters"] = rep.iterations
+    np.savez_compressed(HERE / "known.npz", **out)
+    print({k: float(v) for k, v in out.items()})
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["known", "residuals", "newton", "solve_random", "solve_cfg"]
+    for w in which:
+        globals()[w]()
