@@ -570,8 +570,10 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     if (!P) return fail(OCPQP_E_ARG, "plan is NULL");
     int rc = check_arg(arg);
     if (rc) return rc;
-    if (!iter || !stats || !iter->y || !iter->pi || !iter->lam || !iter->t || !stats->status ||
-        !stats->iterations || !stats->res || !stats->flops)
+    // zero-length vectors (e.g. nc = 0 for an unconstrained QP) may be NULL
+    const Layout& Ly = P->L;
+    if (!iter || !stats || (Ly.ny && !iter->y) || (Ly.ne && !iter->pi) || (Ly.nc && !iter->lam) ||
+        (Ly.nc && !iter->t) || !stats->status || !stats->iterations || !stats->res || !stats->flops)
         return fail(OCPQP_E_ARG, "iterate / stats buffers must not be NULL");
     if (P->B == 0) return OCPQP_OK;
     KParams k;
