@@ -178,6 +178,8 @@ int build_layout(const OcpQpDimC* d, Layout& L) {
     w[WS_T1] = t1;
     w[WS_VEC] = L.nw_max + L.nx_max + std::max(L.nu_max, L.nx_max);
     w[WS_IY] = L.ny; w[WS_IPI] = L.ne; w[WS_ILAM] = L.nc; w[WS_IT] = L.nc;
+    w[WS_RINV] = kfo + L.nx[0];   // sum nu + nx0
+    w[WS_TINV] = L.nc;
     return OCPQP_OK;
 }
 
@@ -203,6 +205,7 @@ struct OcpPlan {
     int NB = 0, NBN = 0, NGN = 0;
     int stage_smem = 0;          // offset (doubles) of the per-stage scratch
     double* d_defaults = nullptr;  // zeros | ones | -inf | +inf, each max_flen long
+    long long* dbg = nullptr;      // optional phase counters (ocpqp_debug_phases)
     long long max_flen = 1;
     int ws_off[WS_NUM] = {0};
     long long ws_slot = 0;
@@ -303,6 +306,7 @@ void fill_kparams(const OcpPlan* P, KParams& k, const OcpQpDataC* data, bool use
     k.NB = P->NB; k.NBN = P->NBN; k.NGN = P->NGN;
     k.stage_smem = P->stage_smem;
     k.team_stride = P->team_stride;
+    k.dbg = P->dbg;
 }
 
 // The shaped kernel reads every field unconditionally: absent fields point at
@@ -385,13 +389,16 @@ void place_fast(OcpPlan* P, long long budget_per_cta) {
     P->ws_slot = std::max(2ll, off);
     const long long tile = align2(fast_stage_smem_doubles(P->shape)) * 8;
     long long budget = budget_per_cta / teams - tile;
-    static const int prio0[] = {WS_ILAM, WS_IT, WS_ACT, WS_DVEC, WS_IY, WS_IPI, WS_GAM, WS_RD, WS_WALL,
-                                WS_DIR_LAM, WS_DIR_T, WS_AFF_LAM, WS_AFF_T, WS_CROW, WS_ROWV, WS_COEF,
-                                WS_PV, WS_KFF, WS_L, WS_LP0, WS_K, WS_P, WS_RG, WS_RB, WS_RHAT, WS_DIR_Y,
-                                WS_DIR_PI, WS_AFF_Y, WS_AFF_PI};
+    // team kernel: the factor store and the per-stage vectors read inside the
+    // sequential sweeps first, then the slot vectors of the parallel passes
+    static const int prio0[] = {WS_L, WS_RINV, WS_K, WS_KFF, WS_PV, WS_LP0, WS_P, WS_RB, WS_RHAT,
+                                WS_DIR_Y, WS_DIR_PI, WS_ILAM, WS_IT, WS_DVEC, WS_TINV, WS_GAM,
+                                WS_WALL, WS_RD, WS_DIR_LAM, WS_DIR_T, WS_AFF_LAM, WS_AFF_T, WS_IY,
+                                WS_IPI, WS_CROW, WS_ROWV, WS_COEF, WS_RG};
     static const int prio1[] = {WS_DVEC, WS_ILAM, WS_IT, WS_GAM, WS_RD, WS_WALL, WS_DIR_LAM, WS_DIR_T,
                                 WS_AFF_LAM, WS_AFF_T, WS_IY, WS_DIR_Y, WS_RG, WS_IPI, WS_DIR_PI, WS_RB,
-                                WS_CROW, WS_COEF, WS_L, WS_K, WS_KFF, WS_PV, WS_LP0, WS_P};
+                                WS_CROW, WS_COEF, WS_TINV, WS_RINV, WS_L, WS_K, WS_KFF, WS_PV, WS_LP0,
+                                WS_P};
     const int* prio = P->shape.kind == 1 ? prio1 : prio0;
     const int np = P->shape.kind == 1 ? (int)(sizeof(prio1) / sizeof(int)) : (int)(sizeof(prio0) / sizeof(int));
     long long used = 0;
@@ -555,6 +562,14 @@ int ocpqp_plan_destroy(OcpPlan* P) {
 
 // Plan introspection for the host bindings: threads, slots, smem bytes,
 // smem mask, workspace doubles per slot.
+// Internal diagnostics (not in the public header): make the shaped kernels
+// accumulate clock64 cycles per IPM phase into dev_buf [B, 8] (nullptr = off).
+int ocpqp_debug_phases(OcpPlan* P, int64_t* dev_buf) {
+    if (!P) return fail(OCPQP_E_ARG, "plan is NULL");
+    P->dbg = (long long*)dev_buf;
+    return OCPQP_OK;
+}
+
 int ocpqp_plan_info(const OcpPlan* P, int64_t* out, int32_t out_len) {
     if (!P || !out || out_len < 8) return fail(OCPQP_E_ARG, "bad arguments");
     out[0] = P->threads; out[1] = P->slots; out[2] = (int64_t)P->smem_bytes;

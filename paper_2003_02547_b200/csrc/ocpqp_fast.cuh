@@ -140,13 +140,14 @@ struct MV {
 // warp (lane i: row[j] = A[i][j], j <= i).  Pivot test as LAPACK potrf: a
 // pivot that is not > 0 (or NaN) fails (linalg.py:81-118).
 template <int NN>
-__device__ __forceinline__ bool warp_chol(double (&row)[NN], int lane) {
+__device__ __forceinline__ bool warp_chol(double (&row)[NN], int lane, double& rin) {
 #pragma unroll
     for (int k = 0; k < NN; ++k) {
         const double piv = __shfl_sync(FULL, row[k], k);
         if (!(piv > 0.0)) return false;
         const double dkk = sqrt(piv);
-        const double inv = 1.0 / dkk;
+        const double inv = rsqrt(piv);  // 1 / L_kk, kept for the triangular solves
+        if (lane == k) rin = inv;
         const double lik = lane == k ? dkk : row[k] * inv;
         if (lane >= k) row[k] = lik;
 #pragma unroll
@@ -160,18 +161,21 @@ __device__ __forceinline__ bool warp_chol(double (&row)[NN], int lane) {
 
 // Team Cholesky of an n x n matrix in place (lower; upper zeroed), any n.
 template <int TEAM>
-__device__ bool team_chol(double* L, int n, int* flag) {
+__device__ bool team_chol(double* L, int n, int* flag, double* rinv) {
     const int tid = threadIdx.x;
     for (int k = 0; k < n; ++k) {
         if (tid == 0) {
             const double d = L[k * n + k];
             const int ok = d > 0.0;
-            if (ok) L[k * n + k] = sqrt(d);
+            if (ok) {
+                L[k * n + k] = sqrt(d);
+                rinv[k] = rsqrt(d);
+            }
             *flag = ok;
         }
         bar<TEAM>();
         if (!*flag) return false;
-        const double inv = 1.0 / L[k * n + k];
+        const double inv = rinv[k];
         for (int i = k + 1 + tid; i < n; i += TEAM) L[i * n + k] *= inv;
         bar<TEAM>();
         const int rem = n - k - 1;
@@ -197,19 +201,42 @@ struct FCtx {
     int flag;
     int q;
     double n_act;
+    long long ph[DBG_NUM];  // clock64 phase accumulators (KParams::dbg)
+    long long tk;
 };
+
+// Team loop over TOTAL (compile-time) outputs, unrolled so independent outputs
+// of one thread overlap their load / FMA-chain latencies.
+#define TEAM_FOR(idx, TOTAL)                                                        \
+    _Pragma("unroll 4") for (int _it = 0; _it < ((TOTAL) + TEAM - 1) / TEAM; ++_it) { \
+        const int idx = threadIdx.x + _it * TEAM;                                   \
+        if (idx < (TOTAL)) {
+#define TEAM_END \
+    }            \
+    }
+
+// accumulate the cycles since the previous tick into phase `slot` (thread 0)
+#define OCPQP_TICK(c, slot)                                       \
+    do {                                                          \
+        if (p.dbg && threadIdx.x == 0) {                          \
+            const long long n_ = clock64();                       \
+            (c).ph[slot] += n_ - (c).tk;                          \
+            (c).tk = n_;                                          \
+        }                                                         \
+    } while (0)
 
 // runtime structure (uniform stages)
 struct RD {
     int N, NB, M, NBN, NGN, MN, nc, nv, ne, msum;
+    float inv_m, inv_2m;  // 1/M, 1/(2M): stage decode by float multiply (exact for k < 2^20)
     __device__ __forceinline__ int slot_stage(int k) const {
         if (M == 0) return N;
-        const int n = k / (2 * M);
+        const int n = __float2int_rz(((float)k + 0.5f) * inv_2m);
         return n < N ? n : N;
     }
     __device__ __forceinline__ int row_stage(int r) const {
         if (M == 0) return N;
-        const int n = r / M;
+        const int n = __float2int_rz(((float)r + 0.5f) * inv_m);
         return n < N ? n : N;
     }
 };
@@ -244,8 +271,7 @@ struct Kern {
 
     // ---------------- setup: d vector, activity (view.py:108-129, 156-184) ----------------
     __device__ static void setup(FCtx& c, const RD& d) {
-        double* dvec = c.w[WS_DVEC];
-        double* act = c.w[WS_ACT];
+        double* dvec = c.w[WS_DVEC];   // d (view.py:156-157); NaN marks an inactive side
         double cnt = 0.0;
         for (int k = threadIdx.x; k < d.nc; k += TEAM) {
             const int n = d.slot_stage(k);
@@ -259,8 +285,7 @@ struct Kern {
             else bound = c.f[lo ? OCPQP_F_lg : OCPQP_F_ug][n * NG + (i - nb)];
             const double mask = c.f[lo ? OCPQP_F_maskl : OCPQP_F_masku][n * d.M + i];
             const bool a = (mask != 0.0) && isfinite(bound);
-            act[k] = a ? 1.0 : 0.0;
-            dvec[k] = a ? (lo ? bound : -bound) : 0.0;
+            dvec[k] = a ? (lo ? bound : -bound) : __longlong_as_double(0x7ff8000000000000ll);
             cnt += a ? 1.0 : 0.0;
         }
         const double tot = tsum<TEAM>(cnt, c.red);
@@ -324,7 +349,7 @@ struct Kern {
     // ---------------- residuals (view.py:272-288) ----------------
     __device__ static Res residuals(FCtx& c, const RD& d, const KParams& p, const double* y,
                                     const double* pi, const double* lam, const double* t) {
-        const double* act = c.w[WS_ACT];
+        const double* act = c.w[WS_DVEC];  // NaN = inactive
         const double* dvec = c.w[WS_DVEC];
         double* rowv = c.w[WS_ROWV];
         double* crow = c.w[WS_CROW];
@@ -337,8 +362,8 @@ struct Kern {
             const int i = r - n * d.M;
             const int m = n < d.N ? d.M : d.MN;
             const int k = n * 2 * d.M + i;
-            const double ll = act[k] != 0.0 ? lam[k] : 0.0;
-            const double lu = act[k + m] != 0.0 ? lam[k + m] : 0.0;
+            const double ll = !isnan(act[k]) ? lam[k] : 0.0;
+            const double lu = !isnan(act[k + m]) ? lam[k + m] : 0.0;
             crow[r] = ll - lu;
         }
         bar<TEAM>();
@@ -417,7 +442,7 @@ struct Kern {
         }
         for (int k = threadIdx.x; k < d.nc; k += TEAM) {
             double rd = 0.0, rm = 0.0;
-            if (act[k] != 0.0) {
+            if (!isnan(act[k])) {
                 rd = (-slot_cy(d, k, rowv) + dvec[k]) + t[k];
                 rm = lam[k] * t[k];
                 musum += rm;
@@ -441,7 +466,7 @@ struct Kern {
     __device__ static int factor(FCtx& c, const RD& d, const KParams& p, double* stg,
                                  const double* lam, const double* t, double reg, long long& flops) {
         const int tid = threadIdx.x;
-        const double* act = c.w[WS_ACT];
+        const double* act = c.w[WS_DVEC];  // NaN = inactive
         double* gam = c.w[WS_GAM];
         double* coef = c.w[WS_COEF];
         double* Pst = c.w[WS_P];
@@ -451,14 +476,17 @@ struct Kern {
         double* T1 = Pc + NX * NX;              // NX*NW
         double* Gu = T1 + S::T1N;               // NU*NW
         double* vec = Gu + NU * NW;
+        double* tinv = c.w[WS_TINV];
         int bad = 0;
         for (int k = tid; k < d.nc; k += TEAM) {
-            double g = 0.0;
-            if (act[k] != 0.0) {
+            double g = 0.0, ti = 0.0;
+            if (!isnan(act[k])) {
                 if (lam[k] <= 0.0 || t[k] <= 0.0) bad = 1;
-                g = lam[k] / t[k];
+                ti = 1.0 / t[k];
+                g = lam[k] * ti;
             }
             gam[k] = g;
+            tinv[k] = ti;
         }
         if (any_of<TEAM>(bad)) return -2;
         bar<TEAM>();
@@ -496,20 +524,21 @@ struct Kern {
             if (NG > 0 && ng > 0) flops += 2ll * NX * NX * ng;
             bar<TEAM>();
             double* Pn = Pst + n * NX * NX;
-            for (int idx = tid; idx < NX * NX; idx += TEAM) {
+            TEAM_FOR(idx, NX * NX)
                 const int i = idx / NX, j = idx - i * NX;
                 const double v = 0.5 * (T1[idx] + T1[j * NX + i]);
                 Pc[idx] = v;
                 Pn[idx] = v;
-            }
+            TEAM_END
             bar<TEAM>();
         }
         // ---- stages N-1 .. 0 ----
         for (int n = N - 1; n >= 0; --n) {
+            OCPQP_TICK(c, DBG_F_P);
             const double* An = A(c, n);
             const double* Bn = Bm(c, n);
             // T1 = P_{n+1} [B A]   (kkt_ocp.py:232)
-            for (int idx = tid; idx < NX * NW; idx += TEAM) {
+            TEAM_FOR(idx, NX * NW)
                 const int i = idx / NW, j = idx - i * NW;
                 const double* Pr = Pc + i * NX;
                 double a = 0.0;
@@ -522,14 +551,15 @@ struct Kern {
                     for (int k = 0; k < NX; ++k) a = fma(Pr[k], Ac[k * NX], a);
                 }
                 T1[idx] = a;
-            }
+            TEAM_END
             bar<TEAM>();
+            OCPQP_TICK(c, DBG_F_T1);
             // G = [B A]' T1 + M~ (kkt_ocp.py:233, 70-80): input rows -> Gu, G_xx -> Pc
             const double* Qn = Q(c, n);
             const double* Rn = R(c, n);
             const double* Sn = Sm(c, n);
             const double* cf = coef + n * d.M;
-            for (int idx = tid; idx < NU * NW + NX * NX; idx += TEAM) {
+            TEAM_FOR(idx, NU * NW + NX * NX)
                 int i, j;
                 if (idx < NU * NW) { i = idx / NW; j = idx - i * NW; }
                 else { const int e = idx - NU * NW; i = NU + e / NX; j = NU + (e % NX); }
@@ -563,39 +593,44 @@ struct Kern {
                 const double g = a + h;
                 if (i < NU) Gu[idx] = g;
                 else Pc[idx - NU * NW] = g;
-            }
+            TEAM_END
             if (NG > 0) flops += 2ll * NW * NW * NG;
             flops += 2ll * NX * NW * NX + 2ll * NW * NW * NX;
             bar<TEAM>();
+            OCPQP_TICK(c, DBG_F_G);
             // L_uu = chol(G_uu)
             double* Ln = Lst + n * NU * NU;
+            double* Rinv_n = c.w[WS_RINV] + n * NU;
             double* rinv = vec;  // NU
             flops += (long long)NU * NU * NU / 3;
             if constexpr (NU <= 32) {
                 if (tid < 32) {
                     double row[NU];
+                    double rin = 0.0;
 #pragma unroll
                     for (int j = 0; j < NU; ++j) row[j] = (tid < NU && j <= tid) ? Gu[tid * NW + j] : 0.0;
-                    const bool ok = warp_chol<NU>(row, tid);
+                    const bool ok = warp_chol<NU>(row, tid, rin);
                     if (tid == 0) c.flag = ok;
                     if (ok && tid < NU) {
 #pragma unroll
                         for (int j = 0; j < NU; ++j) Ln[tid * NU + j] = j <= tid ? row[j] : 0.0;
+                        rinv[tid] = rin;
+                        Rinv_n[tid] = rin;
                     }
                 }
                 bar<TEAM>();
                 if (!c.flag) return n;
-                for (int i = tid; i < NU; i += TEAM) rinv[i] = 1.0 / Ln[i * NU + i];
             } else {
                 for (int idx = tid; idx < NU * NU; idx += TEAM) {
                     const int i = idx / NU, j = idx - i * NU;
                     Ln[idx] = Gu[i * NW + j];
                 }
                 bar<TEAM>();
-                if (!team_chol<TEAM>(Ln, NU, &c.flag)) return n;
-                for (int i = tid; i < NU; i += TEAM) rinv[i] = 1.0 / Ln[i * NU + i];
+                if (!team_chol<TEAM>(Ln, NU, &c.flag, rinv)) return n;
+                for (int i = tid; i < NU; i += TEAM) Rinv_n[i] = rinv[i];
+                bar<TEAM>();
             }
-            bar<TEAM>();
+            OCPQP_TICK(c, DBG_F_CHOL);
             // K = -L'^{-1} L^{-1} G_ux (kkt_ocp.py:240-243), one column per thread
             double* Kn = Kst + n * NU * NX;
             for (int j = tid; j < NX; j += TEAM) {
@@ -633,38 +668,42 @@ struct Kern {
             }
             flops += 2ll * NU * NU * NX;
             bar<TEAM>();
+            OCPQP_TICK(c, DBG_F_K);
             // P = G_xx + G_ux' K, symmetrised (kkt_ocp.py:244, 251)
-            for (int idx = tid; idx < NX * NX; idx += TEAM) {
+            TEAM_FOR(idx, NX * NX)
                 const int i = idx / NX, j = idx - i * NX;
                 double a = 0.0;
 #pragma unroll
                 for (int k = 0; k < NU; ++k) a = fma(Gu[k * NW + NU + i], Kn[k * NX + j], a);
                 T1[idx] = a + Pc[idx];
-            }
+            TEAM_END
             flops += 2ll * NX * NX * NU;
             bar<TEAM>();
             double* Pn = Pst + n * NX * NX;
-            for (int idx = tid; idx < NX * NX; idx += TEAM) {
+            TEAM_FOR(idx, NX * NX)
                 const int i = idx / NX, j = idx - i * NX;
                 const double v = 0.5 * (T1[idx] + T1[j * NX + i]);
                 Pc[idx] = v;
                 Pn[idx] = v;
-            }
+            TEAM_END
             bar<TEAM>();
         }
+        OCPQP_TICK(c, DBG_F_P);
         // L_P0 = chol(P_0) (kkt_ocp.py:193-200)
         double* LP0 = c.w[WS_LP0];
         flops += (long long)NX * NX * NX / 3;
         if constexpr (NX <= 32) {
             if (tid < 32) {
                 double row[NX];
+                double rin = 0.0;
 #pragma unroll
                 for (int j = 0; j < NX; ++j) row[j] = (tid < NX && j <= tid) ? Pc[tid * NX + j] : 0.0;
-                const bool ok = warp_chol<NX>(row, tid);
+                const bool ok = warp_chol<NX>(row, tid, rin);
                 if (tid == 0) c.flag = ok;
                 if (ok && tid < NX) {
 #pragma unroll
                     for (int j = 0; j < NX; ++j) LP0[tid * NX + j] = j <= tid ? row[j] : 0.0;
+                    c.w[WS_RINV][N * NU + tid] = rin;
                 }
             }
             bar<TEAM>();
@@ -672,7 +711,7 @@ struct Kern {
         } else {
             for (int idx = tid; idx < NX * NX; idx += TEAM) LP0[idx] = Pc[idx];
             bar<TEAM>();
-            if (!team_chol<TEAM>(LP0, NX, &c.flag)) return 0;
+            if (!team_chol<TEAM>(LP0, NX, &c.flag, c.w[WS_RINV] + N * NU)) return 0;
         }
         return -1;
     }
@@ -680,20 +719,21 @@ struct Kern {
     // warp-0 cho_solve of an n-vector: x <- (L L')^{-1} x, L row-major n x n.
     // Right-looking: one broadcast per step.  Result written to out[] (scaled by sgn).
     template <int NN>
-    __device__ static void warp_cho_solve(const double* L, const double* xin, double* out, double sgn) {
+    __device__ static void warp_cho_solve(const double* L, const double* rv, const double* xin,
+                                          double* out, double sgn) {
         const int lane = threadIdx.x;
         if constexpr (NN <= 32) {
             double z = lane < NN ? xin[lane] : 0.0;
-            const double dii = lane < NN ? L[lane * NN + lane] : 1.0;
+            const double rii = lane < NN ? rv[lane] : 1.0;
 #pragma unroll
             for (int k = 0; k < NN; ++k) {
-                if (lane == k) z = z / dii;
+                if (lane == k) z = z * rii;
                 const double zk = __shfl_sync(FULL, z, k);
                 if (lane > k && lane < NN) z = fma(-L[lane * NN + k], zk, z);
             }
 #pragma unroll
             for (int k = NN - 1; k >= 0; --k) {
-                if (lane == k) z = z / dii;
+                if (lane == k) z = z * rii;
                 const double zk = __shfl_sync(FULL, z, k);
                 if (lane < k) z = fma(-L[k * NN + lane], zk, z);
             }
@@ -704,12 +744,12 @@ struct Kern {
                 for (int i = 0; i < NN; ++i) {
                     double a = out[i];
                     for (int k = 0; k < i; ++k) a = fma(-L[i * NN + k], out[k], a);
-                    out[i] = a / L[i * NN + i];
+                    out[i] = a * rv[i];
                 }
                 for (int i = NN - 1; i >= 0; --i) {
                     double a = out[i];
                     for (int k = i + 1; k < NN; ++k) a = fma(-L[k * NN + i], out[k], a);
-                    out[i] = a / L[i * NN + i];
+                    out[i] = a * rv[i];
                 }
                 for (int i = 0; i < NN; ++i) out[i] *= sgn;
             }
@@ -723,12 +763,13 @@ struct Kern {
                                 double tau, const double* dla, const double* dta, double* dy,
                                 double* dpi, double* dlam, double* dt, long long& flops) {
         const int tid = threadIdx.x;
-        const double* act = c.w[WS_ACT];
+        const double* act = c.w[WS_DVEC];  // NaN = inactive
         const double* gam = c.w[WS_GAM];
         const double* r_g = c.w[WS_RG];
         const double* r_b = c.w[WS_RB];
         const double* r_d = c.w[WS_RD];
         double* wall = c.w[WS_WALL];
+        const double* tinv = c.w[WS_TINV];
         double* crow = c.w[WS_CROW];
         double* rhat = c.w[WS_RHAT];
         const double* Pst = c.w[WS_P];
@@ -743,7 +784,7 @@ struct Kern {
         // fold_rhs (kkt_common.py:118-137)
         for (int k = tid; k < d.nc; k += TEAM) {
             double w = 0.0;
-            if (act[k] != 0.0) {
+            if (!isnan(act[k])) {
                 double rmk;
                 if (rm_ext) {
                     rmk = rm_ext[k];
@@ -751,7 +792,7 @@ struct Kern {
                     rmk = lam[k] * t[k] - tau;
                     if (dla) rmk = rmk + dla[k] * dta[k];
                 }
-                w = (lam[k] * r_d[k] - rmk) / t[k];
+                w = (lam[k] * r_d[k] - rmk) * tinv[k];
             }
             wall[k] = w;
         }
@@ -771,6 +812,7 @@ struct Kern {
         }
         bar<TEAM>();
         const int N = d.N;
+        OCPQP_TICK(c, DBG_S_PRE);
         // backward sweep (kkt_ocp.py:276-289); terminal stage: nu = 0
         for (int i = tid; i < NX; i += TEAM) pv[N * NX + i] = rhat[N * NW + i];
         bar<TEAM>();
@@ -795,12 +837,13 @@ struct Kern {
             MV<NX, NU, TEAM>::run([&](int i, int k) { return Kn[k * NX + i]; },
                                   [&](int k) { return win[k]; },
                                   [&](int i, double v) { pvc[i] = win[NU + i] + v; });
-            if (tid < 32) warp_cho_solve<NU>(Lst + n * NU * NU, win, kff + n * NU, -1.0);
+            if (tid < 32) warp_cho_solve<NU>(Lst + n * NU * NU, c.w[WS_RINV] + n * NU, win, kff + n * NU, -1.0);
             flops += 2ll * NU * NU;
             bar<TEAM>();
         }
+        OCPQP_TICK(c, DBG_S_BWD);
         // x0 step
-        if (tid < 32) warp_cho_solve<NX>(c.w[WS_LP0], pv, dy + NU, -1.0);
+        if (tid < 32) warp_cho_solve<NX>(c.w[WS_LP0], c.w[WS_RINV] + N * NU, pv, dy + NU, -1.0);
         flops += 2ll * NX * NX;
         bar<TEAM>();
         // forward rollout (kkt_ocp.py:293-305)
@@ -823,6 +866,7 @@ struct Kern {
                 [&](int i, double v) { xn[i] = v + rb[i]; });
             bar<TEAM>();
         }
+        OCPQP_TICK(c, DBG_S_FWD);
         // dpi_n = P_{n+1} x_{n+1} + pv_{n+1}, all stages in parallel
         for (int e2 = tid; e2 < d.ne; e2 += TEAM) {
             const int n = e2 / NX;
@@ -844,7 +888,7 @@ struct Kern {
         bar<TEAM>();
         for (int k = tid; k < d.nc; k += TEAM) {
             double dl = 0.0, dtt = 0.0;
-            if (act[k] != 0.0) {
+            if (!isnan(act[k])) {
                 const double cy = slot_cy(d, k, rowv);
                 dl = wall[k] - gam[k] * cy;
                 dtt = -r_d[k] + cy;
@@ -853,15 +897,17 @@ struct Kern {
             dt[k] = dtt;
             if (!isfinite(dl) || !isfinite(dtt)) nonfinite = 1;
         }
-        return any_of<TEAM>(nonfinite);
+        const int nfr = any_of<TEAM>(nonfinite);
+        OCPQP_TICK(c, DBG_S_PRE);
+        return nfr;
     }
 
     __device__ static double max_step(FCtx& c, const RD& d, const double* lam, const double* t,
                                       const double* dlam, const double* dt, double ftb) {
-        const double* act = c.w[WS_ACT];
+        const double* act = c.w[WS_DVEC];  // NaN = inactive
         double ratio = INFINITY;
         for (int k = threadIdx.x; k < d.nc; k += TEAM) {
-            if (act[k] != 0.0) {
+            if (!isnan(act[k])) {
                 if (dlam[k] < 0.0) ratio = fmin(ratio, -lam[k] / dlam[k]);
                 if (dt[k] < 0.0) ratio = fmin(ratio, -t[k] / dt[k]);
             }
@@ -872,10 +918,10 @@ struct Kern {
 
     __device__ static double trial_mu(FCtx& c, const RD& d, const double* lam, const double* t,
                                       const double* dlam, const double* dt, double alpha) {
-        const double* act = c.w[WS_ACT];
+        const double* act = c.w[WS_DVEC];  // NaN = inactive
         double s = 0.0;
         for (int k = threadIdx.x; k < d.nc; k += TEAM)
-            if (act[k] != 0.0) s += (lam[k] + alpha * dlam[k]) * (t[k] + alpha * dt[k]);
+            if (!isnan(act[k])) s += (lam[k] + alpha * dlam[k]) * (t[k] + alpha * dt[k]);
         s = tsum<TEAM>(s, c.red);
         return c.n_act > 0.0 ? s / c.n_act : 0.0;
     }
@@ -893,7 +939,7 @@ struct Kern {
         double* pi = c.w[WS_IPI];
         double* lam = c.w[WS_ILAM];
         double* t = c.w[WS_IT];
-        double *ay = c.w[WS_AFF_Y], *api = c.w[WS_AFF_PI], *alam = c.w[WS_AFF_LAM], *at = c.w[WS_AFF_T];
+        double *alam = c.w[WS_AFF_LAM], *at = c.w[WS_AFF_T];
         double *dy = c.w[WS_DIR_Y], *dpi = c.w[WS_DIR_PI], *dlam = c.w[WS_DIR_LAM], *dt = c.w[WS_DIR_T];
         setup(c, d);
         // initial iterate (solver.py:113-142)
@@ -903,7 +949,7 @@ struct Kern {
         for (int k = tid; k < d.nc; k += TEAM) lam[k] = warm == 2 ? glam[k] : 0.0;
         bar<TEAM>();
         {
-            const double* act = c.w[WS_ACT];
+            const double* act = c.w[WS_DVEC];  // NaN = inactive
             const double* dvec = c.w[WS_DVEC];
             double* rowv = c.w[WS_ROWV];
             double floor = arg.t0;
@@ -914,7 +960,7 @@ struct Kern {
             if (warm == 2) {
                 double gd = 0.0, gb = 0.0;
                 for (int k = tid; k < d.nc; k += TEAM)
-                    if (act[k] != 0.0) gd = fmax(gd, dvec[k] - slot_cy(d, k, rowv));
+                    if (!isnan(act[k])) gd = fmax(gd, dvec[k] - slot_cy(d, k, rowv));
                 for (int e = tid; e < d.ne; e += TEAM) {
                     const int n = e / NX, i = e - n * NX;
                     const double* u = y + n * NW;
@@ -933,7 +979,7 @@ struct Kern {
             const double lfloor = fmax(1e-8, arg.lam_min);
             for (int k = tid; k < d.nc; k += TEAM) {
                 double tv = 0.0, lv = 0.0;
-                if (act[k] != 0.0) {
+                if (!isnan(act[k])) {
                     const double cy = warm ? slot_cy(d, k, rowv) : 0.0;
                     tv = fmax(cy - dvec[k], floor);
                     lv = warm == 2 ? fmax(lam[k], lfloor) : arg.mu0 / tv;
@@ -949,6 +995,11 @@ struct Kern {
         int it = 0, status = -1;
         Res res;
         const double reg2 = arg.reg_prim > 0.0 ? 2.0 * arg.reg_prim : 1e-8;
+        const long long t_start = clock64();
+        if (p.dbg && tid == 0) {
+            for (int i = 0; i < DBG_NUM; ++i) c.ph[i] = 0;
+            c.tk = t_start;
+        }
         while (true) {
             res = residuals(c, d, p, y, pi, lam, t);
             const double mu = res.mu;
@@ -961,17 +1012,21 @@ struct Kern {
                 status = OCPQP_STATUS_SUCCESS;
             else if (it >= arg.iter_max)
                 status = OCPQP_STATUS_MAXITER;
+            OCPQP_TICK(c, DBG_RES);
             if (status >= 0) break;
             bar<TEAM>();
             int fs = factor(c, d, p, stg, lam, t, arg.reg_prim, flops);
             if (fs >= 0) { bar<TEAM>(); fs = factor(c, d, p, stg, lam, t, reg2, flops); }
             if (fs == -2) { status = OCPQP_STATUS_NONPOSITIVE_ITERATE; break; }
             if (fs >= 0) { status = OCPQP_STATUS_FAILURE; break; }
-            if (solve(c, d, p, stg, lam, t, nullptr, 0.0, nullptr, nullptr, ay, api, alam, at, flops)) {
+            OCPQP_TICK(c, DBG_FACTOR);
+            // the affine dy / dpi are scratch (only dlam_aff, dt_aff are used later)
+            if (solve(c, d, p, stg, lam, t, nullptr, 0.0, nullptr, nullptr, dy, dpi, alam, at, flops)) {
                 status = OCPQP_STATUS_NAN;
                 break;
             }
             bar<TEAM>();
+            OCPQP_TICK(c, DBG_SOLVE_AFF);
             const double alpha_aff = max_step(c, d, lam, t, alam, at, 1.0);
             const double mu_aff = trial_mu(c, d, lam, t, alam, at, alpha_aff);
             double sigma = 0.0;
@@ -988,15 +1043,16 @@ struct Kern {
                     bar<TEAM>();
                 }
             }
+            OCPQP_TICK(c, DBG_SOLVE_DIR);
             if (nf) { status = OCPQP_STATUS_NAN; break; }
             const double alpha = max_step(c, d, lam, t, dlam, dt, arg.ftb);
-            const double* act = c.w[WS_ACT];
+            const double* act = c.w[WS_DVEC];  // NaN = inactive
             for (int i = tid; i < d.nv; i += TEAM) y[i] += alpha * dy[i];
             for (int i = tid; i < d.ne; i += TEAM) pi[i] += alpha * dpi[i];
             for (int k = tid; k < d.nc; k += TEAM) {
                 double lv = lam[k] + alpha * dlam[k];
                 double tv = t[k] + alpha * dt[k];
-                if (act[k] != 0.0) {
+                if (!isnan(act[k])) {
                     lv = fmax(lv, arg.lam_min);
                     tv = fmax(tv, arg.t_min);
                 }
@@ -1011,6 +1067,7 @@ struct Kern {
             bar<TEAM>();
             alpha_last = alpha;
             ++it;
+            OCPQP_TICK(c, DBG_STEP);
         }
         bar<TEAM>();
         for (int i = tid; i < d.nv; i += TEAM) gy[i] = y[i];
@@ -1022,6 +1079,11 @@ struct Kern {
             double* r = sp.res + (long long)q * 5;
             r[0] = res.g; r[1] = res.b; r[2] = res.d; r[3] = res.m; r[4] = res.mu;
             sp.flops[q] = flops;
+            if (p.dbg) {
+                c.ph[DBG_TOTAL] = clock64() - t_start;
+                c.ph[DBG_ITERS] = it;
+                for (int i = 0; i < DBG_NUM; ++i) p.dbg[(long long)q * DBG_NUM + i] = c.ph[i];
+            }
         }
     }
 };
@@ -1034,6 +1096,8 @@ __global__ void __launch_bounds__(S::TEAM) k_fast_solve(KParams p, SolveParams s
     RD d;
     d.N = p.N; d.NB = p.NB; d.M = p.NB + S::NG; d.NBN = p.NBN; d.NGN = p.NGN;
     d.MN = p.NBN + p.NGN; d.nc = p.nc; d.nv = p.nv; d.ne = p.ne; d.msum = p.msum;
+    d.inv_m = d.M ? 1.0f / (float)d.M : 0.0f;
+    d.inv_2m = d.M ? 0.5f / (float)d.M : 0.0f;
     for (int b = threadIdx.x; b < WS_NUM; b += S::TEAM)
         c.w[b] = ((p.smem_mask >> b) & 1u) ? smem + p.smem_off[b] : gslot + p.ws_off[b];
     double* stg = smem + p.stage_smem;

@@ -49,6 +49,8 @@ enum WsBuf {
     WS_T1,                                   // stage temp (max(nx' * nw, nx^2))
     WS_VEC,                                  // small stage vectors (4 * nw_max)
     WS_IY, WS_IPI, WS_ILAM, WS_IT,           // working iterate (shaped kernel)
+    WS_RINV,                                 // 1 / L_ii of every stage factor and of L_P0
+    WS_TINV,                                 // 1 / t on active slots (nc), per iteration
     WS_NUM
 };
 
@@ -76,7 +78,15 @@ struct KParams {
     int NB, NBN, NGN;         // box rows (n < N), box / general rows at N
     int stage_smem;           // doubles: offset of the per-stage scratch / per-team tile
     int team_stride;          // doubles of shared memory per team (row kernel)
+    long long* dbg;           // optional [B, 8] phase-cycle counters (nullptr = off)
 };
+
+// phase ids of the optional clock64 instrumentation (KParams::dbg)
+enum DbgPhase { DBG_RES = 0, DBG_FACTOR, DBG_SOLVE_AFF, DBG_SOLVE_DIR, DBG_STEP, DBG_TOTAL,
+                DBG_ITERS, DBG_SPARE,
+                // sub-phases (team kernel): factor stage parts, solve parts
+                DBG_F_T1, DBG_F_G, DBG_F_CHOL, DBG_F_K, DBG_F_P, DBG_S_PRE, DBG_S_BWD, DBG_S_FWD,
+                DBG_NUM = 16 };
 
 struct SolveParams {
     OcpIpmArgC arg;

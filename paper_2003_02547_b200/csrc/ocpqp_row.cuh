@@ -889,6 +889,9 @@ struct RKern {
         int it = 0, status = -1;
         Res res;
         const double reg2 = arg.reg_prim > 0.0 ? 2.0 * arg.reg_prim : 1e-8;
+        long long ph[DBG_NUM] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const long long t_start = clock64();
+        long long tc = t_start;
         while (true) {
             res = residuals(c, T, p, d, y, pi, lam, t);
             const double mu = res.mu;
@@ -901,16 +904,19 @@ struct RKern {
                 status = OCPQP_STATUS_SUCCESS;
             else if (it >= arg.iter_max)
                 status = OCPQP_STATUS_MAXITER;
+            if (p.dbg) { const long long n_ = clock64(); ph[DBG_RES] += n_ - tc; tc = n_; }
             if (status >= 0) break;
             int fs = factor(c, T, p, d, lam, t, arg.reg_prim, flops);
             if (fs >= 0) { T.sync(); fs = factor(c, T, p, d, lam, t, reg2, flops); }
             if (fs == -2) { status = OCPQP_STATUS_NONPOSITIVE_ITERATE; break; }
             if (fs >= 0) { status = OCPQP_STATUS_FAILURE; break; }
+            if (p.dbg) { const long long n_ = clock64(); ph[DBG_FACTOR] += n_ - tc; tc = n_; }
             if (solve(c, T, p, d, lam, t, nullptr, 0.0, nullptr, nullptr, dy, dpi, alam, at, flops)) {
                 status = OCPQP_STATUS_NAN;
                 break;
             }
             T.sync();
+            if (p.dbg) { const long long n_ = clock64(); ph[DBG_SOLVE_AFF] += n_ - tc; tc = n_; }
             const double alpha_aff = max_step(c, T, d, lam, t, alam, at, 1.0);
             const double mu_aff = trial_mu(c, T, d, lam, t, alam, at, alpha_aff);
             double sigma = 0.0;
@@ -927,6 +933,7 @@ struct RKern {
                     T.sync();
                 }
             }
+            if (p.dbg) { const long long n_ = clock64(); ph[DBG_SOLVE_DIR] += n_ - tc; tc = n_; }
             if (nf) { status = OCPQP_STATUS_NAN; break; }
             const double alpha = max_step(c, T, d, lam, t, dlam, dt, arg.ftb);
             for (int i = a; i < d.nv; i += G) y[i] += alpha * dy[i];
@@ -949,6 +956,7 @@ struct RKern {
             T.sync();
             alpha_last = alpha;
             ++it;
+            if (p.dbg) { const long long n_ = clock64(); ph[DBG_STEP] += n_ - tc; tc = n_; }
         }
         T.sync();
         for (int i = a; i < d.nv; i += G) gy[i] = y[i];
@@ -960,6 +968,11 @@ struct RKern {
             double* r = sp.res + (long long)q * 5;
             r[0] = res.g; r[1] = res.b; r[2] = res.d; r[3] = res.m; r[4] = res.mu;
             sp.flops[q] = flops;
+            if (p.dbg) {
+                ph[DBG_TOTAL] = clock64() - t_start;
+                ph[DBG_ITERS] = it;
+                for (int i = 0; i < DBG_NUM; ++i) p.dbg[(long long)q * DBG_NUM + i] = ph[i];
+            }
         }
     }
 };

@@ -183,8 +183,13 @@ def _guess_arrays(guess, batch, torch, device):
 
 
 def solve_ocp_qp_batch(batch, arg=None, guess=None, device="cuda", trace=True,
-                       stream=None, out=None) -> BatchReport:
-    """Solve every QP of a batch with the fused GPU IPM (one kernel launch)."""
+                       stream=None, out=None, phase_debug=None) -> BatchReport:
+    """Solve every QP of a batch with the fused GPU IPM (one kernel launch).
+
+    ``phase_debug`` (diagnostics): an int64 device tensor [B, 8] receiving the
+    clock64 cycles each QP spent in residuals / factor / affine solve /
+    corrector solve(s) / step+update, the total and the iteration count.
+    """
     arg = _check_arg(arg)
     torch = _torch()
     batch = _as_batch(batch)
@@ -220,6 +225,12 @@ def solve_ocp_qp_batch(batch, arg=None, guess=None, device="cuda", trace=True,
                        out["flops"].data_ptr(),
                        out["trace"].data_ptr() if out["trace"] is not None else None)
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    if phase_debug is not None or getattr(plan, "_dbg_on", False):
+        L = nat.lib()
+        L.ocpqp_debug_phases.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        nat.check(L.ocpqp_debug_phases(plan.handle, None if phase_debug is None
+                                       else ctypes.c_void_p(phase_debug.data_ptr())))
+        plan._dbg_on = phase_debug is not None
     nat.check(nat.lib().ocpqp_solve(plan.handle, ctypes.byref(dc), ctypes.byref(carg),
                                     ctypes.byref(it), ctypes.byref(st),
                                     ctypes.c_void_p(s.cuda_stream)))

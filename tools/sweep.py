@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--env", nargs="*", default=[])
+    ap.add_argument("--phases", action="store_true")
     a = ap.parse_args()
     for kv in a.env:
         k, v = kv.split("=", 1)
@@ -70,11 +71,25 @@ def main():
                 ts.append(e0.elapsed_time(e1))
             its = rep.iterations.cpu().numpy()
             info = S.get_plan(batch).info()
+            phases = None
+            if a.phases and kind != "g":
+                dbg = torch.zeros((B, 16), dtype=torch.int64, device="cuda")
+                solve_ocp_qp_batch(batch, arg, trace=False, phase_debug=dbg)
+                torch.cuda.synchronize()
+                solve_ocp_qp_batch(batch, arg, trace=False)  # switch instrumentation off
+                ph = dbg.cpu().numpy().astype(float)
+                n_it = np.maximum(ph[:, 6], 1)
+                names = {0: "res", 1: "factor_rest", 2: "aff_rest", 3: "dir_rest", 4: "step",
+                         8: "f_T1", 9: "f_G", 10: "f_chol", 11: "f_K", 12: "f_P",
+                         13: "s_pre_post", 14: "s_bwd", 15: "s_fwd"}
+                phases = {nm: round(float(np.mean(ph[:, i] / n_it))) for i, nm in names.items()}
+                phases["total_per_iter"] = float(np.mean(ph[:, 5] / n_it))
+                phases["max_total_cycles"] = float(ph[:, 5].max())
             print(json.dumps({"cfg": cfg, "kind": kind, "B": B, "gen_s": round(tg, 1),
                               "best_ms": min(ts), "median_ms": float(np.median(ts)),
                               "solves_per_s": B / (min(ts) * 1e-3),
                               "iters": [int(its.min()), float(its.mean()), int(its.max())],
-                              "plan": info}), flush=True)
+                              "cycles_per_iter": phases, "plan": info}), flush=True)
 
 
 if __name__ == "__main__":
