@@ -212,6 +212,34 @@ int ocpqp_factor_export(OcpPlan* plan, int32_t qp, double* P_out, double* K_out)
  * doubles per slot. */
 int ocpqp_plan_info(const OcpPlan* plan, int64_t* out, int32_t out_len);
 
+/* ---- partial condensing (reference condensing.py:451-619) ----
+ * A partial-condensing plan holds the block structure and the row routing of
+ * partial_condense(qp, N1) for one (dims, idxb) structure; the arithmetic is
+ * batched on the device.  Soft rows are not supported (OCPQP_E_UNSUPPORTED). */
+typedef struct OcpPcPlan OcpPcPlan;
+
+/* partial_condense block structure (condensing.py:451-550). */
+int ocpqp_pc_create(const OcpQpDimC* dim, int32_t N1, OcpPcPlan** out);
+int ocpqp_pc_destroy(OcpPcPlan* plan);
+
+/* Dimensions of the condensed QP; returns N2 = ceil(N / N1).  Non-NULL arrays
+ * receive N2+1 entries (nx, nu, nb, ng) and the concatenated new idxb. */
+int ocpqp_pc_dims(const OcpPcPlan* plan, int32_t* nx, int32_t* nu, int32_t* nb, int32_t* ng,
+                  int32_t* idxb);
+
+/* Condense a device batch of B QPs (`in`: every field present) into `out`
+ * (device, every field per QP, batch stride = condensed field length).
+ * Replaces partial_condense (condensing.py:451-550) for the whole batch. */
+int ocpqp_pc_condense(OcpPcPlan* plan, int32_t B, const OcpQpDataC* in, OcpQpDataC* out,
+                      void* stream);
+
+/* Expand condensed solutions back to the full horizon (partial_expand,
+ * condensing.py:553-619); device pointers. */
+int ocpqp_pc_expand(OcpPcPlan* plan, int32_t B, const OcpQpDataC* in, const OcpIterC* short_sol,
+                    OcpIterC* full_sol, void* stream);
+
+const char* ocpqp_pc_last_error(void);
+
 /* fp64 peak microbenchmarks (roofline denominators): DFMA and DMMA
  * (mma.sync.m8n8k4.f64) throughput of the current device in TFLOP/s. */
 int ocpqp_fp64_peak(double* dfma_tflops, double* dmma_tflops);

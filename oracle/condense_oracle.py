@@ -1,0 +1,206 @@
+"""CPU restatement of partial condensing / expansion (TEST INFRASTRUCTURE ONLY).
+
+numpy restatement of the reference's partial_condense / partial_expand
+(/root/reference/pkg/src/mpcqp/condensing.py:451-619, with condense(keep_x0=True)
+:160-340, _cost_recursion (classical) :128-157, expand_solution :343-429), for
+QPs without soft rows.  Pinned to the reference by tests/test_condense_oracle.py
+against tests/golden/pcond.npz; used by the GPU parity tests as the checker of
+csrc/ocpqp_condense.cu.  Operates on this package's OcpQp / QpSolution objects.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def _blocks(N, N1):
+    starts = list(range(0, N, N1))
+    return [(n0, min(n0 + N1, N)) for n0 in starts]
+
+
+def _condense_block(qp, n0, n1):
+    """Condensed data of stages n0..n1-1 (sub-QP with zero-cost terminal at n1)."""
+    d = qp.dim
+    L = n1 - n0
+    st = [qp._stages[n] for n in range(n0, n1)]
+    dy = [qp._dyn[n] for n in range(n0, n1)]
+    nx0 = int(d.nx[n0])
+    u_off, off = [], nx0
+    for i in range(L):
+        nu = int(d.nu[n0 + i])
+        u_off.append(off if nu else None)
+        off += nu
+    nv = off
+    # predictions (condensing.py:196-207)
+    pred = [np.zeros((int(d.nx[n0 + i]), nv)) for i in range(L + 1)]
+    pred[0][:, :nx0] = np.eye(nx0)
+    gamma = [np.zeros(nx0)]
+    for i in range(L):
+        A, B, b = dy[i]["A"], dy[i]["B"], dy[i]["b"]
+        pred[i + 1] = A @ pred[i]
+        if u_off[i] is not None:
+            pred[i + 1][:, u_off[i]: u_off[i] + B.shape[1]] += B
+        gamma.append(A @ gamma[i] + b)
+    # cost recursion with a zero-cost terminal placeholder (condensing.py:148-157)
+    nxL = int(d.nx[n1])
+    P = [None] * (L + 1)
+    Y = [None] * L
+    P[L] = np.zeros((nxL, nxL))
+    for i in range(L - 1, -1, -1):
+        A, B = dy[i]["A"], dy[i]["B"]
+        PA = P[i + 1] @ A
+        PB = P[i + 1] @ B
+        Y[i] = A.T @ PB + st[i]["S"].T
+        Pn = A.T @ PA + st[i]["Q"]
+        P[i] = 0.5 * (Pn + Pn.T)
+    beta = [None] * (L + 1)
+    beta[L] = np.zeros(nxL)
+    for i in range(L - 1, -1, -1):
+        beta[i] = st[i]["q"] + st[i]["Q"] @ gamma[i] + dy[i]["A"].T @ beta[i + 1]
+    Hc = np.zeros((nv, nv))
+    gc = np.zeros(nv)
+    Hc[:nx0, :nx0] = P[0]
+    gc[:nx0] = beta[0]
+    for j in range(L):
+        nu = int(d.nu[n0 + j])
+        if not nu:
+            continue
+        o = u_off[j]
+        Bj = dy[j]["B"]
+        Hc[o: o + nu, o: o + nu] = st[j]["R"] + Bj.T @ (P[j + 1] @ Bj)
+        gc[o: o + nu] = st[j]["r"] + st[j]["S"] @ gamma[j] + Bj.T @ beta[j + 1]
+        cols = pred[j].T @ Y[j]
+        Hc[:, o: o + nu] += cols
+        Hc[o: o + nu, :] += cols.T
+    Hc = 0.5 * (Hc + Hc.T)
+    # constraint routing (condensing.py:251-288)
+    box, gen = [], []
+    for i in range(L):
+        n = n0 + i
+        nu = int(d.nu[n])
+        s = st[i]
+        for r, k in enumerate(s["idxb"]):
+            if k < nu:
+                box.append((u_off[i] + int(k), i, r))
+            elif i == 0:
+                box.append((int(k) - nu, i, r))
+            else:
+                c = int(k) - nu
+                gen.append((pred[i][c].copy(), s["lb"][r] - gamma[i][c], s["ub"][r] - gamma[i][c],
+                            i, r))
+        for g in range(int(d.ng[n])):
+            row = np.zeros(nv)
+            if nu:
+                row[u_off[i]: u_off[i] + nu] = s["D"][g]
+            row += s["C"][g] @ pred[i]
+            sh = float(s["C"][g] @ gamma[i])
+            gen.append((row, s["lg"][g] - sh, s["ug"][g] - sh, i, int(d.nb[n]) + g))
+    box.sort(key=lambda e: e[0])
+    return dict(nx0=nx0, nv=nv, u_off=u_off, pred=pred, gamma=gamma, Hc=Hc, gc=gc, box=box,
+                gen=gen, L=L, n0=n0)
+
+
+def partial_condense(qp, N1):
+    """(fields per new stage, blocks) of the condensed QP; fields as dicts."""
+    d = qp.dim
+    out = []
+    blocks = []
+    for n0, n1 in _blocks(d.N, N1):
+        c = _condense_block(qp, n0, n1)
+        nx0, nv = c["nx0"], c["nv"]
+        nun = nv - nx0
+        zidx = np.array([e[0] for e in c["box"]], dtype=int)
+        new_idx = np.where(zidx < nx0, zidx + nun, zidx - nx0)
+        perm = np.argsort(new_idx, kind="stable")
+        st = {}
+        H, g = c["Hc"], c["gc"]
+        st["Q"], st["S"], st["R"] = H[:nx0, :nx0], H[nx0:, :nx0], H[nx0:, nx0:]
+        st["q"], st["r"] = g[:nx0], g[nx0:]
+        pL = c["pred"][-1]
+        st["A"], st["B"], st["b"] = pL[:, :nx0], pL[:, nx0:], c["gamma"][-1]
+        src = [(e[1], e[2]) for e in c["box"]]
+        st["idxb"] = new_idx[perm]
+        st["lb"] = np.array([qp._stages[n0 + src[j][0]]["lb"][src[j][1]] for j in perm])
+        st["ub"] = np.array([qp._stages[n0 + src[j][0]]["ub"][src[j][1]] for j in perm])
+        Cz = np.array([e[0] for e in c["gen"]]).reshape(len(c["gen"]), nv)
+        st["C"], st["D"] = Cz[:, :nx0], Cz[:, nx0:]
+        st["lg"] = np.array([e[1] for e in c["gen"]])
+        st["ug"] = np.array([e[2] for e in c["gen"]])
+        rows = [src[j] for j in perm] + [(e[3], e[4]) for e in c["gen"]]
+        st["maskl"] = np.array([qp._stages[n0 + i]["maskl"][r] for i, r in rows])
+        st["masku"] = np.array([qp._stages[n0 + i]["masku"][r] for i, r in rows])
+        out.append(st)
+        blocks.append(dict(n0=n0, n1=n1, cond=c, rows=rows, m=len(rows)))
+    return out, blocks
+
+
+def partial_expand(qp, blocks, short):
+    """Full-horizon (y, pi, lam, t) from the condensed solution arrays.
+
+    ``short`` holds y/pi/lam/t of the condensed QP plus its layout offsets
+    (u_off, x_off, pi_off, c_off lists); ``qp`` provides the full layout.
+    """
+    from paper_2003_02547_b200.layout import OcpLayout
+
+    d = qp.dim
+    lay = OcpLayout(d)
+    y = np.zeros(lay.ny)
+    pi = np.zeros(lay.ne)
+    lam = np.zeros(lay.nc)
+    t = np.zeros(lay.nc)
+    sl = short["layout"]
+    for k, blk in enumerate(blocks):
+        c = blk["cond"]
+        n0, L, nx0 = blk["n0"], c["L"], c["nx0"]
+        xk = short["y"][sl.x_off[k]: sl.x_off[k] + nx0]
+        uk = short["y"][sl.u_off[k]: sl.u_off[k] + c["nv"] - nx0]
+        xs = [xk.copy()]
+        for i in range(L):
+            n = n0 + i
+            nu = int(d.nu[n])
+            u = uk[c["u_off"][i] - nx0: c["u_off"][i] - nx0 + nu] if nu else np.zeros(0)
+            y[lay.u_off[n]: lay.u_off[n] + nu] = u
+            y[lay.x_off[n]: lay.x_off[n] + int(d.nx[n])] = xs[i]
+            dyn = qp._dyn[n]
+            xs.append(dyn["A"] @ xs[i] + dyn["B"] @ u + dyn["b"])
+        m = blk["m"]
+        cs = sl.c_off[k]
+        for r, (i, src) in enumerate(blk["rows"]):
+            n = n0 + i
+            mo = int(d.nb[n] + d.ng[n])
+            lam[lay.c_off[n] + src] = short["lam"][cs + r]
+            lam[lay.c_off[n] + mo + src] = short["lam"][cs + m + r]
+            t[lay.c_off[n] + src] = short["t"][cs + r]
+            t[lay.c_off[n] + mo + src] = short["t"][cs + m + r]
+        # costate recursion (condensing.py:397-412)
+        pim = short["pi"][sl.pi_off[k]: sl.pi_off[k] + int(d.nx[n0 + L])]
+        pi[lay.pi_off[n0 + L - 1]: lay.pi_off[n0 + L - 1] + pim.size] = pim
+        for mm in range(L - 1, 0, -1):
+            n = n0 + mm
+            s = qp._stages[n]
+            nu = int(d.nu[n])
+            lm = lam[lay.c_off[n]: lay.c_off[n] + 2 * int(d.nb[n] + d.ng[n])]
+            mo = int(d.nb[n] + d.ng[n])
+            lo = np.concatenate([s["lb"], s["lg"]])
+            up = np.concatenate([s["ub"], s["ug"]])
+            al = (s["maskl"] != 0) & np.isfinite(lo)
+            au = (s["masku"] != 0) & np.isfinite(up)
+            coef = np.where(al, lm[:mo], 0.0) - np.where(au, lm[mo:], 0.0)
+            ct = np.zeros(nu + int(d.nx[n]))
+            np.add.at(ct, s["idxb"], coef[: int(d.nb[n])])
+            if int(d.ng[n]):
+                ct += np.hstack([s["D"], s["C"]]).T @ coef[int(d.nb[n]):]
+            u = y[lay.u_off[n]: lay.u_off[n] + nu]
+            val = s["Q"] @ xs[mm] + s["S"].T @ u + s["q"] - ct[nu:]
+            val = val + qp._dyn[n]["A"].T @ pim
+            pi[lay.pi_off[n - 1]: lay.pi_off[n - 1] + val.size] = val
+            pim = val
+    N = d.N
+    Np = len(blocks)
+    for k in range(Np + 1):
+        n = blocks[k]["n0"] if k < Np else N
+        y[lay.x_off[n]: lay.x_off[n] + int(d.nx[n])] = short["y"][sl.x_off[k]: sl.x_off[k] + int(d.nx[n])]
+    ncN = lay.stage_nc(N)
+    lam[lay.c_off[N]: lay.c_off[N] + ncN] = short["lam"][sl.c_off[Np]: sl.c_off[Np] + ncN]
+    t[lay.c_off[N]: lay.c_off[N] + ncN] = short["t"][sl.c_off[Np]: sl.c_off[Np] + ncN]
+    return y, pi, lam, t

@@ -8,6 +8,13 @@ steps of every QP in one launch).  See DESIGN.md.
 """
 
 from .batch import OcpQpBatch
+from .condensing import (
+    PartialCondensingMap,
+    partial_condense,
+    partial_condense_batch,
+    partial_expand,
+    partial_expand_batch,
+)
 from .errors import (
     CondenseError,
     DimensionMismatch,
@@ -48,5 +55,6 @@ __all__ = [
     "SolverStats", "Status", "mode_preset", "OcpLayout", "QpResiduals", "QpSolution",
     "OcpQp", "OcpQpDim", "Violation", "validate", "BatchReport", "SolveReport",
     "compute_residuals", "newton_step", "solve_ocp_qp", "solve_ocp_qp_batch",
-    "solve_ocp_qp_host", "__version__",
+    "solve_ocp_qp_host", "PartialCondensingMap", "partial_condense", "partial_condense_batch",
+    "partial_expand", "partial_expand_batch", "__version__",
 ]

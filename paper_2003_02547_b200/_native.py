@@ -30,6 +30,8 @@ EXPORTED_SYMBOLS = (
     "ocpqp_layout", "ocpqp_plan_create", "ocpqp_plan_destroy", "ocpqp_solve",
     "ocpqp_solve_host", "ocpqp_residuals", "ocpqp_newton_step", "ocpqp_factor_export",
     "ocpqp_plan_info", "ocpqp_fp64_peak", "ocpqp_abi_version", "ocpqp_last_error",
+    "ocpqp_pc_create", "ocpqp_pc_destroy", "ocpqp_pc_dims", "ocpqp_pc_condense",
+    "ocpqp_pc_expand", "ocpqp_pc_last_error",
 )
 
 _i32p = ctypes.POINTER(ctypes.c_int32)
@@ -101,7 +103,7 @@ def lib():
     L.ocpqp_last_error.argtypes = []
     L.ocpqp_last_error.restype = ctypes.c_char_p
     for name in EXPORTED_SYMBOLS:
-        if name != "ocpqp_last_error":
+        if name not in ("ocpqp_last_error", "ocpqp_pc_last_error"):
             getattr(L, name).restype = ctypes.c_int
     _LIB = L
     return L

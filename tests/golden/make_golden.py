@@ -192,7 +192,54 @@ def known():
     print({k: float(v) for k, v in out.items()})
 
 
+# partial condensing cases: (name, source, N1) -- source is a RANDOM_CASES-style
+# (seed, kwargs) without soft rows, or ("cfg", cfg, N) for a BASELINE generator
+PCOND_CASES = [
+    ("r21", (21, dict(N=8, nx=3, nu=2, nb=4, ng=1, ns=0, fix_x0=True)), 4),
+    ("r22", (22, dict(N=7, nx=2, nu=1, nb=3, ng=0, ns=0, fix_x0=True)), 3),
+    ("r23", (23, dict(N=6, nx=3, nu=2, nb=5, ng=2, ns=0, fix_x0=True)), 1),
+    ("r24", (24, dict(N=5, nx=4, nu=2, nb=6, ng=1, ns=0, fix_x0=True, mask_last=False)), 5),
+    ("c4", ("cfg", 4, 10), 5),
+    ("c1", ("cfg", 1, None), 5),
+]
+PCOND_FIELDS = ("Q", "S", "R", "q", "r", "idxb", "lb", "ub", "C", "D", "lg", "ug", "maskl", "masku")
+
+
+def pcond_source(src):
+    if src[0] == "cfg":
+        _, cfg, N = src
+        return to_ref(make_batch(cfg, batch=1, start=0, N=N).qp(0))
+    seed, kw = src
+    return qpgen.build_qp(mpcqp, *qpgen.random_ocp_fields(seed, **kw))
+
+
+def pcond():
+    out = {}
+    for name, src, N1 in PCOND_CASES:
+        qp = pcond_source(src)
+        qp2, pmap = mpcqp.partial_condense(qp, N1)
+        d2 = qp2.dim
+        out[f"{name}_dims"] = np.array([d2.nx, d2.nu, d2.nb, d2.ng])
+        for n in range(d2.N + 1):
+            for f in PCOND_FIELDS:
+                out[f"{name}_s{n}_{f}"] = qp2.get_field(f, n)
+            if n < d2.N:
+                for f in ("A", "B", "b"):
+                    out[f"{name}_s{n}_{f}"] = qp2.get_field(f, n)
+        rep = mpcqp.solve_ocp_qp(qp2, ARG)
+        full = mpcqp.partial_expand(rep.solution, pmap, qp)
+        for k, v in pack_report(rep).items():
+            out[f"{name}_short_{k}"] = v
+        for k in ("y", "pi", "lam", "t"):
+            out[f"{name}_full_{k}"] = getattr(full, k)
+        direct = mpcqp.solve_ocp_qp(qp, ARG)
+        out[f"{name}_direct_iters"] = direct.iterations
+        out[f"{name}_direct_y"] = direct.solution.y
+        print("pcond", name, d2.N, rep.status.value, rep.iterations, direct.iterations, flush=True)
+    np.savez_compressed(HERE / "pcond.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["known", "residuals", "newton", "solve_random", "solve_cfg"]
+    which = sys.argv[1:] or ["known", "residuals", "newton", "solve_random", "solve_cfg", "pcond"]
     for w in which:
         globals()[w]()
