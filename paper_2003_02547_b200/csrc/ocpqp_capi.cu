@@ -344,8 +344,8 @@ bool detect_fast(OcpPlan* P) {
     const char* envw = getenv("OCPQP_WPB");
     const int want_kind = envk ? atoi(envk) : -1;
     FastShape pick{-1, 0, 0, 0, 0, 0, 0};
-    // row kernel
-    if (want_kind != 0) {
+    // row kernel: only on request (measured slower than the team kernel on configs 1-4)
+    if (want_kind == 1) {
         const int gdef = (NX <= 8 && NU <= 8) ? 8 : (NX <= 16 && NU <= 16) ? 16 : 32;
         const int g = envt && want_kind == 1 ? atoi(envt) : gdef;
         const int wpbs[] = {envw ? atoi(envw) : 1, 1, 2, 4};
@@ -361,7 +361,7 @@ bool detect_fast(OcpPlan* P) {
             if (!fast_supported(FastShape{0, NX, NU, NG, NB, team, 1})) team = 0;
         } else {
             const int cands[] = {32, 64, 128, 256};
-            int pref = NX + NU <= 12 ? 32 : NX + NU <= 32 ? 64 : NX + NU <= 48 ? 128 : 256;
+            int pref = NX + NU <= 32 ? 64 : NX + NU <= 48 ? 128 : 256;
             if (fast_supported(FastShape{0, NX, NU, NG, NB, pref, 1})) team = pref;
             for (int c : cands)
                 if (!team && fast_supported(FastShape{0, NX, NU, NG, NB, c, 1})) team = c;
