@@ -305,6 +305,7 @@ void fill_kparams(const OcpPlan* P, KParams& k, const OcpQpDataC* data, bool use
     k.counter = P->d_counter;
     k.NB = P->NB; k.NBN = P->NBN; k.NGN = P->NGN;
     k.stage_smem = P->stage_smem;
+    k.sstage = P->shape.sstage;
     k.team_stride = P->team_stride;
     k.dbg = P->dbg;
 }
@@ -366,7 +367,14 @@ bool detect_fast(OcpPlan* P) {
             for (int c : cands)
                 if (!team && fast_supported(FastShape{0, NX, NU, NG, NB, c, 1})) team = c;
         }
-        if (team) pick = FastShape{0, NX, NU, NG, NB, team, 1};
+        if (team) {
+            pick = FastShape{0, NX, NU, NG, NB, team, 1};
+            const char* envs = getenv("OCPQP_SSTAGE");
+            // measured: staging pays where the stage operands are large and the
+            // factor store cannot stay in shared memory (config 3); the smaller
+            // shapes lose more occupancy / issue slots than they gain
+            pick.sstage = envs ? atoi(envs) : (NX * (NX + NU) >= 1000 ? 1 : 0);
+        }
     }
     if (pick.kind < 0) return false;
     P->fast = true;
@@ -423,7 +431,11 @@ void place_fast(OcpPlan* P, long long budget_per_cta) {
 bool plan_fast(OcpPlan* P, int* occ_out) {
     const int teams = fast_teams_per_cta(P->shape);
     const int ctas_needed = (P->B + teams - 1) / teams;
-    const int per_sm = std::max(1, (ctas_needed + P->num_sms - 1) / P->num_sms);
+    int per_sm = std::max(1, (ctas_needed + P->num_sms - 1) / P->num_sms);
+    // never plan for more CTAs per SM than registers / threads allow
+    const int tile_bytes = (int)(align2(fast_stage_smem_doubles(P->shape)) * 8) * teams;
+    const int occ_max = fast_occupancy(P->shape, (size_t)tile_bytes);
+    if (occ_max > 0) per_sm = std::min(per_sm, occ_max);
     const char* envs = getenv("OCPQP_SMEM_KB");
     long long budget;
     if (envs) budget = (long long)atoi(envs) * 1024;

@@ -215,6 +215,70 @@ struct FCtx {
     }            \
     }
 
+// ---- cp.async (LDGSTS) staging helpers ------------------------------------
+__device__ __forceinline__ void cpa8(double* dst_smem, const double* src_gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst_smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src_gmem) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cpa_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory");
+}
+
+// ---- register-tiled team GEMM ---------------------------------------------
+// C(i, j) = sum_k a(i, k) b(k, j), i < M, j < N, k < K (k ascending, one fma
+// chain per output as a dot product).  Each thread owns TM x TN outputs and
+// reuses every loaded operand TN (resp. TM) times.  Tile choice: the smallest
+// TM*TN (TM, TN <= 4) whose tile count fits the team -- minimal dependent
+// chain per thread when the team is wide, fewer loads per FMA when it is not.
+__host__ __device__ constexpr int gemm_pick(int M, int N, int TEAM) {
+    int best = 4 * 8 + 4;  // packed TM * 8 + TN; default 4 x 4
+    int best_sz = 1 << 30;
+    for (int tm = 1; tm <= 4; ++tm)
+        for (int tn = 1; tn <= 4; ++tn) {
+            const int tiles = ((M + tm - 1) / tm) * ((N + tn - 1) / tn);
+            const int sz = tm * tn;
+            if (tiles <= TEAM && (sz < best_sz || (sz == best_sz && tn > (best & 7)))) {
+                best = tm * 8 + tn;
+                best_sz = sz;
+            }
+        }
+    return best;
+}
+
+template <int M, int N, int K, int TEAM, class FA, class FB, class FE>
+__device__ __forceinline__ void tile_gemm(FA a, FB b, FE epi) {
+    constexpr int PK = gemm_pick(M, N, TEAM);
+    constexpr int TM = PK / 8, TN = PK % 8;
+    constexpr int MT = (M + TM - 1) / TM, NT = (N + TN - 1) / TN, TILES = MT * NT;
+    for (int t = threadIdx.x; t < TILES; t += TEAM) {
+        const int r0 = (t / NT) * TM, c0 = (t % NT) * TN;
+        double acc[TM][TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
+#pragma unroll 4
+        for (int k = 0; k < K; ++k) {
+            double av[TM], bv[TN];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) av[i] = a(r0 + i < M ? r0 + i : M - 1, k);
+#pragma unroll
+            for (int j = 0; j < TN; ++j) bv[j] = b(k, c0 + j < N ? c0 + j : N - 1);
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j)
+                if (r0 + i < M && c0 + j < N) epi(r0 + i, c0 + j, acc[i][j]);
+    }
+}
+
 // accumulate the cycles since the previous tick into phase `slot` (thread 0)
 #define OCPQP_TICK(c, slot)                                       \
     do {                                                          \
@@ -246,7 +310,21 @@ struct Shape {
     static constexpr int NX = NX_, NU = NU_, NG = NG_, TEAM = TEAM_, NW = NU_ + NX_;
     static constexpr int T1N = NX * (NW > NX ? NW : NX);
     static constexpr int VEC = 2 * NW + 3 * NX + 2 * NU + 16;
-    static constexpr int STAGE = NX * NX + T1N + NU * NW + VEC;
+    // [B A] is staged in shared memory for small / medium stages only; large
+    // stages read it through L1 so that two QPs' tiles fit per SM
+    static constexpr bool STAGE_BA = NX * NW <= 2048;
+    // double-buffered per-stage operands of the solve sweeps (cp.async one stage
+    // ahead): P_{n+1}, [B A]_n, K_n, L_n, 1/L_ii, r_b,n, rhat_n, kff_n
+    static constexpr int HALF = NX * NX + NX * NW + NU * NX + NU * NU + NU + NX + NW + NU + 4;
+    static constexpr bool STAGE_SOLVE = HALF <= 4096;
+    static constexpr int SOLVE_BUF = STAGE_SOLVE ? 2 * HALF : 0;
+    static constexpr int BA_BUF = STAGE_BA ? NX * NW : 0;
+    static constexpr int STAGE0 = NX * NX + T1N + NU * NW + VEC;
+    static constexpr int STAGE = STAGE0 + (BA_BUF > SOLVE_BUF ? BA_BUF : SOLVE_BUF);  // staging on
+    static constexpr int STAGE_NOSS = STAGE0 + BA_BUF;                                // staging off
+    // resident CTAs per SM the register allocation must allow (latency hiding
+    // across QPs): 512 threads per SM
+    static constexpr int MINB = TEAM >= 512 ? 1 : 512 / TEAM;
 };
 
 template <class S>
@@ -273,6 +351,7 @@ struct Kern {
     __device__ static void setup(FCtx& c, const RD& d) {
         double* dvec = c.w[WS_DVEC];   // d (view.py:156-157); NaN marks an inactive side
         double cnt = 0.0;
+        #pragma unroll 4
         for (int k = threadIdx.x; k < d.nc; k += TEAM) {
             const int n = d.slot_stage(k);
             const int m = n < d.N ? d.M : d.MN;
@@ -296,6 +375,7 @@ struct Kern {
     // row values Jc w for all rows (ConBlock.rows_w, view.py:91-97)
     __device__ static void rows_values(const FCtx& c, const RD& d, const int* idxb, const double* y,
                                        double* rowv) {
+        #pragma unroll 4
         for (int r = threadIdx.x; r < d.msum; r += TEAM) {
             const int n = d.row_stage(r);
             const int i = r - n * d.M;
@@ -357,6 +437,7 @@ struct Kern {
         double* r_b = c.w[WS_RB];
         double* r_d = c.w[WS_RD];
         rows_values(c, d, p.idxb, y, rowv);
+        #pragma unroll 4
         for (int r = threadIdx.x; r < d.msum; r += TEAM) {
             const int n = d.row_stage(r);
             const int i = r - n * d.M;
@@ -369,6 +450,7 @@ struct Kern {
         bar<TEAM>();
         AbsMax ag, ab, ad, am;
         double musum = 0.0;
+        #pragma unroll 4
         for (int j = threadIdx.x; j < d.nv; j += TEAM) {
             int n = j / NW;
             if (n > d.N) n = d.N;
@@ -423,6 +505,7 @@ struct Kern {
             r_g[j] = r;
             ag.add(r);
         }
+        #pragma unroll 4
         for (int e = threadIdx.x; e < d.ne; e += TEAM) {
             const int n = e / NX;
             const int i = e - n * NX;
@@ -440,6 +523,7 @@ struct Kern {
             r_b[e] = r;
             ab.add(r);
         }
+        #pragma unroll 4
         for (int k = threadIdx.x; k < d.nc; k += TEAM) {
             double rd = 0.0, rm = 0.0;
             if (!isnan(act[k])) {
@@ -476,8 +560,10 @@ struct Kern {
         double* T1 = Pc + NX * NX;              // NX*NW
         double* Gu = T1 + S::T1N;               // NU*NW
         double* vec = Gu + NU * NW;
+        double* BAs = vec + S::VEC;             // NX x NW staged [B A] of the stage
         double* tinv = c.w[WS_TINV];
         int bad = 0;
+        #pragma unroll 4
         for (int k = tid; k < d.nc; k += TEAM) {
             double g = 0.0, ti = 0.0;
             if (!isnan(act[k])) {
@@ -490,6 +576,7 @@ struct Kern {
         }
         if (any_of<TEAM>(bad)) return -2;
         bar<TEAM>();
+        #pragma unroll 4
         for (int r = tid; r < d.msum; r += TEAM) {
             const int n = d.row_stage(r);
             const int i = r - n * d.M;
@@ -537,41 +624,32 @@ struct Kern {
             OCPQP_TICK(c, DBG_F_P);
             const double* An = A(c, n);
             const double* Bn = Bm(c, n);
+            // stage [B A] (kkt_ocp.py:177) in shared memory
+            if constexpr (S::STAGE_BA) {
+                TEAM_FOR(e, NX * NW)
+                    const int k = e / NW, j = e - k * NW;
+                    BAs[e] = j < NU ? Bn[k * NU + j] : An[k * NX + (j - NU)];
+                TEAM_END
+                bar<TEAM>();
+            }
+            auto BA = [&](int k, int j) -> double {
+                if constexpr (S::STAGE_BA) return BAs[k * NW + j];
+                else return j < NU ? Bn[k * NU + j] : An[k * NX + (j - NU)];
+            };
             // T1 = P_{n+1} [B A]   (kkt_ocp.py:232)
-            TEAM_FOR(idx, NX * NW)
-                const int i = idx / NW, j = idx - i * NW;
-                const double* Pr = Pc + i * NX;
-                double a = 0.0;
-                if (j < NU) {
-#pragma unroll 8
-                    for (int k = 0; k < NX; ++k) a = fma(Pr[k], Bn[k * NU + j], a);
-                } else {
-                    const double* Ac = An + (j - NU);
-#pragma unroll 8
-                    for (int k = 0; k < NX; ++k) a = fma(Pr[k], Ac[k * NX], a);
-                }
-                T1[idx] = a;
-            TEAM_END
+            tile_gemm<NX, NW, NX, TEAM>([&](int i, int k) { return Pc[i * NX + k]; },
+                                        [&](int k, int j) { return BA(k, j); },
+                                        [&](int i, int j, double v) { T1[i * NW + j] = v; });
             bar<TEAM>();
             OCPQP_TICK(c, DBG_F_T1);
-            // G = [B A]' T1 + M~ (kkt_ocp.py:233, 70-80): input rows -> Gu, G_xx -> Pc
+            // G = [B A]' T1 + M~ (kkt_ocp.py:233, 70-80; kkt_common.py:100-115):
+            // input rows -> Gu (NU x NW), G_xx -> Pc (P_{n+1} is dead after T1)
             const double* Qn = Q(c, n);
             const double* Rn = R(c, n);
             const double* Sn = Sm(c, n);
             const double* cf = coef + n * d.M;
-            TEAM_FOR(idx, NU * NW + NX * NX)
-                int i, j;
-                if (idx < NU * NW) { i = idx / NW; j = idx - i * NW; }
-                else { const int e = idx - NU * NW; i = NU + e / NX; j = NU + (e % NX); }
-                double a = 0.0;
-                if (i < NU) {
-#pragma unroll 8
-                    for (int k = 0; k < NX; ++k) a = fma(Bn[k * NU + i], T1[k * NW + j], a);
-                } else {
-                    const double* Ac = An + (i - NU);
-#pragma unroll 8
-                    for (int k = 0; k < NX; ++k) a = fma(Ac[k * NX], T1[k * NW + j], a);
-                }
+            const bool full_box = d.NB == NW;
+            auto Mt = [&](int i, int j) -> double {
                 double mij, mji;
                 if (i < NU && j < NU) { mij = Rn[i * NU + j]; mji = Rn[j * NU + i]; }
                 else if (i < NU) { mij = Sn[i * NX + (j - NU)]; mji = mij; }
@@ -579,21 +657,25 @@ struct Kern {
                 else { mij = Qn[(i - NU) * NX + (j - NU)]; mji = Qn[(j - NU) * NX + (i - NU)]; }
                 double h = 0.5 * (mij + mji);
                 if (i == j) {
-                    const int kb = p.var_box[n * NW + i];
+                    const int kb = full_box ? i : p.var_box[n * NW + i];
                     if (kb >= 0) h += cf[kb];
                 }
                 if (NG > 0) {
-                    double s = 0.0;
+                    double sg = 0.0;
 #pragma unroll 4
                     for (int r = 0; r < NG; ++r)
-                        s = fma(Jg(c, n, NU, r, i), cf[d.NB + r] * Jg(c, n, NU, r, j), s);
-                    h = s + h;
+                        sg = fma(Jg(c, n, NU, r, i), cf[d.NB + r] * Jg(c, n, NU, r, j), sg);
+                    h = sg + h;
                 }
                 if (i == j && reg != 0.0) h += reg;
-                const double g = a + h;
-                if (i < NU) Gu[idx] = g;
-                else Pc[idx - NU * NW] = g;
-            TEAM_END
+                return h;
+            };
+            tile_gemm<NU, NW, NX, TEAM>([&](int i, int k) { return BA(k, i); },
+                                        [&](int k, int j) { return T1[k * NW + j]; },
+                                        [&](int i, int j, double v) { Gu[i * NW + j] = v + Mt(i, j); });
+            tile_gemm<NX, NX, NX, TEAM>([&](int i, int k) { return BA(k, NU + i); },
+                                        [&](int k, int j) { return T1[k * NW + NU + j]; },
+                                        [&](int i, int j, double v) { Pc[i * NX + j] = v + Mt(NU + i, NU + j); });
             if (NG > 0) flops += 2ll * NW * NW * NG;
             flops += 2ll * NX * NW * NX + 2ll * NW * NW * NX;
             bar<TEAM>();
@@ -670,13 +752,9 @@ struct Kern {
             bar<TEAM>();
             OCPQP_TICK(c, DBG_F_K);
             // P = G_xx + G_ux' K, symmetrised (kkt_ocp.py:244, 251)
-            TEAM_FOR(idx, NX * NX)
-                const int i = idx / NX, j = idx - i * NX;
-                double a = 0.0;
-#pragma unroll
-                for (int k = 0; k < NU; ++k) a = fma(Gu[k * NW + NU + i], Kn[k * NX + j], a);
-                T1[idx] = a + Pc[idx];
-            TEAM_END
+            tile_gemm<NX, NX, NU, TEAM>([&](int i, int k) { return Gu[k * NW + NU + i]; },
+                                        [&](int k, int j) { return Kn[k * NX + j]; },
+                                        [&](int i, int j, double v) { T1[i * NX + j] = v + Pc[i * NX + j]; });
             flops += 2ll * NX * NX * NU;
             bar<TEAM>();
             double* Pn = Pst + n * NX * NX;
@@ -782,6 +860,7 @@ struct Kern {
         double* e = vec + NW;           // NX
         int nonfinite = 0;
         // fold_rhs (kkt_common.py:118-137)
+        #pragma unroll 4
         for (int k = tid; k < d.nc; k += TEAM) {
             double w = 0.0;
             if (!isnan(act[k])) {
@@ -797,6 +876,7 @@ struct Kern {
             wall[k] = w;
         }
         bar<TEAM>();
+        #pragma unroll 4
         for (int r = tid; r < d.msum; r += TEAM) {
             const int n = d.row_stage(r);
             const int i = r - n * d.M;
@@ -805,6 +885,7 @@ struct Kern {
             crow[r] = wall[k] - wall[k + m];
         }
         bar<TEAM>();
+        #pragma unroll 4
         for (int j = tid; j < d.nv; j += TEAM) {
             int n = j / NW;
             if (n > d.N) n = d.N;
@@ -813,61 +894,137 @@ struct Kern {
         bar<TEAM>();
         const int N = d.N;
         OCPQP_TICK(c, DBG_S_PRE);
+        // ---- per-stage operand staging (global -> smem, one stage ahead) ----
+        double* pvs = vec + NW + NX;            // NX: pv_{n+1} of the sweep
+        double* xv = pvs + NX;                  // NX: x_n in the forward sweep
+        double* uv = xv + NX;                   // NU: u_n in the forward sweep
+        double* SB = vec + S::VEC;              // 2 x HALF
+        const unsigned long long sm = p.smem_mask;
+        const bool gP = !((sm >> WS_P) & 1ull), gK = !((sm >> WS_K) & 1ull);
+        const bool gL = !((sm >> WS_L) & 1ull), gR = !((sm >> WS_RINV) & 1ull);
+        const bool gRB = !((sm >> WS_RB) & 1ull), gRH = !((sm >> WS_RHAT) & 1ull);
+        const bool gKF = !((sm >> WS_KFF) & 1ull);
+        const double* Rst = c.w[WS_RINV];
+        // half layout offsets
+        constexpr int oP = 0, oBA = NX * NX, oK = oBA + NX * NW, oL = oK + NU * NX, oR = oL + NU * NU;
+        constexpr int oRB = oR + NU, oRH = oRB + NX, oKF = oRH + NW;
+        const bool ss = S::STAGE_SOLVE && p.sstage;
+        auto issue = [&](int n, int h, bool bwd) {
+            if (ss) {
+                double* H = SB + h * S::HALF;
+                const double* An = A(c, n);
+                const double* Bn = Bm(c, n);
+                for (int e2 = tid; e2 < NX * NW; e2 += TEAM) {
+                    const int k = e2 / NW, j = e2 - k * NW;
+                    cpa8(H + oBA + e2, j < NU ? Bn + k * NU + j : An + k * NX + (j - NU));
+                }
+                if (gK) for (int e2 = tid; e2 < NU * NX; e2 += TEAM) cpa8(H + oK + e2, Kst + n * NU * NX + e2);
+                if (gRB) for (int e2 = tid; e2 < NX; e2 += TEAM) cpa8(H + oRB + e2, r_b + n * NX + e2);
+                if (bwd) {
+                    if (gP) for (int e2 = tid; e2 < NX * NX; e2 += TEAM) cpa8(H + oP + e2, Pst + (n + 1) * NX * NX + e2);
+                    if (gL) for (int e2 = tid; e2 < NU * NU; e2 += TEAM) cpa8(H + oL + e2, Lst + n * NU * NU + e2);
+                    if (gR) for (int e2 = tid; e2 < NU; e2 += TEAM) cpa8(H + oR + e2, Rst + n * NU + e2);
+                    if (gRH) for (int e2 = tid; e2 < NW; e2 += TEAM) cpa8(H + oRH + e2, rhat + n * NW + e2);
+                } else {
+                    if (gKF) for (int e2 = tid; e2 < NU; e2 += TEAM) cpa8(H + oKF + e2, kff + n * NU + e2);
+                }
+                cpa_commit();
+            }
+        };
         // backward sweep (kkt_ocp.py:276-289); terminal stage: nu = 0
-        for (int i = tid; i < NX; i += TEAM) pv[N * NX + i] = rhat[N * NW + i];
-        bar<TEAM>();
+        if (N > 0) issue(N - 1, (N - 1) & 1, true);
+        for (int i = tid; i < NX; i += TEAM) {
+            const double v = rhat[N * NW + i];
+            pv[N * NX + i] = v;
+            pvs[i] = v;
+        }
         for (int n = N - 1; n >= 0; --n) {
-            const double* Pn = Pst + (n + 1) * NX * NX;
-            const double* rb = r_b + n * NX;
-            const double* pvn = pv + (n + 1) * NX;
-            MV<NX, NX, TEAM>::run([&](int i, int k) { return Pn[i * NX + k]; },
-                                  [&](int k) { return rb[k]; },
-                                  [&](int i, double v) { e[i] = v + pvn[i]; });
+            const int h = n & 1;
+            if (n > 0) issue(n - 1, h ^ 1, true);
+            if (ss) {
+                if (n > 0) cpa_wait<1>(); else cpa_wait<0>();
+            }
             bar<TEAM>();
+            const double* H = SB + h * S::HALF;
+            const bool st = ss;
+            const double* Pn = (st && gP) ? H + oP : Pst + (n + 1) * NX * NX;
+            const double* rb = (st && gRB) ? H + oRB : r_b + n * NX;
+            const double* Kn = (st && gK) ? H + oK : Kst + n * NU * NX;
+            const double* Ln = (st && gL) ? H + oL : Lst + n * NU * NU;
+            const double* Rn = (st && gR) ? H + oR : Rst + n * NU;
+            const double* rh = (st && gRH) ? H + oRH : rhat + n * NW;
             const double* An = A(c, n);
             const double* Bn = Bm(c, n);
-            const double* rh = rhat + n * NW;
-            MV<NW, NX, TEAM>::run(
-                [&](int j, int k) { return j < NU ? Bn[k * NU + j] : An[k * NX + (j - NU)]; },
-                [&](int k) { return e[k]; },
-                [&](int j, double v) { win[j] = rh[j] + v; });
+            auto BA = [&](int k, int j) -> double {
+                return ss ? H[oBA + k * NW + j] : (j < NU ? Bn[k * NU + j] : An[k * NX + (j - NU)]);
+            };
+            MV<NX, NX, TEAM>::run([&](int i, int k) { return Pn[i * NX + k]; },
+                                  [&](int k) { return rb[k]; },
+                                  [&](int i, double v) { e[i] = v + pvs[i]; });
             bar<TEAM>();
-            const double* Kn = Kst + n * NU * NX;
+            MV<NW, NX, TEAM>::run([&](int j, int k) { return BA(k, j); },
+                                  [&](int k) { return e[k]; },
+                                  [&](int j, double v) { win[j] = rh[j] + v; });
+            bar<TEAM>();
             double* pvc = pv + n * NX;
             MV<NX, NU, TEAM>::run([&](int i, int k) { return Kn[k * NX + i]; },
                                   [&](int k) { return win[k]; },
-                                  [&](int i, double v) { pvc[i] = win[NU + i] + v; });
-            if (tid < 32) warp_cho_solve<NU>(Lst + n * NU * NU, c.w[WS_RINV] + n * NU, win, kff + n * NU, -1.0);
+                                  [&](int i, double v) {
+                                      const double r = win[NU + i] + v;
+                                      pvc[i] = r;
+                                      pvs[i] = r;
+                                  });
+            if (tid < 32) warp_cho_solve<NU>(Ln, Rn, win, kff + n * NU, -1.0);
             flops += 2ll * NU * NU;
             bar<TEAM>();
         }
         OCPQP_TICK(c, DBG_S_BWD);
+        if (N == 0) bar<TEAM>();
         // x0 step
-        if (tid < 32) warp_cho_solve<NX>(c.w[WS_LP0], c.w[WS_RINV] + N * NU, pv, dy + NU, -1.0);
+        if (tid < 32) warp_cho_solve<NX>(c.w[WS_LP0], Rst + N * NU, pvs, xv, -1.0);
         flops += 2ll * NX * NX;
+        if (N > 0) issue(0, 0, false);
         bar<TEAM>();
         // forward rollout (kkt_ocp.py:293-305)
         for (int n = 0; n < N; ++n) {
-            const double* xi = dy + n * NW + NU;
-            const double* Kn = Kst + n * NU * NX;
-            const double* kf = kff + n * NU;
-            double* du = dy + n * NW;
-            MV<NU, NX, TEAM>::run([&](int i, int k) { return Kn[i * NX + k]; },
-                                  [&](int k) { return xi[k]; },
-                                  [&](int i, double v) { du[i] = v + kf[i]; });
+            const int h = n & 1;
+            if (n + 1 < N) issue(n + 1, h ^ 1, false);
+            if (ss) {
+                if (n + 1 < N) cpa_wait<1>(); else cpa_wait<0>();
+            }
+            for (int i = tid; i < NX; i += TEAM) dy[n * NW + NU + i] = xv[i];
             bar<TEAM>();
+            const double* H = SB + h * S::HALF;
+            const bool st = ss;
+            const double* Kn = (st && gK) ? H + oK : Kst + n * NU * NX;
+            const double* kf = (st && gKF) ? H + oKF : kff + n * NU;
+            const double* rb = (st && gRB) ? H + oRB : r_b + n * NX;
             const double* An = A(c, n);
             const double* Bn = Bm(c, n);
-            const double* rb = r_b + n * NX;
-            double* xn = dy + (n + 1) * NW + (n + 1 < N ? NU : 0);
-            MV<NX, NW, TEAM>::run(
-                [&](int i, int k) { return k < NX ? An[i * NX + k] : Bn[i * NU + (k - NX)]; },
-                [&](int k) { return k < NX ? xi[k] : du[k - NX]; },
-                [&](int i, double v) { xn[i] = v + rb[i]; });
+            double* du = dy + n * NW;
+            MV<NU, NX, TEAM>::run([&](int i, int k) { return Kn[i * NX + k]; },
+                                  [&](int k) { return xv[k]; },
+                                  [&](int i, double v) {
+                                      const double u = v + kf[i];
+                                      du[i] = u;
+                                      uv[i] = u;
+                                  });
             bar<TEAM>();
+            MV<NX, NW, TEAM>::run(
+                [&](int i, int k) {
+                    if (ss) return k < NX ? H[oBA + i * NW + NU + k] : H[oBA + i * NW + (k - NX)];
+                    return k < NX ? An[i * NX + k] : Bn[i * NU + (k - NX)];
+                },
+                [&](int k) { return k < NX ? xv[k] : uv[k - NX]; },
+                [&](int i, double v) { e[i] = v + rb[i]; });
+            bar<TEAM>();
+            for (int i = tid; i < NX; i += TEAM) xv[i] = e[i];
         }
+        for (int i = tid; i < NX; i += TEAM) dy[N * NW + i] = xv[i];
+        bar<TEAM>();
         OCPQP_TICK(c, DBG_S_FWD);
         // dpi_n = P_{n+1} x_{n+1} + pv_{n+1}, all stages in parallel
+        #pragma unroll 4
         for (int e2 = tid; e2 < d.ne; e2 += TEAM) {
             const int n = e2 / NX;
             const int i = e2 - n * NX;
@@ -880,12 +1037,14 @@ struct Kern {
             dpi[e2] = v;
             if (!isfinite(v)) nonfinite = 1;
         }
+        #pragma unroll 4
         for (int j = tid; j < d.nv; j += TEAM)
             if (!isfinite(dy[j])) nonfinite = 1;
         // recover_block (kkt_common.py:140-163)
         double* rowv = c.w[WS_ROWV];
         rows_values(c, d, p.idxb, dy, rowv);
         bar<TEAM>();
+        #pragma unroll 4
         for (int k = tid; k < d.nc; k += TEAM) {
             double dl = 0.0, dtt = 0.0;
             if (!isnan(act[k])) {
@@ -906,6 +1065,7 @@ struct Kern {
                                       const double* dlam, const double* dt, double ftb) {
         const double* act = c.w[WS_DVEC];  // NaN = inactive
         double ratio = INFINITY;
+        #pragma unroll 4
         for (int k = threadIdx.x; k < d.nc; k += TEAM) {
             if (!isnan(act[k])) {
                 if (dlam[k] < 0.0) ratio = fmin(ratio, -lam[k] / dlam[k]);
@@ -920,6 +1080,7 @@ struct Kern {
                                       const double* dlam, const double* dt, double alpha) {
         const double* act = c.w[WS_DVEC];  // NaN = inactive
         double s = 0.0;
+        #pragma unroll 4
         for (int k = threadIdx.x; k < d.nc; k += TEAM)
             if (!isnan(act[k])) s += (lam[k] + alpha * dlam[k]) * (t[k] + alpha * dt[k]);
         s = tsum<TEAM>(s, c.red);
@@ -944,8 +1105,11 @@ struct Kern {
         setup(c, d);
         // initial iterate (solver.py:113-142)
         const int warm = arg.warm_start;
+        #pragma unroll 4
         for (int i = tid; i < d.nv; i += TEAM) y[i] = warm ? gy[i] : 0.0;
+        #pragma unroll 4
         for (int i = tid; i < d.ne; i += TEAM) pi[i] = warm == 2 ? gpi[i] : 0.0;
+        #pragma unroll 4
         for (int k = tid; k < d.nc; k += TEAM) lam[k] = warm == 2 ? glam[k] : 0.0;
         bar<TEAM>();
         {
@@ -959,8 +1123,10 @@ struct Kern {
             }
             if (warm == 2) {
                 double gd = 0.0, gb = 0.0;
+                #pragma unroll 4
                 for (int k = tid; k < d.nc; k += TEAM)
                     if (!isnan(act[k])) gd = fmax(gd, dvec[k] - slot_cy(d, k, rowv));
+                #pragma unroll 4
                 for (int e = tid; e < d.ne; e += TEAM) {
                     const int n = e / NX, i = e - n * NX;
                     const double* u = y + n * NW;
@@ -977,6 +1143,7 @@ struct Kern {
                 floor = fmax(fmax(1e-8, arg.t_min), fmin(1.0, fmax(gd, gb)));
             }
             const double lfloor = fmax(1e-8, arg.lam_min);
+            #pragma unroll 4
             for (int k = tid; k < d.nc; k += TEAM) {
                 double tv = 0.0, lv = 0.0;
                 if (!isnan(act[k])) {
@@ -1047,8 +1214,11 @@ struct Kern {
             if (nf) { status = OCPQP_STATUS_NAN; break; }
             const double alpha = max_step(c, d, lam, t, dlam, dt, arg.ftb);
             const double* act = c.w[WS_DVEC];  // NaN = inactive
+            #pragma unroll 4
             for (int i = tid; i < d.nv; i += TEAM) y[i] += alpha * dy[i];
+            #pragma unroll 4
             for (int i = tid; i < d.ne; i += TEAM) pi[i] += alpha * dpi[i];
+            #pragma unroll 4
             for (int k = tid; k < d.nc; k += TEAM) {
                 double lv = lam[k] + alpha * dlam[k];
                 double tv = t[k] + alpha * dt[k];
@@ -1070,8 +1240,11 @@ struct Kern {
             OCPQP_TICK(c, DBG_STEP);
         }
         bar<TEAM>();
+        #pragma unroll 4
         for (int i = tid; i < d.nv; i += TEAM) gy[i] = y[i];
+        #pragma unroll 4
         for (int i = tid; i < d.ne; i += TEAM) gpi[i] = pi[i];
+        #pragma unroll 4
         for (int k = tid; k < d.nc; k += TEAM) { glam[k] = lam[k]; gt[k] = t[k]; }
         if (tid == 0) {
             sp.status[q] = status;
@@ -1089,7 +1262,7 @@ struct Kern {
 };
 
 template <class S>
-__global__ void __launch_bounds__(S::TEAM) k_fast_solve(KParams p, SolveParams sp) {
+__global__ void __launch_bounds__(S::TEAM, S::MINB) k_fast_solve(KParams p, SolveParams sp) {
     extern __shared__ double smem[];
     __shared__ FCtx c;
     double* gslot = p.ws + (long long)blockIdx.x * p.ws_slot;
@@ -1115,7 +1288,7 @@ __global__ void __launch_bounds__(S::TEAM) k_fast_solve(KParams p, SolveParams s
 }
 
 template <class S>
-int stage_doubles() { return S::STAGE; }
+int stage_doubles(int sstage) { return sstage && S::STAGE_SOLVE ? S::STAGE : S::STAGE_NOSS; }
 
 template <class S>
 cudaError_t launch(const KParams& p, const SolveParams& sp, int grid, size_t smem, cudaStream_t st) {

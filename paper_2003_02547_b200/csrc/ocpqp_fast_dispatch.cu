@@ -12,7 +12,7 @@ cudaError_t launch(const KParams& p, const SolveParams& sp, int grid, size_t sme
 template <class S>
 int occupancy(size_t smem);
 template <class S>
-int stage_doubles();
+int stage_doubles(int sstage);
 }  // namespace fastk
 namespace rowk {
 template <int NX_, int NU_, int NG_, int NB_, int G_, int WPB_>
@@ -63,7 +63,7 @@ bool fast_supported(const FastShape& s) {
 int fast_teams_per_cta(const FastShape& s) { return s.kind == 1 ? (32 / s.team) * s.wpb : 1; }
 
 int fast_stage_smem_doubles(const FastShape& s) {
-#define X(a, b, c_, t) if (OCPQP_MATCH(a, b, c_, t)) return fastk::stage_doubles<fastk::Shape<a, b, c_, t>>();
+#define X(a, b, c_, t) if (OCPQP_MATCH(a, b, c_, t)) return fastk::stage_doubles<fastk::Shape<a, b, c_, t>>(s.sstage);
     OCPQP_FAST_SHAPES(X)
 #undef X
 #define X(a, b, c_, nb, g, w) \
