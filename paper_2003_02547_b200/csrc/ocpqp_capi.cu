@@ -373,7 +373,7 @@ bool detect_fast(OcpPlan* P) {
             // measured: staging pays where the stage operands are large and the
             // factor store cannot stay in shared memory (config 3); the smaller
             // shapes lose more occupancy / issue slots than they gain
-            pick.sstage = envs ? atoi(envs) : (NX * (NX + NU) >= 1000 ? 1 : 0);
+            pick.sstage = envs ? atoi(envs) : (NX * (NX + NU) >= 1000 ? 3 : 0);
         }
     }
     if (pick.kind < 0) return false;

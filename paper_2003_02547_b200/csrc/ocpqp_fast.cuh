@@ -159,6 +159,51 @@ __device__ __forceinline__ bool warp_chol(double (&row)[NN], int lane, double& r
     return true;
 }
 
+// Register Cholesky of the NN x NN leading block of G (row stride ld), computed
+// redundantly by every thread that needs it.  Left-looking; pivot test as
+// LAPACK potrf (linalg.py:81-118): a pivot that is not > 0 (or NaN) fails.
+// L_kk = piv * rsqrt(piv); ri[k] = 1 / L_kk.
+template <int NN>
+__device__ __forceinline__ bool reg_chol(const double* G, int ld, double (&L)[NN][NN], double (&ri)[NN]) {
+#pragma unroll
+    for (int k = 0; k < NN; ++k) {
+        double piv = G[k * ld + k];
+#pragma unroll
+        for (int m = 0; m < k; ++m) piv = fma(-L[k][m], L[k][m], piv);
+        if (!(piv > 0.0)) return false;
+        const double r = rsqrt(piv);
+        ri[k] = r;
+        L[k][k] = piv * r;
+#pragma unroll
+        for (int i = k + 1; i < NN; ++i) {
+            double a = G[i * ld + k];
+#pragma unroll
+            for (int m = 0; m < k; ++m) a = fma(-L[i][m], L[k][m], a);
+            L[i][k] = a * r;
+        }
+    }
+    return true;
+}
+
+// z <- (L L')^{-1} z with L, 1/L_ii in registers.
+template <int NN>
+__device__ __forceinline__ void reg_cho_solve(const double (&L)[NN][NN], const double (&ri)[NN], double (&z)[NN]) {
+#pragma unroll
+    for (int i = 0; i < NN; ++i) {
+        double a = z[i];
+#pragma unroll
+        for (int m = 0; m < i; ++m) a = fma(-L[i][m], z[m], a);
+        z[i] = a * ri[i];
+    }
+#pragma unroll
+    for (int i = NN - 1; i >= 0; --i) {
+        double a = z[i];
+#pragma unroll
+        for (int m = i + 1; m < NN; ++m) a = fma(-L[m][i], z[m], a);
+        z[i] = a * ri[i];
+    }
+}
+
 // Team Cholesky of an n x n matrix in place (lower; upper zeroed), any n.
 template <int TEAM>
 __device__ bool team_chol(double* L, int n, int* flag, double* rinv) {
@@ -233,15 +278,19 @@ __device__ __forceinline__ void cpa_wait() {
 // TM*TN (TM, TN <= 4) whose tile count fits the team -- minimal dependent
 // chain per thread when the team is wide, fewer loads per FMA when it is not.
 __host__ __device__ constexpr int gemm_pick(int M, int N, int TEAM) {
-    int best = 4 * 8 + 4;  // packed TM * 8 + TN; default 4 x 4
-    int best_sz = 1 << 30;
+    // per k step a thread issues TM*TN DFMAs (2 issue cycles each) and TM+TN
+    // operand loads, and waits at least one DFMA latency (~9 cycles); team
+    // passes run back to back: cost = passes x max(9, 2*TM*TN + TM + TN)
+    int best = 4 * 8 + 4;  // packed TM * 8 + TN
+    int best_cost = 1 << 30;
     for (int tm = 1; tm <= 4; ++tm)
-        for (int tn = 1; tn <= 4; ++tn) {
+        for (int tn = 1; tn <= 6; ++tn) {
             const int tiles = ((M + tm - 1) / tm) * ((N + tn - 1) / tn);
-            const int sz = tm * tn;
-            if (tiles <= TEAM && (sz < best_sz || (sz == best_sz && tn > (best & 7)))) {
+            const int per = 2 * tm * tn + tm + tn;
+            const int cost = ((tiles + TEAM - 1) / TEAM) * (per > 9 ? per : 9);
+            if (cost < best_cost || (cost == best_cost && tm * tn < (best / 8) * (best & 7))) {
                 best = tm * 8 + tn;
-                best_sz = sz;
+                best_cost = cost;
             }
         }
     return best;
@@ -325,6 +374,9 @@ struct Shape {
     // resident CTAs per SM the register allocation must allow (latency hiding
     // across QPs): 512 threads per SM
     static constexpr int MINB = TEAM >= 512 ? 1 : 512 / TEAM;
+    // small input dimension: every thread factors G_uu in registers (no warp
+    // Cholesky / flag round trip) and the sweeps fuse their per-stage steps
+    static constexpr bool SMALL = NU <= 4;
 };
 
 template <class S>
@@ -586,6 +638,27 @@ struct Kern {
         }
         bar<TEAM>();
         const int N = d.N;
+        // stage data prefetch (cp.async, one stage ahead): [B A]_n, Q_n, S_n, R_n
+        const bool fpf = S::STAGE_SOLVE && (p.sstage & 2);
+        double* FB = vec + S::VEC;
+        constexpr int fQ = NX * NW, fS = fQ + NX * NX, fR = fS + NU * NX;
+        auto prefetch = [&](int n, int h) {
+            double* H = FB + h * S::HALF;
+            const double* An = A(c, n);
+            const double* Bn = Bm(c, n);
+            const double* Qn = Q(c, n);
+            const double* Sn = Sm(c, n);
+            const double* Rn = R(c, n);
+            for (int e2 = tid; e2 < NX * NW; e2 += TEAM) {
+                const int k = e2 / NW, j = e2 - k * NW;
+                cpa8(H + e2, j < NU ? Bn + k * NU + j : An + k * NX + (j - NU));
+            }
+            for (int e2 = tid; e2 < NX * NX; e2 += TEAM) cpa8(H + fQ + e2, Qn + e2);
+            for (int e2 = tid; e2 < NU * NX; e2 += TEAM) cpa8(H + fS + e2, Sn + e2);
+            for (int e2 = tid; e2 < NU * NU; e2 += TEAM) cpa8(H + fR + e2, Rn + e2);
+            cpa_commit();
+        };
+        if (fpf) prefetch(N - 1, (N - 1) & 1);
         // ---- terminal stage: P_N = sym(M~_N) ----
         {
             const int n = N;
@@ -624,8 +697,18 @@ struct Kern {
             OCPQP_TICK(c, DBG_F_P);
             const double* An = A(c, n);
             const double* Bn = Bm(c, n);
+            double* H = FB + (n & 1) * S::HALF;
+            if (fpf) {
+                if (n > 0) {
+                    prefetch(n - 1, (n & 1) ^ 1);
+                    cpa_wait<1>();
+                } else {
+                    cpa_wait<0>();
+                }
+                bar<TEAM>();
+            }
             // stage [B A] (kkt_ocp.py:177) in shared memory
-            if constexpr (S::STAGE_BA) {
+            else if constexpr (S::STAGE_BA) {
                 TEAM_FOR(e, NX * NW)
                     const int k = e / NW, j = e - k * NW;
                     BAs[e] = j < NU ? Bn[k * NU + j] : An[k * NX + (j - NU)];
@@ -633,6 +716,7 @@ struct Kern {
                 bar<TEAM>();
             }
             auto BA = [&](int k, int j) -> double {
+                if (fpf) return H[k * NW + j];
                 if constexpr (S::STAGE_BA) return BAs[k * NW + j];
                 else return j < NU ? Bn[k * NU + j] : An[k * NX + (j - NU)];
             };
@@ -644,9 +728,9 @@ struct Kern {
             OCPQP_TICK(c, DBG_F_T1);
             // G = [B A]' T1 + M~ (kkt_ocp.py:233, 70-80; kkt_common.py:100-115):
             // input rows -> Gu (NU x NW), G_xx -> Pc (P_{n+1} is dead after T1)
-            const double* Qn = Q(c, n);
-            const double* Rn = R(c, n);
-            const double* Sn = Sm(c, n);
+            const double* Qn = fpf ? H + fQ : Q(c, n);
+            const double* Rn = fpf ? H + fR : R(c, n);
+            const double* Sn = fpf ? H + fS : Sm(c, n);
             const double* cf = coef + n * d.M;
             const bool full_box = d.NB == NW;
             auto Mt = [&](int i, int j) -> double {
@@ -683,6 +767,39 @@ struct Kern {
             // L_uu = chol(G_uu)
             double* Ln = Lst + n * NU * NU;
             double* Rinv_n = c.w[WS_RINV] + n * NU;
+            double* Kn = Kst + n * NU * NX;
+            if constexpr (S::SMALL) {
+                // every thread factors G_uu in registers; thread j < NX solves
+                // column j of K = -L'^{-1} L^{-1} G_ux (kkt_ocp.py:237-243)
+                double Lr[NU][NU], ri[NU];
+                const bool ok = reg_chol<NU>(Gu, NW, Lr, ri);
+                flops += (long long)NU * NU * NU / 3;
+                if (!ok) {
+                    if (fpf) cpa_wait<0>();
+                    return n;
+                }
+                if (tid < NX) {
+                    double z[NU];
+#pragma unroll
+                    for (int i = 0; i < NU; ++i) z[i] = Gu[i * NW + NU + tid];
+                    reg_cho_solve<NU>(Lr, ri, z);
+#pragma unroll
+                    for (int i = 0; i < NU; ++i) {
+                        Kn[i * NX + tid] = -z[i];
+                    }
+                }
+                if (tid == 0) {
+#pragma unroll
+                    for (int i = 0; i < NU; ++i) {
+                        Rinv_n[i] = ri[i];
+#pragma unroll
+                        for (int j = 0; j < NU; ++j) Ln[i * NU + j] = j <= i ? Lr[i][j] : 0.0;
+                    }
+                }
+                flops += 2ll * NU * NU * NX;
+                bar<TEAM>();
+            } else {
+
             double* rinv = vec;  // NU
             flops += (long long)NU * NU * NU / 3;
             if constexpr (NU <= 32) {
@@ -701,20 +818,25 @@ struct Kern {
                     }
                 }
                 bar<TEAM>();
-                if (!c.flag) return n;
+                if (!c.flag) {
+                    if (fpf) cpa_wait<0>();
+                    return n;
+                }
             } else {
                 for (int idx = tid; idx < NU * NU; idx += TEAM) {
                     const int i = idx / NU, j = idx - i * NU;
                     Ln[idx] = Gu[i * NW + j];
                 }
                 bar<TEAM>();
-                if (!team_chol<TEAM>(Ln, NU, &c.flag, rinv)) return n;
+                if (!team_chol<TEAM>(Ln, NU, &c.flag, rinv)) {
+                    if (fpf) cpa_wait<0>();
+                    return n;
+                }
                 for (int i = tid; i < NU; i += TEAM) Rinv_n[i] = rinv[i];
                 bar<TEAM>();
             }
             OCPQP_TICK(c, DBG_F_CHOL);
             // K = -L'^{-1} L^{-1} G_ux (kkt_ocp.py:240-243), one column per thread
-            double* Kn = Kst + n * NU * NX;
             for (int j = tid; j < NX; j += TEAM) {
                 if constexpr (NU <= 32) {
                     double z[NU];
@@ -750,6 +872,7 @@ struct Kern {
             }
             flops += 2ll * NU * NU * NX;
             bar<TEAM>();
+            }
             OCPQP_TICK(c, DBG_F_K);
             // P = G_xx + G_ux' K, symmetrised (kkt_ocp.py:244, 251)
             tile_gemm<NX, NX, NU, TEAM>([&](int i, int k) { return Gu[k * NW + NU + i]; },
@@ -908,7 +1031,7 @@ struct Kern {
         // half layout offsets
         constexpr int oP = 0, oBA = NX * NX, oK = oBA + NX * NW, oL = oK + NU * NX, oR = oL + NU * NU;
         constexpr int oRB = oR + NU, oRH = oRB + NX, oKF = oRH + NW;
-        const bool ss = S::STAGE_SOLVE && p.sstage;
+        const bool ss = S::STAGE_SOLVE && (p.sstage & 1);
         auto issue = [&](int n, int h, bool bwd) {
             if (ss) {
                 double* H = SB + h * S::HALF;
