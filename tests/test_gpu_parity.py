@@ -282,3 +282,41 @@ def test_gpu_warm_start_not_slower(cuda, speed_arg):
     ci = cold.iterations.cpu().numpy()
     assert np.all(warm.status_code.cpu().numpy() == 0)
     assert np.all(wi <= ci)
+
+
+# ------------------------------------------- shaped kernel on random structure
+FAST_SHAPES = [(8, 3, 0), (24, 4, 0), (30, 10, 10)]
+
+
+@pytest.mark.parametrize("nx,nu,ng", FAST_SHAPES)
+@pytest.mark.parametrize("seed,N,nb,inf_side,mask_last",
+                         [(11, 1, 5, True, True), (12, 7, 4, True, False), (13, 12, 2, False, True),
+                          (17, 20, 200, True, True), (15, 3, 0, False, False)])
+def test_gpu_shaped_kernel_random_structure(cuda, oracle, speed_arg, nx, nu, ng, seed, N, nb,
+                                            inf_side, mask_last):
+    """The compile-time-shaped team kernel on structure the configs never hit:
+    box subsets with per-stage idxb, one-sided rows (inf bound), masked sides,
+    no boxes at all, horizons 1..20, general rows with a terminal block."""
+    import qpgen
+
+    # A scaled to spectral radius ~0.9 so long horizons stay well conditioned
+    # (a diverging MaxIter run amplifies rounding beyond any fixed tolerance)
+    dims, stages, dyn = qpgen.random_ocp_fields(seed, N=N, nx=nx, nu=nu, nb=nb, ng=ng, ns=0,
+                                                inf_side=inf_side, mask_last=mask_last,
+                                                decay=0.9 / np.sqrt(nx))
+    batch = OcpQpBatch.from_qps([qpgen.build_qp(pkg, dims, stages, dyn)])
+    use_kind("auto")
+    assert S.get_plan(batch).info()["kernel"] == "team"
+    arg = pkg.mode_preset("speed").with_tol(1e-6)
+    got = host(solve_ocp_qp_batch(batch, arg))
+    ref = oracle.solve(batch, arg)
+    if ref["status"][0] == 4:
+        # classical-Riccati breakdown (Failure after the regularised retry):
+        # rounding-borderline -- the stage and iteration of the breakdown
+        # differ even between the reference and its C restatement (SURVEY
+        # §8(d) "borderline" class), so only the status is compared
+        assert got["status"][0] == 4
+        return
+    assert_parity(got, ref, allow_lam_frac=1.0 if ng else 0.0)
+    if ng:  # lam: bounded like the config-3 known-hard row
+        assert rel_err(got["lam"][0], ref["lam"][0]) <= 1e-6
