@@ -155,7 +155,19 @@ def ptr_of(x):
 
 
 def data_c(batch):
-    """OcpQpDataC of a packed batch (fields: torch tensors or numpy arrays)."""
+    """OcpQpDataC of a packed batch (fields: torch tensors or numpy arrays).
+
+    Cached on the batch while its field objects are unchanged."""
+    sig = tuple((name, id(arr), ptr_of(arr)) for name, arr in batch.fields.items())
+    cached = getattr(batch, "_datac", None)
+    if cached is not None and cached[0] == sig:
+        return cached[1]
+    d = _data_c(batch)
+    batch._datac = (sig, d)
+    return d
+
+
+def _data_c(batch):
     d = OcpQpDataC()
     lay = batch.layout
     for i, name in enumerate(FIELD_ORDER):

@@ -84,8 +84,13 @@ class OcpQpBatch:
         return (np.concatenate(self.idxs) if self.idxs else np.zeros(0)).astype(np.int32)
 
     def structure_key(self):
-        return (self.dim.key(), tuple(self.idxb_concat().tolist()),
-                tuple(self.idxs_concat().tolist()))
+        # idxb / idxs are fixed at construction; the key is cached
+        key = getattr(self, "_skey", None)
+        if key is None:
+            key = (self.dim.key(), tuple(self.idxb_concat().tolist()),
+                   tuple(self.idxs_concat().tolist()))
+            self._skey = key
+        return key
 
     # -- conversions -----------------------------------------------------------
     def to(self, device):

@@ -623,6 +623,19 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     return OCPQP_OK;
 }
 
+// Device-side address of a page-locked (pinned or registered) host buffer,
+// nullptr for pageable / device / NULL pointers.
+static void* mapped_host(void* p) {
+    if (!p) return nullptr;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (at.type != cudaMemoryTypeHost || !at.devicePointer) return nullptr;
+    return at.devicePointer;
+}
+
 int ocpqp_solve_host(OcpPlan* P, const OcpQpDataC* hd, const OcpIpmArgC* arg, OcpIterC* hit,
                      OcpStatsC* hst, void* stream_) {
     if (!P || !hd || !hit || !hst) return fail(OCPQP_E_ARG, "NULL argument");
@@ -671,8 +684,30 @@ int ocpqp_solve_host(OcpPlan* P, const OcpQpDataC* hd, const OcpIpmArgC* arg, Oc
     }
     OcpIterC di{P->hy, P->hpi, P->hlam, P->ht};
     OcpStatsC ds{P->hstatus, P->hiters, P->hres, (int64_t*)P->hflops, hst->trace ? P->htrace : nullptr};
+    // Page-locked result buffers are written by the kernel directly (mapped
+    // host memory): each QP stores its solution and statistics when it
+    // finishes, overlapping the transfer with the QPs still iterating instead
+    // of a device->host copy after the slowest one.
+    void* my = mapped_host(hit->y);
+    void* mpi = mapped_host(hit->pi);
+    void* mlam = mapped_host(hit->lam);
+    void* mt = mapped_host(hit->t);
+    void* mst = mapped_host(hst->status);
+    void* mit = mapped_host(hst->iterations);
+    void* mres = mapped_host(hst->res);
+    void* mfl = mapped_host(hst->flops);
+    const bool direct = my && mpi && mlam && mt && mst && mit && mres && mfl && !hst->trace &&
+                        arg->warm_start == 0 && !getenv("OCPQP_NO_MAPPED");
+    if (direct) {
+        di = OcpIterC{(double*)my, (double*)mpi, (double*)mlam, (double*)mt};
+        ds = OcpStatsC{(int32_t*)mst, (int32_t*)mit, (double*)mres, (int64_t*)mfl, nullptr};
+    }
     rc = ocpqp_solve(P, &dd, arg, &di, &ds, stream);
     if (rc) return rc;
+    if (direct) {
+        CUDA_TRY(cudaStreamSynchronize(stream));
+        return OCPQP_OK;
+    }
     if (hit->y) CUDA_TRY(cudaMemcpyAsync(hit->y, P->hy, sizeof(double) * B * L.ny, cudaMemcpyDeviceToHost, stream));
     if (hit->pi) CUDA_TRY(cudaMemcpyAsync(hit->pi, P->hpi, sizeof(double) * B * L.ne, cudaMemcpyDeviceToHost, stream));
     if (hit->lam) CUDA_TRY(cudaMemcpyAsync(hit->lam, P->hlam, sizeof(double) * B * L.nc, cudaMemcpyDeviceToHost, stream));

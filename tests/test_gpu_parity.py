@@ -197,6 +197,31 @@ def test_gpu_host_buffer_path_matches_device_path(cuda, speed_arg):
     assert np.array_equal(a["iters"], b.iterations)
 
 
+def test_gpu_host_path_pinned_outputs_written_by_kernel(cuda, speed_arg):
+    """Page-locked result buffers are written directly by the kernel (mapped
+    host memory, no device->host copy); results equal the device path."""
+    import torch
+
+    batch = make_batch(2, batch=40)
+    lay = batch.layout
+    B = batch.B
+    a = host(solve_ocp_qp_batch(batch, speed_arg, trace=False))
+    out = dict(y=torch.full((B, lay.ny), np.nan, dtype=torch.float64).pin_memory(),
+               pi=torch.full((B, lay.ne), np.nan, dtype=torch.float64).pin_memory(),
+               lam=torch.full((B, lay.nc), np.nan, dtype=torch.float64).pin_memory(),
+               t=torch.full((B, lay.nc), np.nan, dtype=torch.float64).pin_memory(),
+               status=torch.full((B,), -7, dtype=torch.int32).pin_memory(),
+               iters=torch.zeros(B, dtype=torch.int32).pin_memory(),
+               res=torch.zeros((B, 5), dtype=torch.float64).pin_memory(),
+               flops=torch.zeros(B, dtype=torch.int64).pin_memory(), trace=None)
+    pkg.solve_ocp_qp_host(batch.pin_memory(), speed_arg, out=out)
+    for k in ("y", "pi", "lam", "t"):
+        assert np.array_equal(a[k], out[k].numpy()), k
+    assert np.array_equal(a["iters"], out["iters"].numpy())
+    assert np.array_equal(a["status"], out["status"].numpy())
+    assert np.array_equal(a["flops"], out["flops"].numpy())
+
+
 def test_gpu_drop_in_single_solve(cuda, speed_arg, golden):
     g = golden("solve_cfg")
     qp = make_batch(1, batch=1, start=3).qp(0)
