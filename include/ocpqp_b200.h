@@ -209,7 +209,9 @@ int ocpqp_factor_export(OcpPlan* plan, int32_t qp, double* P_out, double* K_out)
 
 /* Plan introspection: out[0..4] = threads per CTA, resident CTA slots,
  * dynamic shared memory bytes per CTA, shared-memory buffer mask, workspace
- * doubles per slot. */
+ * doubles per slot; out[5] kernel kind (0 generic, 1 team, 2 row), out[6]
+ * lanes per QP, out[7] grid; out[8] (if out_len >= 9) 1 when the team kernel
+ * keeps its factor store at fixed shared-memory offsets. */
 int ocpqp_plan_info(const OcpPlan* plan, int64_t* out, int32_t out_len);
 
 /* ---- partial condensing (reference condensing.py:451-619) ----

@@ -194,12 +194,12 @@ class Plan:
         self.handle = h
 
     def info(self):
-        out = (ctypes.c_int64 * 8)()
-        check(lib().ocpqp_plan_info(self.handle, out, 8))
+        out = (ctypes.c_int64 * 9)()
+        check(lib().ocpqp_plan_info(self.handle, out, 9))
         kind = {0: "generic", 1: "team", 2: "row"}[int(out[5])]
         return dict(kernel=kind, threads_per_cta=out[0], slots=out[1], smem_bytes=out[2],
                     smem_mask=out[3], ws_doubles_per_slot=out[4], lanes_per_qp=out[6],
-                    grid=out[7])
+                    grid=out[7], store_in_smem=bool(out[8]))
 
     def close(self):
         if getattr(self, "handle", None):

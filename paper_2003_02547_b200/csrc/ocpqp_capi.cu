@@ -305,7 +305,6 @@ void fill_kparams(const OcpPlan* P, KParams& k, const OcpQpDataC* data, bool use
     k.counter = P->d_counter;
     k.NB = P->NB; k.NBN = P->NBN; k.NGN = P->NGN;
     k.stage_smem = P->stage_smem;
-    k.sstage = P->shape.sstage;
     k.team_stride = P->team_stride;
     k.dbg = P->dbg;
 }
@@ -369,11 +368,13 @@ bool detect_fast(OcpPlan* P) {
         }
         if (team) {
             pick = FastShape{0, NX, NU, NG, NB, team, 1};
-            const char* envs = getenv("OCPQP_SSTAGE");
-            // measured: staging pays where the stage operands are large and the
-            // factor store cannot stay in shared memory (config 3); the smaller
-            // shapes lose more occupancy / issue slots than they gain
-            pick.sstage = envs ? atoi(envs) : (NX * (NX + NU) >= 1000 ? 3 : 0);
+            // the variant with the factor store at fixed shared-memory offsets
+            // (Shape<..., SM=1>) is used when instantiated and requested;
+            // measured no faster than generic addressing on config 1
+            FastShape sm = pick;
+            sm.sm = 1;
+            const char* envm = getenv("OCPQP_SM");
+            if (envm && atoi(envm) == 1 && fast_supported(sm)) pick = sm;
         }
     }
     if (pick.kind < 0) return false;
@@ -428,7 +429,25 @@ void place_fast(OcpPlan* P, long long budget_per_cta) {
 
 // Plan the shaped kernel: choose a shared-memory budget so that the CTAs the
 // batch needs can be resident, check occupancy, and size the slot count.
+bool plan_fast_once(OcpPlan* P, int* occ_out);
+
+// Buffers the SM variant of the team kernel addresses at fixed shared offsets.
+static const int kSmRequired[] = {WS_P, WS_K, WS_L, WS_LP0, WS_RINV, WS_PV, WS_KFF, WS_RB, WS_RHAT};
+
 bool plan_fast(OcpPlan* P, int* occ_out) {
+    if (P->shape.kind == 0 && P->shape.sm) {
+        if (plan_fast_once(P, occ_out)) {
+            bool ok = true;
+            for (int b : kSmRequired)
+                if (P->L.ws_size[b] > 0 && !((P->smem_mask >> b) & 1ull)) ok = false;
+            if (ok) return true;
+        }
+        P->shape.sm = 0;
+    }
+    return plan_fast_once(P, occ_out);
+}
+
+bool plan_fast_once(OcpPlan* P, int* occ_out) {
     const int teams = fast_teams_per_cta(P->shape);
     const int ctas_needed = (P->B + teams - 1) / teams;
     int per_sm = std::max(1, (ctas_needed + P->num_sms - 1) / P->num_sms);
@@ -589,6 +608,7 @@ int ocpqp_plan_info(const OcpPlan* P, int64_t* out, int32_t out_len) {
     out[5] = P->fast ? 1 + P->shape.kind : 0;   /* 0 generic, 1 team kernel, 2 row kernel */
     out[6] = P->fast ? P->shape.team : P->threads;
     out[7] = P->grid;
+    if (out_len >= 9) out[8] = P->fast && P->shape.kind == 0 ? P->shape.sm : 0;
     return OCPQP_OK;
 }
 

@@ -25,6 +25,9 @@
 namespace ocpqp {
 namespace fastk {
 
+// the dynamic shared-memory window (aliases the kernel's extern smem array)
+extern __shared__ double ocpqp_dsmem[];
+
 constexpr unsigned FULL = 0xffffffffu;
 
 template <int TEAM>
@@ -354,9 +357,13 @@ struct RD {
     }
 };
 
-template <int NX_, int NU_, int NG_, int TEAM_>
+template <int NX_, int NU_, int NG_, int TEAM_, int SM_ = 0>
 struct Shape {
     static constexpr int NX = NX_, NU = NU_, NG = NG_, TEAM = TEAM_, NW = NU_ + NX_;
+    // SM: the factor store (P, K, L, L_P0, 1/L_ii), p, k and the sweep RHS
+    // vectors (r_b, r^) are guaranteed shared-memory resident by the plan and
+    // addressed through the shared window (32-bit LDS/STS, no generic loads)
+    static constexpr bool SM = SM_ != 0;
     static constexpr int T1N = NX * (NW > NX ? NW : NX);
     static constexpr int VEC = 2 * NW + 3 * NX + 2 * NU + 16;
     // [B A] is staged in shared memory for small / medium stages only; large
@@ -369,8 +376,11 @@ struct Shape {
     static constexpr int SOLVE_BUF = STAGE_SOLVE ? 2 * HALF : 0;
     static constexpr int BA_BUF = STAGE_BA ? NX * NW : 0;
     static constexpr int STAGE0 = NX * NX + T1N + NU * NW + VEC;
-    static constexpr int STAGE = STAGE0 + (BA_BUF > SOLVE_BUF ? BA_BUF : SOLVE_BUF);  // staging on
-    static constexpr int STAGE_NOSS = STAGE0 + BA_BUF;                                // staging off
+    // cp.async staging (bit 1: solve-sweep operands, bit 2: factor stage data):
+    // measured to pay only where the stage operands are large (config 3); on
+    // the small shapes the bigger tile costs more occupancy than it saves
+    static constexpr int SSTAGE = (STAGE_SOLVE && NX * NW >= 1000) ? 3 : 0;
+    static constexpr int STAGE = STAGE0 + (SSTAGE ? (BA_BUF > SOLVE_BUF ? BA_BUF : SOLVE_BUF) : BA_BUF);
     // resident CTAs per SM the register allocation must allow (latency hiding
     // across QPs): 512 threads per SM
     static constexpr int MINB = TEAM >= 512 ? 1 : 512 / TEAM;
@@ -382,6 +392,13 @@ struct Shape {
 template <class S>
 struct Kern {
     static constexpr int NX = S::NX, NU = S::NU, NG = S::NG, NW = S::NW, TEAM = S::TEAM;
+
+    // workspace buffer b: shared window when the plan guarantees residency (SM)
+    template <int B>
+    __device__ static __forceinline__ double* wsb(const FCtx& c, const KParams& p) {
+        if constexpr (S::SM) return ocpqp_dsmem + p.smem_off[B];
+        else return c.w[B];
+    }
 
     // ---- field access (uniform-stage formula offsets) ----
     __device__ static __forceinline__ const double* A(const FCtx& c, int n) { return c.f[OCPQP_F_A] + n * NX * NX; }
@@ -605,9 +622,9 @@ struct Kern {
         const double* act = c.w[WS_DVEC];  // NaN = inactive
         double* gam = c.w[WS_GAM];
         double* coef = c.w[WS_COEF];
-        double* Pst = c.w[WS_P];
-        double* Kst = c.w[WS_K];
-        double* Lst = c.w[WS_L];
+        double* Pst = wsb<WS_P>(c, p);
+        double* Kst = wsb<WS_K>(c, p);
+        double* Lst = wsb<WS_L>(c, p);
         double* Pc = stg;                       // NX*NX: P_{n+1}, then G_xx / P_n
         double* T1 = Pc + NX * NX;              // NX*NW
         double* Gu = T1 + S::T1N;               // NU*NW
@@ -639,7 +656,7 @@ struct Kern {
         bar<TEAM>();
         const int N = d.N;
         // stage data prefetch (cp.async, one stage ahead): [B A]_n, Q_n, S_n, R_n
-        const bool fpf = S::STAGE_SOLVE && (p.sstage & 2);
+        constexpr bool fpf = (S::SSTAGE & 2) != 0;
         double* FB = vec + S::VEC;
         constexpr int fQ = NX * NW, fS = fQ + NX * NX, fR = fS + NU * NX;
         auto prefetch = [&](int n, int h) {
@@ -766,7 +783,7 @@ struct Kern {
             OCPQP_TICK(c, DBG_F_G);
             // L_uu = chol(G_uu)
             double* Ln = Lst + n * NU * NU;
-            double* Rinv_n = c.w[WS_RINV] + n * NU;
+            double* Rinv_n = wsb<WS_RINV>(c, p) + n * NU;
             double* Kn = Kst + n * NU * NX;
             if constexpr (S::SMALL) {
                 // every thread factors G_uu in registers; thread j < NX solves
@@ -891,7 +908,7 @@ struct Kern {
         }
         OCPQP_TICK(c, DBG_F_P);
         // L_P0 = chol(P_0) (kkt_ocp.py:193-200)
-        double* LP0 = c.w[WS_LP0];
+        double* LP0 = wsb<WS_LP0>(c, p);
         flops += (long long)NX * NX * NX / 3;
         if constexpr (NX <= 32) {
             if (tid < 32) {
@@ -904,7 +921,7 @@ struct Kern {
                 if (ok && tid < NX) {
 #pragma unroll
                     for (int j = 0; j < NX; ++j) LP0[tid * NX + j] = j <= tid ? row[j] : 0.0;
-                    c.w[WS_RINV][N * NU + tid] = rin;
+                    wsb<WS_RINV>(c, p)[N * NU + tid] = rin;
                 }
             }
             bar<TEAM>();
@@ -912,7 +929,7 @@ struct Kern {
         } else {
             for (int idx = tid; idx < NX * NX; idx += TEAM) LP0[idx] = Pc[idx];
             bar<TEAM>();
-            if (!team_chol<TEAM>(LP0, NX, &c.flag, c.w[WS_RINV] + N * NU)) return 0;
+            if (!team_chol<TEAM>(LP0, NX, &c.flag, wsb<WS_RINV>(c, p) + N * NU)) return 0;
         }
         return -1;
     }
@@ -920,7 +937,7 @@ struct Kern {
     // warp-0 cho_solve of an n-vector: x <- (L L')^{-1} x, L row-major n x n.
     // Right-looking: one broadcast per step.  Result written to out[] (scaled by sgn).
     template <int NN>
-    __device__ static void warp_cho_solve(const double* L, const double* rv, const double* xin,
+    __device__ static __forceinline__ void warp_cho_solve(const double* L, const double* rv, const double* xin,
                                           double* out, double sgn) {
         const int lane = threadIdx.x;
         if constexpr (NN <= 32) {
@@ -967,17 +984,17 @@ struct Kern {
         const double* act = c.w[WS_DVEC];  // NaN = inactive
         const double* gam = c.w[WS_GAM];
         const double* r_g = c.w[WS_RG];
-        const double* r_b = c.w[WS_RB];
+        const double* r_b = wsb<WS_RB>(c, p);
         const double* r_d = c.w[WS_RD];
         double* wall = c.w[WS_WALL];
         const double* tinv = c.w[WS_TINV];
         double* crow = c.w[WS_CROW];
-        double* rhat = c.w[WS_RHAT];
-        const double* Pst = c.w[WS_P];
-        const double* Kst = c.w[WS_K];
-        const double* Lst = c.w[WS_L];
-        double* pv = c.w[WS_PV];
-        double* kff = c.w[WS_KFF];
+        double* rhat = wsb<WS_RHAT>(c, p);
+        const double* Pst = wsb<WS_P>(c, p);
+        const double* Kst = wsb<WS_K>(c, p);
+        const double* Lst = wsb<WS_L>(c, p);
+        double* pv = wsb<WS_PV>(c, p);
+        double* kff = wsb<WS_KFF>(c, p);
         double* vec = stg + NX * NX + S::T1N + NU * NW;
         double* win = vec;              // NW
         double* e = vec + NW;           // NX
@@ -1027,11 +1044,11 @@ struct Kern {
         const bool gL = !((sm >> WS_L) & 1ull), gR = !((sm >> WS_RINV) & 1ull);
         const bool gRB = !((sm >> WS_RB) & 1ull), gRH = !((sm >> WS_RHAT) & 1ull);
         const bool gKF = !((sm >> WS_KFF) & 1ull);
-        const double* Rst = c.w[WS_RINV];
+        const double* Rst = wsb<WS_RINV>(c, p);
         // half layout offsets
         constexpr int oP = 0, oBA = NX * NX, oK = oBA + NX * NW, oL = oK + NU * NX, oR = oL + NU * NU;
         constexpr int oRB = oR + NU, oRH = oRB + NX, oKF = oRH + NW;
-        const bool ss = S::STAGE_SOLVE && (p.sstage & 1);
+        constexpr bool ss = (S::SSTAGE & 1) != 0;
         auto issue = [&](int n, int h, bool bwd) {
             if (ss) {
                 double* H = SB + h * S::HALF;
@@ -1104,7 +1121,7 @@ struct Kern {
         OCPQP_TICK(c, DBG_S_BWD);
         if (N == 0) bar<TEAM>();
         // x0 step
-        if (tid < 32) warp_cho_solve<NX>(c.w[WS_LP0], Rst + N * NU, pvs, xv, -1.0);
+        if (tid < 32) warp_cho_solve<NX>(wsb<WS_LP0>(c, p), Rst + N * NU, pvs, xv, -1.0);
         flops += 2ll * NX * NX;
         if (N > 0) issue(0, 0, false);
         bar<TEAM>();
@@ -1411,7 +1428,7 @@ __global__ void __launch_bounds__(S::TEAM, S::MINB) k_fast_solve(KParams p, Solv
 }
 
 template <class S>
-int stage_doubles(int sstage) { return sstage && S::STAGE_SOLVE ? S::STAGE : S::STAGE_NOSS; }
+int stage_doubles() { return S::STAGE; }
 
 template <class S>
 cudaError_t launch(const KParams& p, const SolveParams& sp, int grid, size_t smem, cudaStream_t st) {

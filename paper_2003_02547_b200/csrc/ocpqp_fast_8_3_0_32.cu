@@ -6,6 +6,6 @@ namespace fastk {
 using S_8_3_0_32 = Shape<8,3,0,32>;
 template cudaError_t launch<S_8_3_0_32>(const KParams&, const SolveParams&, int, size_t, cudaStream_t);
 template int occupancy<S_8_3_0_32>(size_t);
-template int stage_doubles<S_8_3_0_32>(int);
+template int stage_doubles<S_8_3_0_32>();
 }  // namespace fastk
 }  // namespace ocpqp

@@ -5,14 +5,14 @@
 
 namespace ocpqp {
 namespace fastk {
-template <int NX_, int NU_, int NG_, int TEAM_>
+template <int NX_, int NU_, int NG_, int TEAM_, int SM_>
 struct Shape;
 template <class S>
 cudaError_t launch(const KParams& p, const SolveParams& sp, int grid, size_t smem, cudaStream_t st);
 template <class S>
 int occupancy(size_t smem);
 template <class S>
-int stage_doubles(int sstage);
+int stage_doubles();
 }  // namespace fastk
 namespace rowk {
 template <int NX_, int NU_, int NG_, int NB_, int G_, int WPB_>
@@ -36,22 +36,22 @@ int row_team_tile();
      s.team == (g_) && s.wpb == (w_))
 
 #define OCPQP_FAST_SHAPES(X) \
-    X(8, 3, 0, 32)           \
-    X(8, 3, 0, 64)           \
-    X(24, 4, 0, 64)          \
-    X(24, 4, 0, 128)         \
-    X(30, 10, 10, 128)       \
-    X(30, 10, 10, 64)        \
-    X(60, 20, 0, 256)        \
-    X(60, 20, 0, 128)        \
-    X(60, 100, 240, 256)
+    X(8, 3, 0, 32, 0)           \
+    X(8, 3, 0, 64, 0)           \
+    X(24, 4, 0, 64, 0)          \
+    X(24, 4, 0, 128, 0)         \
+    X(30, 10, 10, 128, 0)       \
+    X(30, 10, 10, 64, 0)        \
+    X(60, 20, 0, 256, 0)        \
+    X(60, 20, 0, 128, 0)        \
+    X(60, 100, 240, 256, 0)
 
 
-#define OCPQP_MATCH(nx_, nu_, ng_, team_) \
-    (s.kind == 0 && s.nx == (nx_) && s.nu == (nu_) && s.ng == (ng_) && s.team == (team_))
+#define OCPQP_MATCH(nx_, nu_, ng_, team_, sm_) \
+    (s.kind == 0 && s.nx == (nx_) && s.nu == (nu_) && s.ng == (ng_) && s.team == (team_) && s.sm == (sm_))
 
 bool fast_supported(const FastShape& s) {
-#define X(a, b, c_, t) if (OCPQP_MATCH(a, b, c_, t)) return true;
+#define X(a, b, c_, t, m) if (OCPQP_MATCH(a, b, c_, t, m)) return true;
     OCPQP_FAST_SHAPES(X)
 #undef X
 #define X(a, b, c_, nb, g, w) if (OCPQP_RMATCH(a, b, c_, nb, g, w)) return true;
@@ -63,7 +63,7 @@ bool fast_supported(const FastShape& s) {
 int fast_teams_per_cta(const FastShape& s) { return s.kind == 1 ? (32 / s.team) * s.wpb : 1; }
 
 int fast_stage_smem_doubles(const FastShape& s) {
-#define X(a, b, c_, t) if (OCPQP_MATCH(a, b, c_, t)) return fastk::stage_doubles<fastk::Shape<a, b, c_, t>>(s.sstage);
+#define X(a, b, c_, t, m) if (OCPQP_MATCH(a, b, c_, t, m)) return fastk::stage_doubles<fastk::Shape<a, b, c_, t, m>>();
     OCPQP_FAST_SHAPES(X)
 #undef X
 #define X(a, b, c_, nb, g, w) \
@@ -75,8 +75,8 @@ int fast_stage_smem_doubles(const FastShape& s) {
 
 cudaError_t launch_fast_solve(const FastShape& s, const KParams& p, const SolveParams& sp, int grid,
                               size_t smem, cudaStream_t stream) {
-#define X(a, b, c_, t) \
-    if (OCPQP_MATCH(a, b, c_, t)) return fastk::launch<fastk::Shape<a, b, c_, t>>(p, sp, grid, smem, stream);
+#define X(a, b, c_, t, m) \
+    if (OCPQP_MATCH(a, b, c_, t, m)) return fastk::launch<fastk::Shape<a, b, c_, t, m>>(p, sp, grid, smem, stream);
     OCPQP_FAST_SHAPES(X)
 #undef X
 #define X(a, b, c_, nb, g, w) \
@@ -88,7 +88,7 @@ cudaError_t launch_fast_solve(const FastShape& s, const KParams& p, const SolveP
 }
 
 int fast_occupancy(const FastShape& s, size_t smem) {
-#define X(a, b, c_, t) if (OCPQP_MATCH(a, b, c_, t)) return fastk::occupancy<fastk::Shape<a, b, c_, t>>(smem);
+#define X(a, b, c_, t, m) if (OCPQP_MATCH(a, b, c_, t, m)) return fastk::occupancy<fastk::Shape<a, b, c_, t, m>>(smem);
     OCPQP_FAST_SHAPES(X)
 #undef X
 #define X(a, b, c_, nb, g, w) \

@@ -78,7 +78,6 @@ struct KParams {
     int NB, NBN, NGN;         // box rows (n < N), box / general rows at N
     int stage_smem;           // doubles: offset of the per-stage scratch / per-team tile
     int team_stride;          // doubles of shared memory per team (row kernel)
-    int sstage;               // team kernel: solve-sweep operand staging on/off
     long long* dbg;           // optional [B, 8] phase-cycle counters (nullptr = off)
 };
 
@@ -114,7 +113,7 @@ int ipm_occupancy(int threads, size_t smem);
 // kind 1: row kernel (ocpqp_row.cuh), `team` lanes per QP, `wpb` warps per CTA.
 struct FastShape {
     int kind, nx, nu, ng, nb, team, wpb;
-    int sstage = 0;  // team kernel: stage the solve-sweep operands through smem (cp.async)
+    int sm = 0;  // team kernel: factor store + sweep vectors at fixed shared-memory offsets
 };
 int fast_teams_per_cta(const FastShape& s);
 bool fast_supported(const FastShape& s);
