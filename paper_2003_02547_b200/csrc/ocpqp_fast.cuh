@@ -115,6 +115,8 @@ __device__ __forceinline__ double tabsmax(const AbsMax& a, double* red) {
 // per row reduce with butterflies; all lanes take part in the shuffles.
 template <int R, int KD, int TEAM>
 struct MV {
+    // widest lane group the team allows (<= 8): consecutive lanes read
+    // consecutive k of one row, so the operand loads coalesce
     static constexpr int cap = TEAM / (R > 0 ? R : 1);
     static constexpr int GS0 = cap >= 8 ? 8 : cap >= 4 ? 4 : cap >= 2 ? 2 : 1;
     static constexpr int GS = (KD >= 8 ? GS0 : (KD >= 4 ? (GS0 < 4 ? GS0 : 4) : (KD >= 2 ? (GS0 < 2 ? GS0 : 2) : 1)));
@@ -1078,13 +1080,14 @@ struct Kern {
             pv[N * NX + i] = v;
             pvs[i] = v;
         }
+        if (!ss) bar<TEAM>();
         for (int n = N - 1; n >= 0; --n) {
             const int h = n & 1;
-            if (n > 0) issue(n - 1, h ^ 1, true);
             if (ss) {
+                if (n > 0) issue(n - 1, h ^ 1, true);
                 if (n > 0) cpa_wait<1>(); else cpa_wait<0>();
+                bar<TEAM>();
             }
-            bar<TEAM>();
             const double* H = SB + h * S::HALF;
             const bool st = ss;
             const double* Pn = (st && gP) ? H + oP : Pst + (n + 1) * NX * NX;
@@ -1125,43 +1128,53 @@ struct Kern {
         flops += 2ll * NX * NX;
         if (N > 0) issue(0, 0, false);
         bar<TEAM>();
-        // forward rollout (kkt_ocp.py:293-305)
-        for (int n = 0; n < N; ++n) {
-            const int h = n & 1;
-            if (n + 1 < N) issue(n + 1, h ^ 1, false);
-            if (ss) {
-                if (n + 1 < N) cpa_wait<1>(); else cpa_wait<0>();
+        // forward rollout (kkt_ocp.py:293-305); x ping-pongs between xa / xb
+        {
+            double* xa = xv;
+            double* xb = uv + NU;  // NX
+            for (int i = tid; i < NX; i += TEAM) dy[(N > 0 ? NU : 0) + i] = xa[i];
+            for (int n = 0; n < N; ++n) {
+                const int h = n & 1;
+                if (ss) {
+                    if (n + 1 < N) issue(n + 1, h ^ 1, false);
+                    if (n + 1 < N) cpa_wait<1>(); else cpa_wait<0>();
+                    bar<TEAM>();
+                }
+                const double* H = SB + h * S::HALF;
+                const bool st = ss;
+                const double* Kn = (st && gK) ? H + oK : Kst + n * NU * NX;
+                const double* kf = (st && gKF) ? H + oKF : kff + n * NU;
+                const double* rb = (st && gRB) ? H + oRB : r_b + n * NX;
+                const double* An = A(c, n);
+                const double* Bn = Bm(c, n);
+                double* du = dy + n * NW;
+                MV<NU, NX, TEAM>::run([&](int i, int k) { return Kn[i * NX + k]; },
+                                      [&](int k) { return xa[k]; },
+                                      [&](int i, double v) {
+                                          const double u = v + kf[i];
+                                          du[i] = u;
+                                          uv[i] = u;
+                                      });
+                bar<TEAM>();
+                double* xd = dy + (n + 1) * NW + (n + 1 < N ? NU : 0);
+                MV<NX, NW, TEAM>::run(
+                    [&](int i, int k) {
+                        if (ss) return k < NX ? H[oBA + i * NW + NU + k] : H[oBA + i * NW + (k - NX)];
+                        return k < NX ? An[i * NX + k] : Bn[i * NU + (k - NX)];
+                    },
+                    [&](int k) { return k < NX ? xa[k] : uv[k - NX]; },
+                    [&](int i, double v) {
+                        const double x = v + rb[i];
+                        xb[i] = x;
+                        xd[i] = x;
+                    });
+                bar<TEAM>();
+                double* sw = xa;
+                xa = xb;
+                xb = sw;
             }
-            for (int i = tid; i < NX; i += TEAM) dy[n * NW + NU + i] = xv[i];
-            bar<TEAM>();
-            const double* H = SB + h * S::HALF;
-            const bool st = ss;
-            const double* Kn = (st && gK) ? H + oK : Kst + n * NU * NX;
-            const double* kf = (st && gKF) ? H + oKF : kff + n * NU;
-            const double* rb = (st && gRB) ? H + oRB : r_b + n * NX;
-            const double* An = A(c, n);
-            const double* Bn = Bm(c, n);
-            double* du = dy + n * NW;
-            MV<NU, NX, TEAM>::run([&](int i, int k) { return Kn[i * NX + k]; },
-                                  [&](int k) { return xv[k]; },
-                                  [&](int i, double v) {
-                                      const double u = v + kf[i];
-                                      du[i] = u;
-                                      uv[i] = u;
-                                  });
-            bar<TEAM>();
-            MV<NX, NW, TEAM>::run(
-                [&](int i, int k) {
-                    if (ss) return k < NX ? H[oBA + i * NW + NU + k] : H[oBA + i * NW + (k - NX)];
-                    return k < NX ? An[i * NX + k] : Bn[i * NU + (k - NX)];
-                },
-                [&](int k) { return k < NX ? xv[k] : uv[k - NX]; },
-                [&](int i, double v) { e[i] = v + rb[i]; });
-            bar<TEAM>();
-            for (int i = tid; i < NX; i += TEAM) xv[i] = e[i];
+            if (N == 0) bar<TEAM>();
         }
-        for (int i = tid; i < NX; i += TEAM) dy[N * NW + i] = xv[i];
-        bar<TEAM>();
         OCPQP_TICK(c, DBG_S_FWD);
         // dpi_n = P_{n+1} x_{n+1} + pv_{n+1}, all stages in parallel
         #pragma unroll 4
