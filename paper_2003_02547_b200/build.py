@@ -24,7 +24,7 @@ HEADERS = [CSRC / "ocpqp_internal.h", CSRC / "ocpqp_fast.cuh", ROOT / "include" 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-]
+] + os.environ.get("OCPQP_NVCC_EXTRA", "").split()
 
 
 def nvcc():

@@ -22,6 +22,22 @@
 #pragma once
 #include "ocpqp_internal.h"
 
+// Unroll factors (code size vs per-thread ILP; the kernel is large enough for
+// instruction-fetch stalls to matter).  Team-strided vector passes have
+// runtime trip counts of a few elements per thread: measured, 1 beats 2 and 4.
+#ifndef OCPQP_PASS_UNROLL_N
+#define OCPQP_PASS_UNROLL_N 1
+#endif
+#ifndef OCPQP_TEAMFOR_UNROLL_N
+#define OCPQP_TEAMFOR_UNROLL_N 4
+#endif
+#ifndef OCPQP_K_UNROLL_N
+#define OCPQP_K_UNROLL_N 8
+#endif
+#define OCPQP_STR2(x) #x
+#define OCPQP_STR(x) OCPQP_STR2(x)
+#define OCPQP_PASS_UNROLL _Pragma(OCPQP_STR(unroll OCPQP_PASS_UNROLL_N))
+
 namespace ocpqp {
 namespace fastk {
 
@@ -131,7 +147,7 @@ struct MV {
             const int i = i0 + r0;
             double acc = 0.0;
             if (i < R) {
-#pragma unroll 4
+                _Pragma(OCPQP_STR(unroll OCPQP_K_UNROLL_N))
                 for (int k = g; k < KD; k += GS) acc = fma(a(i, k), x(k), acc);
             }
 #pragma unroll
@@ -258,7 +274,7 @@ struct FCtx {
 // Team loop over TOTAL (compile-time) outputs, unrolled so independent outputs
 // of one thread overlap their load / FMA-chain latencies.
 #define TEAM_FOR(idx, TOTAL)                                                        \
-    _Pragma("unroll 4") for (int _it = 0; _it < ((TOTAL) + TEAM - 1) / TEAM; ++_it) { \
+    _Pragma(OCPQP_STR(unroll OCPQP_TEAMFOR_UNROLL_N)) for (int _it = 0; _it < ((TOTAL) + TEAM - 1) / TEAM; ++_it) { \
         const int idx = threadIdx.x + _it * TEAM;                                   \
         if (idx < (TOTAL)) {
 #define TEAM_END \
@@ -313,7 +329,9 @@ __device__ __forceinline__ void tile_gemm(FA a, FB b, FE epi) {
         for (int i = 0; i < TM; ++i)
 #pragma unroll
             for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
-#pragma unroll 4
+        // k unroll: 8 measured best for K <= 30, 16 for the K = 60 stages
+        constexpr int KU = K >= 48 ? 2 * OCPQP_K_UNROLL_N : OCPQP_K_UNROLL_N;
+#pragma unroll KU
         for (int k = 0; k < K; ++k) {
             double av[TM], bv[TN];
 #pragma unroll
@@ -422,7 +440,7 @@ struct Kern {
     __device__ static void setup(FCtx& c, const RD& d) {
         double* dvec = c.w[WS_DVEC];   // d (view.py:156-157); NaN marks an inactive side
         double cnt = 0.0;
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int k = threadIdx.x; k < d.nc; k += TEAM) {
             const int n = d.slot_stage(k);
             const int m = n < d.N ? d.M : d.MN;
@@ -446,7 +464,7 @@ struct Kern {
     // row values Jc w for all rows (ConBlock.rows_w, view.py:91-97)
     __device__ static void rows_values(const FCtx& c, const RD& d, const int* idxb, const double* y,
                                        double* rowv) {
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int r = threadIdx.x; r < d.msum; r += TEAM) {
             const int n = d.row_stage(r);
             const int i = r - n * d.M;
@@ -508,7 +526,7 @@ struct Kern {
         double* r_b = c.w[WS_RB];
         double* r_d = c.w[WS_RD];
         rows_values(c, d, p.idxb, y, rowv);
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int r = threadIdx.x; r < d.msum; r += TEAM) {
             const int n = d.row_stage(r);
             const int i = r - n * d.M;
@@ -521,7 +539,7 @@ struct Kern {
         bar<TEAM>();
         AbsMax ag, ab, ad, am;
         double musum = 0.0;
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int j = threadIdx.x; j < d.nv; j += TEAM) {
             int n = j / NW;
             if (n > d.N) n = d.N;
@@ -576,7 +594,7 @@ struct Kern {
             r_g[j] = r;
             ag.add(r);
         }
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int e = threadIdx.x; e < d.ne; e += TEAM) {
             const int n = e / NX;
             const int i = e - n * NX;
@@ -594,7 +612,7 @@ struct Kern {
             r_b[e] = r;
             ab.add(r);
         }
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int k = threadIdx.x; k < d.nc; k += TEAM) {
             double rd = 0.0, rm = 0.0;
             if (!isnan(act[k])) {
@@ -634,7 +652,7 @@ struct Kern {
         double* BAs = vec + S::VEC;             // NX x NW staged [B A] of the stage
         double* tinv = c.w[WS_TINV];
         int bad = 0;
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int k = tid; k < d.nc; k += TEAM) {
             double g = 0.0, ti = 0.0;
             if (!isnan(act[k])) {
@@ -647,7 +665,7 @@ struct Kern {
         }
         if (any_of<TEAM>(bad)) return -2;
         bar<TEAM>();
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int r = tid; r < d.msum; r += TEAM) {
             const int n = d.row_stage(r);
             const int i = r - n * d.M;
@@ -1002,7 +1020,7 @@ struct Kern {
         double* e = vec + NW;           // NX
         int nonfinite = 0;
         // fold_rhs (kkt_common.py:118-137)
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int k = tid; k < d.nc; k += TEAM) {
             double w = 0.0;
             if (!isnan(act[k])) {
@@ -1018,7 +1036,7 @@ struct Kern {
             wall[k] = w;
         }
         bar<TEAM>();
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int r = tid; r < d.msum; r += TEAM) {
             const int n = d.row_stage(r);
             const int i = r - n * d.M;
@@ -1027,7 +1045,7 @@ struct Kern {
             crow[r] = wall[k] - wall[k + m];
         }
         bar<TEAM>();
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int j = tid; j < d.nv; j += TEAM) {
             int n = j / NW;
             if (n > d.N) n = d.N;
@@ -1177,7 +1195,7 @@ struct Kern {
         }
         OCPQP_TICK(c, DBG_S_FWD);
         // dpi_n = P_{n+1} x_{n+1} + pv_{n+1}, all stages in parallel
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int e2 = tid; e2 < d.ne; e2 += TEAM) {
             const int n = e2 / NX;
             const int i = e2 - n * NX;
@@ -1190,14 +1208,14 @@ struct Kern {
             dpi[e2] = v;
             if (!isfinite(v)) nonfinite = 1;
         }
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int j = tid; j < d.nv; j += TEAM)
             if (!isfinite(dy[j])) nonfinite = 1;
         // recover_block (kkt_common.py:140-163)
         double* rowv = c.w[WS_ROWV];
         rows_values(c, d, p.idxb, dy, rowv);
         bar<TEAM>();
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int k = tid; k < d.nc; k += TEAM) {
             double dl = 0.0, dtt = 0.0;
             if (!isnan(act[k])) {
@@ -1218,7 +1236,7 @@ struct Kern {
                                       const double* dlam, const double* dt, double ftb) {
         const double* act = c.w[WS_DVEC];  // NaN = inactive
         double ratio = INFINITY;
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int k = threadIdx.x; k < d.nc; k += TEAM) {
             if (!isnan(act[k])) {
                 if (dlam[k] < 0.0) ratio = fmin(ratio, -lam[k] / dlam[k]);
@@ -1233,7 +1251,7 @@ struct Kern {
                                       const double* dlam, const double* dt, double alpha) {
         const double* act = c.w[WS_DVEC];  // NaN = inactive
         double s = 0.0;
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int k = threadIdx.x; k < d.nc; k += TEAM)
             if (!isnan(act[k])) s += (lam[k] + alpha * dlam[k]) * (t[k] + alpha * dt[k]);
         s = tsum<TEAM>(s, c.red);
@@ -1258,11 +1276,11 @@ struct Kern {
         setup(c, d);
         // initial iterate (solver.py:113-142)
         const int warm = arg.warm_start;
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int i = tid; i < d.nv; i += TEAM) y[i] = warm ? gy[i] : 0.0;
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int i = tid; i < d.ne; i += TEAM) pi[i] = warm == 2 ? gpi[i] : 0.0;
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int k = tid; k < d.nc; k += TEAM) lam[k] = warm == 2 ? glam[k] : 0.0;
         bar<TEAM>();
         {
@@ -1276,10 +1294,10 @@ struct Kern {
             }
             if (warm == 2) {
                 double gd = 0.0, gb = 0.0;
-                #pragma unroll 4
+                OCPQP_PASS_UNROLL
                 for (int k = tid; k < d.nc; k += TEAM)
                     if (!isnan(act[k])) gd = fmax(gd, dvec[k] - slot_cy(d, k, rowv));
-                #pragma unroll 4
+                OCPQP_PASS_UNROLL
                 for (int e = tid; e < d.ne; e += TEAM) {
                     const int n = e / NX, i = e - n * NX;
                     const double* u = y + n * NW;
@@ -1296,7 +1314,7 @@ struct Kern {
                 floor = fmax(fmax(1e-8, arg.t_min), fmin(1.0, fmax(gd, gb)));
             }
             const double lfloor = fmax(1e-8, arg.lam_min);
-            #pragma unroll 4
+            OCPQP_PASS_UNROLL
             for (int k = tid; k < d.nc; k += TEAM) {
                 double tv = 0.0, lv = 0.0;
                 if (!isnan(act[k])) {
@@ -1367,11 +1385,11 @@ struct Kern {
             if (nf) { status = OCPQP_STATUS_NAN; break; }
             const double alpha = max_step(c, d, lam, t, dlam, dt, arg.ftb);
             const double* act = c.w[WS_DVEC];  // NaN = inactive
-            #pragma unroll 4
+            OCPQP_PASS_UNROLL
             for (int i = tid; i < d.nv; i += TEAM) y[i] += alpha * dy[i];
-            #pragma unroll 4
+            OCPQP_PASS_UNROLL
             for (int i = tid; i < d.ne; i += TEAM) pi[i] += alpha * dpi[i];
-            #pragma unroll 4
+            OCPQP_PASS_UNROLL
             for (int k = tid; k < d.nc; k += TEAM) {
                 double lv = lam[k] + alpha * dlam[k];
                 double tv = t[k] + alpha * dt[k];
@@ -1393,11 +1411,11 @@ struct Kern {
             OCPQP_TICK(c, DBG_STEP);
         }
         bar<TEAM>();
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int i = tid; i < d.nv; i += TEAM) gy[i] = y[i];
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int i = tid; i < d.ne; i += TEAM) gpi[i] = pi[i];
-        #pragma unroll 4
+        OCPQP_PASS_UNROLL
         for (int k = tid; k < d.nc; k += TEAM) { glam[k] = lam[k]; gt[k] = t[k]; }
         if (tid == 0) {
             sp.status[q] = status;
