@@ -34,6 +34,13 @@
 #ifndef OCPQP_K_UNROLL_N
 #define OCPQP_K_UNROLL_N 8
 #endif
+// the factor (called twice: retry) and the solve (2-3 calls per iteration)
+// are kept out of line when OCPQP_NOINLINE is set
+#ifdef OCPQP_NOINLINE
+#define OCPQP_BIGFN __device__ __noinline__
+#else
+#define OCPQP_BIGFN __device__
+#endif
 #define OCPQP_STR2(x) #x
 #define OCPQP_STR(x) OCPQP_STR2(x)
 #define OCPQP_PASS_UNROLL _Pragma(OCPQP_STR(unroll OCPQP_PASS_UNROLL_N))
@@ -511,6 +518,28 @@ struct Kern {
         return kk < m ? rowv[n * d.M + kk] : -rowv[n * d.M + kk - m];
     }
 
+    // ---- box-only shapes (NG == 0): every row is the box row of exactly one
+    // variable, so row quantities are gathered directly instead of through a
+    // materialised row vector (saves a pass and a barrier each time) ----
+    // slot pair (lower, upper) of variable j's box row, or -1
+    __device__ static __forceinline__ int box_slot(const RD& d, const int* var_box, int j, int n, int& kup) {
+        const int kb = var_box[j];
+        if (kb < 0) return -1;
+        const int k = n * 2 * d.M + kb;
+        kup = k + (n < d.N ? d.M : d.MN);
+        return k;
+    }
+    // C y of the row of slot k (signed per side), read straight from y
+    __device__ static __forceinline__ double slot_cy_direct(const RD& d, const int* idxb, int k, const double* y) {
+        const int n = d.slot_stage(k);
+        const int m = n < d.N ? d.M : d.MN;
+        const int kk = k - n * 2 * d.M;
+        const bool lo = kk < m;
+        const int i = lo ? kk : kk - m;
+        const double v = y[n * NW + idxb[n * d.NB + i]];
+        return lo ? v : -v;
+    }
+
     struct Res {
         double g, b, d, m, mu;
     };
@@ -525,18 +554,20 @@ struct Kern {
         double* r_g = c.w[WS_RG];
         double* r_b = c.w[WS_RB];
         double* r_d = c.w[WS_RD];
-        rows_values(c, d, p.idxb, y, rowv);
-        OCPQP_PASS_UNROLL
-        for (int r = threadIdx.x; r < d.msum; r += TEAM) {
-            const int n = d.row_stage(r);
-            const int i = r - n * d.M;
-            const int m = n < d.N ? d.M : d.MN;
-            const int k = n * 2 * d.M + i;
-            const double ll = !isnan(act[k]) ? lam[k] : 0.0;
-            const double lu = !isnan(act[k + m]) ? lam[k + m] : 0.0;
-            crow[r] = ll - lu;
+        if constexpr (NG > 0) {
+            rows_values(c, d, p.idxb, y, rowv);
+            OCPQP_PASS_UNROLL
+            for (int r = threadIdx.x; r < d.msum; r += TEAM) {
+                const int n = d.row_stage(r);
+                const int i = r - n * d.M;
+                const int m = n < d.N ? d.M : d.MN;
+                const int k = n * 2 * d.M + i;
+                const double ll = !isnan(act[k]) ? lam[k] : 0.0;
+                const double lu = !isnan(act[k + m]) ? lam[k + m] : 0.0;
+                crow[r] = ll - lu;
+            }
+            bar<TEAM>();
         }
-        bar<TEAM>();
         AbsMax ag, ab, ad, am;
         double musum = 0.0;
         OCPQP_PASS_UNROLL
@@ -590,7 +621,19 @@ struct Kern {
                 const double atp = d.N > 0 ? pi[(n - 1) * NX + jj] : 0.0;
                 r -= atp;
             }
-            r -= rows_t(c, d, p.var_box, n, j, jj, crow);
+            if constexpr (NG > 0) {
+                r -= rows_t(c, d, p.var_box, n, j, jj, crow);
+            } else {
+                int kup;
+                const int klo = box_slot(d, p.var_box, j, n, kup);
+                double rt = 0.0;
+                if (klo >= 0) {
+                    const double ll = !isnan(act[klo]) ? lam[klo] : 0.0;
+                    const double lu = !isnan(act[kup]) ? lam[kup] : 0.0;
+                    rt = ll - lu;
+                }
+                r -= rt;
+            }
             r_g[j] = r;
             ag.add(r);
         }
@@ -616,7 +659,8 @@ struct Kern {
         for (int k = threadIdx.x; k < d.nc; k += TEAM) {
             double rd = 0.0, rm = 0.0;
             if (!isnan(act[k])) {
-                rd = (-slot_cy(d, k, rowv) + dvec[k]) + t[k];
+                const double cy = NG > 0 ? slot_cy(d, k, rowv) : slot_cy_direct(d, p.idxb, k, y);
+                rd = (-cy + dvec[k]) + t[k];
                 rm = lam[k] * t[k];
                 musum += rm;
             }
@@ -636,7 +680,7 @@ struct Kern {
 
     // ---------------- classical Riccati factor ----------------
     // returns -1 ok, failing stage, -2 non-positive iterate
-    __device__ static int factor(FCtx& c, const RD& d, const KParams& p, double* stg,
+    OCPQP_BIGFN static int factor(FCtx& c, const RD& d, const KParams& p, double* stg,
                                  const double* lam, const double* t, double reg, long long& flops) {
         const int tid = threadIdx.x;
         const double* act = c.w[WS_DVEC];  // NaN = inactive
@@ -663,17 +707,28 @@ struct Kern {
             gam[k] = g;
             tinv[k] = ti;
         }
-        if (any_of<TEAM>(bad)) return -2;
-        bar<TEAM>();
-        OCPQP_PASS_UNROLL
-        for (int r = tid; r < d.msum; r += TEAM) {
-            const int n = d.row_stage(r);
-            const int i = r - n * d.M;
-            const int m = n < d.N ? d.M : d.MN;
-            const int k = n * 2 * d.M + i;
-            coef[r] = gam[k] + gam[k + m];
+        if (any_of<TEAM>(bad)) return -2;  // (block-wide barrier for TEAM > 32)
+        if constexpr (TEAM == 32) bar<TEAM>();
+        if constexpr (NG > 0) {
+            OCPQP_PASS_UNROLL
+            for (int r = tid; r < d.msum; r += TEAM) {
+                const int n = d.row_stage(r);
+                const int i = r - n * d.M;
+                const int m = n < d.N ? d.M : d.MN;
+                const int k = n * 2 * d.M + i;
+                coef[r] = gam[k] + gam[k + m];
+            }
+            bar<TEAM>();
         }
-        bar<TEAM>();
+        // gamma_lo + gamma_up of box row kb of stage n (kkt_common.py:100-115)
+        auto cfv = [&](int n, int kb) -> double {
+            if constexpr (NG > 0) {
+                return coef[n * d.M + kb];
+            } else {
+                const int k = n * 2 * d.M + kb;
+                return gam[k] + gam[k + (n < d.N ? d.M : d.MN)];
+            }
+        };
         const int N = d.N;
         // stage data prefetch (cp.async, one stage ahead): [B A]_n, Q_n, S_n, R_n
         constexpr bool fpf = (S::SSTAGE & 2) != 0;
@@ -707,7 +762,7 @@ struct Kern {
                 double h = 0.5 * (Qn[i * NX + j] + Qn[j * NX + i]);
                 if (i == j) {
                     const int kb = p.var_box[n * NW + i];
-                    if (kb >= 0) h += cf[kb];
+                    if (kb >= 0) h += cfv(n, kb);
                 }
                 if (NG > 0 && ng > 0) {
                     const double* Cn = Cm(c, n);
@@ -779,7 +834,7 @@ struct Kern {
                 double h = 0.5 * (mij + mji);
                 if (i == j) {
                     const int kb = full_box ? i : p.var_box[n * NW + i];
-                    if (kb >= 0) h += cf[kb];
+                    if (kb >= 0) h += cfv(n, kb);
                 }
                 if (NG > 0) {
                     double sg = 0.0;
@@ -996,7 +1051,7 @@ struct Kern {
 
     // ---------------- Riccati solve (kkt_ocp.py:254-320) ----------------
     // r_m(k) = act ? (lam t - tau) + [dlam_a dt_a] : 0, or rm_ext (masked)
-    __device__ static int solve(FCtx& c, const RD& d, const KParams& p, double* stg,
+    OCPQP_BIGFN static int solve(FCtx& c, const RD& d, const KParams& p, double* stg,
                                 const double* lam, const double* t, const double* rm_ext,
                                 double tau, const double* dla, const double* dta, double* dy,
                                 double* dpi, double* dlam, double* dt, long long& flops) {
@@ -1020,8 +1075,7 @@ struct Kern {
         double* e = vec + NW;           // NX
         int nonfinite = 0;
         // fold_rhs (kkt_common.py:118-137)
-        OCPQP_PASS_UNROLL
-        for (int k = tid; k < d.nc; k += TEAM) {
+        auto fold = [&](int k) -> double {
             double w = 0.0;
             if (!isnan(act[k])) {
                 double rmk;
@@ -1033,23 +1087,44 @@ struct Kern {
                 }
                 w = (lam[k] * r_d[k] - rmk) * tinv[k];
             }
-            wall[k] = w;
-        }
-        bar<TEAM>();
-        OCPQP_PASS_UNROLL
-        for (int r = tid; r < d.msum; r += TEAM) {
-            const int n = d.row_stage(r);
-            const int i = r - n * d.M;
-            const int m = n < d.N ? d.M : d.MN;
-            const int k = n * 2 * d.M + i;
-            crow[r] = wall[k] - wall[k + m];
-        }
-        bar<TEAM>();
-        OCPQP_PASS_UNROLL
-        for (int j = tid; j < d.nv; j += TEAM) {
-            int n = j / NW;
-            if (n > d.N) n = d.N;
-            rhat[j] = r_g[j] - rows_t(c, d, p.var_box, n, j, j - n * NW, crow);
+            return w;
+        };
+        if constexpr (NG == 0) {
+            // one pass: each variable folds the two slots of its box row
+            OCPQP_PASS_UNROLL
+            for (int j = tid; j < d.nv; j += TEAM) {
+                int n = j / NW;
+                if (n > d.N) n = d.N;
+                int kup;
+                const int klo = box_slot(d, p.var_box, j, n, kup);
+                double rt = 0.0;
+                if (klo >= 0) {
+                    const double wl = fold(klo), wu = fold(kup);
+                    wall[klo] = wl;
+                    wall[kup] = wu;
+                    rt = wl - wu;
+                }
+                rhat[j] = r_g[j] - rt;
+            }
+        } else {
+            OCPQP_PASS_UNROLL
+            for (int k = tid; k < d.nc; k += TEAM) wall[k] = fold(k);
+            bar<TEAM>();
+            OCPQP_PASS_UNROLL
+            for (int r = tid; r < d.msum; r += TEAM) {
+                const int n = d.row_stage(r);
+                const int i = r - n * d.M;
+                const int m = n < d.N ? d.M : d.MN;
+                const int k = n * 2 * d.M + i;
+                crow[r] = wall[k] - wall[k + m];
+            }
+            bar<TEAM>();
+            OCPQP_PASS_UNROLL
+            for (int j = tid; j < d.nv; j += TEAM) {
+                int n = j / NW;
+                if (n > d.N) n = d.N;
+                rhat[j] = r_g[j] - rows_t(c, d, p.var_box, n, j, j - n * NW, crow);
+            }
         }
         bar<TEAM>();
         const int N = d.N;
@@ -1213,13 +1288,15 @@ struct Kern {
             if (!isfinite(dy[j])) nonfinite = 1;
         // recover_block (kkt_common.py:140-163)
         double* rowv = c.w[WS_ROWV];
-        rows_values(c, d, p.idxb, dy, rowv);
-        bar<TEAM>();
+        if constexpr (NG > 0) {
+            rows_values(c, d, p.idxb, dy, rowv);
+            bar<TEAM>();
+        }
         OCPQP_PASS_UNROLL
         for (int k = tid; k < d.nc; k += TEAM) {
             double dl = 0.0, dtt = 0.0;
             if (!isnan(act[k])) {
-                const double cy = slot_cy(d, k, rowv);
+                const double cy = NG > 0 ? slot_cy(d, k, rowv) : slot_cy_direct(d, p.idxb, k, dy);
                 dl = wall[k] - gam[k] * cy;
                 dtt = -r_d[k] + cy;
             }
