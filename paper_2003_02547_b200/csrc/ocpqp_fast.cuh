@@ -1210,7 +1210,25 @@ struct Kern {
                                       pvc[i] = r;
                                       pvs[i] = r;
                                   });
-            if (tid < 32) warp_cho_solve<NU>(Ln, Rn, win, kff + n * NU, -1.0);
+            if constexpr (S::SMALL && TEAM > 32) {
+                // k_n = -G_uu^{-1} rr in one thread of the second warp, in
+                // registers, concurrent with p_n on the first warp
+                if (tid == 32) {
+                    double Lr[NU][NU], ri[NU], z[NU];
+#pragma unroll
+                    for (int i = 0; i < NU; ++i) {
+                        ri[i] = Rn[i];
+                        z[i] = win[i];
+#pragma unroll
+                        for (int j = 0; j < i; ++j) Lr[i][j] = Ln[i * NU + j];
+                    }
+                    reg_cho_solve<NU>(Lr, ri, z);
+#pragma unroll
+                    for (int i = 0; i < NU; ++i) kff[n * NU + i] = -z[i];
+                }
+            } else {
+                if (tid < 32) warp_cho_solve<NU>(Ln, Rn, win, kff + n * NU, -1.0);
+            }
             flops += 2ll * NU * NU;
             bar<TEAM>();
         }
