@@ -861,8 +861,9 @@ struct Kern {
             double* Rinv_n = wsb<WS_RINV>(c, p) + n * NU;
             double* Kn = Kst + n * NU * NX;
             if constexpr (S::SMALL) {
-                // every thread factors G_uu in registers; thread j < NX solves
-                // column j of K = -L'^{-1} L^{-1} G_ux (kkt_ocp.py:237-243)
+                // every thread factors G_uu in registers (measured faster than
+                // factoring in the K threads only and broadcasting the pivot
+                // test); thread j < NX solves column j of K = -L'^{-1} L^{-1} G_ux (kkt_ocp.py:237-243)
                 double Lr[NU][NU], ri[NU];
                 const bool ok = reg_chol<NU>(Gu, NW, Lr, ri);
                 flops += (long long)NU * NU * NU / 3;
@@ -1330,14 +1331,25 @@ struct Kern {
     __device__ static double max_step(FCtx& c, const RD& d, const double* lam, const double* t,
                                       const double* dlam, const double* dt, double ftb) {
         const double* act = c.w[WS_DVEC];  // NaN = inactive
-        double ratio = INFINITY;
+        // ipm_core.py:217-233.  The thread's smallest ratio a/b (b = -delta > 0)
+        // is tracked as a fraction (a/b < A/B <=> a*B < A*b) and divided once,
+        // instead of one fp64 division per candidate.
+        double A = 1.0, B = 0.0;  // A / B = +inf
         OCPQP_PASS_UNROLL
         for (int k = threadIdx.x; k < d.nc; k += TEAM) {
             if (!isnan(act[k])) {
-                if (dlam[k] < 0.0) ratio = fmin(ratio, -lam[k] / dlam[k]);
-                if (dt[k] < 0.0) ratio = fmin(ratio, -t[k] / dt[k]);
+                const double dl = dlam[k], dtk = dt[k];
+                if (dl < 0.0) {
+                    const double a = lam[k], b = -dl;
+                    if (a * B < A * b) { A = a; B = b; }
+                }
+                if (dtk < 0.0) {
+                    const double a = t[k], b = -dtk;
+                    if (a * B < A * b) { A = a; B = b; }
+                }
             }
         }
+        double ratio = A / B;
         ratio = tmin<TEAM>(ratio, c.red);
         return fmin(1.0, ftb * ratio);
     }
