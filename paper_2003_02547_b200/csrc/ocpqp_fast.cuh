@@ -358,6 +358,55 @@ __device__ __forceinline__ void tile_gemm(FA a, FB b, FE epi) {
     }
 }
 
+// ---- FP64 tensor-core GEMM (DMMA, mma.sync m8n8k4 f64) -------------------
+// Same contract as tile_gemm.  Each warp owns 8 x 16 output tiles (two 8x8
+// accumulators sharing the A fragment), k in steps of 4; out-of-range rows /
+// columns / k are fed as zeros.  Fragments (PTX m8n8k4 .f64): A row = lane/4,
+// col = lane%4; B row = lane%4, col = lane/4; D row = lane/4, cols 2*(lane%4)+{0,1}.
+__device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int M, int N, int K, int TEAM, class FA, class FB, class FE>
+__device__ __forceinline__ void tile_mma(FA a, FB b, FE epi) {
+    constexpr int NWARP = TEAM / 32;
+    constexpr int MB = (M + 7) / 8, NB = (N + 15) / 16, KS = (K + 3) / 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gr = lane >> 2, tg = lane & 3;
+    for (int t = warp; t < MB * NB; t += NWARP) {
+        const int r0 = (t / NB) * 8, c0 = (t % NB) * 16;
+        const int ar = r0 + gr, bc0 = c0 + gr, bc1 = c0 + 8 + gr;
+        double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+#pragma unroll 5
+        for (int ks = 0; ks < KS; ++ks) {
+            const int k = ks * 4 + tg;
+            const bool kin = (K % 4 == 0) || k < K;
+            const double av = (ar < M && kin) ? a(ar, k) : 0.0;
+            const double b0 = (bc0 < N && kin) ? b(k, bc0) : 0.0;
+            const double b1 = (bc1 < N && kin) ? b(k, bc1) : 0.0;
+            dmma_acc(c00, c01, av, b0);
+            dmma_acc(c10, c11, av, b1);
+        }
+        const int i = r0 + gr;
+        if (i < M) {
+            const int j0 = c0 + 2 * tg, j1 = c0 + 8 + 2 * tg;
+            if (j0 < N) epi(i, j0, c00);
+            if (j0 + 1 < N) epi(i, j0 + 1, c01);
+            if (j1 < N) epi(i, j1, c10);
+            if (j1 + 1 < N) epi(i, j1 + 1, c11);
+        }
+    }
+}
+
+// stage GEMM: DMMA tiles on the large shapes, register-tiled DFMA otherwise
+template <bool MMA, int M, int N, int K, int TEAM, class FA, class FB, class FE>
+__device__ __forceinline__ void stage_gemm(FA a, FB b, FE epi) {
+    if constexpr (MMA) tile_mma<M, N, K, TEAM>(a, b, epi);
+    else tile_gemm<M, N, K, TEAM>(a, b, epi);
+}
+
 // accumulate the cycles since the previous tick into phase `slot` (thread 0)
 #define OCPQP_TICK(c, slot)                                       \
     do {                                                          \
@@ -414,6 +463,15 @@ struct Shape {
     // small input dimension: every thread factors G_uu in registers (no warp
     // Cholesky / flag round trip) and the sweeps fuse their per-stage steps
     static constexpr bool SMALL = NU <= 4;
+    // FP64 tensor-core (DMMA) stage GEMMs.  Measured per config (tools/sweep.py,
+    // DMMA vs register-tiled DFMA): config 4 198 -> 164 ms, config 2 102 ->
+    // 96.5 ms; slower on config 1 (8x11 stages) and config 3 (nu = 10 pads
+    // G_u to 16 rows; general rows).  OCPQP_DMMA=0/1 forces it off/on.
+#ifdef OCPQP_DMMA
+    static constexpr bool DMMA = OCPQP_DMMA != 0;
+#else
+    static constexpr bool DMMA = NX >= 20 && NG == 0;
+#endif
 };
 
 template <class S>
@@ -813,7 +871,7 @@ struct Kern {
                 else return j < NU ? Bn[k * NU + j] : An[k * NX + (j - NU)];
             };
             // T1 = P_{n+1} [B A]   (kkt_ocp.py:232)
-            tile_gemm<NX, NW, NX, TEAM>([&](int i, int k) { return Pc[i * NX + k]; },
+            stage_gemm<S::DMMA, NX, NW, NX, TEAM>([&](int i, int k) { return Pc[i * NX + k]; },
                                         [&](int k, int j) { return BA(k, j); },
                                         [&](int i, int j, double v) { T1[i * NW + j] = v; });
             bar<TEAM>();
@@ -846,10 +904,10 @@ struct Kern {
                 if (i == j && reg != 0.0) h += reg;
                 return h;
             };
-            tile_gemm<NU, NW, NX, TEAM>([&](int i, int k) { return BA(k, i); },
+            stage_gemm<S::DMMA, NU, NW, NX, TEAM>([&](int i, int k) { return BA(k, i); },
                                         [&](int k, int j) { return T1[k * NW + j]; },
                                         [&](int i, int j, double v) { Gu[i * NW + j] = v + Mt(i, j); });
-            tile_gemm<NX, NX, NX, TEAM>([&](int i, int k) { return BA(k, NU + i); },
+            stage_gemm<S::DMMA, NX, NX, NX, TEAM>([&](int i, int k) { return BA(k, NU + i); },
                                         [&](int k, int j) { return T1[k * NW + NU + j]; },
                                         [&](int i, int j, double v) { Pc[i * NX + j] = v + Mt(NU + i, NU + j); });
             if (NG > 0) flops += 2ll * NW * NW * NG;
@@ -968,7 +1026,7 @@ struct Kern {
             }
             OCPQP_TICK(c, DBG_F_K);
             // P = G_xx + G_ux' K, symmetrised (kkt_ocp.py:244, 251)
-            tile_gemm<NX, NX, NU, TEAM>([&](int i, int k) { return Gu[k * NW + NU + i]; },
+            stage_gemm<S::DMMA, NX, NX, NU, TEAM>([&](int i, int k) { return Gu[k * NW + NU + i]; },
                                         [&](int k, int j) { return Kn[k * NX + j]; },
                                         [&](int i, int j, double v) { T1[i * NX + j] = v + Pc[i * NX + j]; });
             flops += 2ll * NX * NX * NU;
