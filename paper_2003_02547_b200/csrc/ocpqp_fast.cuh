@@ -369,33 +369,46 @@ __device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, doubl
                  : "d"(a), "d"(b));
 }
 
+#ifndef OCPQP_MMA_NBW
+#define OCPQP_MMA_NBW 2
+#endif
 template <int M, int N, int K, int TEAM, class FA, class FB, class FE>
 __device__ __forceinline__ void tile_mma(FA a, FB b, FE epi) {
     constexpr int NWARP = TEAM / 32;
-    constexpr int MB = (M + 7) / 8, NB = (N + 15) / 16, KS = (K + 3) / 4;
+    // warp tile 8 x (8*NBW): NBW independent accumulators share the A fragment
+    constexpr int NBW0 = OCPQP_MMA_NBW;
+    constexpr int NBW = (N + 7) / 8 < NBW0 ? (N + 7) / 8 : NBW0;
+    constexpr int MB = (M + 7) / 8, NB = (N + 8 * NBW - 1) / (8 * NBW), KS = (K + 3) / 4;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gr = lane >> 2, tg = lane & 3;
     for (int t = warp; t < MB * NB; t += NWARP) {
-        const int r0 = (t / NB) * 8, c0 = (t % NB) * 16;
-        const int ar = r0 + gr, bc0 = c0 + gr, bc1 = c0 + 8 + gr;
-        double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+        const int r0 = (t / NB) * 8, c0 = (t % NB) * (8 * NBW);
+        const int ar = r0 + gr;
+        double acc[NBW][2];
+#pragma unroll
+        for (int q = 0; q < NBW; ++q) acc[q][0] = acc[q][1] = 0.0;
 #pragma unroll 5
         for (int ks = 0; ks < KS; ++ks) {
             const int k = ks * 4 + tg;
             const bool kin = (K % 4 == 0) || k < K;
             const double av = (ar < M && kin) ? a(ar, k) : 0.0;
-            const double b0 = (bc0 < N && kin) ? b(k, bc0) : 0.0;
-            const double b1 = (bc1 < N && kin) ? b(k, bc1) : 0.0;
-            dmma_acc(c00, c01, av, b0);
-            dmma_acc(c10, c11, av, b1);
+            double bv[NBW];
+#pragma unroll
+            for (int q = 0; q < NBW; ++q) {
+                const int bc = c0 + 8 * q + gr;
+                bv[q] = (bc < N && kin) ? b(k, bc) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < NBW; ++q) dmma_acc(acc[q][0], acc[q][1], av, bv[q]);
         }
         const int i = r0 + gr;
         if (i < M) {
-            const int j0 = c0 + 2 * tg, j1 = c0 + 8 + 2 * tg;
-            if (j0 < N) epi(i, j0, c00);
-            if (j0 + 1 < N) epi(i, j0 + 1, c01);
-            if (j1 < N) epi(i, j1, c10);
-            if (j1 + 1 < N) epi(i, j1 + 1, c11);
+#pragma unroll
+            for (int q = 0; q < NBW; ++q) {
+                const int j = c0 + 8 * q + 2 * tg;
+                if (j < N) epi(i, j, acc[q][0]);
+                if (j + 1 < N) epi(i, j + 1, acc[q][1]);
+            }
         }
     }
 }
