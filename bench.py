@@ -297,6 +297,28 @@ def main():
             "peak_source": "measured live: DFMA microbenchmark (ocpqp_fp64_peak), "
                            f"DMMA m8n8k4 {peak_dmma:.1f} TFLOP/s" if peak_dmma else "n/a",
             "stream_bytes_per_qp_iter": rf.stream_bytes(batch.dim, lay)}
+    # Riccati share of the kernel time (the metric's "Riccati % of roofline"):
+    # one extra, untimed solve with the kernel's clock64 phase counters; the
+    # factor recursion (T1, G, Cholesky, K, P) and the backward / forward
+    # sweeps are the Riccati phases, the rest are the IPM vector passes
+    if plan_info.get("kernel") == "team":
+        try:
+            dbg = torch.zeros((B, 16), dtype=torch.int64, device="cuda")
+            solve_ocp_qp_batch(dev, arg, trace=False, phase_debug=dbg, stream=stream)
+            torch.cuda.synchronize()
+            solve_ocp_qp_batch(dev, arg, trace=False, stream=stream)  # instrumentation off
+            ph = dbg.cpu().numpy().astype(np.float64)
+            ric = ph[:, [8, 9, 10, 11, 12, 14, 15]].sum()
+            tot = ph[:, 5].sum()
+            if tot > 0 and ric > 0:
+                share = float(ric / tot)
+                roof["riccati"] = {
+                    "share_of_kernel_time": share,
+                    "achieved": achieved / share, "frac": roof["frac"] / share if roof["frac"] else None,
+                    "phases": "factor recursion (T1, G, Cholesky, K, P) + backward/forward sweeps; "
+                              "clock64 phase counters summed over QPs, one extra untimed solve"}
+        except Exception as exc:  # diagnostics only
+            roof["riccati"] = {"error": str(exc)[:120]}
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():
         try:
