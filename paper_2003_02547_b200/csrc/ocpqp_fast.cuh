@@ -457,10 +457,23 @@ struct Shape {
     static constexpr int VEC = 2 * NW + 3 * NX + 2 * NU + 16;
     // [B A] is staged in shared memory for small / medium stages only; large
     // stages read it through L1 so that two QPs' tiles fit per SM
-    static constexpr bool STAGE_BA = NX * NW <= 2048;
+#ifndef OCPQP_STAGE_BA_MAX
+#define OCPQP_STAGE_BA_MAX 0  // measured: staging [B A] per stage costs more than it saves
+#endif
+    static constexpr bool STAGE_BA = NX * NW <= OCPQP_STAGE_BA_MAX;
     // double-buffered per-stage operands of the solve sweeps (cp.async one stage
     // ahead): P_{n+1}, [B A]_n, K_n, L_n, 1/L_ii, r_b,n, rhat_n, kff_n
-    static constexpr int HALF = NX * NX + NX * NW + NU * NX + NU * NU + NU + NX + NW + NU + 4;
+#ifndef OCPQP_STAGE_P
+#define OCPQP_STAGE_P 1
+#endif
+#ifndef OCPQP_PF_QSR
+#define OCPQP_PF_QSR 1
+#endif
+    static constexpr bool STAGE_P = OCPQP_STAGE_P != 0;   // sweep staging includes P_{n+1}
+    static constexpr bool PF_QSR = OCPQP_PF_QSR != 0;     // factor prefetch includes Q, S, R
+    static constexpr int HALF_S = (STAGE_P ? NX * NX : 0) + NX * NW + NU * NX + NU * NU + NU + NX + NW + NU + 4;
+    static constexpr int HALF_F = NX * NW + (PF_QSR ? NX * NX + NU * NX + NU * NU : 0);
+    static constexpr int HALF = HALF_S > HALF_F ? HALF_S : HALF_F;
     static constexpr bool STAGE_SOLVE = HALF <= 4096;
     static constexpr int SOLVE_BUF = STAGE_SOLVE ? 2 * HALF : 0;
     static constexpr int BA_BUF = STAGE_BA ? NX * NW : 0;
@@ -816,9 +829,11 @@ struct Kern {
                 const int k = e2 / NW, j = e2 - k * NW;
                 cpa8(H + e2, j < NU ? Bn + k * NU + j : An + k * NX + (j - NU));
             }
-            for (int e2 = tid; e2 < NX * NX; e2 += TEAM) cpa8(H + fQ + e2, Qn + e2);
-            for (int e2 = tid; e2 < NU * NX; e2 += TEAM) cpa8(H + fS + e2, Sn + e2);
-            for (int e2 = tid; e2 < NU * NU; e2 += TEAM) cpa8(H + fR + e2, Rn + e2);
+            if constexpr (S::PF_QSR) {
+                for (int e2 = tid; e2 < NX * NX; e2 += TEAM) cpa8(H + fQ + e2, Qn + e2);
+                for (int e2 = tid; e2 < NU * NX; e2 += TEAM) cpa8(H + fS + e2, Sn + e2);
+                for (int e2 = tid; e2 < NU * NU; e2 += TEAM) cpa8(H + fR + e2, Rn + e2);
+            }
             cpa_commit();
         };
         if (fpf) prefetch(N - 1, (N - 1) & 1);
@@ -891,9 +906,10 @@ struct Kern {
             OCPQP_TICK(c, DBG_F_T1);
             // G = [B A]' T1 + M~ (kkt_ocp.py:233, 70-80; kkt_common.py:100-115):
             // input rows -> Gu (NU x NW), G_xx -> Pc (P_{n+1} is dead after T1)
-            const double* Qn = fpf ? H + fQ : Q(c, n);
-            const double* Rn = fpf ? H + fR : R(c, n);
-            const double* Sn = fpf ? H + fS : Sm(c, n);
+            constexpr bool pq = fpf && S::PF_QSR;
+            const double* Qn = pq ? H + fQ : Q(c, n);
+            const double* Rn = pq ? H + fR : R(c, n);
+            const double* Sn = pq ? H + fS : Sm(c, n);
             const double* cf = coef + n * d.M;
             const bool full_box = d.NB == NW;
             auto Mt = [&](int i, int j) -> double {
@@ -1213,7 +1229,7 @@ struct Kern {
         const bool gKF = !((sm >> WS_KFF) & 1ull);
         const double* Rst = wsb<WS_RINV>(c, p);
         // half layout offsets
-        constexpr int oP = 0, oBA = NX * NX, oK = oBA + NX * NW, oL = oK + NU * NX, oR = oL + NU * NU;
+        constexpr int oP = 0, oBA = S::STAGE_P ? NX * NX : 0, oK = oBA + NX * NW, oL = oK + NU * NX, oR = oL + NU * NU;
         constexpr int oRB = oR + NU, oRH = oRB + NX, oKF = oRH + NW;
         constexpr bool ss = (S::SSTAGE & 1) != 0;
         auto issue = [&](int n, int h, bool bwd) {
@@ -1228,7 +1244,8 @@ struct Kern {
                 if (gK) for (int e2 = tid; e2 < NU * NX; e2 += TEAM) cpa8(H + oK + e2, Kst + n * NU * NX + e2);
                 if (gRB) for (int e2 = tid; e2 < NX; e2 += TEAM) cpa8(H + oRB + e2, r_b + n * NX + e2);
                 if (bwd) {
-                    if (gP) for (int e2 = tid; e2 < NX * NX; e2 += TEAM) cpa8(H + oP + e2, Pst + (n + 1) * NX * NX + e2);
+                    if (S::STAGE_P && gP)
+                        for (int e2 = tid; e2 < NX * NX; e2 += TEAM) cpa8(H + oP + e2, Pst + (n + 1) * NX * NX + e2);
                     if (gL) for (int e2 = tid; e2 < NU * NU; e2 += TEAM) cpa8(H + oL + e2, Lst + n * NU * NU + e2);
                     if (gR) for (int e2 = tid; e2 < NU; e2 += TEAM) cpa8(H + oR + e2, Rst + n * NU + e2);
                     if (gRH) for (int e2 = tid; e2 < NW; e2 += TEAM) cpa8(H + oRH + e2, rhat + n * NW + e2);
@@ -1255,7 +1272,7 @@ struct Kern {
             }
             const double* H = SB + h * S::HALF;
             const bool st = ss;
-            const double* Pn = (st && gP) ? H + oP : Pst + (n + 1) * NX * NX;
+            const double* Pn = (st && S::STAGE_P && gP) ? H + oP : Pst + (n + 1) * NX * NX;
             const double* rb = (st && gRB) ? H + oRB : r_b + n * NX;
             const double* Kn = (st && gK) ? H + oK : Kst + n * NU * NX;
             const double* Ln = (st && gL) ? H + oL : Lst + n * NU * NU;
