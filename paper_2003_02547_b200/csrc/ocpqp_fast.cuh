@@ -127,6 +127,54 @@ struct AbsMax {
     }
 };
 
+// The four residual inf-norms and the complementarity sum in one team
+// reduction: five interleaved butterflies, one shared-memory exchange.
+// Same results as four tabsmax + one tsum (same combination order).
+template <int TEAM>
+__device__ __forceinline__ void tred_res(AbsMax (&a)[4], double& sum, double* red) {
+    double v[4] = {a[0].m, a[1].m, a[2].m, a[3].m};
+    unsigned nanbits = (unsigned)a[0].nan | ((unsigned)a[1].nan << 1) | ((unsigned)a[2].nan << 2) |
+                       ((unsigned)a[3].nan << 3);
+    double sm = sum;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = fmax(v[i], __shfl_xor_sync(FULL, v[i], o));
+        sm += __shfl_xor_sync(FULL, sm, o);
+    }
+    nanbits = __reduce_or_sync(FULL, nanbits);
+    if constexpr (TEAM > 32) {
+        constexpr int NWp = TEAM / 32;
+        __syncthreads();
+        const int w = threadIdx.x >> 5;
+        if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) red[i * NWp + w] = v[i];
+            red[4 * NWp + w] = sm;
+            reinterpret_cast<unsigned*>(red + 5 * NWp)[w] = nanbits;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            double x = red[i * NWp];
+#pragma unroll
+            for (int q = 1; q < NWp; ++q) x = fmax(x, red[i * NWp + q]);
+            v[i] = x;
+        }
+        double s2 = 0.0;
+#pragma unroll
+        for (int q = 0; q < NWp; ++q) s2 += red[4 * NWp + q];
+        sm = s2;
+        unsigned nb = 0;
+#pragma unroll
+        for (int q = 0; q < NWp; ++q) nb |= reinterpret_cast<const unsigned*>(red + 5 * NWp)[q];
+        nanbits = nb;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i].m = ((nanbits >> i) & 1u) ? qnan() : v[i];
+    sum = sm;
+}
+
 template <int TEAM>
 __device__ __forceinline__ double tabsmax(const AbsMax& a, double* red) {
     const int nan = any_of<TEAM>(a.nan);
@@ -270,7 +318,7 @@ __device__ bool team_chol(double* L, int n, int* flag, double* rinv) {
 struct FCtx {
     const double* f[OCPQP_NUM_FIELDS];
     double* w[WS_NUM];
-    double red[32];
+    double red[56];  // team reductions (tred_res: 6 x warps)
     int flag;
     int q;
     double n_act;
@@ -753,11 +801,13 @@ struct Kern {
             am.add(rm);
         }
         Res o;
-        o.g = tabsmax<TEAM>(ag, c.red);
-        o.b = tabsmax<TEAM>(ab, c.red);
-        o.d = tabsmax<TEAM>(ad, c.red);
-        o.m = tabsmax<TEAM>(am, c.red);
-        const double tot = tsum<TEAM>(musum, c.red);
+        AbsMax all[4] = {ag, ab, ad, am};
+        double tot = musum;
+        tred_res<TEAM>(all, tot, c.red);
+        o.g = all[0].m;
+        o.b = all[1].m;
+        o.d = all[2].m;
+        o.m = all[3].m;
         o.mu = c.n_act > 0.0 ? tot / c.n_act : 0.0;
         return o;
     }
