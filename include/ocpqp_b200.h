@@ -178,7 +178,12 @@ int ocpqp_solve(OcpPlan* plan, const OcpQpDataC* data, const OcpIpmArgC* arg,
 
 /* Same as ocpqp_solve with HOST buffers: copies data in, solves and copies the
  * solution and stats out, then synchronizes `stream`.  This is the call an FFI
- * binding of the reference makes with numpy arrays. */
+ * binding of the reference makes with numpy arrays.  When every result buffer
+ * is page-locked (cudaHostAlloc / cudaHostRegister, e.g. torch pin_memory) and
+ * no trace / warm start is requested, the kernel writes each QP's solution and
+ * statistics straight into them as the QP finishes (mapped host memory), so
+ * the transfer overlaps the QPs still iterating; pageable buffers go through
+ * device staging and a copy after the solve. */
 int ocpqp_solve_host(OcpPlan* plan, const OcpQpDataC* host_data,
                      const OcpIpmArgC* arg, OcpIterC* host_iter,
                      OcpStatsC* host_stats, void* stream);
