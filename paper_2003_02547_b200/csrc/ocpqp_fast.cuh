@@ -221,8 +221,8 @@ __device__ __forceinline__ bool warp_chol(double (&row)[NN], int lane, double& r
     for (int k = 0; k < NN; ++k) {
         const double piv = __shfl_sync(FULL, row[k], k);
         if (!(piv > 0.0)) return false;
-        const double dkk = sqrt(piv);
         const double inv = rsqrt(piv);  // 1 / L_kk, kept for the triangular solves
+        const double dkk = piv * inv;   // L_kk (the solves only use 1 / L_kk)
         if (lane == k) rin = inv;
         const double lik = lane == k ? dkk : row[k] * inv;
         if (lane >= k) row[k] = lik;
