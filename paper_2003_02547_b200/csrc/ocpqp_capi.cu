@@ -412,10 +412,13 @@ void place_fast(OcpPlan* P, long long budget_per_cta) {
     const int np = P->shape.kind == 1 ? (int)(sizeof(prio1) / sizeof(int)) : (int)(sizeof(prio0) / sizeof(int));
     long long used = 0;
     P->smem_mask = 0;
+    // experiments: OCPQP_NOSMEM = bitmask of workspace buffers kept in global memory
+    const char* envx = getenv("OCPQP_NOSMEM");
+    const unsigned long long nosmem = envx ? strtoull(envx, nullptr, 0) : 0ull;
     for (int i = 0; i < np; ++i) {
         const int b = prio[i];
         const long long bytes = align2(L.ws_size[b]) * 8;
-        if (bytes == 0) continue;
+        if (bytes == 0 || ((nosmem >> b) & 1ull)) continue;
         if (used + bytes <= budget) {
             P->smem_mask |= 1ull << b;
             P->smem_off[b] = (int)(used / 8);
