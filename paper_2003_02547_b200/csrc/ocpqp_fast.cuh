@@ -118,6 +118,14 @@ __device__ __forceinline__ double tmin(double v, double* red) {
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
+// L2 prefetch of n doubles at a global address, one 128-byte line per thread
+// slot (prefetch.global.L2: no register result, no smem)
+template <int TEAM>
+__device__ __forceinline__ void team_pf_l2(const double* p, int n) {
+    for (int i = threadIdx.x * 16; i < n; i += TEAM * 16)
+        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p + i));
+}
+
 struct AbsMax {
     double m = 0.0;
     int nan = 0;
@@ -537,6 +545,14 @@ struct Shape {
     // small input dimension: every thread factors G_uu in registers (no warp
     // Cholesky / flag round trip) and the sweeps fuse their per-stage steps
     static constexpr bool SMALL = NU <= 4;
+    // L2 prefetch of the next stage's operands (data and factor store) in the
+    // sequential recursions: large shapes, whose per-QP data / store live in
+    // L2 or HBM (OCPQP_L2PF=0/1 forces it off/on)
+#ifdef OCPQP_L2PF
+    static constexpr bool L2PF = OCPQP_L2PF != 0;
+#else
+    static constexpr bool L2PF = NX >= 20;
+#endif
     // FP64 tensor-core (DMMA) stage GEMMs.  Measured per config (tools/sweep.py,
     // DMMA vs register-tiled DFMA): config 4 198 -> 164 ms, config 2 102 ->
     // 96.5 ms; slower on config 1 (8x11 stages) and config 3 (nu = 10 pads
@@ -925,6 +941,15 @@ struct Kern {
             OCPQP_TICK(c, DBG_F_P);
             const double* An = A(c, n);
             const double* Bn = Bm(c, n);
+            if constexpr (S::L2PF) {
+                if (n > 0) {
+                    team_pf_l2<TEAM>(A(c, n - 1), NX * NX);
+                    team_pf_l2<TEAM>(Bm(c, n - 1), NX * NU);
+                    team_pf_l2<TEAM>(Q(c, n - 1), NX * NX);
+                    team_pf_l2<TEAM>(Sm(c, n - 1), NU * NX);
+                    team_pf_l2<TEAM>(R(c, n - 1), NU * NU);
+                }
+            }
             double* H = FB + (n & 1) * S::HALF;
             if (fpf) {
                 if (n > 0) {
@@ -1315,6 +1340,14 @@ struct Kern {
         if (!ss) bar<TEAM>();
         for (int n = N - 1; n >= 0; --n) {
             const int h = n & 1;
+            if constexpr (S::L2PF && !ss) {
+                if (n > 0) {  // next stage's operands toward L2 while this one computes
+                    if (gP) team_pf_l2<TEAM>(Pst + n * NX * NX, NX * NX);
+                    team_pf_l2<TEAM>(A(c, n - 1), NX * NX);
+                    team_pf_l2<TEAM>(Bm(c, n - 1), NX * NU);
+                    if (gK) team_pf_l2<TEAM>(Kst + (n - 1) * NU * NX, NU * NX);
+                }
+            }
             if (ss) {
                 if (n > 0) issue(n - 1, h ^ 1, true);
                 if (n > 0) cpa_wait<1>(); else cpa_wait<0>();
@@ -1385,6 +1418,13 @@ struct Kern {
             for (int i = tid; i < NX; i += TEAM) dy[(N > 0 ? NU : 0) + i] = xa[i];
             for (int n = 0; n < N; ++n) {
                 const int h = n & 1;
+                if constexpr (S::L2PF && !ss) {
+                    if (n + 1 < N) {
+                        if (gK) team_pf_l2<TEAM>(Kst + (n + 1) * NU * NX, NU * NX);
+                        team_pf_l2<TEAM>(A(c, n + 1), NX * NX);
+                        team_pf_l2<TEAM>(Bm(c, n + 1), NX * NU);
+                    }
+                }
                 if (ss) {
                     if (n + 1 < N) issue(n + 1, h ^ 1, false);
                     if (n + 1 < N) cpa_wait<1>(); else cpa_wait<0>();
