@@ -19,6 +19,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #pragma once
 #include "ocpqp_internal.h"
 
@@ -380,18 +382,28 @@ __host__ __device__ constexpr int gemm_pick(int M, int N, int TEAM) {
     return best;
 }
 
-template <int M, int N, int K, int TEAM, class FA, class FB, class FE>
-__device__ __forceinline__ void tile_gemm(FA a, FB b, FE epi) {
+// Epilogue operand: pre(i, j) is evaluated BEFORE the k loop (its loads overlap
+// the GEMM), epi(i, j, acc, pre_value) stores.  NoPre: no operand.
+struct NoPre {
+    __device__ __forceinline__ double operator()(int, int) const { return 0.0; }
+};
+
+template <int M, int N, int K, int TEAM, class FA, class FB, class FP, class FE>
+__device__ __forceinline__ void tile_gemm(FA a, FB b, FP pre, FE epi) {
     constexpr int PK = gemm_pick(M, N, TEAM);
     constexpr int TM = PK / 8, TN = PK % 8;
     constexpr int MT = (M + TM - 1) / TM, NT = (N + TN - 1) / TN, TILES = MT * NT;
+    constexpr bool HASPRE = !std::is_same<FP, NoPre>::value;
     for (int t = threadIdx.x; t < TILES; t += TEAM) {
         const int r0 = (t / NT) * TM, c0 = (t % NT) * TN;
-        double acc[TM][TN];
+        double acc[TM][TN], pv[TM][TN];
 #pragma unroll
         for (int i = 0; i < TM; ++i)
 #pragma unroll
-            for (int j = 0; j < TN; ++j) acc[i][j] = 0.0;
+            for (int j = 0; j < TN; ++j) {
+                acc[i][j] = 0.0;
+                pv[i][j] = (HASPRE && r0 + i < M && c0 + j < N) ? pre(r0 + i, c0 + j) : 0.0;
+            }
         // k unroll: 8 measured best for K <= 30, 16 for the K = 60 stages
         constexpr int KU = K >= 48 ? 2 * OCPQP_K_UNROLL_N : OCPQP_K_UNROLL_N;
 #pragma unroll KU
@@ -410,7 +422,7 @@ __device__ __forceinline__ void tile_gemm(FA a, FB b, FE epi) {
         for (int i = 0; i < TM; ++i)
 #pragma unroll
             for (int j = 0; j < TN; ++j)
-                if (r0 + i < M && c0 + j < N) epi(r0 + i, c0 + j, acc[i][j]);
+                if (r0 + i < M && c0 + j < N) epi(r0 + i, c0 + j, acc[i][j], pv[i][j]);
     }
 }
 
@@ -428,8 +440,9 @@ __device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, doubl
 #ifndef OCPQP_MMA_NBW
 #define OCPQP_MMA_NBW 2
 #endif
-template <int M, int N, int K, int TEAM, class FA, class FB, class FE>
-__device__ __forceinline__ void tile_mma(FA a, FB b, FE epi) {
+template <int M, int N, int K, int TEAM, class FA, class FB, class FP, class FE>
+__device__ __forceinline__ void tile_mma(FA a, FB b, FP pre, FE epi) {
+    constexpr bool HASPRE = !std::is_same<FP, NoPre>::value;
     constexpr int NWARP = TEAM / 32;
     // warp tile 8 x (8*NBW): NBW independent accumulators share the A fragment
     constexpr int NBW0 = OCPQP_MMA_NBW;
@@ -440,9 +453,17 @@ __device__ __forceinline__ void tile_mma(FA a, FB b, FE epi) {
     for (int t = warp; t < MB * NB; t += NWARP) {
         const int r0 = (t / NB) * 8, c0 = (t % NB) * (8 * NBW);
         const int ar = r0 + gr;
-        double acc[NBW][2];
+        double acc[NBW][2], pv[NBW][2];
+        {
+            const int i = r0 + gr;
 #pragma unroll
-        for (int q = 0; q < NBW; ++q) acc[q][0] = acc[q][1] = 0.0;
+            for (int q = 0; q < NBW; ++q) {
+                acc[q][0] = acc[q][1] = 0.0;
+                const int j = c0 + 8 * q + 2 * tg;
+                pv[q][0] = (HASPRE && i < M && j < N) ? pre(i, j) : 0.0;
+                pv[q][1] = (HASPRE && i < M && j + 1 < N) ? pre(i, j + 1) : 0.0;
+            }
+        }
 #pragma unroll 5
         for (int ks = 0; ks < KS; ++ks) {
             const int k = ks * 4 + tg;
@@ -462,18 +483,18 @@ __device__ __forceinline__ void tile_mma(FA a, FB b, FE epi) {
 #pragma unroll
             for (int q = 0; q < NBW; ++q) {
                 const int j = c0 + 8 * q + 2 * tg;
-                if (j < N) epi(i, j, acc[q][0]);
-                if (j + 1 < N) epi(i, j + 1, acc[q][1]);
+                if (j < N) epi(i, j, acc[q][0], pv[q][0]);
+                if (j + 1 < N) epi(i, j + 1, acc[q][1], pv[q][1]);
             }
         }
     }
 }
 
 // stage GEMM: DMMA tiles on the large shapes, register-tiled DFMA otherwise
-template <bool MMA, int M, int N, int K, int TEAM, class FA, class FB, class FE>
-__device__ __forceinline__ void stage_gemm(FA a, FB b, FE epi) {
-    if constexpr (MMA) tile_mma<M, N, K, TEAM>(a, b, epi);
-    else tile_gemm<M, N, K, TEAM>(a, b, epi);
+template <bool MMA, int M, int N, int K, int TEAM, class FA, class FB, class FP, class FE>
+__device__ __forceinline__ void stage_gemm(FA a, FB b, FP pre, FE epi) {
+    if constexpr (MMA) tile_mma<M, N, K, TEAM>(a, b, pre, epi);
+    else tile_gemm<M, N, K, TEAM>(a, b, pre, epi);
 }
 
 // accumulate the cycles since the previous tick into phase `slot` (thread 0)
@@ -975,8 +996,8 @@ struct Kern {
             };
             // T1 = P_{n+1} [B A]   (kkt_ocp.py:232)
             stage_gemm<S::DMMA, NX, NW, NX, TEAM>([&](int i, int k) { return Pc[i * NX + k]; },
-                                        [&](int k, int j) { return BA(k, j); },
-                                        [&](int i, int j, double v) { T1[i * NW + j] = v; });
+                                        [&](int k, int j) { return BA(k, j); }, NoPre(),
+                                        [&](int i, int j, double v, double) { T1[i * NW + j] = v; });
             bar<TEAM>();
             OCPQP_TICK(c, DBG_F_T1);
             // G = [B A]' T1 + M~ (kkt_ocp.py:233, 70-80; kkt_common.py:100-115):
@@ -1008,12 +1029,15 @@ struct Kern {
                 if (i == j && reg != 0.0) h += reg;
                 return h;
             };
+            // M~ entries are fetched before the k loops (their loads overlap the GEMMs)
             stage_gemm<S::DMMA, NU, NW, NX, TEAM>([&](int i, int k) { return BA(k, i); },
                                         [&](int k, int j) { return T1[k * NW + j]; },
-                                        [&](int i, int j, double v) { Gu[i * NW + j] = v + Mt(i, j); });
+                                        [&](int i, int j) { return Mt(i, j); },
+                                        [&](int i, int j, double v, double m) { Gu[i * NW + j] = v + m; });
             stage_gemm<S::DMMA, NX, NX, NX, TEAM>([&](int i, int k) { return BA(k, NU + i); },
                                         [&](int k, int j) { return T1[k * NW + NU + j]; },
-                                        [&](int i, int j, double v) { Pc[i * NX + j] = v + Mt(NU + i, NU + j); });
+                                        [&](int i, int j) { return Mt(NU + i, NU + j); },
+                                        [&](int i, int j, double v, double m) { Pc[i * NX + j] = v + m; });
             if (NG > 0) flops += 2ll * NW * NW * NG;
             flops += 2ll * NX * NW * NX + 2ll * NW * NW * NX;
             bar<TEAM>();
@@ -1132,7 +1156,8 @@ struct Kern {
             // P = G_xx + G_ux' K, symmetrised (kkt_ocp.py:244, 251)
             stage_gemm<S::DMMA, NX, NX, NU, TEAM>([&](int i, int k) { return Gu[k * NW + NU + i]; },
                                         [&](int k, int j) { return Kn[k * NX + j]; },
-                                        [&](int i, int j, double v) { T1[i * NX + j] = v + Pc[i * NX + j]; });
+                                        [&](int i, int j) { return Pc[i * NX + j]; },
+                                        [&](int i, int j, double v, double g) { T1[i * NX + j] = v + g; });
             flops += 2ll * NX * NX * NU;
             bar<TEAM>();
             double* Pn = Pst + n * NX * NX;
