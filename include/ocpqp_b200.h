@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define OCPQP_ABI_VERSION 1
+#define OCPQP_ABI_VERSION 2
 
 /* error codes */
 #define OCPQP_OK 0
@@ -66,6 +66,10 @@ extern "C" {
  * (kkt_common.py:84-87) out of the solve; the library reports them per QP */
 #define OCPQP_STATUS_NONPOSITIVE_ITERATE 5
 #define OCPQP_STATUS_SINGULAR_SLACK 6
+/* reference raises RankDeficient (linalg.py:180-184) out of the solve when the
+ * QR array algorithm meets a rank-deficient stage stack outside the per-stage
+ * fallback (kkt_ocp.py:174-191 with use_qr) */
+#define OCPQP_STATUS_RANK_DEFICIENT 7
 
 /* stage-data field ids (reference catalog qp_data.py:248-270, :329-336) */
 enum OcpQpField {
@@ -114,8 +118,11 @@ typedef struct OcpQpDataC {
     int64_t batch_stride[OCPQP_NUM_FIELDS];
 } OcpQpDataC;
 
-/* IpmArg (ipm_core.py:66-128) restricted to what the speed-mode loop reads.
- * ocpqp_solve rejects (OCPQP_E_UNSUPPORTED) the settings of other modes. */
+/* IpmArg (ipm_core.py:66-128).  The leading block is what the speed-mode loop
+ * reads; the trailing block (ABI version 2) selects the other modes of
+ * mode_preset (ipm_core.py:131-168): square-root Riccati, QR array algorithm,
+ * iterative refinement and the absolute formulation.  Unused: reg_dual (not
+ * applied on the OCP backend, kkt_ocp.py:39-41) and kkt_method (dense QPs). */
 typedef struct OcpIpmArgC {
     int32_t iter_max;
     int32_t pred_corr;       /* bool */
@@ -133,6 +140,17 @@ typedef struct OcpIpmArgC {
     double t0;
     double corr_ratio;
     double ftb;
+    /* ABI v2: modes beyond speed */
+    int32_t itref_pred_max;   /* refinement steps on the prediction */
+    int32_t itref_corr_max;   /* refinement steps on the combined direction */
+    int32_t use_qr_fallback;  /* bool: per-stage / whole-factor QR retry */
+    int32_t use_qr_always;    /* bool: every factor by the QR array algorithm */
+    int32_t riccati_variant;  /* 0 classical, 1 square_root */
+    int32_t abs_form;         /* bool: absolute formulation (speed_abs) */
+    int32_t comp_res_pred;    /* bool: residuals every iteration */
+    int32_t mu_only_exit;     /* bool: exit test on mu only (mode speed_abs, ipm_core.py:303-304) */
+    double itref_stop_ratio;
+    double qr_fallback_ratio;
 } OcpIpmArgC;
 
 /* Primal-dual point, batched: y [B,ny], pi [B,ne], lam [B,nc], t [B,nc].

@@ -54,7 +54,13 @@ class OcpIpmArgC(ctypes.Structure):
                 ("tol_ineq", ctypes.c_double), ("tol_comp", ctypes.c_double),
                 ("reg_prim", ctypes.c_double), ("lam_min", ctypes.c_double),
                 ("t_min", ctypes.c_double), ("t0", ctypes.c_double),
-                ("corr_ratio", ctypes.c_double), ("ftb", ctypes.c_double)]
+                ("corr_ratio", ctypes.c_double), ("ftb", ctypes.c_double),
+                # ABI v2: modes beyond speed
+                ("itref_pred_max", ctypes.c_int32), ("itref_corr_max", ctypes.c_int32),
+                ("use_qr_fallback", ctypes.c_int32), ("use_qr_always", ctypes.c_int32),
+                ("riccati_variant", ctypes.c_int32), ("abs_form", ctypes.c_int32),
+                ("comp_res_pred", ctypes.c_int32), ("mu_only_exit", ctypes.c_int32),
+                ("itref_stop_ratio", ctypes.c_double), ("qr_fallback_ratio", ctypes.c_double)]
 
 
 class OcpIterC(ctypes.Structure):
@@ -142,7 +148,13 @@ def arg_to_c(arg):
                       warm, float(arg.alpha_min), float(arg.mu0), float(arg.tol_stat),
                       float(arg.tol_eq), float(arg.tol_ineq), float(arg.tol_comp),
                       float(arg.reg_prim), float(arg.lam_min), float(arg.t_min), float(arg.t0),
-                      float(arg.corr_ratio), float(arg.ftb))
+                      float(arg.corr_ratio), float(arg.ftb),
+                      int(arg.itref_pred_max), int(arg.itref_corr_max),
+                      int(bool(arg.use_qr_fallback)), int(bool(arg.use_qr_always)),
+                      {"classical": 0, "square_root": 1}[arg.riccati_variant],
+                      int(bool(arg.abs_form)), int(bool(arg.comp_res_pred)),
+                      int(arg.mode == "speed_abs"),
+                      float(arg.itref_stop_ratio), float(arg.qr_fallback_ratio))
 
 
 def ptr_of(x):

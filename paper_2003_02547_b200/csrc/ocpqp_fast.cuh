@@ -327,7 +327,7 @@ __device__ bool team_chol(double* L, int n, int* flag, double* rinv) {
 // per-CTA context in shared memory
 struct FCtx {
     const double* f[OCPQP_NUM_FIELDS];
-    double* w[WS_NUM];
+    double* w[WS_EXT0];  // base workspace only (speed mode)
     double red[56];  // team reductions (tred_res: 6 x warps)
     int flag;
     int q;
@@ -1752,7 +1752,7 @@ __global__ void __launch_bounds__(S::TEAM, S::MINB) k_fast_solve(KParams p, Solv
     d.MN = p.NBN + p.NGN; d.nc = p.nc; d.nv = p.nv; d.ne = p.ne; d.msum = p.msum;
     d.inv_m = d.M ? 1.0f / (float)d.M : 0.0f;
     d.inv_2m = d.M ? 0.5f / (float)d.M : 0.0f;
-    for (int b = threadIdx.x; b < WS_NUM; b += S::TEAM)
+    for (int b = threadIdx.x; b < WS_EXT0; b += S::TEAM)
         c.w[b] = ((p.smem_mask >> b) & 1u) ? smem + p.smem_off[b] : gslot + p.ws_off[b];
     double* stg = smem + p.stage_smem;
     while (true) {

@@ -51,8 +51,20 @@ enum WsBuf {
     WS_IY, WS_IPI, WS_ILAM, WS_IT,           // working iterate (shaped kernel)
     WS_RINV,                                 // 1 / L_ii of every stage factor and of L_P0
     WS_TINV,                                 // 1 / t on active slots (nc), per iteration
+    // extended workspace (modes beyond speed; generic kernel only), allocated
+    // on first use in a separate per-slot region (KParams::ws2)
+    WS_LPS,                                  // L_P[n] per stage (nx^2, P_off layout)
+    WS_HASLP,                                // per stage: 1.0 when L_P[n] is present (N+1)
+    WS_MST,                                  // stage Hessian M~ (nw_max^2)
+    WS_QR,                                   // QR stack ((nw_max + nx_max) * nw_max + nx_max^2)
+    WS_RMD,                                  // materialised r_m of the refined direction (nc)
+    WS_GF, WS_BF,                            // view.grad() (ny), view.b() (ne): absolute form
+    WS_RFY, WS_RFPI, WS_RFLAM, WS_RFT,       // refinement residual
+    WS_BY, WS_BPI, WS_BLAM, WS_BT,           // refinement best direction
+    WS_ZT,                                   // L_P' x temporaries of the dpi pass (ne)
     WS_NUM
 };
+constexpr int WS_EXT0 = WS_LPS;              // first buffer of the extended workspace
 
 struct KParams {
     // structure
@@ -70,6 +82,8 @@ struct KParams {
     // workspace
     double* ws;               // slots * ws_slot doubles
     long long ws_slot;        // doubles per slot
+    double* ws2;              // extended workspace: slots * ws2_slot doubles (nullptr = none)
+    long long ws2_slot;
     int ws_off[WS_NUM];       // offsets within a slot
     unsigned long long smem_mask;  // bit b set: buffer b lives in shared memory
     int smem_off[WS_NUM];     // offsets within dynamic smem (doubles)

@@ -121,7 +121,7 @@ __device__ __forceinline__ double cho_solve_lanes(const Team<G>& T, const double
 
 struct RCtx {
     const double* f[OCPQP_NUM_FIELDS];
-    double* w[WS_NUM];
+    double* w[WS_EXT0];  // base workspace only (speed mode)
     double* tile;
     double n_act;
 };
@@ -990,7 +990,7 @@ __global__ void __launch_bounds__(S::THREADS) k_row_solve(KParams p, SolveParams
     RCtx& c = ctx[team];
     double* tsm = smem + (long long)team * p.team_stride;
     double* gslot = p.ws + ((long long)blockIdx.x * S::TEAMS + team) * p.ws_slot;
-    for (int b = T.lane; b < WS_NUM; b += S::G)
+    for (int b = T.lane; b < WS_EXT0; b += S::G)
         c.w[b] = ((p.smem_mask >> b) & 1ull) ? tsm + p.smem_off[b] : gslot + p.ws_off[b];
     if (T.lane == 0) c.tile = tsm + p.stage_smem;
     typename RKern<S>::Dims d;

@@ -18,6 +18,8 @@ Fixtures:
                      with the cost-to-go matrices P[n] and gains K[n]
   residuals.npz      compute_residuals at random points
   known.npz          hand-derivable answers (scalar LQR) and failure statuses
+  modes.npz          balance / robust / square-root / speed_abs solves (MODES),
+                     their Failure ladders and the robust-mode RankDeficient raise
 """
 
 from __future__ import annotations
@@ -239,7 +241,73 @@ def pcond():
     np.savez_compressed(HERE / "pcond.npz", **out)
 
 
+# modes beyond speed (ipm_core.py:131-168): (name, preset, tol, overrides)
+MODES = [
+    ("balance6", "balance", 1e-6, {}),
+    ("balance8", "balance", 1e-8, {}),
+    ("robust6", "robust", 1e-6, {}),
+    ("sqrt8", "speed", 1e-8, {"riccati_variant": "square_root"}),
+    ("abs8", "speed_abs", 1e-8, {}),
+    ("sqrtbal6", "balance", 1e-6, {"riccati_variant": "square_root"}),
+]
+MODE_SOURCES = ([("r%d" % s, ("rnd", s)) for s, _ in RANDOM_CASES]
+                + [("c0q0", ("cfg", 0, 0)), ("c1q1", ("cfg", 1, 1)), ("c1q2", ("cfg", 1, 2)),
+                   ("c2q0", ("cfg", 2, 0)), ("c3q0", ("cfg", 3, 0)), ("c3q1", ("cfg", 3, 1))])
+MODE_HEAVY = [("c4q56", ("cfg", 4, 56), ("balance6", "sqrt8", "robust6"))]
+
+
+def mode_arg(name):
+    import dataclasses
+
+    for n, preset, tol, over in MODES:
+        if n == name:
+            return dataclasses.replace(mpcqp.mode_preset(preset).with_tol(tol), **over)
+    raise KeyError(name)
+
+
+def mode_source(src):
+    if src[0] == "rnd":
+        kw = dict(RANDOM_CASES)[src[1]]
+        return qpgen.build_qp(mpcqp, *qpgen.random_ocp_fields(src[1], **kw))
+    _, cfg, i = src
+    return to_ref(make_batch(cfg, batch=1, start=i).qp(0))
+
+
+def solve_modes():
+    out = {}
+    jobs = [(name, src, m) for name, src in MODE_SOURCES for m, *_ in MODES]
+    jobs += [(name, src, m) for name, src, ms in MODE_HEAVY for m in ms]
+    for name, src, m in jobs:
+        rep = mpcqp.solve_ocp_qp(mode_source(src), mode_arg(m))
+        for k, v in pack_report(rep).items():
+            out[f"{name}_{m}_{k}"] = v
+        print("modes", name, m, rep.status.value, rep.iterations, rep.stats.flops, flush=True)
+    # ladders that end in Failure: the indefinite scalar LQR of known()
+    for m, *_ in MODES:
+        q = qpgen.scalar_lqr(mpcqp)
+        q.set_field("r", 0, [1.0])
+        q.set_field("R", 0, [[-1.0]])
+        q.set_field("Q", 0, [[-1.0]])
+        q.set_field("Q", 1, [[-1.0]])
+        rep = mpcqp.solve_ocp_qp(q, mode_arg(m))
+        out[f"indef_{m}_status"] = STATUS[rep.status.value]
+        out[f"indef_{m}_iters"] = rep.iterations
+        out[f"indef_{m}_flops"] = rep.stats.flops
+    # RankDeficient escapes the QR factor in robust mode (linalg.py:180-184)
+    for m, *_ in MODES:
+        try:
+            rep = mpcqp.solve_ocp_qp(qpgen.rank_deficient(mpcqp), mode_arg(m))
+            out[f"rankdef_{m}_raised"] = 0
+            for k, v in pack_report(rep).items():
+                out[f"rankdef_{m}_{k}"] = v
+        except mpcqp.errors.RankDeficient:
+            out[f"rankdef_{m}_raised"] = 1
+        print("rankdef", m, int(out[f"rankdef_{m}_raised"]), flush=True)
+    np.savez_compressed(HERE / "modes.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["known", "residuals", "newton", "solve_random", "solve_cfg", "pcond"]
+    which = sys.argv[1:] or ["known", "residuals", "newton", "solve_random", "solve_cfg", "pcond",
+                            "solve_modes"]
     for w in which:
         globals()[w]()

@@ -117,3 +117,20 @@ def scalar_lqr(module, bounds=False):
     qp.set_field("A", 0, [[1.0]])
     qp.set_field("B", 0, [[1.0]])
     return qp
+
+
+def rank_deficient(module):
+    """Two-state QP whose terminal stage Hessian diag(1, 1e-34) is positive
+    definite (Cholesky succeeds) but numerically rank deficient for the QR
+    array algorithm (linalg.py:176-184): robust mode raises RankDeficient."""
+    qp = module.OcpQp(module.OcpQpDim(1, nx=[2, 2], nu=[1, 0], nb=[1, 0]))
+    qp.set_field("idxb", 0, [0])
+    qp.set_field("lb", 0, [-1.0])
+    qp.set_field("ub", 0, [1.0])
+    qp.set_field("Q", 0, [[1.0, 0.0], [0.0, 1e-34]])
+    qp.set_field("R", 0, [[1.0]])
+    qp.set_field("q", 0, [1.0, 0.0])
+    qp.set_field("Q", 1, [[1.0, 0.0], [0.0, 1e-34]])
+    qp.set_field("A", 0, [[1.0, 0.0], [0.0, 1.0]])
+    qp.set_field("B", 0, [[1.0], [0.0]])
+    return qp

@@ -41,7 +41,7 @@ def test_header_declares_expected_entry_points():
 def test_library_exports_every_declared_symbol(lib):
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.ocpqp_abi_version() == 1
+    assert lib.ocpqp_abi_version() == 2
 
 
 def test_enum_order_matches_host_field_order():
