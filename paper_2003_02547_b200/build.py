@@ -19,7 +19,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = ROOT / "build" / "obj"
 OUT = PKG / "_lib" / "libocpqp_b200.so"
-HEADERS = [CSRC / "ocpqp_internal.h", CSRC / "ocpqp_fast.cuh", ROOT / "include" / "ocpqp_b200.h"]
+HEADERS = [CSRC / "ocpqp_internal.h", CSRC / "ocpqp_fast.cuh", CSRC / "ocpqp_row.cuh",
+           ROOT / "include" / "ocpqp_b200.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

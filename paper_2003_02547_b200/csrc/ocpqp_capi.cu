@@ -180,6 +180,13 @@ int build_layout(const OcpQpDimC* d, Layout& L) {
     w[WS_IY] = L.ny; w[WS_IPI] = L.ne; w[WS_ILAM] = L.nc; w[WS_IT] = L.nc;
     w[WS_RINV] = kfo + L.nx[0];   // sum nu + nx0
     w[WS_TINV] = L.nc;
+    // extended workspace (modes beyond speed)
+    w[WS_LPS] = Po; w[WS_HASLP] = S; w[WS_MST] = (long long)L.nw_max * L.nw_max;
+    w[WS_QR] = (long long)(L.nw_max + L.nx_max) * L.nw_max + (long long)L.nx_max * L.nx_max;
+    w[WS_RMD] = L.nc; w[WS_GF] = L.ny; w[WS_BF] = L.ne;
+    w[WS_RFY] = w[WS_BY] = L.ny; w[WS_RFPI] = w[WS_BPI] = L.ne;
+    w[WS_RFLAM] = w[WS_RFT] = w[WS_BLAM] = w[WS_BT] = L.nc;
+    w[WS_ZT] = L.ne;
     return OCPQP_OK;
 }
 
@@ -217,6 +224,8 @@ struct OcpPlan {
     int* d_row_slack = nullptr;
     int* d_counter = nullptr;
     double* d_ws = nullptr;
+    double* d_ws2 = nullptr;     // extended workspace (allocated on the first non-speed solve)
+    long long ws2_slot = 0;
     // host-path device buffers (allocated on first use)
     double* h_field[OCPQP_NUM_FIELDS] = {nullptr};
     long long h_field_len[OCPQP_NUM_FIELDS] = {0};
@@ -250,7 +259,7 @@ void place_workspace(OcpPlan* P) {
     threads = std::min(512, std::max(32, (threads + 31) / 32 * 32));
     P->threads = threads;
     long long off = 0;
-    for (int b = 0; b < WS_NUM; ++b) {
+    for (int b = 0; b < WS_EXT0; ++b) {
         P->ws_off[b] = (int)off;
         off += align2(L.ws_size[b]);
     }
@@ -300,6 +309,7 @@ void fill_kparams(const OcpPlan* P, KParams& k, const OcpQpDataC* data, bool use
         k.bs[f] = present ? data->batch_stride[f] : 0;
     }
     k.ws = P->d_ws; k.ws_slot = P->ws_slot;
+    k.ws2 = P->d_ws2; k.ws2_slot = P->ws2_slot;
     for (int b = 0; b < WS_NUM; ++b) { k.ws_off[b] = P->ws_off[b]; k.smem_off[b] = P->smem_off[b]; }
     k.smem_mask = use_smem ? P->smem_mask : 0ull;
     k.counter = P->d_counter;
@@ -391,7 +401,7 @@ void place_fast(OcpPlan* P, long long budget_per_cta) {
     const int teams = fast_teams_per_cta(P->shape);
     P->threads = P->shape.kind == 1 ? 32 * P->shape.wpb : P->shape.team;
     long long off = 0;
-    for (int b = 0; b < WS_NUM; ++b) {
+    for (int b = 0; b < WS_EXT0; ++b) {
         P->ws_off[b] = (int)off;
         off += align2(L.ws_size[b]);
     }
@@ -481,6 +491,33 @@ int check_arg(const OcpIpmArgC* a) {
     if (a->lam_min < 0.0 || a->t_min < 0.0) return fail(OCPQP_E_ARG, "lam_min and t_min must be >= 0");
     if (a->warm_start < 0 || a->warm_start > 2) return fail(OCPQP_E_ARG, "unknown warm_start");
     if (a->iter_max < 0) return fail(OCPQP_E_ARG, "iter_max must be >= 0");
+    if (a->riccati_variant != 0 && a->riccati_variant != 1)
+        return fail(OCPQP_E_ARG, "unknown riccati_variant");
+    if (a->itref_corr_max < 0 || a->itref_pred_max < 0)
+        return fail(OCPQP_E_ARG, "refinement step counts must be >= 0");
+    // the reference's loop reads res.r_g etc. without per-iteration residuals
+    // unless the absolute formulation supplies the rhs (solver.py:191-216)
+    if (!a->comp_res_pred && !a->abs_form)
+        return fail(OCPQP_E_UNSUPPORTED, "comp_res_pred=False needs abs_form=True");
+    return OCPQP_OK;
+}
+
+// modes beyond the classical speed loop run on the generic kernel with the
+// extended workspace
+bool needs_ext(const OcpIpmArgC* a) {
+    return a->itref_corr_max > 0 || a->itref_pred_max > 0 || a->use_qr_fallback ||
+           a->use_qr_always || a->riccati_variant != 0 || a->abs_form || !a->comp_res_pred;
+}
+
+int ensure_ext(OcpPlan* P) {
+    if (P->d_ws2) return OCPQP_OK;
+    long long off = 0;
+    for (int b = WS_EXT0; b < WS_NUM; ++b) {
+        P->ws_off[b] = (int)off;
+        off += align2(P->L.ws_size[b]);
+    }
+    P->ws2_slot = std::max(2ll, off);
+    CUDA_TRY(cudaMalloc(&P->d_ws2, sizeof(double) * (size_t)P->ws2_slot * P->slots));
     return OCPQP_OK;
 }
 
@@ -586,6 +623,7 @@ int ocpqp_plan_destroy(OcpPlan* P) {
     if (!P) return OCPQP_OK;
     cudaFree(P->d_st); cudaFree(P->d_idxb); cudaFree(P->d_idxs); cudaFree(P->d_var_box);
     cudaFree(P->d_row_slack); cudaFree(P->d_counter); cudaFree(P->d_ws); cudaFree(P->d_defaults);
+    cudaFree(P->d_ws2);
     for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) cudaFree(P->h_field[f]);
     cudaFree(P->hy); cudaFree(P->hpi); cudaFree(P->hlam); cudaFree(P->ht);
     cudaFree(P->hstatus); cudaFree(P->hiters); cudaFree(P->hres); cudaFree(P->hflops);
@@ -626,8 +664,11 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
         (Ly.nc && !iter->t) || !stats->status || !stats->iterations || !stats->res || !stats->flops)
         return fail(OCPQP_E_ARG, "iterate / stats buffers must not be NULL");
     if (P->B == 0) return OCPQP_OK;
+    const bool ext = needs_ext(arg);
+    if (ext && (rc = ensure_ext(P))) return rc;
     KParams k;
-    fill_kparams(P, k, data, true);
+    // the generic kernel on a shaped-kernel plan keeps its workspace in global memory
+    fill_kparams(P, k, data, !(ext && P->fast));
     SolveParams sp;
     memset(&sp, 0, sizeof(sp));
     sp.arg = *arg;
@@ -635,12 +676,13 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     sp.status = stats->status; sp.iters = stats->iterations; sp.res = stats->res;
     sp.flops = (long long*)stats->flops; sp.trace = stats->trace;
     cudaError_t e;
-    if (P->fast) {
+    if (P->fast && !ext) {
         fill_defaults(P, k);
         e = launch_fast_solve(P->shape, k, sp, P->grid, P->smem_bytes, (cudaStream_t)stream);
         if (e != cudaSuccess) return cuda_fail(e, "k_fast_solve launch");
     } else {
-        e = launch_ipm_solve(k, sp, P->slots, P->threads, P->smem_bytes, (cudaStream_t)stream);
+        e = launch_ipm_solve(k, sp, P->slots, P->threads, P->fast ? 0 : P->smem_bytes,
+                             (cudaStream_t)stream);
         if (e != cudaSuccess) return cuda_fail(e, "k_ipm_solve launch");
     }
     return OCPQP_OK;
@@ -719,8 +761,11 @@ int ocpqp_solve_host(OcpPlan* P, const OcpQpDataC* hd, const OcpIpmArgC* arg, Oc
     void* mit = mapped_host(hst->iterations);
     void* mres = mapped_host(hst->res);
     void* mfl = mapped_host(hst->flops);
+    // only the shaped kernels keep their iterate on chip; the generic kernel
+    // iterates in the output buffers, which must then be device memory
     const bool direct = my && mpi && mlam && mt && mst && mit && mres && mfl && !hst->trace &&
-                        arg->warm_start == 0 && !getenv("OCPQP_NO_MAPPED");
+                        arg->warm_start == 0 && P->fast && !needs_ext(arg) &&
+                        !getenv("OCPQP_NO_MAPPED");
     if (direct) {
         di = OcpIterC{(double*)my, (double*)mpi, (double*)mlam, (double*)mt};
         ds = OcpStatsC{(int32_t*)mst, (int32_t*)mit, (double*)mres, (int64_t*)mfl, nullptr};

@@ -242,10 +242,15 @@ struct ResNorms {
     double g, b, d, m, mu;
 };
 
-__device__ ResNorms residuals(Ctx& c, const double* y, const double* pi, const double* lam,
+// With lamI / tI non-null: the exact KKT matrix action kkt_apply_vec
+// (kkt_common.py:166-181) on the direction (y, pi, lam, t) at the iterate
+// (lamI, tI) -- the same operators without g, b, d and a_m = t dlam + lam dt.
+__device__ __noinline__ ResNorms residuals(Ctx& c, const double* y, const double* pi, const double* lam,
                               const double* t, double* r_g, double* r_b, double* r_d,
-                              double* r_m /* may be null */) {
+                              double* r_m /* may be null */, const double* lamI = nullptr,
+                              const double* tI = nullptr) {
     const KParams& p = *c.p;
+    const bool homog = lamI != nullptr;
     const int N = c.N;
     const double* act = c.w[WS_ACT];
     const double* dvec = c.w[WS_DVEC];
@@ -282,7 +287,7 @@ __device__ ResNorms residuals(Ctx& c, const double* y, const double* pi, const d
                 for (int k = 0; k < s.nx; ++k) h2 = fma(fget(c, OCPQP_F_Q, s, jx * s.nx + k, 0.0), w[nu + k], h2);
                 g = fget(c, OCPQP_F_q, s, jx, 0.0);
             }
-            double r = (h1 + h2) + g;
+            double r = homog ? h1 + h2 : (h1 + h2) + g;
             // at_pi (view.py:400-409): +pi_{n-1} on x_n, -B'pi_n / -A'pi_n on (u_n, x_n)
             double atp = 0.0;
             if (j >= nu && n > 0) atp = pi[c.st[n - 1].pi_off + (j - nu)];
@@ -312,8 +317,10 @@ __device__ ResNorms residuals(Ctx& c, const double* y, const double* pi, const d
                 const double lsl = (act[kl] != 0.0 ? lam[kl] : 0.0) + (act[ksl] != 0.0 ? lam[ksl] : 0.0);
                 const double lsu = (act[ku] != 0.0 ? lam[ku] : 0.0) + (act[ksu] != 0.0 ? lam[ksu] : 0.0);
                 const int yl = p.nv + s.s_off + j, yu = p.nv + p.ns_tot + s.s_off + j;
-                const double rl = (fget(c, OCPQP_F_Zl, s, j, 0.0) * y[yl] + fget(c, OCPQP_F_zl, s, j, 0.0)) - lsl;
-                const double ru = (fget(c, OCPQP_F_Zu, s, j, 0.0) * y[yu] + fget(c, OCPQP_F_zu, s, j, 0.0)) - lsu;
+                const double gl = homog ? 0.0 : fget(c, OCPQP_F_zl, s, j, 0.0);
+                const double gu = homog ? 0.0 : fget(c, OCPQP_F_zu, s, j, 0.0);
+                const double rl = (fget(c, OCPQP_F_Zl, s, j, 0.0) * y[yl] + gl) - lsl;
+                const double ru = (fget(c, OCPQP_F_Zu, s, j, 0.0) * y[yu] + gu) - lsu;
                 r_g[yl] = rl;
                 r_g[yu] = ru;
                 ag.add(rl);
@@ -331,7 +338,7 @@ __device__ ResNorms residuals(Ctx& c, const double* y, const double* pi, const d
             double ax = 0.0, bu = 0.0;
             for (int k = 0; k < s.nx; ++k) ax = fma(Aget(c, s, i, k), x[k], ax);
             for (int k = 0; k < s.nu; ++k) bu = fma(Bget(c, s, i, k), u[k], bu);
-            const double r = -((xn - ax) - bu) + fget(c, OCPQP_F_b, s, i, 0.0);
+            const double r = homog ? -((xn - ax) - bu) : -((xn - ax) - bu) + fget(c, OCPQP_F_b, s, i, 0.0);
             r_b[s.pi_off + i] = r;
             ab.add(r);
         }
@@ -344,9 +351,14 @@ __device__ ResNorms residuals(Ctx& c, const double* y, const double* pi, const d
             double rd = 0.0, rm = 0.0;
             if (act[kk] != 0.0) {
                 const double cy = slot_cy(c, s, k, rowv, y);
-                rd = (-cy + dvec[kk]) + t[kk];
-                rm = lam[kk] * t[kk];
-                musum += rm;
+                if (homog) {
+                    rd = -cy + t[kk];
+                    rm = tI[kk] * lam[kk] + lamI[kk] * t[kk];
+                } else {
+                    rd = (-cy + dvec[kk]) + t[kk];
+                    rm = lam[kk] * t[kk];
+                    musum += rm;
+                }
             }
             r_d[kk] = rd;
             if (r_m) r_m[kk] = rm;
@@ -414,11 +426,259 @@ __device__ __forceinline__ void cho_solve_serial(const double* L, int n, double*
 }
 
 // ---------------------------------------------------------------------------
-// classical Riccati factor (kkt_ocp.py:142-201, 231-251; kkt_common.py:57-115)
-// returns -1 on success, the failing stage otherwise; -2 non-positive iterate,
-// -3 singular soft-slack block.  flops follow linalg.py counting rules.
+// Householder QR of the m x n (m >= n) row-major stack S in place (LAPACK
+// dgeqr2 / dlarfg reflectors, the arithmetic of np.linalg.qr(mode="r")), then
+// qr_cholesky's rank test and row-sign normalisation (linalg.py:152-187).
+// Returns false on RankDeficient.  Column-parallel reflector application.
 // ---------------------------------------------------------------------------
-__device__ int factor(Ctx& c, const double* lam, const double* t, double reg, long long& flops) {
+__device__ __noinline__ bool team_qr(Ctx& c, double* S, int m, int n) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    for (int k = 0; k < n; ++k) {
+        double ss = 0.0;
+        for (int i = k + 1 + tid; i < m; i += T) ss = fma(S[i * n + k], S[i * n + k], ss);
+        ss = team_sum(ss, c.red);   // same value in every thread
+        if (ss == 0.0) continue;    // H = I (tau = 0)
+        const double alpha = S[k * n + k];
+        const double beta = -copysign(hypot(alpha, sqrt(ss)), alpha);
+        const double tau = (beta - alpha) / beta;
+        const double sc = 1.0 / (alpha - beta);
+        for (int i = k + 1 + tid; i < m; i += T) S[i * n + k] *= sc;
+        tsync();
+        for (int j = k + 1 + tid; j < n; j += T) {
+            double w = S[k * n + j];
+            for (int i = k + 1; i < m; ++i) w = fma(S[i * n + k], S[i * n + j], w);
+            w *= tau;
+            S[k * n + j] -= w;
+            for (int i = k + 1; i < m; ++i) S[i * n + j] = fma(-w, S[i * n + k], S[i * n + j]);
+        }
+        if (tid == 0) S[k * n + k] = beta;
+        tsync();
+    }
+    double dmax = 0.0;
+    for (int i = 0; i < n; ++i) dmax = fmax(dmax, fabs(S[i * n + i]));
+    const double tol = (m > n ? m : n) * 2.220446049250313e-16 * dmax;
+    int bad = 0;
+    for (int i = 0; i < n; ++i)
+        if (!(fabs(S[i * n + i]) > tol)) bad = 1;
+    tsync();
+    if (bad) return false;
+    for (int i = tid; i < n; i += T) {
+        const double sg = S[i * n + i] < 0.0 ? -1.0 : 1.0;
+        for (int j = 0; j < n; ++j) S[i * n + j] = j < i ? 0.0 : sg * S[i * n + j];
+    }
+    tsync();
+    return true;
+}
+
+enum { LINALG_OK = 0, LINALG_NPD = 1, LINALG_RANK = 2 };
+
+// classical stage (kkt_ocp.py:231-251); the stage Hessian M~ is in Mb (== G
+// when it need not survive the stage).  LINALG_OK / LINALG_NPD.
+__device__ __noinline__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops) {
+    const int N = c.N;
+    const int tid = threadIdx.x, T = blockDim.x;
+    const StageInfo& s = c.st[n];
+    const int nu = s.nu, nx = s.nx, nw = s.nw, nxn = s.nxn;
+    double* G = c.w[WS_G];
+    double* T1 = c.w[WS_T1];
+    double* Pall = c.w[WS_P];
+    if (c.w[WS_HASLP] && tid == 0) c.w[WS_HASLP][n] = 0.0;
+    if (n < N) {
+        const double* Pn = Pall + c.st[n + 1].P_off;
+        // T1 = P[n+1] [B A]  (nx' x nw)
+        for (int idx = tid; idx < nxn * nw; idx += T) {
+            const int i = idx / nw, j = idx - i * nw;
+            double a = 0.0;
+            for (int k = 0; k < nxn; ++k) a = fma(Pn[i * nxn + k], BAget(c, s, k, j), a);
+            T1[idx] = a;
+        }
+        tsync();
+        // G = [B A]' T1 + M~
+        for (int idx = tid; idx < nw * nw; idx += T) {
+            const int i = idx / nw, j = idx - i * nw;
+            double a = 0.0;
+            for (int k = 0; k < nxn; ++k) a = fma(BAget(c, s, k, i), T1[k * nw + j], a);
+            G[idx] = a + Mb[idx];
+        }
+        flops += 2ll * nxn * nw * nxn + 2ll * nw * nw * nxn;
+        tsync();
+    } else if (Mb != G) {
+        for (int idx = tid; idx < nw * nw; idx += T) G[idx] = Mb[idx];
+        tsync();
+    }
+    double* P = Pall + s.P_off;
+    if (nu) {
+        double* L = c.w[WS_L] + s.L_off;
+        double* K = c.w[WS_K] + s.K_off;
+        for (int idx = tid; idx < nu * nu; idx += T) {
+            const int i = idx / nu, j = idx - i * nu;
+            L[idx] = G[i * nw + j];
+        }
+        tsync();
+        flops += (long long)nu * nu * nu / 3;
+        if (!team_chol(L, nu, nu, c.iflag)) return LINALG_NPD;
+        // K = -L'^{-1} L^{-1} G_ux  (kkt_ocp.py:240-243), one column per thread
+        for (int j = tid; j < nx; j += T) {
+            for (int i = 0; i < nu; ++i) {
+                double a = G[i * nw + nu + j];
+                for (int k = 0; k < i; ++k) a -= L[i * nu + k] * K[k * nx + j];
+                K[i * nx + j] = a / L[i * nu + i];
+            }
+            for (int i = nu - 1; i >= 0; --i) {
+                double a = K[i * nx + j];
+                for (int k = i + 1; k < nu; ++k) a -= L[k * nu + i] * K[k * nx + j];
+                K[i * nx + j] = a / L[i * nu + i];
+            }
+            for (int i = 0; i < nu; ++i) K[i * nx + j] = -K[i * nx + j];
+        }
+        flops += 2ll * nu * nu * nx;
+        tsync();
+        // P = G_xx + G_ux' K (kkt_ocp.py:244)
+        for (int idx = tid; idx < nx * nx; idx += T) {
+            const int i = idx / nx, j = idx - i * nx;
+            double a = 0.0;
+            for (int k = 0; k < nu; ++k) a = fma(G[k * nw + nu + i], K[k * nx + j], a);
+            T1[idx] = a + G[(nu + i) * nw + nu + j];
+        }
+        flops += 2ll * nx * nx * nu;
+    } else {
+        for (int idx = tid; idx < nx * nx; idx += T) {
+            const int i = idx / nx, j = idx - i * nx;
+            T1[idx] = G[(nu + i) * nw + nu + j];
+        }
+    }
+    tsync();
+    // symmetrise (kkt_ocp.py:251)
+    for (int idx = tid; idx < nx * nx; idx += T) {
+        const int i = idx / nx, j = idx - i * nx;
+        P[idx] = 0.5 * (T1[idx] + T1[j * nx + i]);
+    }
+    tsync();
+    return LINALG_OK;
+}
+
+// square-root / QR stage (kkt_ocp.py:206-230) and _split_stage_factor
+// (:83-91); M~ in WS_MST (extended workspace).  LINALG_OK / NPD / RANK.
+__device__ __noinline__ int stage_sqrt(Ctx& c, int n, bool use_qr, bool classical, long long& flops) {
+    const int N = c.N;
+    const int tid = threadIdx.x, T = blockDim.x;
+    const StageInfo& s = c.st[n];
+    const int nu = s.nu, nx = s.nx, nw = s.nw, nxn = s.nxn;
+    const bool hasW = n < N;
+    const double* M = c.w[WS_MST];
+    double* W = c.w[WS_T1];     // nxn x nw: W = L_{n+1}' [B A]
+    double* LG = c.w[WS_G];     // nw x nw lower
+    double* QR = c.w[WS_QR];
+    double* LPs = c.w[WS_LPS];
+    double* haslp = c.w[WS_HASLP];
+    if (hasW) {
+        const double* Ln;
+        if (haslp[n + 1] != 0.0) {
+            Ln = LPs + c.st[n + 1].P_off;
+        } else {
+            // per-stage QR retry inside a classical sweep (kkt_ocp.py:210-212)
+            const double* Pn = c.w[WS_P] + c.st[n + 1].P_off;
+            for (int idx = tid; idx < nxn * nxn; idx += T) QR[idx] = Pn[idx];
+            tsync();
+            flops += (long long)nxn * nxn * nxn / 3;
+            if (!team_chol(QR, nxn, nxn, c.iflag)) return LINALG_NPD;
+            Ln = QR;
+        }
+        for (int idx = tid; idx < nxn * nw; idx += T) {
+            const int i = idx / nw, j = idx - i * nw;
+            double a = 0.0;
+            for (int k = i; k < nxn; ++k) a = fma(Ln[k * nxn + i], BAget(c, s, k, j), a);
+            W[idx] = a;
+        }
+        flops += 2ll * nxn * nw * nxn;
+        tsync();
+    }
+    if (use_qr) {
+        for (int idx = tid; idx < nw * nw; idx += T) LG[idx] = M[idx];
+        tsync();
+        flops += (long long)nw * nw * nw / 3;
+        if (!team_chol(LG, nw, nw, c.iflag)) return LINALG_NPD;
+        const int mr = nw + (hasW ? nxn : 0);
+        for (int idx = tid; idx < mr * nw; idx += T) {
+            const int i = idx / nw, j = idx - i * nw;
+            QR[idx] = i < nw ? LG[j * nw + i] : W[(i - nw) * nw + j];
+        }
+        tsync();
+        const long long qf = 2ll * mr * nw * nw - (2ll * nw * nw * nw) / 3;
+        flops += qf > 0 ? qf : 0;
+        if (!team_qr(c, QR, mr, nw)) return LINALG_RANK;
+        for (int idx = tid; idx < nw * nw; idx += T) {
+            const int i = idx / nw, j = idx - i * nw;
+            LG[idx] = j <= i ? QR[j * nw + i] : 0.0;
+        }
+        tsync();
+    } else {
+        // G = W' W + M~ (matmul_acc(1, W, W, 1, M, transA), kkt_ocp.py:220)
+        for (int idx = tid; idx < nw * nw; idx += T) {
+            const int i = idx / nw, j = idx - i * nw;
+            double v = M[idx];
+            if (hasW) {
+                double a = 0.0;
+                for (int k = 0; k < nxn; ++k) a = fma(W[k * nw + i], W[k * nw + j], a);
+                v = a + v;
+            }
+            LG[idx] = v;
+        }
+        if (hasW) flops += 2ll * nw * nw * nxn;
+        tsync();
+        flops += (long long)nw * nw * nw / 3;
+        if (!team_chol(LG, nw, nw, c.iflag)) return LINALG_NPD;
+    }
+    // split: L_uu, K = -L_uu^{-T} L_xu', L_P (kkt_ocp.py:83-91)
+    double* LP = LPs + s.P_off;
+    if (nu) {
+        double* L = c.w[WS_L] + s.L_off;
+        for (int idx = tid; idx < nu * nu; idx += T) {
+            const int i = idx / nu, j = idx - i * nu;
+            L[idx] = LG[i * nw + j];
+        }
+        tsync();
+        double* K = c.w[WS_K] + s.K_off;
+        for (int j = tid; j < nx; j += T) {
+            for (int i = nu - 1; i >= 0; --i) {
+                double a = LG[(nu + j) * nw + i];
+                for (int k = i + 1; k < nu; ++k) a -= L[k * nu + i] * K[k * nx + j];
+                K[i * nx + j] = a / L[i * nu + i];
+            }
+            for (int i = 0; i < nu; ++i) K[i * nx + j] = -K[i * nx + j];
+        }
+        flops += (long long)nu * nu * nx;
+    }
+    for (int idx = tid; idx < nx * nx; idx += T) {
+        const int i = idx / nx, j = idx - i * nx;
+        LP[idx] = LG[(nu + i) * nw + nu + j];
+    }
+    if (tid == 0) haslp[n] = 1.0;
+    tsync();
+    if (classical) {
+        // explicit P for the classical stages below (kkt_ocp.py:227-229)
+        double* P = c.w[WS_P] + s.P_off;
+        for (int idx = tid; idx < nx * nx; idx += T) {
+            const int i = idx / nx, j = idx - i * nx;
+            const int kk = i < j ? i : j;
+            double a = 0.0;
+            for (int k = 0; k <= kk; ++k) a = fma(LP[i * nx + k], LP[j * nx + k], a);
+            P[idx] = a;
+        }
+        tsync();
+    }
+    return LINALG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// riccati_factor (kkt_ocp.py:142-201; kkt_common.py:57-115).  Returns -1 on
+// success, the failing stage on FactorizationFailed; -2 NonPositiveIterate,
+// -3 singular soft-slack block, -4 RankDeficient escaping the QR factor.
+// sqrt_variant / use_qr / stage_fb need the extended workspace.  flops follow
+// the linalg.py counting rules.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ int factor(Ctx& c, const double* lam, const double* t, double reg, long long& flops,
+                      bool sqrt_variant = false, bool use_qr = false, bool stage_fb = false) {
     const KParams& p = *c.p;
     const int N = c.N;
     const int tid = threadIdx.x, T = blockDim.x;
@@ -428,10 +688,9 @@ __device__ int factor(Ctx& c, const double* lam, const double* t, double reg, lo
     double* Dl = c.w[WS_DL];
     double* Du = c.w[WS_DU];
     double* G = c.w[WS_G];
-    double* T1 = c.w[WS_T1];
     double* Pall = c.w[WS_P];
-    double* Kall = c.w[WS_K];
-    double* Lall = c.w[WS_L];
+    const bool sqrt_mode = sqrt_variant || use_qr;
+    double* Mb = (sqrt_mode || stage_fb) ? c.w[WS_MST] : G;
     // block_scales for every stage (kkt_common.py:57-97)
     int bad = 0;
     FOR_STAGE_ITEMS(N + 1, p.nc_max, n, k)
@@ -484,7 +743,7 @@ __device__ int factor(Ctx& c, const double* lam, const double* t, double reg, lo
 
     for (int n = N; n >= 0; --n) {
         const StageInfo& s = c.st[n];
-        const int nu = s.nu, nx = s.nx, nw = s.nw, nxn = s.nxn, ng = s.ng;
+        const int nw = s.nw, ng = s.ng;
         const double* cf = coef + s.m_off;
         // stage Hessian M~ (kkt_ocp.py:70-80 + add_reduced_hessian kkt_common.py:100-115)
         for (int idx = tid; idx < nw * nw; idx += T) {
@@ -501,82 +760,24 @@ __device__ int factor(Ctx& c, const double* lam, const double* t, double reg, lo
                 h = a + h;
             }
             if (i == j && reg != 0.0) h += reg;
-            G[idx] = h;
+            Mb[idx] = h;
         }
         if (ng) flops += 2ll * nw * nw * ng;
         tsync();
-        if (n < N) {
-            const double* Pn = Pall + c.st[n + 1].P_off;
-            // T1 = P[n+1] [B A]  (nx' x nw)
-            for (int idx = tid; idx < nxn * nw; idx += T) {
-                const int i = idx / nw, j = idx - i * nw;
-                double a = 0.0;
-                for (int k = 0; k < nxn; ++k) a = fma(Pn[i * nxn + k], BAget(c, s, k, j), a);
-                T1[idx] = a;
-            }
-            tsync();
-            // G = [B A]' T1 + M~
-            for (int idx = tid; idx < nw * nw; idx += T) {
-                const int i = idx / nw, j = idx - i * nw;
-                double a = 0.0;
-                for (int k = 0; k < nxn; ++k) a = fma(BAget(c, s, k, i), T1[k * nw + j], a);
-                G[idx] = a + G[idx];
-            }
-            flops += 2ll * nxn * nw * nxn + 2ll * nw * nw * nxn;
-            tsync();
+        // _factor_stage with the per-stage QR retry (kkt_ocp.py:180-191)
+        const int rc = sqrt_mode ? stage_sqrt(c, n, use_qr, !sqrt_variant, flops)
+                                 : stage_classical(c, n, Mb, flops);
+        if (rc == LINALG_NPD) {
+            if (stage_fb && !use_qr && stage_sqrt(c, n, true, !sqrt_variant, flops) == LINALG_OK)
+                continue;
+            return n;
         }
-        double* P = Pall + s.P_off;
-        if (nu) {
-            double* L = Lall + s.L_off;
-            double* K = Kall + s.K_off;
-            for (int idx = tid; idx < nu * nu; idx += T) {
-                const int i = idx / nu, j = idx - i * nu;
-                L[idx] = G[i * nw + j];
-            }
-            tsync();
-            flops += (long long)nu * nu * nu / 3;
-            if (!team_chol(L, nu, nu, c.iflag)) return n;
-            // K = -L'^{-1} L^{-1} G_ux  (kkt_ocp.py:240-243), one column per thread
-            for (int j = tid; j < nx; j += T) {
-                for (int i = 0; i < nu; ++i) {
-                    double a = G[i * nw + nu + j];
-                    for (int k = 0; k < i; ++k) a -= L[i * nu + k] * K[k * nx + j];
-                    K[i * nx + j] = a / L[i * nu + i];
-                }
-                for (int i = nu - 1; i >= 0; --i) {
-                    double a = K[i * nx + j];
-                    for (int k = i + 1; k < nu; ++k) a -= L[k * nu + i] * K[k * nx + j];
-                    K[i * nx + j] = a / L[i * nu + i];
-                }
-                for (int i = 0; i < nu; ++i) K[i * nx + j] = -K[i * nx + j];
-            }
-            flops += 2ll * nu * nu * nx;
-            tsync();
-            // P = G_xx + G_ux' K (kkt_ocp.py:244)
-            for (int idx = tid; idx < nx * nx; idx += T) {
-                const int i = idx / nx, j = idx - i * nx;
-                double a = 0.0;
-                for (int k = 0; k < nu; ++k) a = fma(G[k * nw + nu + i], K[k * nx + j], a);
-                T1[idx] = a + G[(nu + i) * nw + nu + j];
-            }
-            flops += 2ll * nx * nx * nu;
-        } else {
-            for (int idx = tid; idx < nx * nx; idx += T) {
-                const int i = idx / nx, j = idx - i * nx;
-                T1[idx] = G[(nu + i) * nw + nu + j];
-            }
-        }
-        tsync();
-        // symmetrise (kkt_ocp.py:251)
-        for (int idx = tid; idx < nx * nx; idx += T) {
-            const int i = idx / nx, j = idx - i * nx;
-            P[idx] = 0.5 * (T1[idx] + T1[j * nx + i]);
-        }
-        tsync();
+        if (rc == LINALG_RANK) return -4;
     }
     // L_P0 = chol(P[0]) (kkt_ocp.py:193-200)
     const int nx0 = c.st[0].nx;
-    if (nx0) {
+    const bool lp0 = c.w[WS_HASLP] && c.w[WS_HASLP][0] != 0.0;
+    if (nx0 && !sqrt_variant && !lp0) {
         double* LP0 = c.w[WS_LP0];
         const double* P0 = Pall + c.st[0].P_off;
         for (int idx = tid; idx < nx0 * nx0; idx += T) LP0[idx] = P0[idx];
@@ -598,9 +799,11 @@ struct RmSpec {
     double tau;           // centering shift
     const double* dlam;   // affine step for the corrector term, or nullptr
     const double* dt;
+    int absf = 0;         // absolute formulation: 1 affine (-comp), 2 direction (- 2 comp)
+    double* out = nullptr;  // materialise the active r_m (0 elsewhere) for refinement
 };
 
-__device__ int solve(Ctx& c, const double* lam, const double* t, const double* r_g,
+__device__ __noinline__ int solve(Ctx& c, const double* lam, const double* t, const double* r_g,
                      const double* r_b, const double* r_d, const RmSpec& rm,
                      double* dy, double* dpi, double* dlam, double* dt, long long& flops) {
     const KParams& p = *c.p;
@@ -622,24 +825,30 @@ __device__ int solve(Ctx& c, const double* lam, const double* t, const double* r
     double* pv = c.w[WS_PV];
     double* kff = c.w[WS_KFF];
     double* vec = c.w[WS_VEC];
+    const double* haslp = c.w[WS_HASLP];   // nullptr without the extended workspace
+    const double* LPs = c.w[WS_LPS];
     int nonfinite = 0;
     // fold: w_all = act ? (lam r_d - r_m) / t : 0
     FOR_STAGE_ITEMS(N + 1, p.nc_max, n, k)
         const StageInfo& s = c.st[n];
         if (k < s.nc) {
             const int kk = s.c_off + k;
-            double w = 0.0;
+            double w = 0.0, rmk = 0.0;
             if (act[kk] != 0.0) {
-                double rmk;
                 if (rm.ext) {
                     rmk = rm.ext[kk];
+                } else if (rm.absf == 1) {
+                    rmk = -(lam[kk] * t[kk]);
                 } else {
-                    rmk = lam[kk] * t[kk] - rm.tau;
+                    const double comp = lam[kk] * t[kk];
+                    rmk = comp - rm.tau;
                     if (rm.dlam) rmk = rmk + rm.dlam[kk] * rm.dt[kk];
+                    if (rm.absf == 2) rmk = rmk - 2.0 * comp;
                 }
                 w = (lam[kk] * r_d[kk] - rmk) / t[kk];
             }
             wall[kk] = w;
+            if (rm.out) rm.out[kk] = rmk;
         }
     END_FOR_STAGE_ITEMS
     tsync();
@@ -690,13 +899,29 @@ __device__ int solve(Ctx& c, const double* lam, const double* t, const double* r
         const StageInfo& s = c.st[n];
         const int nu = s.nu, nx = s.nx, nw = s.nw, nxn = s.nxn;
         if (n < N) {
-            const double* Pn = Pall + c.st[n + 1].P_off;
             const double* rb = r_b + s.pi_off;
             const double* pvnext = pv + (c.st[n + 1].pv_off);
-            for (int i = tid; i < nxn; i += T) {
-                double a = 0.0;
-                for (int k = 0; k < nxn; ++k) a = fma(Pn[i * nxn + k], rb[k], a);
-                e[i] = a + pvnext[i];
+            if (haslp && haslp[n + 1] != 0.0) {
+                // p_apply = L_P (L_P' v) (kkt_ocp.py:110-113)
+                const double* Lp = LPs + c.st[n + 1].P_off;
+                for (int i = tid; i < nxn; i += T) {
+                    double a = 0.0;
+                    for (int k = i; k < nxn; ++k) a = fma(Lp[k * nxn + i], rb[k], a);
+                    z[i] = a;
+                }
+                tsync();
+                for (int i = tid; i < nxn; i += T) {
+                    double a = 0.0;
+                    for (int k = 0; k <= i; ++k) a = fma(Lp[i * nxn + k], z[k], a);
+                    e[i] = a + pvnext[i];
+                }
+            } else {
+                const double* Pn = Pall + c.st[n + 1].P_off;
+                for (int i = tid; i < nxn; i += T) {
+                    double a = 0.0;
+                    for (int k = 0; k < nxn; ++k) a = fma(Pn[i * nxn + k], rb[k], a);
+                    e[i] = a + pvnext[i];
+                }
             }
             tsync();
         }
@@ -731,7 +956,7 @@ __device__ int solve(Ctx& c, const double* lam, const double* t, const double* r
     const int nx0 = c.st[0].nx;
     if (nx0) {
         if (tid == 0) {
-            const double* LP0 = c.w[WS_LP0];
+            const double* LP0 = (haslp && haslp[0] != 0.0) ? LPs + c.st[0].P_off : c.w[WS_LP0];
             for (int i = 0; i < nx0; ++i) z[i] = pv[c.st[0].pv_off + i];
             cho_solve_serial(LP0, nx0, z);
             for (int i = 0; i < nx0; ++i) dy[c.st[0].x_off + i] = -z[i];
@@ -767,15 +992,36 @@ __device__ int solve(Ctx& c, const double* lam, const double* t, const double* r
             tsync();
         }
     }
-    // dpi_n = P[n+1] x_{n+1} + pv[n+1]
+    // dpi_n = P[n+1] x_{n+1} + pv[n+1]; square-root stages: L_P (L_P' x)
+    double* zt = c.w[WS_ZT];
+    if (haslp) {
+        FOR_STAGE_ITEMS(N, p.nx_max, n, i)
+            const StageInfo& s = c.st[n];
+            if (i < s.nxn && haslp[n + 1] != 0.0) {
+                const StageInfo& s1 = c.st[n + 1];
+                const double* Lp = LPs + s1.P_off;
+                const double* xn = dy + s1.x_off;
+                double a = 0.0;
+                for (int k = i; k < s.nxn; ++k) a = fma(Lp[k * s.nxn + i], xn[k], a);
+                zt[s.pi_off + i] = a;
+            }
+        END_FOR_STAGE_ITEMS
+        tsync();
+    }
     FOR_STAGE_ITEMS(N, p.nx_max, n, i)
         const StageInfo& s = c.st[n];
         if (i < s.nxn) {
             const StageInfo& s1 = c.st[n + 1];
-            const double* Pn = Pall + s1.P_off;
             const double* xn = dy + s1.x_off;
             double a = 0.0;
-            for (int k = 0; k < s.nxn; ++k) a = fma(Pn[i * s.nxn + k], xn[k], a);
+            if (haslp && haslp[n + 1] != 0.0) {
+                const double* Lp = LPs + s1.P_off;
+                const double* zz = zt + s.pi_off;
+                for (int k = 0; k <= i; ++k) a = fma(Lp[i * s.nxn + k], zz[k], a);
+            } else {
+                const double* Pn = Pall + s1.P_off;
+                for (int k = 0; k < s.nxn; ++k) a = fma(Pn[i * s.nxn + k], xn[k], a);
+            }
             const double v = a + pv[s1.pv_off + i];
             dpi[s.pi_off + i] = v;
             if (!isfinite(v)) nonfinite = 1;
@@ -824,15 +1070,19 @@ __device__ int solve(Ctx& c, const double* lam, const double* t, const double* r
 // IPM vector kernels (ipm_core.py:201-272)
 // ---------------------------------------------------------------------------
 // max_step: largest alpha in (0,1] keeping lam, t >= 0, scaled by ftb
+// The step is (dlam, dt), or (dlam - lam, dt - t) with `absd` (the absolute
+// formulation's solution minus the iterate, ipm_core.py:275-283).
 __device__ double max_step(Ctx& c, const double* lam, const double* t, const double* dlam,
-                           const double* dt, double ftb) {
+                           const double* dt, double ftb, bool absd = false) {
     const KParams& p = *c.p;
     const double* act = c.w[WS_ACT];
     double ratio = INFINITY;
     for (int k = threadIdx.x; k < p.nc; k += blockDim.x) {
         if (act[k] != 0.0) {
-            if (dlam[k] < 0.0) ratio = fmin(ratio, -lam[k] / dlam[k]);
-            if (dt[k] < 0.0) ratio = fmin(ratio, -t[k] / dt[k]);
+            const double dl = absd ? dlam[k] - lam[k] : dlam[k];
+            const double dd = absd ? dt[k] - t[k] : dt[k];
+            if (dl < 0.0) ratio = fmin(ratio, -lam[k] / dl);
+            if (dd < 0.0) ratio = fmin(ratio, -t[k] / dd);
         }
     }
     ratio = team_min(ratio, c.red);
@@ -841,14 +1091,91 @@ __device__ double max_step(Ctx& c, const double* lam, const double* t, const dou
 
 // duality measure at lam + alpha dlam, t + alpha dt
 __device__ double trial_mu(Ctx& c, const double* lam, const double* t, const double* dlam,
-                           const double* dt, double alpha) {
+                           const double* dt, double alpha, bool absd = false) {
     const KParams& p = *c.p;
     const double* act = c.w[WS_ACT];
     double s = 0.0;
     for (int k = threadIdx.x; k < p.nc; k += blockDim.x)
-        if (act[k] != 0.0) s += (lam[k] + alpha * dlam[k]) * (t[k] + alpha * dt[k]);
+        if (act[k] != 0.0) {
+            const double dl = absd ? dlam[k] - lam[k] : dlam[k];
+            const double dd = absd ? dt[k] - t[k] : dt[k];
+            s += (lam[k] + alpha * dl) * (t[k] + alpha * dd);
+        }
     s = team_sum(s, c.red);
     return c.n_act > 0.0 ? s / c.n_act : 0.0;
+}
+
+// every entry of the four vectors finite (QpSolution.isfinite, view.py:666-672)
+__device__ bool team_finite4(Ctx& c, const double* y, const double* pi, const double* lam,
+                             const double* t) {
+    const KParams& p = *c.p;
+    int bad = 0;
+    for (int i = threadIdx.x; i < p.ny; i += blockDim.x) bad |= !isfinite(y[i]);
+    for (int i = threadIdx.x; i < p.ne; i += blockDim.x) bad |= !isfinite(pi[i]);
+    for (int i = threadIdx.x; i < p.nc; i += blockDim.x) bad |= !isfinite(lam[i]) || !isfinite(t[i]);
+    return !team_or(bad);
+}
+
+// x -= base over the four vectors (recover_step_absolute)
+__device__ void sub4(Ctx& c, double* y, double* pi, double* lam, double* t, const double* by,
+                     const double* bpi, const double* blam, const double* bt) {
+    const KParams& p = *c.p;
+    for (int i = threadIdx.x; i < p.ny; i += blockDim.x) y[i] = y[i] - by[i];
+    for (int i = threadIdx.x; i < p.ne; i += blockDim.x) pi[i] = pi[i] - bpi[i];
+    for (int i = threadIdx.x; i < p.nc; i += blockDim.x) {
+        lam[i] = lam[i] - blam[i];
+        t[i] = t[i] - bt[i];
+    }
+    tsync();
+}
+
+__device__ void copy4(Ctx& c, double* y, double* pi, double* lam, double* t, const double* sy,
+                      const double* spi, const double* slam, const double* st) {
+    const KParams& p = *c.p;
+    for (int i = threadIdx.x; i < p.ny; i += blockDim.x) y[i] = sy[i];
+    for (int i = threadIdx.x; i < p.ne; i += blockDim.x) pi[i] = spi[i];
+    for (int i = threadIdx.x; i < p.nc; i += blockDim.x) {
+        lam[i] = slam[i];
+        t[i] = st[i];
+    }
+    tsync();
+}
+
+// max |kkt_rhs_flat(r_g, r_b, r_d, r_m)| with NaN propagation (solver.py:331-333)
+__device__ double rhs_norm(Ctx& c, const double* rg, const double* rb, const double* rd,
+                           const double* rm) {
+    const KParams& p = *c.p;
+    const double* act = c.w[WS_ACT];
+    AbsMax a;
+    for (int i = threadIdx.x; i < p.ny; i += blockDim.x) a.add(rg[i]);
+    for (int i = threadIdx.x; i < p.ne; i += blockDim.x) a.add(rb[i]);
+    for (int k = threadIdx.x; k < p.nc; k += blockDim.x) {
+        a.add(act[k] != 0.0 ? rd[k] : 0.0);
+        a.add(act[k] != 0.0 ? rm[k] : 0.0);
+    }
+    return team_absmax(a, c.red);
+}
+
+// refinement residual kkt_apply_vec(delta) + rhs into WS_RF* (ipm_core.py:335);
+// returns its max |.|
+__device__ double refine_residual(Ctx& c, const double* lam, const double* t, const double* rg,
+                                  const double* rb, const double* rd, const double* rm,
+                                  const double* dy, const double* dpi, const double* dl,
+                                  const double* dt) {
+    const KParams& p = *c.p;
+    const double* act = c.w[WS_ACT];
+    double *ry = c.w[WS_RFY], *rpi = c.w[WS_RFPI], *rl = c.w[WS_RFLAM], *rt = c.w[WS_RFT];
+    residuals(c, dy, dpi, dl, dt, ry, rpi, rl, rt, lam, t);
+    AbsMax a;
+    for (int i = threadIdx.x; i < p.ny; i += blockDim.x) { ry[i] = ry[i] + rg[i]; a.add(ry[i]); }
+    for (int i = threadIdx.x; i < p.ne; i += blockDim.x) { rpi[i] = rpi[i] + rb[i]; a.add(rpi[i]); }
+    for (int k = threadIdx.x; k < p.nc; k += blockDim.x) {
+        rl[k] = rl[k] + (act[k] != 0.0 ? rd[k] : 0.0);
+        rt[k] = rt[k] + (act[k] != 0.0 ? rm[k] : 0.0);
+        a.add(rl[k]);
+        a.add(rt[k]);
+    }
+    return team_absmax(a, c.red);   // includes the barriers that publish WS_RF*
 }
 
 // ---------------------------------------------------------------------------
@@ -856,13 +1183,15 @@ __device__ double trial_mu(Ctx& c, const double* lam, const double* t, const dou
 // ---------------------------------------------------------------------------
 __device__ void make_ctx(Ctx& c, const KParams& p, int q, double* gslot, double* smem,
                          double* red, int* iflag) {
+    double* gslot2 = p.ws2 ? p.ws2 + (long long)blockIdx.x * p.ws2_slot : nullptr;
     c.p = &p;
     c.st = p.st;
     c.N = p.N;
     for (int f = 0; f < OCPQP_NUM_FIELDS; ++f)
         c.f[f] = p.f[f] ? p.f[f] + (long long)q * p.bs[f] : nullptr;
-    for (int b = 0; b < WS_NUM; ++b)
+    for (int b = 0; b < WS_EXT0; ++b)
         c.w[b] = ((p.smem_mask >> b) & 1u) ? smem + p.smem_off[b] : gslot + p.ws_off[b];
+    for (int b = WS_EXT0; b < WS_NUM; ++b) c.w[b] = gslot2 ? gslot2 + p.ws_off[b] : nullptr;
     c.red = red;
     c.iflag = iflag;
     c.n_act = 0.0;
@@ -931,7 +1260,82 @@ __device__ void init_iterate(Ctx& c, const OcpIpmArgC& arg, double* y, double* p
 }
 
 // ---------------------------------------------------------------------------
-// the fused IPM solve of one QP (solver.py:180-308, speed mode)
+// iterative_refinement (ipm_core.py:317-359) through _refine (solver.py:311-321):
+// refines the direction d = (dy, dpi, dl, dt) in place against the rhs
+// (rg, rb, rd, rm; rm materialised, 0 on inactive slots).  The corrections are
+// solved into (cy, cpi, cl, ct).  Returns the final (best) residual norm.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ double refine(Ctx& c, const double* lam, const double* t, const double* rg,
+                         const double* rb, const double* rd, const double* rm, double* dy,
+                         double* dpi, double* dl, double* dt, double* cy, double* cpi, double* cl,
+                         double* ct, int max_steps, double stop_ratio, long long& flops) {
+    const KParams& p = *c.p;
+    const double rn = rhs_norm(c, rg, rb, rd, rm);
+    const double sc = isnan(rn) ? 1.0 : fmax(1.0, rn);
+    double best = refine_residual(c, lam, t, rg, rb, rd, rm, dy, dpi, dl, dt);
+    if (max_steps <= 0 || best <= stop_ratio * sc) return best;
+    double *by = c.w[WS_BY], *bpi = c.w[WS_BPI], *bl = c.w[WS_BLAM], *bt = c.w[WS_BT];
+    copy4(c, by, bpi, bl, bt, dy, dpi, dl, dt);
+    double norm = best;
+    int grew = 0;
+    for (int st = 0; st < max_steps; ++st) {
+        RmSpec rs{c.w[WS_RFT], 0.0, nullptr, nullptr};
+        solve(c, lam, t, c.w[WS_RFY], c.w[WS_RFPI], c.w[WS_RFLAM], rs, cy, cpi, cl, ct, flops);
+        for (int i = threadIdx.x; i < p.ny; i += blockDim.x) dy[i] = dy[i] + cy[i];
+        for (int i = threadIdx.x; i < p.ne; i += blockDim.x) dpi[i] = dpi[i] + cpi[i];
+        for (int k = threadIdx.x; k < p.nc; k += blockDim.x) {
+            dl[k] = dl[k] + cl[k];
+            dt[k] = dt[k] + ct[k];
+        }
+        tsync();
+        const double nn = refine_residual(c, lam, t, rg, rb, rd, rm, dy, dpi, dl, dt);
+        if (nn < best) {
+            copy4(c, by, bpi, bl, bt, dy, dpi, dl, dt);
+            best = nn;
+        }
+        grew = (nn >= norm) ? grew + 1 : 0;
+        norm = nn;
+        if (nn <= stop_ratio * sc) break;
+        if (grew >= 2) break;
+    }
+    copy4(c, dy, dpi, dl, dt, by, bpi, bl, bt);
+    return best;
+}
+
+// ---------------------------------------------------------------------------
+// _factor_with_policy (solver.py:145-164): -1 ok (used_qr set), >= 0 Failure,
+// < -1 an exception of the reference (NonPositiveIterate / SingularSlackBlock /
+// RankDeficient).
+// ---------------------------------------------------------------------------
+__device__ int factor_policy(Ctx& c, const OcpIpmArgC& arg, const double* lam, const double* t,
+                             long long& flops, bool& used_qr) {
+    bool use_qr = arg.use_qr_always != 0;
+    const bool sv = arg.riccati_variant != 0, fb = arg.use_qr_fallback != 0;
+    int fs = factor(c, lam, t, arg.reg_prim, flops, sv, use_qr, fb);
+    if (fs == -1) { used_qr = use_qr; return -1; }
+    if (fs < -1) return fs;
+    if (fb && !use_qr) {
+        fs = factor(c, lam, t, arg.reg_prim, flops, sv, true, fb);
+        if (fs == -1) { used_qr = true; return -1; }
+        if (fs < -1) return fs;
+        use_qr = true;
+    }
+    const double reg2 = arg.reg_prim > 0.0 ? 2.0 * arg.reg_prim : 1e-8;
+    fs = factor(c, lam, t, reg2, flops, sv, use_qr, fb);
+    if (fs == -1) used_qr = use_qr;
+    return fs;
+}
+
+__device__ __forceinline__ int raise_status(int fs) {
+    return fs == -2 ? OCPQP_STATUS_NONPOSITIVE_ITERATE
+         : fs == -3 ? OCPQP_STATUS_SINGULAR_SLACK
+         : fs == -4 ? OCPQP_STATUS_RANK_DEFICIENT : OCPQP_STATUS_FAILURE;
+}
+
+// ---------------------------------------------------------------------------
+// the fused IPM solve of one QP (solver.py:180-308), every mode: speed
+// (classical or square-root Riccati), balance / robust (QR array algorithm,
+// fallback ladder, iterative refinement), speed_abs (absolute formulation)
 // ---------------------------------------------------------------------------
 __device__ void ipm_one(Ctx& c, const SolveParams& sp, int q) {
     const KParams& p = *c.p;
@@ -946,65 +1350,126 @@ __device__ void ipm_one(Ctx& c, const SolveParams& sp, int q) {
     double* r_d = c.w[WS_RD];
     double *ay = c.w[WS_AFF_Y], *api = c.w[WS_AFF_PI], *alam = c.w[WS_AFF_LAM], *at = c.w[WS_AFF_T];
     double *dy = c.w[WS_DIR_Y], *dpi = c.w[WS_DIR_PI], *dlam = c.w[WS_DIR_LAM], *dt = c.w[WS_DIR_T];
+    const double* act = c.w[WS_ACT];
+    const bool absf = arg.abs_form != 0, crp = arg.comp_res_pred != 0;
 
     setup_constraints(c);
     init_iterate(c, arg, y, pi, lam, t);
+    if (absf) {
+        // g_full = view.grad(), b_vec = view.b() (solver.py:184-186): the residual
+        // operators at the zero point
+        double *zy = c.w[WS_BY], *zpi = c.w[WS_BPI], *zl = c.w[WS_BLAM], *zt = c.w[WS_BT];
+        for (int i = threadIdx.x; i < p.ny; i += blockDim.x) zy[i] = 0.0;
+        for (int i = threadIdx.x; i < p.ne; i += blockDim.x) zpi[i] = 0.0;
+        for (int i = threadIdx.x; i < p.nc; i += blockDim.x) { zl[i] = 0.0; zt[i] = 0.0; }
+        tsync();
+        residuals(c, zy, zpi, zl, zt, c.w[WS_GF], c.w[WS_BF], c.w[WS_RFLAM], nullptr);
+    }
+    const double* rg = absf ? c.w[WS_GF] : r_g;
+    const double* rb = absf ? c.w[WS_BF] : r_b;
+    const double* rd = absf ? c.w[WS_DVEC] : r_d;
 
     long long flops = 0;
     double alpha_last = 1.0;
     int it = 0;
     int status = -1;
-    ResNorms res;
-    const double reg2 = arg.reg_prim > 0.0 ? 2.0 * arg.reg_prim : 1e-8;
+    ResNorms res{qnan(), qnan(), qnan(), qnan(), qnan()};
     while (true) {
-        res = residuals(c, y, pi, lam, t, r_g, r_b, r_d, nullptr);
-        const double mu = res.mu;
+        double mu;
+        if (crp) {
+            res = residuals(c, y, pi, lam, t, r_g, r_b, r_d, nullptr);
+            mu = res.mu;
+        } else {
+            // duality_measure of the iterate (ipm_core.py:201-214)
+            double sm = 0.0;
+            for (int k = threadIdx.x; k < p.nc; k += blockDim.x)
+                if (act[k] != 0.0) sm += lam[k] * t[k];
+            sm = team_sum(sm, c.red);
+            mu = c.n_act > 0.0 ? sm / c.n_act : 0.0;
+            if (!team_finite4(c, y, pi, lam, t)) { status = OCPQP_STATUS_NAN; break; }
+        }
         // check_termination (ipm_core.py:286-314)
-        if (!isfinite(res.g) || !isfinite(res.b) || !isfinite(res.d) || !isfinite(res.m) ||
-            !isfinite(mu)) {
+        if (crp && (!isfinite(res.g) || !isfinite(res.b) || !isfinite(res.d) || !isfinite(res.m))) {
+            status = OCPQP_STATUS_NAN;
+        } else if (!isfinite(mu)) {
             status = OCPQP_STATUS_NAN;
         } else if (alpha_last < arg.alpha_min) {
             status = OCPQP_STATUS_MINSTEP;
-        } else if (mu <= arg.tol_comp && res.g <= arg.tol_stat && res.b <= arg.tol_eq &&
-                   res.d <= arg.tol_ineq && res.m <= arg.tol_comp) {
+        } else if (mu <= arg.tol_comp &&
+                   (arg.mu_only_exit || !crp ||
+                    (res.g <= arg.tol_stat && res.b <= arg.tol_eq && res.d <= arg.tol_ineq &&
+                     res.m <= arg.tol_comp))) {
             status = OCPQP_STATUS_SUCCESS;
         } else if (it >= arg.iter_max) {
             status = OCPQP_STATUS_MAXITER;
         }
         if (status >= 0) break;
-        // factorization with the speed-mode ladder (solver.py:145-164)
-        int fs = factor(c, lam, t, arg.reg_prim, flops);
-        if (fs >= 0) fs = factor(c, lam, t, reg2, flops);
-        if (fs == -2) { status = OCPQP_STATUS_NONPOSITIVE_ITERATE; break; }
-        if (fs == -3) { status = OCPQP_STATUS_SINGULAR_SLACK; break; }
-        if (fs >= 0) { status = OCPQP_STATUS_FAILURE; break; }
-        // affine prediction
-        RmSpec rs{nullptr, 0.0, nullptr, nullptr};
-        if (solve(c, lam, t, r_g, r_b, r_d, rs, ay, api, alam, at, flops)) {
-            status = OCPQP_STATUS_NAN;
-            break;
+        bool used_qr = false;
+        const int fs = factor_policy(c, arg, lam, t, flops, used_qr);
+        if (fs != -1) { status = raise_status(fs); break; }
+        // affine prediction (solver.py:207-226)
+        RmSpec ra{nullptr, 0.0, nullptr, nullptr, absf ? 1 : 0,
+                  arg.itref_pred_max > 0 ? c.w[WS_RMD] : nullptr};
+        int nf = solve(c, lam, t, rg, rb, rd, ra, ay, api, alam, at, flops);
+        if (arg.itref_pred_max > 0) {
+            tsync();
+            refine(c, lam, t, rg, rb, rd, c.w[WS_RMD], ay, api, alam, at, dy, dpi, dlam, dt,
+                   arg.itref_pred_max, arg.itref_stop_ratio, flops);
         }
+        if (absf) {
+            sub4(c, ay, api, alam, at, y, pi, lam, t);
+            nf = !team_finite4(c, ay, api, alam, at);
+        } else if (arg.itref_pred_max > 0) {
+            nf = !team_finite4(c, ay, api, alam, at);
+        }
+        if (nf) { status = OCPQP_STATUS_NAN; break; }
         const double alpha_aff = max_step(c, lam, t, alam, at, 1.0);
         const double mu_aff = trial_mu(c, lam, t, alam, at, alpha_aff);
         double sigma = 0.0;
         if (mu > 0.0) sigma = fmin(1.0, fmax(0.0, pow(mu_aff / mu, 3.0)));
         const double tau = sigma * mu;
-        // combined predictor-corrector direction
-        rs.tau = tau;
+        // combined predictor-corrector direction; rm_dir materialised for refinement
+        const bool refine_dir = arg.itref_corr_max > 0;
+        double* rmd = refine_dir ? c.w[WS_RMD] : nullptr;
+        RmSpec rs{nullptr, tau, nullptr, nullptr, absf ? 2 : 0, rmd};
         if (arg.pred_corr) { rs.dlam = alam; rs.dt = at; }
-        int nf = solve(c, lam, t, r_g, r_b, r_d, rs, dy, dpi, dlam, dt, flops);
+        nf = solve(c, lam, t, rg, rb, rd, rs, dy, dpi, dlam, dt, flops);
         if (arg.pred_corr && arg.cond_pred_corr) {
-            const double a_t = max_step(c, lam, t, dlam, dt, 1.0);
-            const double mu_t = trial_mu(c, lam, t, dlam, dt, a_t);
+            const double a_t = max_step(c, lam, t, dlam, dt, 1.0, absf);
+            const double mu_t = trial_mu(c, lam, t, dlam, dt, a_t, absf);
             if (!(mu_t <= arg.corr_ratio * mu_aff)) {
-                RmSpec rc{nullptr, tau, nullptr, nullptr};
-                nf = solve(c, lam, t, r_g, r_b, r_d, rc, dy, dpi, dlam, dt, flops);
+                RmSpec rc{nullptr, tau, nullptr, nullptr, absf ? 2 : 0, rmd};
+                nf = solve(c, lam, t, rg, rb, rd, rc, dy, dpi, dlam, dt, flops);
             }
         }
+        if (refine_dir) {
+            tsync();
+            double ir = refine(c, lam, t, rg, rb, rd, rmd, dy, dpi, dlam, dt, ay, api, alam, at,
+                               arg.itref_corr_max, arg.itref_stop_ratio, flops);
+            if (arg.use_qr_fallback && !used_qr) {
+                const double rn = rhs_norm(c, rg, rb, rd, rmd);
+                if (ir > arg.qr_fallback_ratio * (isnan(rn) ? 1.0 : fmax(1.0, rn))) {
+                    // refactor by the QR array algorithm (solver.py:266-280)
+                    const int f2 = factor(c, lam, t, arg.reg_prim, flops, arg.riccati_variant != 0,
+                                          true, arg.use_qr_fallback != 0);
+                    if (f2 == -1) {
+                        RmSpec rx{rmd, 0.0, nullptr, nullptr};
+                        solve(c, lam, t, rg, rb, rd, rx, dy, dpi, dlam, dt, flops);
+                        tsync();
+                        refine(c, lam, t, rg, rb, rd, rmd, dy, dpi, dlam, dt, ay, api, alam, at,
+                               arg.itref_corr_max, arg.itref_stop_ratio, flops);
+                    } else if (f2 < -1) {
+                        status = raise_status(f2);
+                        break;
+                    }
+                }
+            }
+        }
+        if (absf) sub4(c, dy, dpi, dlam, dt, y, pi, lam, t);
+        if (absf || refine_dir) nf = !team_finite4(c, dy, dpi, dlam, dt);
         if (nf) { status = OCPQP_STATUS_NAN; break; }
         const double alpha = max_step(c, lam, t, dlam, dt, arg.ftb);
         // update_iterate_delta (ipm_core.py:253-272)
-        const double* act = c.w[WS_ACT];
         for (int i = threadIdx.x; i < p.ny; i += blockDim.x) y[i] += alpha * dy[i];
         for (int i = threadIdx.x; i < p.ne; i += blockDim.x) pi[i] += alpha * dpi[i];
         for (int k = threadIdx.x; k < p.nc; k += blockDim.x) {
@@ -1026,8 +1491,9 @@ __device__ void ipm_one(Ctx& c, const SolveParams& sp, int q) {
         alpha_last = alpha;
         ++it;
     }
-    // the final residuals (solver.py:300) are those of the last evaluation: every
-    // exit path leaves the loop before updating the iterate
+    // final residuals (solver.py:300): with per-iteration residuals every exit
+    // leaves the loop before the iterate changes, so they are the last ones
+    if (!crp) res = residuals(c, y, pi, lam, t, r_g, r_b, r_d, nullptr);
     if (threadIdx.x == 0) {
         sp.status[q] = status;
         sp.iters[q] = it;

@@ -3,11 +3,14 @@
 ``IpmArg``, ``mode_preset``, ``Status``, ``IterRecord`` and ``SolverStats``
 carry the same fields, defaults and preset values as the reference
 (mpcqp/ipm_core.py:56-168, :171-198), so an ``arg`` built for the reference
-means the same thing here.  The GPU path implements the ``speed`` preset's
-loop (delta formulation, residuals every iteration, no iterative refinement,
-classical Riccati, Cholesky only); :func:`to_c_arg` rejects the settings of
-the other presets with ``NotImplementedError`` instead of silently running
-something else.
+means the same thing here.  The GPU path implements every preset's loop:
+``speed`` (classical or square-root Riccati), ``balance`` / ``robust``
+(per-stage and whole-factor QR array algorithm, regularised retry, iterative
+refinement of the combined direction) and ``speed_abs`` (absolute
+formulation, duality-measure exit).  ``speed`` with the classical variant runs
+on the shaped kernels; the other settings on the generic kernel.
+:func:`supported_reason` rejects only what the reference itself cannot run
+(``comp_res_pred=False`` without the absolute formulation).
 """
 
 from __future__ import annotations
@@ -145,12 +148,17 @@ class SolverStats:
 
 def supported_reason(arg):
     """None when the GPU loop implements ``arg``; otherwise why not."""
-    if arg.abs_form or not arg.comp_res_pred:
-        return "absolute formulation / speed_abs mode"
-    if arg.itref_corr_max > 0 or arg.itref_pred_max > 0:
-        return "iterative refinement (balance/robust modes)"
-    if arg.use_qr_always or arg.use_qr_fallback:
-        return "QR factorization (balance/robust modes)"
-    if arg.riccati_variant != "classical":
+    if not arg.comp_res_pred and not arg.abs_form:
+        # the reference's loop reads res.r_g of a skipped residual evaluation
+        # (solver.py:191-216) and fails
+        return "comp_res_pred=False without the absolute formulation"
+    if arg.riccati_variant not in ("classical", "square_root"):
         return f"riccati_variant '{arg.riccati_variant}'"
     return None
+
+
+def is_speed_classical(arg):
+    """The setting the shaped (compile-time stage shape) kernels implement."""
+    return (not arg.abs_form and arg.comp_res_pred and arg.itref_corr_max <= 0
+            and arg.itref_pred_max <= 0 and not arg.use_qr_always and not arg.use_qr_fallback
+            and arg.riccati_variant == "classical")

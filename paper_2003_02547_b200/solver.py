@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _native as nat
 from .batch import OcpQpBatch
-from .errors import DimensionMismatch, NonPositiveIterate, SingularSlackBlock
+from .errors import DimensionMismatch, NonPositiveIterate, RankDeficient, SingularSlackBlock
 from .ipm import STATUS_CODES, IpmArg, IterRecord, SolverStats, Status, supported_reason
 from .layout import QpResiduals, QpSolution
 from .qp_data import OcpQp, errors_only, validate
@@ -67,8 +67,7 @@ def _check_arg(arg):
     arg = (arg or IpmArg()).validate()
     why = supported_reason(arg)
     if why is not None:
-        raise NotImplementedError(
-            f"the B200 solver implements the speed-mode loop; unsupported: {why}")
+        raise NotImplementedError(f"unsupported IpmArg setting: {why}")
     return arg
 
 
@@ -140,6 +139,8 @@ class BatchReport:
             raise NonPositiveIterate("lam, t must be > 0 on active rows")
         if code == 6:
             raise SingularSlackBlock("augmented soft-slack diagonal must be > 0")
+        if code == 7:
+            raise RankDeficient("QR array algorithm: rank-deficient stage stack")
         lay = self.batch.layout
         sol = QpSolution(lay, h["y"][i].copy(), h["pi"][i].copy(), h["lam"][i].copy(),
                          h["t"][i].copy())

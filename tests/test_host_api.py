@@ -115,9 +115,14 @@ def test_presets_and_support():
     assert (t.tol_stat, t.tol_eq, t.tol_ineq, t.tol_comp) == (1e-6,) * 4
     assert supported_reason(s) is None
     for m in ("speed_abs", "balance", "robust"):
-        assert supported_reason(mode_preset(m)) is not None
+        assert supported_reason(mode_preset(m)) is None
+    from dataclasses import replace
+
+    # the reference's own loop cannot run this combination (solver.py:191-216)
+    bad = replace(s, comp_res_pred=False)
+    assert supported_reason(bad) is not None
     with pytest.raises(NotImplementedError):
-        pkg.solve_ocp_qp(OcpQp(small_dim()), mode_preset("balance"))
+        pkg.solve_ocp_qp(OcpQp(small_dim()), bad)
     with pytest.raises(ValueError):
         pkg.IpmArg(tol_stat=0.0).validate()
 
