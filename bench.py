@@ -57,10 +57,29 @@ def parse():
                     help="target duration of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="speed",
+                    choices=["speed", "sqrt", "balance", "robust", "speed_abs"],
+                    help="IpmArg preset (sqrt = speed with the square-root Riccati variant); "
+                         "the headline is speed")
+    ap.add_argument("--tol", type=float, default=None,
+                    help="exit tolerance (default 1e-8; 1e-6 for balance / robust, whose "
+                         "lam_min = 1e-10 floors the reachable mu)")
     return ap.parse_args()
 
 
-def workload_name(cfg, B):
+def make_arg(mode, tol):
+    from dataclasses import replace
+
+    from paper_2003_02547_b200.ipm import mode_preset
+
+    if tol is None:
+        tol = 1e-6 if mode in ("balance", "robust") else 1e-8
+    if mode == "sqrt":
+        return replace(mode_preset("speed").with_tol(tol), riccati_variant="square_root"), tol
+    return mode_preset(mode).with_tol(tol), tol
+
+
+def workload_name(cfg, B, mode="speed", tol=1e-8):
     from paper_2003_02547_b200.generators import CONFIGS
 
     s = CONFIGS[cfg]
@@ -70,7 +89,9 @@ def workload_name(cfg, B):
     else:
         desc = (f"{B} x random stage-varying OCP-QP (nx={s.nx}, nu={s.nu}, ng={s.ng}), "
                 f"N={s.N}")
-    return f"BASELINE config {cfg}: {desc}; speed mode, tol 1e-8"
+    mname = "speed mode" if mode == "speed" else (
+        "speed mode, square-root Riccati" if mode == "sqrt" else f"{mode} mode")
+    return f"BASELINE config {cfg}: {desc}; {mname}, tol {tol:g}"
 
 
 class ClockSampler:
@@ -173,11 +194,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     from paper_2003_02547_b200.generators import CONFIGS, make_batch
-    from paper_2003_02547_b200.ipm import mode_preset
 
-    arg = mode_preset("speed").with_tol(1e-8)
+    arg, tol = make_arg(a.mode, a.tol)
     B = a.batch or CONFIGS[a.cfg].batch
-    config = {"workload": workload_name(a.cfg, B), "batch_per_gpu": B,
+    config = {"workload": workload_name(a.cfg, B, a.mode, tol), "batch_per_gpu": B,
               "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
               "l2": "flushed between steps (512 MiB write outside the timed events)"}
 
@@ -250,6 +270,10 @@ def main():
             torch.cuda.synchronize()
     torch.cuda.synchronize()
     plan_info = get_plan(dev).info()
+    from paper_2003_02547_b200.ipm import is_speed_classical
+
+    if not is_speed_classical(arg):
+        plan_info["kernel"] = "generic"   # modes beyond speed run on k_ipm_solve
 
     peak_dfma, peak_dmma = fp64_peak()
     torch.cuda.synchronize()

@@ -230,6 +230,16 @@ int ocpqp_newton_step(OcpPlan* plan, const OcpQpDataC* data, double reg,
  * stage-major row-major, host memory. */
 int ocpqp_factor_export(OcpPlan* plan, int32_t qp, double* P_out, double* K_out);
 
+/* One-stage shift of a batch of solutions into the warm-start guesses of the
+ * next closed-loop MPC solve; replaces mass_spring._shift_guess
+ * (mass_spring.py:152-195): stage n takes stage n+1's x, u, pi, lam, t, the
+ * last input repeats, the terminal state is rolled through the last dynamics,
+ * and the stage-0 initial-state multipliers are rebuilt from the stage-0
+ * stationarity gap.  Needs equal state dimensions over the horizon.  Device
+ * pointers; `guess` must not alias `sol`. */
+int ocpqp_shift_guess(OcpPlan* plan, const OcpQpDataC* data, const OcpIterC* sol,
+                      OcpIterC* guess, void* stream);
+
 /* Plan introspection: out[0..4] = threads per CTA, resident CTA slots,
  * dynamic shared memory bytes per CTA, shared-memory buffer mask, workspace
  * doubles per slot; out[5] kernel kind (0 generic, 1 team, 2 row), out[6]

@@ -49,8 +49,11 @@ def _structs():
     return nat
 
 
-def solve(batch, arg, nthreads=None, trace=True):
-    """Oracle solve of a host OcpQpBatch; returns a dict of numpy arrays."""
+def solve(batch, arg, nthreads=None, trace=True, guess=None):
+    """Oracle solve of a host OcpQpBatch; returns a dict of numpy arrays.
+
+    ``guess`` = (y, pi, lam, t) [B, n] arrays seeds ``arg.warm_start``
+    (solver.py:113-142); without it the solve is cold."""
     nat = _structs()
     b = batch.numpy()
     lay = b.layout
@@ -60,12 +63,17 @@ def solve(batch, arg, nthreads=None, trace=True):
     dc = nat.data_c(b)
     from dataclasses import replace
 
-    carg = nat.arg_to_c(replace(arg, warm_start="none") if arg.warm_start != "none" else arg)
+    if guess is None and arg.warm_start != "none":
+        arg = replace(arg, warm_start="none")
+    carg = nat.arg_to_c(arg)
     out = dict(y=np.zeros((B, lay.ny)), pi=np.zeros((B, lay.ne)), lam=np.zeros((B, lay.nc)),
                t=np.zeros((B, lay.nc)), status=np.zeros(B, dtype=np.int32),
                iters=np.zeros(B, dtype=np.int32), res=np.zeros((B, 5)),
                flops=np.zeros(B, dtype=np.int64),
                trace=np.zeros((B, max(1, arg.iter_max), 8)) if trace else None)
+    if guess is not None:
+        for k, a in zip(("y", "pi", "lam", "t"), guess):
+            out[k][:] = np.asarray(a, dtype=np.float64).reshape(B, -1)
     it = nat.OcpIterC(out["y"].ctypes.data, out["pi"].ctypes.data, out["lam"].ctypes.data,
                       out["t"].ctypes.data)
     st = nat.OcpStatsC(out["status"].ctypes.data, out["iters"].ctypes.data, out["res"].ctypes.data,

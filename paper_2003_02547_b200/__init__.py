@@ -16,6 +16,7 @@ from .condensing import (
     partial_expand_batch,
 )
 from .errors import (
+    ClosedLoopFailed,
     CondenseError,
     DimensionMismatch,
     FactorizationFailed,
@@ -33,6 +34,16 @@ from .errors import (
     UnknownField,
 )
 from .ipm import IpmArg, IterRecord, SolverStats, Status, mode_preset
+from .mpc import (
+    ClosedLoopResult,
+    MassSpringConfig,
+    default_x0,
+    gen_mass_spring,
+    mass_spring_dynamics,
+    run_closed_loop,
+    run_closed_loop_batch,
+    shift_guess,
+)
 from .layout import OcpLayout, QpResiduals, QpSolution
 from .qp_data import OcpQp, OcpQpDim, Violation, validate
 from .solver import (
@@ -48,7 +59,7 @@ from .solver import (
 __version__ = "0.1.0"
 
 __all__ = [
-    "OcpQpBatch", "CondenseError", "DimensionMismatch", "FactorizationFailed",
+    "OcpQpBatch", "ClosedLoopFailed", "CondenseError", "DimensionMismatch", "FactorizationFailed",
     "IndexOutOfRange", "InvalidBlockSize", "InvalidConfig", "InvalidDim", "MpcQpError",
     "NativeLibraryError", "NonPositiveIterate", "NotPositiveDefinite", "RankDeficient",
     "SingularFactor", "SingularSlackBlock", "UnknownField", "IpmArg", "IterRecord",
@@ -56,5 +67,7 @@ __all__ = [
     "OcpQp", "OcpQpDim", "Violation", "validate", "BatchReport", "SolveReport",
     "compute_residuals", "newton_step", "solve_ocp_qp", "solve_ocp_qp_batch",
     "solve_ocp_qp_host", "PartialCondensingMap", "partial_condense", "partial_condense_batch",
-    "partial_expand", "partial_expand_batch", "__version__",
+    "partial_expand", "partial_expand_batch", "ClosedLoopResult", "MassSpringConfig",
+    "default_x0", "gen_mass_spring", "mass_spring_dynamics", "run_closed_loop",
+    "run_closed_loop_batch", "shift_guess", "__version__",
 ]

@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = (
     "ocpqp_solve_host", "ocpqp_residuals", "ocpqp_newton_step", "ocpqp_factor_export",
     "ocpqp_plan_info", "ocpqp_fp64_peak", "ocpqp_abi_version", "ocpqp_last_error",
     "ocpqp_pc_create", "ocpqp_pc_destroy", "ocpqp_pc_dims", "ocpqp_pc_condense",
-    "ocpqp_pc_expand", "ocpqp_pc_last_error",
+    "ocpqp_pc_expand", "ocpqp_pc_last_error", "ocpqp_shift_guess",
 )
 
 _i32p = ctypes.POINTER(ctypes.c_int32)
@@ -105,6 +105,8 @@ def lib():
                                     ctypes.POINTER(OcpIterC), vp, vp, vp, vp,
                                     ctypes.POINTER(OcpIterC), vp, vp]
     L.ocpqp_factor_export.argtypes = [vp, ctypes.c_int32, vp, vp]
+    L.ocpqp_shift_guess.argtypes = [vp, ctypes.POINTER(OcpQpDataC), ctypes.POINTER(OcpIterC),
+                                    ctypes.POINTER(OcpIterC), vp]
     L.ocpqp_abi_version.argtypes = []
     L.ocpqp_last_error.argtypes = []
     L.ocpqp_last_error.restype = ctypes.c_char_p

@@ -816,6 +816,27 @@ int ocpqp_newton_step(OcpPlan* P, const OcpQpDataC* data, double reg, const OcpI
     return OCPQP_OK;
 }
 
+int ocpqp_shift_guess(OcpPlan* P, const OcpQpDataC* data, const OcpIterC* sol, OcpIterC* guess,
+                      void* stream) {
+    if (!P || !sol || !guess) return fail(OCPQP_E_ARG, "NULL argument");
+    const Layout& L = P->L;
+    if ((L.ny && (!sol->y || !guess->y)) || (L.ne && (!sol->pi || !guess->pi)) ||
+        (L.nc && (!sol->lam || !sol->t || !guess->lam || !guess->t)))
+        return fail(OCPQP_E_ARG, "solution / guess buffers must not be NULL");
+    if (sol->y == guess->y) return fail(OCPQP_E_ARG, "guess must not alias the solution");
+    for (int n = 0; n < L.N; ++n)
+        if (L.nx[n] != L.nx[n + 1])
+            return fail(OCPQP_E_DIMENSION, "shift needs equal state dimensions (stage %d)", n);
+    if (P->B == 0) return OCPQP_OK;
+    KParams k;
+    fill_kparams(P, k, data, false);
+    cudaError_t e = launch_shift_guess(k, sol->y, sol->pi, sol->lam, sol->t, guess->y, guess->pi,
+                                       guess->lam, guess->t, P->slots, P->threads,
+                                       (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "k_shift_guess launch");
+    return OCPQP_OK;
+}
+
 int ocpqp_factor_export(OcpPlan* P, int32_t qp, double* P_out, double* K_out) {
     if (!P || qp < 0 || qp >= P->B) return fail(OCPQP_E_ARG, "bad plan or qp index");
     if (P->B > P->slots)

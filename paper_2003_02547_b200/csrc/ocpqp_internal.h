@@ -119,6 +119,10 @@ cudaError_t launch_residuals(const KParams& p, const double* y, const double* pi
                              const double* lam, const double* t, double* rg, double* rb,
                              double* rd, double* rm, double* norms, int grid, int threads,
                              cudaStream_t stream);
+cudaError_t launch_shift_guess(const KParams& p, const double* sy, const double* spi,
+                               const double* slam, const double* st, double* gy, double* gpi,
+                               double* glam, double* gt, int grid, int threads,
+                               cudaStream_t stream);
 int ipm_occupancy(int threads, size_t smem);
 
 // Shaped (compile-time NX, NU, NG, TEAM) fused kernel, ocpqp_fast.cu.  Returns

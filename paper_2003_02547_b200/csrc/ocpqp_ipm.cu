@@ -1586,6 +1586,93 @@ __global__ void __launch_bounds__(512) k_residuals(KParams p, const double* y0, 
 }
 
 // ---------------------------------------------------------------------------
+// _shift_guess (mass_spring.py:152-195): one-stage shift of a solution for the
+// next closed-loop MPC solve.  Stage n takes stage n+1's x, u, pi, lam, t
+// (where the block sizes agree), the last input repeats, the terminal state is
+// rolled once more through the dynamics, and the stage-0 multipliers of the
+// initial-state box rows are rebuilt from the stage-0 stationarity gap.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) k_shift_guess(KParams p, const double* sy, const double* spi,
+                                                     const double* slam, const double* st_,
+                                                     double* gy, double* gpi, double* glam,
+                                                     double* gt) {
+    extern __shared__ double smem[];
+    __shared__ double red[32];
+    __shared__ int iflag[4];
+    double* gslot = p.ws + (long long)blockIdx.x * p.ws_slot;
+    const int N = p.N;
+    for (int q = blockIdx.x; q < p.B; q += gridDim.x) {
+        Ctx c;
+        make_ctx(c, p, q, gslot, smem, red, iflag);
+        setup_constraints(c);
+        const double* y = sy + (long long)q * p.ny;
+        const double* pi = spi + (long long)q * p.ne;
+        const double* lam = slam + (long long)q * p.nc;
+        const double* t = st_ + (long long)q * p.nc;
+        double* Y = gy + (long long)q * p.ny;
+        double* PI = gpi + (long long)q * p.ne;
+        double* LAM = glam + (long long)q * p.nc;
+        double* T = gt + (long long)q * p.nc;
+        // g = copy of sol, then the stage shift (reads sol only)
+        for (int i = threadIdx.x; i < p.ny; i += blockDim.x) Y[i] = y[i];
+        for (int i = threadIdx.x; i < p.ne; i += blockDim.x) PI[i] = pi[i];
+        for (int i = threadIdx.x; i < p.nc; i += blockDim.x) { LAM[i] = lam[i]; T[i] = t[i]; }
+        tsync();
+        if (N >= 1) {
+            FOR_STAGE_ITEMS(N - 1, p.nc_max + p.nw_max + p.nx_max, n, k)
+                const StageInfo& s = c.st[n];
+                const StageInfo& s1 = c.st[n + 1];
+                if (k < p.nx_max) {                       // x(n) = x(n+1), pi(n) = pi(n+1)
+                    if (k < s.nx) Y[s.x_off + k] = y[s1.x_off + k];
+                    if (k < s.nxn && k < s1.nxn) PI[s.pi_off + k] = pi[s1.pi_off + k];
+                } else if (k < p.nx_max + p.nw_max) {     // u(n) = u(n+1) when the shapes agree
+                    const int j = k - p.nx_max;
+                    if (s.nu == s1.nu && j < s.nu) Y[s.u_off + j] = y[s1.u_off + j];
+                } else {                                  // lam / t blocks when the shapes agree
+                    const int j = k - p.nx_max - p.nw_max;
+                    if (s.nc == s1.nc && j < s.nc) {
+                        LAM[s.c_off + j] = lam[s1.c_off + j];
+                        T[s.c_off + j] = t[s1.c_off + j];
+                    }
+                }
+            END_FOR_STAGE_ITEMS
+            const StageInfo& sl = c.st[N - 1];
+            for (int i = threadIdx.x; i < sl.nx; i += blockDim.x) Y[sl.x_off + i] = y[c.st[N].x_off + i];
+            tsync();
+            // x(N) = A x(N-1) + B u(N-1) + b of the shifted guess
+            for (int i = threadIdx.x; i < sl.nxn; i += blockDim.x) {
+                double ax = 0.0, bu = 0.0;
+                for (int k = 0; k < sl.nx; ++k) ax = fma(Aget(c, sl, i, k), Y[sl.x_off + k], ax);
+                for (int k = 0; k < sl.nu; ++k) bu = fma(Bget(c, sl, i, k), Y[sl.u_off + k], bu);
+                Y[c.st[N].x_off + i] = (ax + bu) + fget(c, OCPQP_F_b, sl, i, 0.0);
+            }
+            tsync();
+        }
+        // stage-0 initial-state rows: zero their multipliers, take the gap
+        const StageInfo& s0 = c.st[0];
+        for (int i = threadIdx.x; i < s0.nb; i += blockDim.x)
+            if (p.idxb[s0.ib_off + i] >= s0.nu) {
+                LAM[s0.c_off + i] = 0.0;
+                LAM[s0.c_off + s0.m + i] = 0.0;
+            }
+        tsync();
+        residuals(c, Y, PI, LAM, T, c.w[WS_RG], c.w[WS_RB], c.w[WS_RD], nullptr);
+        const double* rg = c.w[WS_RG];
+        for (int i = threadIdx.x; i < s0.nb; i += blockDim.x) {
+            const int k = p.idxb[s0.ib_off + i];
+            if (k >= s0.nu) {
+                const double gap = rg[s0.x_off + (k - s0.nu)];
+                if (gap >= 0.0) LAM[s0.c_off + i] = gap;
+                else LAM[s0.c_off + s0.m + i] = -gap;
+                T[s0.c_off + i] = 0.0;
+                T[s0.c_off + s0.m + i] = 0.0;
+            }
+        }
+        tsync();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host-side launchers (called from ocpqp_capi.cu)
 // ---------------------------------------------------------------------------
 cudaError_t launch_ipm_solve(const KParams& p, const SolveParams& sp, int grid, int threads,
@@ -1613,6 +1700,14 @@ cudaError_t launch_residuals(const KParams& p, const double* y, const double* pi
                              double* rd, double* rm, double* norms, int grid, int threads,
                              cudaStream_t stream) {
     k_residuals<<<grid, threads, 0, stream>>>(p, y, pi, lam, t, rg, rb, rd, rm, norms);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shift_guess(const KParams& p, const double* sy, const double* spi,
+                               const double* slam, const double* st, double* gy, double* gpi,
+                               double* glam, double* gt, int grid, int threads,
+                               cudaStream_t stream) {
+    k_shift_guess<<<grid, threads, 0, stream>>>(p, sy, spi, slam, st, gy, gpi, glam, gt);
     return cudaGetLastError();
 }
 

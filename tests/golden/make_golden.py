@@ -20,6 +20,8 @@ Fixtures:
   known.npz          hand-derivable answers (scalar LQR) and failure statuses
   modes.npz          balance / robust / square-root / speed_abs solves (MODES),
                      their Failure ladders and the robust-mode RankDeficient raise
+  closed_loop.npz    run_closed_loop trajectories / iteration counts (warm and
+                     cold) and one _shift_guess
 """
 
 from __future__ import annotations
@@ -306,8 +308,42 @@ def solve_modes():
     np.savez_compressed(HERE / "modes.npz", **out)
 
 
+# closed-loop MPC (mass_spring.py:222-273): (name, cfg kwargs, steps, preset, tol, warm)
+CLOSED_LOOP_CASES = [
+    ("m3", dict(masses=3, horizon=10), 8, "balance", 1e-6, "primal_dual"),
+    ("m4", dict(masses=4, horizon=15, x0=[0.5, -0.3, 0.2, -0.6, 0.0, 0.0, 0.0, 0.0]), 6,
+     "speed", 1e-8, "primal_dual"),
+    ("m2", dict(masses=2, horizon=10), 5, "speed", 1e-8, "primal"),
+]
+
+
+def closed_loop():
+    import mpcqp.mass_spring as ms
+
+    out = {}
+    for name, kw, steps, preset, tol, warm in CLOSED_LOOP_CASES:
+        cfg = ms.MassSpringConfig(**kw)
+        res = ms.run_closed_loop(cfg, steps, arg=mpcqp.mode_preset(preset).with_tol(tol),
+                                 warm_start=warm, compare_cold=True)
+        out[f"{name}_states"] = res.states
+        out[f"{name}_inputs"] = res.inputs
+        out[f"{name}_iters"] = np.array([r.iterations for r in res.records])
+        out[f"{name}_cold_iters"] = np.array([r.cold_iterations for r in res.records])
+        out[f"{name}_status"] = np.array([STATUS[r.status] for r in res.records])
+        print("closed loop", name, out[f"{name}_iters"], out[f"{name}_cold_iters"], flush=True)
+    # one shift on its own: solve m3's first QP, shift the solution
+    cfg = ms.MassSpringConfig(masses=3, horizon=10)
+    qp = ms.gen_mass_spring(cfg)
+    rep = mpcqp.solve_ocp_qp(qp, mpcqp.mode_preset("balance").with_tol(1e-6))
+    g = ms._shift_guess(qp, make_view(qp), rep.solution, cfg.horizon)
+    for k in ("y", "pi", "lam", "t"):
+        out[f"shift_sol_{k}"] = getattr(rep.solution, k)
+        out[f"shift_guess_{k}"] = getattr(g, k)
+    np.savez_compressed(HERE / "closed_loop.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["known", "residuals", "newton", "solve_random", "solve_cfg", "pcond",
-                            "solve_modes"]
+                            "solve_modes", "closed_loop"]
     for w in which:
         globals()[w]()
