@@ -223,6 +223,7 @@ struct OcpPlan {
     int* d_var_box = nullptr;
     int* d_row_slack = nullptr;
     int* d_counter = nullptr;
+    int* d_sinv = nullptr;       // stage-invariance mask of the broadcast fields (team kernel)
     double* d_ws = nullptr;
     double* d_ws2 = nullptr;     // extended workspace (allocated on the first non-speed solve)
     long long ws2_slot = 0;
@@ -588,6 +589,7 @@ int ocpqp_plan_create(const OcpQpDimC* dim, int32_t batch, OcpPlan** out) {
     if (e == cudaSuccess) e = cudaMalloc(&P->d_var_box, sizeof(int) * L.var_box.size());
     if (e == cudaSuccess) e = cudaMalloc(&P->d_row_slack, sizeof(int) * L.row_slack.size());
     if (e == cudaSuccess) e = cudaMalloc(&P->d_counter, sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_sinv, sizeof(int));
     for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) P->max_flen = std::max(P->max_flen, L.flen[f]);
     if (e == cudaSuccess) e = cudaMalloc(&P->d_defaults, sizeof(double) * 4 * P->max_flen);
     if (e == cudaSuccess) {
@@ -623,6 +625,7 @@ int ocpqp_plan_destroy(OcpPlan* P) {
     if (!P) return OCPQP_OK;
     cudaFree(P->d_st); cudaFree(P->d_idxb); cudaFree(P->d_idxs); cudaFree(P->d_var_box);
     cudaFree(P->d_row_slack); cudaFree(P->d_counter); cudaFree(P->d_ws); cudaFree(P->d_defaults);
+    cudaFree(P->d_sinv);
     cudaFree(P->d_ws2);
     for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) cudaFree(P->h_field[f]);
     cudaFree(P->hy); cudaFree(P->hpi); cudaFree(P->hlam); cudaFree(P->ht);
@@ -678,6 +681,12 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     cudaError_t e;
     if (P->fast && !ext) {
         fill_defaults(P, k);
+        if (P->shape.kind == 0 && !getenv("OCPQP_NO_SINV")) {
+            e = launch_stage_invariant(k.f, k.bs, P->L.N, P->shape.nx, P->shape.nu, P->d_sinv,
+                                       (cudaStream_t)stream);
+            if (e != cudaSuccess) return cuda_fail(e, "k_stage_invariant launch");
+            k.sinv = P->d_sinv;
+        }
         e = launch_fast_solve(P->shape, k, sp, P->grid, P->smem_bytes, (cudaStream_t)stream);
         if (e != cudaSuccess) return cuda_fail(e, "k_fast_solve launch");
     } else {

@@ -327,6 +327,7 @@ __device__ bool team_chol(double* L, int n, int* flag, double* rinv) {
 // per-CTA context in shared memory
 struct FCtx {
     const double* f[OCPQP_NUM_FIELDS];
+    int ss[OCPQP_F_lb];  // per-stage element stride of A..r (0: identical in every stage)
     double* w[WS_EXT0];  // base workspace only (speed mode)
     double red[56];  // team reductions (tred_res: 6 x warps)
     int flag;
@@ -597,14 +598,14 @@ struct Kern {
     }
 
     // ---- field access (uniform-stage formula offsets) ----
-    __device__ static __forceinline__ const double* A(const FCtx& c, int n) { return c.f[OCPQP_F_A] + n * NX * NX; }
-    __device__ static __forceinline__ const double* Bm(const FCtx& c, int n) { return c.f[OCPQP_F_B] + n * NX * NU; }
-    __device__ static __forceinline__ const double* bv(const FCtx& c, int n) { return c.f[OCPQP_F_b] + n * NX; }
-    __device__ static __forceinline__ const double* Q(const FCtx& c, int n) { return c.f[OCPQP_F_Q] + n * NX * NX; }
-    __device__ static __forceinline__ const double* Sm(const FCtx& c, int n) { return c.f[OCPQP_F_S] + n * NU * NX; }
-    __device__ static __forceinline__ const double* R(const FCtx& c, int n) { return c.f[OCPQP_F_R] + n * NU * NU; }
-    __device__ static __forceinline__ const double* qv(const FCtx& c, int n) { return c.f[OCPQP_F_q] + n * NX; }
-    __device__ static __forceinline__ const double* rv(const FCtx& c, int n) { return c.f[OCPQP_F_r] + n * NU; }
+    __device__ static __forceinline__ const double* A(const FCtx& c, int n) { return c.f[OCPQP_F_A] + n * c.ss[OCPQP_F_A]; }
+    __device__ static __forceinline__ const double* Bm(const FCtx& c, int n) { return c.f[OCPQP_F_B] + n * c.ss[OCPQP_F_B]; }
+    __device__ static __forceinline__ const double* bv(const FCtx& c, int n) { return c.f[OCPQP_F_b] + n * c.ss[OCPQP_F_b]; }
+    __device__ static __forceinline__ const double* Q(const FCtx& c, int n) { return c.f[OCPQP_F_Q] + n * c.ss[OCPQP_F_Q]; }
+    __device__ static __forceinline__ const double* Sm(const FCtx& c, int n) { return c.f[OCPQP_F_S] + n * c.ss[OCPQP_F_S]; }
+    __device__ static __forceinline__ const double* R(const FCtx& c, int n) { return c.f[OCPQP_F_R] + n * c.ss[OCPQP_F_R]; }
+    __device__ static __forceinline__ const double* qv(const FCtx& c, int n) { return c.f[OCPQP_F_q] + n * c.ss[OCPQP_F_q]; }
+    __device__ static __forceinline__ const double* rv(const FCtx& c, int n) { return c.f[OCPQP_F_r] + n * c.ss[OCPQP_F_r]; }
     __device__ static __forceinline__ const double* Cm(const FCtx& c, int n) { return c.f[OCPQP_F_C] + n * NG * NX; }
     __device__ static __forceinline__ const double* Dm(const FCtx& c, int n) { return c.f[OCPQP_F_D] + n * NG * NU; }
     // general-row entry Jg[g][j] = [D C] of stage n (nu_n = NU for n < N, 0 at N)
@@ -1754,6 +1755,14 @@ __global__ void __launch_bounds__(S::TEAM, S::MINB) k_fast_solve(KParams p, Solv
     d.inv_2m = d.M ? 0.5f / (float)d.M : 0.0f;
     for (int b = threadIdx.x; b < WS_EXT0; b += S::TEAM)
         c.w[b] = ((p.smem_mask >> b) & 1u) ? smem + p.smem_off[b] : gslot + p.ws_off[b];
+    if (threadIdx.x == 0) {
+        // stage-invariant broadcast fields (detected on the device by
+        // k_stage_invariant) are read from one copy: stage stride 0
+        constexpr int NX = S::NX, NU = S::NU;
+        const int sz[OCPQP_F_lb] = {NX * NX, NX * NU, NX, NX * NX, NU * NX, NU * NU, NX, NU};
+        const int inv = p.sinv ? *p.sinv : 0;
+        for (int f = 0; f < OCPQP_F_lb; ++f) c.ss[f] = ((inv >> f) & 1) ? 0 : sz[f];
+    }
     double* stg = smem + p.stage_smem;
     while (true) {
         if (threadIdx.x == 0) c.q = atomicAdd(p.counter, 1);

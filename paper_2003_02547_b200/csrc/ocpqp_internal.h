@@ -93,6 +93,8 @@ struct KParams {
     int stage_smem;           // doubles: offset of the per-stage scratch / per-team tile
     int team_stride;          // doubles of shared memory per team (row kernel)
     long long* dbg;           // optional [B, 8] phase-cycle counters (nullptr = off)
+    const int* sinv;          // shaped kernels: bit f set = field f (A..r) identical in every
+                              // stage it is read at (device word, nullptr = none)
 };
 
 // phase ids of the optional clock64 instrumentation (KParams::dbg)
@@ -124,6 +126,10 @@ cudaError_t launch_shift_guess(const KParams& p, const double* sy, const double*
                                double* glam, double* gt, int grid, int threads,
                                cudaStream_t stream);
 int ipm_occupancy(int threads, size_t smem);
+// Stage-invariance detection of the broadcast fields A..r (uniform-stage plans):
+// writes the bit mask consumed by the shaped kernels to *mask.
+cudaError_t launch_stage_invariant(const double* const* f, const long long* bs, int N, int nx,
+                                   int nu, int* mask, cudaStream_t stream);
 
 // Shaped (compile-time NX, NU, NG, TEAM) fused kernel, ocpqp_fast.cu.  Returns
 // cudaErrorNotSupported when no instantiation matches.

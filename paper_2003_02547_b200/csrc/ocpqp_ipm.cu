@@ -1711,6 +1711,37 @@ cudaError_t launch_shift_guess(const KParams& p, const double* sy, const double*
     return cudaGetLastError();
 }
 
+// One block per field A..r: bit f of *mask is set when field f is broadcast
+// (batch stride 0) and every stage the shaped kernels read holds the same bits
+// as stage 0 (A, B, b, S, R, r: stages 0..N-1; Q, q: 0..N).
+struct StageFields {
+    const double* f[OCPQP_F_lb];
+    long long bs[OCPQP_F_lb];
+};
+
+__global__ void k_stage_invariant(StageFields sf, int N, int nx, int nu, int* mask) {
+    const int fi = blockIdx.x;
+    const double* a = sf.f[fi];
+    if (!a || sf.bs[fi] != 0) return;
+    const int sz[OCPQP_F_lb] = {nx * nx, nx * nu, nx, nx * nx, nu * nx, nu * nu, nx, nu};
+    const int last = (fi == OCPQP_F_Q || fi == OCPQP_F_q) ? N : N - 1;
+    const long long L = sz[fi];
+    int diff = 0;
+    for (long long i = threadIdx.x; i < L * last; i += blockDim.x)
+        diff |= __double_as_longlong(a[L + i]) != __double_as_longlong(a[i % L]);
+    if (!__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(mask, 1 << fi);
+}
+
+cudaError_t launch_stage_invariant(const double* const* f, const long long* bs, int N, int nx,
+                                   int nu, int* mask, cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(mask, 0, sizeof(int), stream);
+    if (e != cudaSuccess) return e;
+    StageFields sf;
+    for (int i = 0; i < OCPQP_F_lb; ++i) { sf.f[i] = f[i]; sf.bs[i] = bs[i]; }
+    k_stage_invariant<<<OCPQP_F_lb, 256, 0, stream>>>(sf, N, nx, nu, mask);
+    return cudaGetLastError();
+}
+
 int ipm_occupancy(int threads, size_t smem) {
     int nb = 0;
     cudaFuncSetAttribute(k_ipm_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
