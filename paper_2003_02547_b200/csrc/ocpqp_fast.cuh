@@ -850,6 +850,86 @@ struct Kern {
         return o;
     }
 
+    // L_uu = chol(G_uu) (warp 0, rows in registers; team Cholesky for NU > 32)
+    // and K = -L'^{-1} L^{-1} G_ux, one column per thread (kkt_ocp.py:237-243).
+    // false on a pivot that is not > 0.  Kept out of line so that its NU-long
+    // register arrays do not spill inside the factor.
+    __device__ __noinline__ static bool chol_k(FCtx& c, const long long* dbg, const double* Gu,
+                                               double* Ln, double* Rinv_n, double* rinv,
+                                               double* Kn, double* Z) {
+        struct { const long long* dbg; } p{dbg};  // OCPQP_TICK reads p.dbg
+        const int tid = threadIdx.x;
+        if constexpr (NU <= 32) {
+            if (tid < 32) {
+                double row[NU];
+                double rin = 0.0;
+#pragma unroll
+                for (int j = 0; j < NU; ++j) row[j] = (tid < NU && j <= tid) ? Gu[tid * NW + j] : 0.0;
+                const bool ok = warp_chol<NU>(row, tid, rin);
+                if (tid == 0) c.flag = ok;
+                if (ok && tid < NU) {
+#pragma unroll
+                    for (int j = 0; j < NU; ++j) Ln[tid * NU + j] = j <= tid ? row[j] : 0.0;
+                    rinv[tid] = rin;
+                    Rinv_n[tid] = rin;
+                }
+            }
+            bar<TEAM>();
+            if (!c.flag) return false;
+        } else {
+            for (int idx = tid; idx < NU * NU; idx += TEAM) {
+                const int i = idx / NU, j = idx - i * NU;
+                Ln[idx] = Gu[i * NW + j];
+            }
+            bar<TEAM>();
+            if (!team_chol<TEAM>(Ln, NU, &c.flag, rinv)) return false;
+            for (int i = tid; i < NU; i += TEAM) Rinv_n[i] = rinv[i];
+            bar<TEAM>();
+        }
+        OCPQP_TICK(c, DBG_F_CHOL);
+        // column j of K by forward / back substitution: in registers for small
+        // NU; for larger NU on a shared-memory column (Z: the free T1 tile) --
+        // the register array was demoted to local memory there (NU = 20 spilled)
+        if constexpr (NU <= 16) {
+            for (int j = tid; j < NX; j += TEAM) {
+                double z[NU];
+#pragma unroll
+                for (int i = 0; i < NU; ++i) {
+                    double a = Gu[i * NW + NU + j];
+#pragma unroll
+                    for (int k = 0; k < i; ++k) a = fma(-Ln[i * NU + k], z[k], a);
+                    z[i] = a * rinv[i];
+                }
+#pragma unroll
+                for (int i = NU - 1; i >= 0; --i) {
+                    double a = z[i];
+#pragma unroll
+                    for (int k = i + 1; k < NU; ++k) a = fma(-Ln[k * NU + i], z[k], a);
+                    z[i] = a * rinv[i];
+                }
+#pragma unroll
+                for (int i = 0; i < NU; ++i) Kn[i * NX + j] = -z[i];
+            }
+            return true;
+        }
+        for (int j = tid; j < NX; j += TEAM) {
+            for (int i = 0; i < NU; ++i) {
+                double a = Gu[i * NW + NU + j];
+#pragma unroll 4
+                for (int k = 0; k < i; ++k) a = fma(-Ln[i * NU + k], Z[k * NX + j], a);
+                Z[i * NX + j] = a * rinv[i];
+            }
+            for (int i = NU - 1; i >= 0; --i) {
+                double a = Z[i * NX + j];
+#pragma unroll 4
+                for (int k = i + 1; k < NU; ++k) a = fma(-Ln[k * NU + i], Z[k * NX + j], a);
+                Z[i * NX + j] = a * rinv[i];
+            }
+            for (int i = 0; i < NU; ++i) Kn[i * NX + j] = -Z[i * NX + j];
+        }
+        return true;
+    }
+
     // ---------------- classical Riccati factor ----------------
     // returns -1 ok, failing stage, -2 non-positive iterate
     OCPQP_BIGFN static int factor(FCtx& c, const RD& d, const KParams& p, double* stg,
@@ -1082,73 +1162,10 @@ struct Kern {
 
             double* rinv = vec;  // NU
             flops += (long long)NU * NU * NU / 3;
-            if constexpr (NU <= 32) {
-                if (tid < 32) {
-                    double row[NU];
-                    double rin = 0.0;
-#pragma unroll
-                    for (int j = 0; j < NU; ++j) row[j] = (tid < NU && j <= tid) ? Gu[tid * NW + j] : 0.0;
-                    const bool ok = warp_chol<NU>(row, tid, rin);
-                    if (tid == 0) c.flag = ok;
-                    if (ok && tid < NU) {
-#pragma unroll
-                        for (int j = 0; j < NU; ++j) Ln[tid * NU + j] = j <= tid ? row[j] : 0.0;
-                        rinv[tid] = rin;
-                        Rinv_n[tid] = rin;
-                    }
-                }
-                bar<TEAM>();
-                if (!c.flag) {
-                    if (fpf) cpa_wait<0>();
-                    return n;
-                }
-            } else {
-                for (int idx = tid; idx < NU * NU; idx += TEAM) {
-                    const int i = idx / NU, j = idx - i * NU;
-                    Ln[idx] = Gu[i * NW + j];
-                }
-                bar<TEAM>();
-                if (!team_chol<TEAM>(Ln, NU, &c.flag, rinv)) {
-                    if (fpf) cpa_wait<0>();
-                    return n;
-                }
-                for (int i = tid; i < NU; i += TEAM) Rinv_n[i] = rinv[i];
-                bar<TEAM>();
-            }
-            OCPQP_TICK(c, DBG_F_CHOL);
-            // K = -L'^{-1} L^{-1} G_ux (kkt_ocp.py:240-243), one column per thread
-            for (int j = tid; j < NX; j += TEAM) {
-                if constexpr (NU <= 32) {
-                    double z[NU];
-#pragma unroll
-                    for (int i = 0; i < NU; ++i) {
-                        double a = Gu[i * NW + NU + j];
-#pragma unroll
-                        for (int k = 0; k < i; ++k) a = fma(-Ln[i * NU + k], z[k], a);
-                        z[i] = a * rinv[i];
-                    }
-#pragma unroll
-                    for (int i = NU - 1; i >= 0; --i) {
-                        double a = z[i];
-#pragma unroll
-                        for (int k = i + 1; k < NU; ++k) a = fma(-Ln[k * NU + i], z[k], a);
-                        z[i] = a * rinv[i];
-                    }
-#pragma unroll
-                    for (int i = 0; i < NU; ++i) Kn[i * NX + j] = -z[i];
-                } else {
-                    for (int i = 0; i < NU; ++i) {
-                        double a = Gu[i * NW + NU + j];
-                        for (int k = 0; k < i; ++k) a = fma(-Ln[i * NU + k], Kn[k * NX + j], a);
-                        Kn[i * NX + j] = a * rinv[i];
-                    }
-                    for (int i = NU - 1; i >= 0; --i) {
-                        double a = Kn[i * NX + j];
-                        for (int k = i + 1; k < NU; ++k) a = fma(-Ln[k * NU + i], Kn[k * NX + j], a);
-                        Kn[i * NX + j] = a * rinv[i];
-                    }
-                    for (int i = 0; i < NU; ++i) Kn[i * NX + j] = -Kn[i * NX + j];
-                }
+            // out of line: its row / column registers spill inside the factor
+            if (!chol_k(c, p.dbg, Gu, Ln, Rinv_n, rinv, Kn, T1)) {
+                if (fpf) cpa_wait<0>();
+                return n;
             }
             flops += 2ll * NU * NU * NX;
             bar<TEAM>();

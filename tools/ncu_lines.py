@@ -27,6 +27,8 @@ def main():
     ap.add_argument("obj")
     ap.add_argument("--top", type=int, default=40)
     ap.add_argument("--kernel", default="k_fast_solve")
+    ap.add_argument("--stall", default="Warp Stall Sampling (All Samples)",
+                    help="source-page column to rank by, e.g. stall_long_sb")
     a = ap.parse_args()
     raw = subprocess.run(["ncu", "-i", a.report, "--page", "source", "--csv", "--print-source",
                           "sass"], capture_output=True, text=True).stdout
@@ -48,7 +50,7 @@ def main():
                 return float(row.get(k) or 0)
             except ValueError:
                 return 0.0
-        metrics[addr] = (f("Instructions Executed"), f("Warp Stall Sampling (All Samples)"))
+        metrics[addr] = (f("Instructions Executed"), f(a.stall))
     with tempfile.TemporaryDirectory() as td:
         subprocess.run(["cuobjdump", "-xelf", "all", str(Path(a.obj).resolve())], cwd=td,
                        capture_output=True)
