@@ -224,6 +224,8 @@ struct OcpPlan {
     int* d_row_slack = nullptr;
     int* d_counter = nullptr;
     int* d_sinv = nullptr;       // stage-invariance mask of the broadcast fields (team kernel)
+    double* d_ba = nullptr;      // packed [B A] of every stage (team kernel)
+    long long ba_cap = 0;        // doubles allocated at d_ba
     double* d_ws = nullptr;
     double* d_ws2 = nullptr;     // extended workspace (allocated on the first non-speed solve)
     long long ws2_slot = 0;
@@ -626,6 +628,7 @@ int ocpqp_plan_destroy(OcpPlan* P) {
     cudaFree(P->d_st); cudaFree(P->d_idxb); cudaFree(P->d_idxs); cudaFree(P->d_var_box);
     cudaFree(P->d_row_slack); cudaFree(P->d_counter); cudaFree(P->d_ws); cudaFree(P->d_defaults);
     cudaFree(P->d_sinv);
+    cudaFree(P->d_ba);
     cudaFree(P->d_ws2);
     for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) cudaFree(P->h_field[f]);
     cudaFree(P->hy); cudaFree(P->hpi); cudaFree(P->hlam); cudaFree(P->ht);
@@ -681,11 +684,30 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     cudaError_t e;
     if (P->fast && !ext) {
         fill_defaults(P, k);
-        if (P->shape.kind == 0 && !getenv("OCPQP_NO_SINV")) {
-            e = launch_stage_invariant(k.f, k.bs, P->L.N, P->shape.nx, P->shape.nu, P->d_sinv,
-                                       (cudaStream_t)stream);
-            if (e != cudaSuccess) return cuda_fail(e, "k_stage_invariant launch");
-            k.sinv = P->d_sinv;
+        if (P->shape.kind == 0) {
+            if (!getenv("OCPQP_NO_SINV")) {
+                e = launch_stage_invariant(k.f, k.bs, P->L.N, P->shape.nx, P->shape.nu, P->d_sinv,
+                                           (cudaStream_t)stream);
+                if (e != cudaSuccess) return cuda_fail(e, "k_stage_invariant launch");
+                k.sinv = P->d_sinv;
+            }
+            // [B A] packed per stage: one copy when A and B are broadcast
+            const int nx = P->shape.nx, nu = P->shape.nu;
+            const long long per_qp = (long long)P->L.N * nx * (nx + nu);
+            const bool shared = k.bs[OCPQP_F_A] == 0 && k.bs[OCPQP_F_B] == 0;
+            const long long need = std::max(1ll, per_qp * (shared ? 1 : P->B));
+            if (P->ba_cap < need) {
+                cudaFree(P->d_ba);
+                P->d_ba = nullptr;
+                P->ba_cap = 0;
+                CUDA_TRY(cudaMalloc(&P->d_ba, sizeof(double) * need));
+                P->ba_cap = need;
+            }
+            k.ba = P->d_ba;
+            k.ba_bs = shared ? 0 : per_qp;
+            e = launch_pack_ba(k.f[OCPQP_F_A], k.bs[OCPQP_F_A], k.f[OCPQP_F_B], k.bs[OCPQP_F_B], P->B,
+                               P->L.N, nx, nu, P->d_ba, k.ba_bs, (cudaStream_t)stream);
+            if (e != cudaSuccess) return cuda_fail(e, "k_pack_ba launch");
         }
         e = launch_fast_solve(P->shape, k, sp, P->grid, P->smem_bytes, (cudaStream_t)stream);
         if (e != cudaSuccess) return cuda_fail(e, "k_fast_solve launch");

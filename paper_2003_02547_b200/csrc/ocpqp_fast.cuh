@@ -328,6 +328,8 @@ __device__ bool team_chol(double* L, int n, int* flag, double* rinv) {
 struct FCtx {
     const double* f[OCPQP_NUM_FIELDS];
     int ss[OCPQP_F_lb];  // per-stage element stride of A..r (0: identical in every stage)
+    const double* ba;    // this QP's packed [B A] (NX x NW per stage, KParams::ba)
+    int ba_ss;           // its per-stage stride (0: identical in every stage)
     double* w[WS_EXT0];  // base workspace only (speed mode)
     double red[56];  // team reductions (tred_res: 6 x warps)
     int flag;
@@ -599,6 +601,8 @@ struct Kern {
 
     // ---- field access (uniform-stage formula offsets) ----
     __device__ static __forceinline__ const double* A(const FCtx& c, int n) { return c.f[OCPQP_F_A] + n * c.ss[OCPQP_F_A]; }
+    // packed [B A] of stage n (kkt_ocp.py:177): row k = (B_k., A_k.)
+    __device__ static __forceinline__ const double* BAp(const FCtx& c, int n) { return c.ba + n * c.ba_ss; }
     __device__ static __forceinline__ const double* Bm(const FCtx& c, int n) { return c.f[OCPQP_F_B] + n * c.ss[OCPQP_F_B]; }
     __device__ static __forceinline__ const double* bv(const FCtx& c, int n) { return c.f[OCPQP_F_b] + n * c.ss[OCPQP_F_b]; }
     __device__ static __forceinline__ const double* Q(const FCtx& c, int n) { return c.f[OCPQP_F_Q] + n * c.ss[OCPQP_F_Q]; }
@@ -771,14 +775,10 @@ struct Kern {
                 double atp = (jj >= NU && n > 0) ? pi[(n - 1) * NX + (jj - NU)] : 0.0;
                 double a = 0.0;
                 const double* pn = pi + n * NX;
-                if (jj < NU) {
-                    const double* Bc = Bm(c, n) + jj;
+                {
+                    const double* BAc = BAp(c, n) + jj;   // column jj of [B A]
 #pragma unroll 8
-                    for (int k = 0; k < NX; ++k) a = fma(Bc[k * NU], pn[k], a);
-                } else {
-                    const double* Ac = A(c, n) + (jj - NU);
-#pragma unroll 8
-                    for (int k = 0; k < NX; ++k) a = fma(Ac[k * NX], pn[k], a);
+                    for (int k = 0; k < NX; ++k) a = fma(BAc[k * NW], pn[k], a);
                 }
                 atp -= a;
                 r -= atp;
@@ -814,8 +814,8 @@ struct Kern {
             const double* u = y + n * NW;
             const double* x = u + NU;
             const double xn = y[(n + 1) * NW + (n + 1 < d.N ? NU : 0) + i];
-            const double* Ar = A(c, n) + i * NX;
-            const double* Br = Bm(c, n) + i * NU;
+            const double* Br = BAp(c, n) + i * NW;
+            const double* Ar = Br + NU;
             double ax = 0.0, bu = 0.0;
 #pragma unroll 8
             for (int k = 0; k < NX; ++k) ax = fma(Ar[k], x[k], ax);
@@ -988,15 +988,11 @@ struct Kern {
         constexpr int fQ = NX * NW, fS = fQ + NX * NX, fR = fS + NU * NX;
         auto prefetch = [&](int n, int h) {
             double* H = FB + h * S::HALF;
-            const double* An = A(c, n);
-            const double* Bn = Bm(c, n);
+            const double* BAn = BAp(c, n);
             const double* Qn = Q(c, n);
             const double* Sn = Sm(c, n);
             const double* Rn = R(c, n);
-            for (int e2 = tid; e2 < NX * NW; e2 += TEAM) {
-                const int k = e2 / NW, j = e2 - k * NW;
-                cpa8(H + e2, j < NU ? Bn + k * NU + j : An + k * NX + (j - NU));
-            }
+            for (int e2 = tid; e2 < NX * NW; e2 += TEAM) cpa8(H + e2, BAn + e2);
             if constexpr (S::PF_QSR) {
                 for (int e2 = tid; e2 < NX * NX; e2 += TEAM) cpa8(H + fQ + e2, Qn + e2);
                 for (int e2 = tid; e2 < NU * NX; e2 += TEAM) cpa8(H + fS + e2, Sn + e2);
@@ -1041,12 +1037,10 @@ struct Kern {
         // ---- stages N-1 .. 0 ----
         for (int n = N - 1; n >= 0; --n) {
             OCPQP_TICK(c, DBG_F_P);
-            const double* An = A(c, n);
-            const double* Bn = Bm(c, n);
+            const double* BAn = BAp(c, n);
             if constexpr (S::L2PF) {
                 if (n > 0) {
-                    team_pf_l2<TEAM>(A(c, n - 1), NX * NX);
-                    team_pf_l2<TEAM>(Bm(c, n - 1), NX * NU);
+                    team_pf_l2<TEAM>(BAp(c, n - 1), NX * NW);
                     team_pf_l2<TEAM>(Q(c, n - 1), NX * NX);
                     team_pf_l2<TEAM>(Sm(c, n - 1), NU * NX);
                     team_pf_l2<TEAM>(R(c, n - 1), NU * NU);
@@ -1066,14 +1060,14 @@ struct Kern {
             else if constexpr (S::STAGE_BA) {
                 TEAM_FOR(e, NX * NW)
                     const int k = e / NW, j = e - k * NW;
-                    BAs[e] = j < NU ? Bn[k * NU + j] : An[k * NX + (j - NU)];
+                    BAs[e] = BAn[k * NW + j];
                 TEAM_END
                 bar<TEAM>();
             }
             auto BA = [&](int k, int j) -> double {
                 if (fpf) return H[k * NW + j];
                 if constexpr (S::STAGE_BA) return BAs[k * NW + j];
-                else return j < NU ? Bn[k * NU + j] : An[k * NX + (j - NU)];
+                else return BAn[k * NW + j];
             };
             // T1 = P_{n+1} [B A]   (kkt_ocp.py:232)
             stage_gemm<S::DMMA, NX, NW, NX, TEAM>([&](int i, int k) { return Pc[i * NX + k]; },
@@ -1353,12 +1347,8 @@ struct Kern {
         auto issue = [&](int n, int h, bool bwd) {
             if (ss) {
                 double* H = SB + h * S::HALF;
-                const double* An = A(c, n);
-                const double* Bn = Bm(c, n);
-                for (int e2 = tid; e2 < NX * NW; e2 += TEAM) {
-                    const int k = e2 / NW, j = e2 - k * NW;
-                    cpa8(H + oBA + e2, j < NU ? Bn + k * NU + j : An + k * NX + (j - NU));
-                }
+                const double* BAn = BAp(c, n);
+                for (int e2 = tid; e2 < NX * NW; e2 += TEAM) cpa8(H + oBA + e2, BAn + e2);
                 if (gK) for (int e2 = tid; e2 < NU * NX; e2 += TEAM) cpa8(H + oK + e2, Kst + n * NU * NX + e2);
                 if (gRB) for (int e2 = tid; e2 < NX; e2 += TEAM) cpa8(H + oRB + e2, r_b + n * NX + e2);
                 if (bwd) {
@@ -1386,8 +1376,7 @@ struct Kern {
             if constexpr (S::L2PF && !ss) {
                 if (n > 0) {  // next stage's operands toward L2 while this one computes
                     if (gP) team_pf_l2<TEAM>(Pst + n * NX * NX, NX * NX);
-                    team_pf_l2<TEAM>(A(c, n - 1), NX * NX);
-                    team_pf_l2<TEAM>(Bm(c, n - 1), NX * NU);
+                    team_pf_l2<TEAM>(BAp(c, n - 1), NX * NW);
                     if (gK) team_pf_l2<TEAM>(Kst + (n - 1) * NU * NX, NU * NX);
                 }
             }
@@ -1404,11 +1393,8 @@ struct Kern {
             const double* Ln = (st && gL) ? H + oL : Lst + n * NU * NU;
             const double* Rn = (st && gR) ? H + oR : Rst + n * NU;
             const double* rh = (st && gRH) ? H + oRH : rhat + n * NW;
-            const double* An = A(c, n);
-            const double* Bn = Bm(c, n);
-            auto BA = [&](int k, int j) -> double {
-                return ss ? H[oBA + k * NW + j] : (j < NU ? Bn[k * NU + j] : An[k * NX + (j - NU)]);
-            };
+            const double* BAn = BAp(c, n);
+            auto BA = [&](int k, int j) -> double { return ss ? H[oBA + k * NW + j] : BAn[k * NW + j]; };
             MV<NX, NX, TEAM>::run([&](int i, int k) { return Pn[i * NX + k]; },
                                   [&](int k) { return rb[k]; },
                                   [&](int i, double v) { e[i] = v + pvs[i]; });
@@ -1464,8 +1450,7 @@ struct Kern {
                 if constexpr (S::L2PF && !ss) {
                     if (n + 1 < N) {
                         if (gK) team_pf_l2<TEAM>(Kst + (n + 1) * NU * NX, NU * NX);
-                        team_pf_l2<TEAM>(A(c, n + 1), NX * NX);
-                        team_pf_l2<TEAM>(Bm(c, n + 1), NX * NU);
+                        team_pf_l2<TEAM>(BAp(c, n + 1), NX * NW);
                     }
                 }
                 if (ss) {
@@ -1478,8 +1463,7 @@ struct Kern {
                 const double* Kn = (st && gK) ? H + oK : Kst + n * NU * NX;
                 const double* kf = (st && gKF) ? H + oKF : kff + n * NU;
                 const double* rb = (st && gRB) ? H + oRB : r_b + n * NX;
-                const double* An = A(c, n);
-                const double* Bn = Bm(c, n);
+                const double* BAn = BAp(c, n);
                 double* du = dy + n * NW;
                 MV<NU, NX, TEAM>::run([&](int i, int k) { return Kn[i * NX + k]; },
                                       [&](int k) { return xa[k]; },
@@ -1493,7 +1477,7 @@ struct Kern {
                 MV<NX, NW, TEAM>::run(
                     [&](int i, int k) {
                         if (ss) return k < NX ? H[oBA + i * NW + NU + k] : H[oBA + i * NW + (k - NX)];
-                        return k < NX ? An[i * NX + k] : Bn[i * NU + (k - NX)];
+                        return k < NX ? BAn[i * NW + NU + k] : BAn[i * NW + (k - NX)];
                     },
                     [&](int k) { return k < NX ? xa[k] : uv[k - NX]; },
                     [&](int i, double v) {
@@ -1629,8 +1613,8 @@ struct Kern {
                 for (int e = tid; e < d.ne; e += TEAM) {
                     const int n = e / NX, i = e - n * NX;
                     const double* u = y + n * NW;
-                    const double* Ar = A(c, n) + i * NX;
-                    const double* Br = Bm(c, n) + i * NU;
+                    const double* Br = BAp(c, n) + i * NW;
+                    const double* Ar = Br + NU;
                     double ax = 0.0, bu = 0.0;
                     for (int k = 0; k < NX; ++k) ax = fma(Ar[k], u[NU + k], ax);
                     for (int k = 0; k < NU; ++k) bu = fma(Br[k], u[k], bu);
@@ -1779,6 +1763,7 @@ __global__ void __launch_bounds__(S::TEAM, S::MINB) k_fast_solve(KParams p, Solv
         const int sz[OCPQP_F_lb] = {NX * NX, NX * NU, NX, NX * NX, NU * NX, NU * NU, NX, NU};
         const int inv = p.sinv ? *p.sinv : 0;
         for (int f = 0; f < OCPQP_F_lb; ++f) c.ss[f] = ((inv >> f) & 1) ? 0 : sz[f];
+        c.ba_ss = ((inv & 3) == 3) ? 0 : NX * (NX + NU);   // A and B both invariant
     }
     double* stg = smem + p.stage_smem;
     while (true) {
@@ -1788,6 +1773,7 @@ __global__ void __launch_bounds__(S::TEAM, S::MINB) k_fast_solve(KParams p, Solv
         if (q >= p.B) break;
         for (int f = threadIdx.x; f < OCPQP_NUM_FIELDS; f += S::TEAM)
             c.f[f] = p.f[f] + (long long)q * p.bs[f];
+        if (threadIdx.x == 0) c.ba = p.ba + (long long)q * p.ba_bs;
         bar<S::TEAM>();
         Kern<S>::ipm_one(c, d, p, sp, stg, q);
         bar<S::TEAM>();

@@ -93,6 +93,8 @@ struct KParams {
     int stage_smem;           // doubles: offset of the per-stage scratch / per-team tile
     int team_stride;          // doubles of shared memory per team (row kernel)
     long long* dbg;           // optional [B, 8] phase-cycle counters (nullptr = off)
+    const double* ba;         // shaped kernels: packed [B A] per stage (NX x NW), see
+    long long ba_bs;          //   launch_pack_ba; per-QP stride (0: one copy for the batch)
     const int* sinv;          // shaped kernels: bit f set = field f (A..r) identical in every
                               // stage it is read at (device word, nullptr = none)
 };
@@ -126,6 +128,10 @@ cudaError_t launch_shift_guess(const KParams& p, const double* sy, const double*
                                double* glam, double* gt, int grid, int threads,
                                cudaStream_t stream);
 int ipm_occupancy(int threads, size_t smem);
+// Pack [B A] of every stage (uniform stages 0..N-1) into out: per QP N * nx * (nu + nx)
+// doubles, QP stride out_bs (0 when A and B are both broadcast).
+cudaError_t launch_pack_ba(const double* A, long long bsA, const double* B, long long bsB, int Bn,
+                           int N, int nx, int nu, double* out, long long out_bs, cudaStream_t stream);
 // Stage-invariance detection of the broadcast fields A..r (uniform-stage plans):
 // writes the bit mask consumed by the shaped kernels to *mask.
 cudaError_t launch_stage_invariant(const double* const* f, const long long* bs, int N, int nx,

@@ -15,6 +15,8 @@
 // places in shared memory when it fits and in the slot's global workspace
 // otherwise (ocpqp_capi.cu: place_workspace).
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <math.h>
 #include <stdint.h>
 
@@ -1730,6 +1732,33 @@ __global__ void k_stage_invariant(StageFields sf, int N, int nx, int nu, int* ma
     for (long long i = threadIdx.x; i < L * last; i += blockDim.x)
         diff |= __double_as_longlong(a[L + i]) != __double_as_longlong(a[i % L]);
     if (!__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(mask, 1 << fi);
+}
+
+__global__ void k_pack_ba(const double* A, long long bsA, const double* B, long long bsB, int N,
+                          int nx, int nu, double* out, long long out_bs, long long total) {
+    const int nw = nx + nu;
+    const long long per_qp = (long long)N * nx * nw;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long q = e / per_qp;
+        const long long r = e - q * per_qp;
+        const int n = (int)(r / (nx * nw));
+        const int rem = (int)(r - (long long)n * nx * nw);
+        const int k = rem / nw, j = rem - k * nw;
+        out[q * out_bs + r] = j < nu ? B[q * bsB + ((long long)n * nx + k) * nu + j]
+                                     : A[q * bsA + ((long long)n * nx + k) * nx + (j - nu)];
+    }
+}
+
+cudaError_t launch_pack_ba(const double* A, long long bsA, const double* B, long long bsB, int Bn,
+                           int N, int nx, int nu, double* out, long long out_bs, cudaStream_t stream) {
+    const long long copies = out_bs == 0 ? 1 : Bn;
+    const long long total = copies * N * (long long)nx * (nx + nu);
+    if (total == 0) return cudaSuccess;
+    const int threads = 256;
+    const long long blocks = std::min<long long>((total + threads - 1) / threads, 148ll * 16);
+    k_pack_ba<<<(int)blocks, threads, 0, stream>>>(A, bsA, B, bsB, N, nx, nu, out, out_bs, total);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_stage_invariant(const double* const* f, const long long* bs, int N, int nx,
