@@ -225,6 +225,12 @@ struct OcpPlan {
     int* d_counter = nullptr;
     int* d_sinv = nullptr;       // stage-invariance mask of the broadcast fields (team kernel)
     double* d_ba = nullptr;      // packed [B A] of every stage (team kernel)
+    // generic-kernel shared-memory placement for the modes beyond speed on a
+    // shaped-kernel plan (computed on first use)
+    bool gen_placed = false;
+    unsigned long long gen_mask = 0;
+    int gen_off[WS_NUM] = {0};
+    size_t gen_bytes = 0;
     long long ba_cap = 0;        // doubles allocated at d_ba
     double* d_ws = nullptr;
     double* d_ws2 = nullptr;     // extended workspace (allocated on the first non-speed solve)
@@ -438,6 +444,16 @@ void place_fast(OcpPlan* P, long long budget_per_cta) {
             used += bytes;
         }
     }
+    // A placement that holds only a small part of the per-QP workspace costs
+    // more L1 capacity (the shared-memory carve-out) than it saves: measured on
+    // configs 2 / 3 / 4 (5 % or less of the workspace placed) leaving everything
+    // to the L1 is 5-9 % faster; config 1 (45 % placed) is 10 % slower that way.
+    const char* envp = getenv("OCPQP_PLACE");
+    const bool force = envp && atoi(envp) == 1, never = envp && atoi(envp) == 0;
+    if (never || (!force && used * 5 < P->ws_slot * 8)) {
+        P->smem_mask = 0;
+        used = 0;
+    }
     P->stage_smem = (int)(used / 8);
     P->team_stride = (int)((used + tile) / 8);
     P->smem_bytes = (size_t)(used + tile) * teams;
@@ -503,6 +519,40 @@ int check_arg(const OcpIpmArgC* a) {
     if (!a->comp_res_pred && !a->abs_form)
         return fail(OCPQP_E_UNSUPPORTED, "comp_res_pred=False needs abs_form=True");
     return OCPQP_OK;
+}
+
+// Shared-memory placement of the generic kernel on a shaped-kernel plan (the
+// plan's own placement belongs to the shaped kernel): the generic priority
+// order, a budget that keeps the plan's slots resident, checked by occupancy.
+void place_generic_on_fast(OcpPlan* P) {
+    if (P->gen_placed) return;
+    P->gen_placed = true;
+    const Layout& L = P->L;
+    const int per_sm = std::max(1, (P->slots + P->num_sms - 1) / std::max(1, P->num_sms));
+    long long budget = std::min((228ll * 1024) / per_sm - 2048, 227ll * 1024 - 1024);
+    const int prio[] = {WS_G, WS_T1, WS_VEC, WS_ACT, WS_DVEC, WS_GAM, WS_WALL, WS_COEF,
+                        WS_CROW, WS_ROWV, WS_RHAT, WS_P, WS_K, WS_L, WS_LP0, WS_PV, WS_KFF,
+                        WS_RG, WS_RB, WS_RD, WS_DIR_LAM, WS_DIR_T, WS_AFF_LAM, WS_AFF_T,
+                        WS_DIR_Y, WS_DIR_PI, WS_AFF_Y, WS_AFF_PI, WS_DL, WS_DU, WS_RTSL, WS_RTSU};
+    for (int attempt = 0; attempt < 6 && budget > 0; ++attempt, budget /= 2) {
+        long long used = 0;
+        unsigned long long mask = 0;
+        int off[WS_NUM] = {0};
+        for (int b : prio) {
+            const long long sz = align2(L.ws_size[b]) * 8;
+            if (sz == 0 || used + sz > budget) continue;
+            mask |= 1ull << b;
+            off[b] = (int)(used / 8);
+            used += sz;
+        }
+        if (ipm_occupancy(P->threads, (size_t)used) >= per_sm || attempt == 5) {
+            if (ipm_occupancy(P->threads, (size_t)used) == 0) return;  // keep global memory
+            P->gen_mask = mask;
+            memcpy(P->gen_off, off, sizeof(off));
+            P->gen_bytes = (size_t)used;
+            return;
+        }
+    }
 }
 
 // modes beyond the classical speed loop run on the generic kernel with the
@@ -673,8 +723,18 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     const bool ext = needs_ext(arg);
     if (ext && (rc = ensure_ext(P))) return rc;
     KParams k;
-    // the generic kernel on a shaped-kernel plan keeps its workspace in global memory
     fill_kparams(P, k, data, !(ext && P->fast));
+    size_t gen_smem = P->smem_bytes;
+    if (ext && P->fast && getenv("OCPQP_GEN_SMEM")) {
+        // the generic kernel on a shaped-kernel plan keeps its workspace in
+        // global memory by default: measured faster (the full L1 caches it)
+        // than a shared-memory placement that shrinks the L1 (cfg 1 balance
+        // 6.5 vs 8.9 ms); OCPQP_GEN_SMEM=1 selects the placement
+        place_generic_on_fast(P);
+        k.smem_mask = P->gen_mask;
+        for (int b = 0; b < WS_EXT0; ++b) k.smem_off[b] = P->gen_off[b];
+        gen_smem = P->gen_bytes;
+    }
     SolveParams sp;
     memset(&sp, 0, sizeof(sp));
     sp.arg = *arg;
@@ -712,8 +772,7 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
         e = launch_fast_solve(P->shape, k, sp, P->grid, P->smem_bytes, (cudaStream_t)stream);
         if (e != cudaSuccess) return cuda_fail(e, "k_fast_solve launch");
     } else {
-        e = launch_ipm_solve(k, sp, P->slots, P->threads, P->fast ? 0 : P->smem_bytes,
-                             (cudaStream_t)stream);
+        e = launch_ipm_solve(k, sp, P->slots, P->threads, gen_smem, (cudaStream_t)stream);
         if (e != cudaSuccess) return cuda_fail(e, "k_ipm_solve launch");
     }
     return OCPQP_OK;
