@@ -22,6 +22,7 @@ Fixtures:
                      their Failure ladders and the robust-mode RankDeficient raise
   closed_loop.npz    run_closed_loop trajectories / iteration counts (warm and
                      cold) and one _shift_guess
+  qp_files/          qp_write text files and `mpcqp solve` CLI reports
 """
 
 from __future__ import annotations
@@ -342,8 +343,28 @@ def closed_loop():
     np.savez_compressed(HERE / "closed_loop.npz", **out)
 
 
+def qp_files():
+    """Reference-written QP text files and CLI reports (qp_io.py, cli.py)."""
+    import subprocess
+
+    d = HERE / "qp_files"
+    d.mkdir(exist_ok=True)
+    s, kw = RANDOM_CASES[1]
+    mpcqp.qp_write(str(d / "rand12.qp"), qpgen.build_qp(mpcqp, *qpgen.random_ocp_fields(s, **kw)))
+    env = {"PYTHONPATH": "/root/reference/pkg/src", "PATH": "/usr/bin:/bin"}
+    py = sys.executable
+    subprocess.run([py, "-m", "mpcqp.cli", "gen-mass-spring", "--masses", "3", "--horizon", "6",
+                    "--out", str(d / "mass3.qp")], check=True, env=env, cwd=str(d))
+    for name, extra in (("mass3_balance", []), ("mass3_speed", ["--mode", "speed", "--tol", "1e-8"]),
+                        ("mass3_partial", ["--path", "partial:2"])):
+        r = subprocess.run([py, "-m", "mpcqp.cli", "solve", "--qp", "mass3.qp", *extra],
+                           env=env, cwd=str(d), capture_output=True, text=True)
+        (d / f"{name}.report").write_text(r.stdout)
+        print(name, r.returncode, flush=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["known", "residuals", "newton", "solve_random", "solve_cfg", "pcond",
-                            "solve_modes", "closed_loop"]
+                            "solve_modes", "closed_loop", "qp_files"]
     for w in which:
         globals()[w]()
