@@ -795,7 +795,8 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
             fill_kparams(P, g, data, false);
             g.esc_count = k.esc_count;
             g.esc_list = k.esc_list;
-            e = launch_ipm_solve(g, sp, P->slots, P->threads, 0, (cudaStream_t)stream);
+            // escapes are rare: widest CTAs (the per-QP latency sets their cost)
+            e = launch_ipm_solve(g, sp, P->slots, 512, 0, (cudaStream_t)stream);
             if (e != cudaSuccess) return cuda_fail(e, "k_ipm_solve (escapes) launch");
             if (getenv("OCPQP_ESC_STATS")) {  // diagnostics: escaped QPs of this solve
                 int cnt = 0;
