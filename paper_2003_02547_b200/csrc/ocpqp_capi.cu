@@ -752,6 +752,7 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     sp.y = iter->y; sp.pi = iter->pi; sp.lam = iter->lam; sp.t = iter->t;
     sp.status = stats->status; sp.iters = stats->iterations; sp.res = stats->res;
     sp.flops = (long long*)stats->flops; sp.trace = stats->trace;
+    fill_defaults(P, k);   // no null field pointers in any kernel
     cudaError_t e;
     if (P->fast && (!ext || team)) {
         if (ext && arg->use_qr_fallback) {
@@ -793,6 +794,7 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
             // generic kernel (workspace in global memory, list on the device)
             KParams g;
             fill_kparams(P, g, data, false);
+            fill_defaults(P, g);
             g.esc_count = k.esc_count;
             g.esc_list = k.esc_list;
             // escapes are rare: widest CTAs (the per-QP latency sets their cost)
@@ -920,6 +922,7 @@ int ocpqp_residuals(OcpPlan* P, const OcpQpDataC* data, const OcpIterC* pt, doub
     if (P->B == 0) return OCPQP_OK;
     KParams k;
     fill_kparams(P, k, data, false);
+    fill_defaults(P, k);
     cudaError_t e = launch_residuals(k, pt->y, pt->pi, pt->lam, pt->t, r_g, r_b, r_d, r_m, norms,
                                      P->slots, P->threads, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "k_residuals launch");
@@ -934,6 +937,7 @@ int ocpqp_newton_step(OcpPlan* P, const OcpQpDataC* data, double reg, const OcpI
     if (P->B == 0) return OCPQP_OK;
     KParams k;
     fill_kparams(P, k, data, false);
+    fill_defaults(P, k);
     cudaError_t e = launch_newton_step(k, reg, it->lam, it->t, r_g, r_b, r_d, r_m, step->y,
                                        step->pi, step->lam, step->t, fail_stage, P->slots,
                                        P->threads, (cudaStream_t)stream);
@@ -955,6 +959,7 @@ int ocpqp_shift_guess(OcpPlan* P, const OcpQpDataC* data, const OcpIterC* sol, O
     if (P->B == 0) return OCPQP_OK;
     KParams k;
     fill_kparams(P, k, data, false);
+    fill_defaults(P, k);
     cudaError_t e = launch_shift_guess(k, sol->y, sol->pi, sol->lam, sol->t, guess->y, guess->pi,
                                        guess->lam, guess->t, P->slots, P->threads,
                                        (cudaStream_t)stream);

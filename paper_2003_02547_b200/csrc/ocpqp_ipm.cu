@@ -101,10 +101,15 @@ struct Ctx {
     double n_act;                       // number of active constraint sides
 };
 
+// Absent fields point at the plan's default rows (zeros, ones for masks, -inf /
+// +inf for bounds: fill_defaults in ocpqp_capi.cu), so no field pointer is null
+// and `dflt` only documents the reference's zero-initialised value.
 __device__ __forceinline__ double fget(const Ctx& c, int F, const StageInfo& s, int idx,
-                                       double dflt) {
-    const double* b = c.f[F];
-    return b ? b[s.foff[F] + idx] : dflt;
+                                       double /*dflt*/) {
+    return c.f[F][s.foff[F] + idx];
+}
+__device__ __forceinline__ const double* fptr(const Ctx& c, int F, const StageInfo& s) {
+    return c.f[F] + s.foff[F];
 }
 // A/B of dynamics block n (n < N): A is nx' x nx, B is nx' x nu (row-major)
 __device__ __forceinline__ double Aget(const Ctx& c, const StageInfo& s, int i, int j) {
@@ -487,19 +492,25 @@ __device__ __noinline__ int stage_classical(Ctx& c, int n, const double* Mb, lon
     if (c.w[WS_HASLP] && tid == 0) c.w[WS_HASLP][n] = 0.0;
     if (n < N) {
         const double* Pn = Pall + c.st[n + 1].P_off;
-        // T1 = P[n+1] [B A]  (nx' x nw)
+        const double* An = fptr(c, OCPQP_F_A, s);
+        const double* Bn = fptr(c, OCPQP_F_B, s);
+        // T1 = P[n+1] [B A]  (nx' x nw): column j of [B A] read with stride
         for (int idx = tid; idx < nxn * nw; idx += T) {
             const int i = idx / nw, j = idx - i * nw;
+            const double* col = j < nu ? Bn + j : An + (j - nu);
+            const int ld = j < nu ? nu : nx;
             double a = 0.0;
-            for (int k = 0; k < nxn; ++k) a = fma(Pn[i * nxn + k], BAget(c, s, k, j), a);
+            for (int k = 0; k < nxn; ++k) a = fma(Pn[i * nxn + k], col[k * ld], a);
             T1[idx] = a;
         }
         tsync();
         // G = [B A]' T1 + M~
         for (int idx = tid; idx < nw * nw; idx += T) {
             const int i = idx / nw, j = idx - i * nw;
+            const double* col = i < nu ? Bn + i : An + (i - nu);
+            const int ld = i < nu ? nu : nx;
             double a = 0.0;
-            for (int k = 0; k < nxn; ++k) a = fma(BAget(c, s, k, i), T1[k * nw + j], a);
+            for (int k = 0; k < nxn; ++k) a = fma(col[k * ld], T1[k * nw + j], a);
             G[idx] = a + Mb[idx];
         }
         flops += 2ll * nxn * nw * nxn + 2ll * nw * nw * nxn;
