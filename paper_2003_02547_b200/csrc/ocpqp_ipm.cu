@@ -432,6 +432,26 @@ __device__ __forceinline__ void cho_solve_serial(const double* L, int n, double*
     }
 }
 
+// The same cho_solve by one whole warp for n <= 32, right-looking (lane i owns
+// x_i; one broadcast per pivot instead of n serial dot products; the backward
+// sweep sums in descending k).  out = sgn * x.
+__device__ __forceinline__ void warp_cho_solve(const double* L, int n, const double* xin,
+                                               double* out, double sgn) {
+    const int lane = threadIdx.x & 31;
+    double z = lane < n ? xin[lane] : 0.0;
+    for (int k = 0; k < n; ++k) {
+        if (lane == k) z = z / L[k * n + k];
+        const double zk = __shfl_sync(0xffffffffu, z, k);
+        if (lane > k && lane < n) z = fma(-L[lane * n + k], zk, z);
+    }
+    for (int k = n - 1; k >= 0; --k) {
+        if (lane == k) z = z / L[k * n + k];
+        const double zk = __shfl_sync(0xffffffffu, z, k);
+        if (lane < k) z = fma(-L[k * n + lane], zk, z);
+    }
+    if (lane < n) out[lane] = sgn * z;
+}
+
 // ---------------------------------------------------------------------------
 // Householder QR of the m x n (m >= n) row-major stack S in place (LAPACK
 // dgeqr2 / dlarfg reflectors, the arithmetic of np.linalg.qr(mode="r")), then
@@ -955,7 +975,9 @@ __device__ __noinline__ int solve(Ctx& c, const double* lam, const double* t, co
             for (int k = 0; k < nu; ++k) a = fma(K[k * nx + i], win[k], a);
             pvc[i] = win[nu + i] + a;
         }
-        if (nu && tid == T - 1) {
+        if (nu && nu <= 32 && tid >= T - 32) {
+            warp_cho_solve(Lall + s.L_off, nu, win, kff + s.kff_off, -1.0);
+        } else if (nu > 32 && tid == T - 1) {
             const double* L = Lall + s.L_off;
             for (int i = 0; i < nu; ++i) z[i] = win[i];
             cho_solve_serial(L, nu, z);
@@ -968,8 +990,10 @@ __device__ __noinline__ int solve(Ctx& c, const double* lam, const double* t, co
     // x0 step (kkt_ocp.py:292)
     const int nx0 = c.st[0].nx;
     if (nx0) {
-        if (tid == 0) {
-            const double* LP0 = (haslp && haslp[0] != 0.0) ? LPs + c.st[0].P_off : c.w[WS_LP0];
+        const double* LP0 = (haslp && haslp[0] != 0.0) ? LPs + c.st[0].P_off : c.w[WS_LP0];
+        if (nx0 <= 32) {
+            if (tid < 32) warp_cho_solve(LP0, nx0, pv + c.st[0].pv_off, dy + c.st[0].x_off, -1.0);
+        } else if (tid == 0) {
             for (int i = 0; i < nx0; ++i) z[i] = pv[c.st[0].pv_off + i];
             cho_solve_serial(LP0, nx0, z);
             for (int i = 0; i < nx0; ++i) dy[c.st[0].x_off + i] = -z[i];
