@@ -538,6 +538,9 @@ struct Shape {
     static constexpr int VEC = 2 * NW + 3 * NX + 2 * NU + 16;
     // [B A] is staged in shared memory for small / medium stages only; large
     // stages read it through L1 so that two QPs' tiles fit per SM
+#ifndef OCPQP_MINB_THREADS
+#define OCPQP_MINB_THREADS 512  // resident threads per SM the register cap must allow
+#endif
 #ifndef OCPQP_STAGE_BA_MAX
 #define OCPQP_STAGE_BA_MAX 0  // measured: staging [B A] per stage costs more than it saves
 #endif
@@ -566,7 +569,7 @@ struct Shape {
     static constexpr int STAGE = STAGE0 + (SSTAGE ? (BA_BUF > SOLVE_BUF ? BA_BUF : SOLVE_BUF) : BA_BUF);
     // resident CTAs per SM the register allocation must allow (latency hiding
     // across QPs): 512 threads per SM
-    static constexpr int MINB = TEAM >= 512 ? 1 : 512 / TEAM;
+    static constexpr int MINB = TEAM >= OCPQP_MINB_THREADS ? 1 : OCPQP_MINB_THREADS / TEAM;
     // small input dimension: every thread factors G_uu in registers (no warp
     // Cholesky / flag round trip) and the sweeps fuse their per-stage steps
     static constexpr bool SMALL = NU <= 4;
