@@ -252,7 +252,7 @@ struct ResNorms {
 // With lamI / tI non-null: the exact KKT matrix action kkt_apply_vec
 // (kkt_common.py:166-181) on the direction (y, pi, lam, t) at the iterate
 // (lamI, tI) -- the same operators without g, b, d and a_m = t dlam + lam dt.
-__device__ __noinline__ ResNorms residuals(Ctx& c, const double* y, const double* pi, const double* lam,
+__device__ ResNorms residuals(Ctx& c, const double* y, const double* pi, const double* lam,
                               const double* t, double* r_g, double* r_b, double* r_d,
                               double* r_m /* may be null */, const double* lamI = nullptr,
                               const double* tI = nullptr) {
@@ -501,7 +501,7 @@ enum { LINALG_OK = 0, LINALG_NPD = 1, LINALG_RANK = 2 };
 
 // classical stage (kkt_ocp.py:231-251); the stage Hessian M~ is in Mb (== G
 // when it need not survive the stage).  LINALG_OK / LINALG_NPD.
-__device__ __noinline__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops) {
+__device__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops) {
     const int N = c.N;
     const int tid = threadIdx.x, T = blockDim.x;
     const StageInfo& s = c.st[n];
@@ -836,7 +836,7 @@ struct RmSpec {
     double* out = nullptr;  // materialise the active r_m (0 elsewhere) for refinement
 };
 
-__device__ __noinline__ int solve(Ctx& c, const double* lam, const double* t, const double* r_g,
+__device__ int solve(Ctx& c, const double* lam, const double* t, const double* r_g,
                      const double* r_b, const double* r_d, const RmSpec& rm,
                      double* dy, double* dpi, double* dlam, double* dt, long long& flops) {
     const KParams& p = *c.p;
