@@ -592,7 +592,7 @@ __device__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops
 
 // square-root / QR stage (kkt_ocp.py:206-230) and _split_stage_factor
 // (:83-91); M~ in WS_MST (extended workspace).  LINALG_OK / NPD / RANK.
-__device__ __noinline__ int stage_sqrt(Ctx& c, int n, bool use_qr, bool classical, long long& flops) {
+__device__ int stage_sqrt(Ctx& c, int n, bool use_qr, bool classical, long long& flops) {
     const int N = c.N;
     const int tid = threadIdx.x, T = blockDim.x;
     const StageInfo& s = c.st[n];
@@ -710,7 +710,7 @@ __device__ __noinline__ int stage_sqrt(Ctx& c, int n, bool use_qr, bool classica
 // sqrt_variant / use_qr / stage_fb need the extended workspace.  flops follow
 // the linalg.py counting rules.
 // ---------------------------------------------------------------------------
-__device__ __noinline__ int factor(Ctx& c, const double* lam, const double* t, double reg, long long& flops,
+__device__ int factor(Ctx& c, const double* lam, const double* t, double reg, long long& flops,
                       bool sqrt_variant = false, bool use_qr = false, bool stage_fb = false) {
     const KParams& p = *c.p;
     const int N = c.N;
