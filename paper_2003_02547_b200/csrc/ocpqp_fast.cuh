@@ -917,6 +917,53 @@ struct Kern {
             }
             return true;
         }
+        // larger NU: four lanes per column (lane q of a quad owns rows q, q+4,
+        // ...), right-looking: each pivot is one quad broadcast.  The forward
+        // substitution updates every row in the serial order; the backward one
+        // sums in descending k (as the sweeps' warp solves do).
+        if constexpr (NU <= 32 && NX * 4 <= TEAM) {
+            constexpr int RW = (NU + 3) / 4;
+            const int lane = tid & 31;
+            const int j = tid >> 2, q = tid & 3;
+            const unsigned qmask = 0xFu << (lane & ~3);
+            const int qbase = lane & ~3;
+            if (j < NX) {
+                double z[RW];
+#pragma unroll
+                for (int r = 0; r < RW; ++r) {
+                    const int k = q + 4 * r;
+                    z[r] = k < NU ? Gu[k * NW + NU + j] : 0.0;
+                }
+#pragma unroll
+                for (int i = 0; i < NU; ++i) {
+                    const int ri = i >> 2, oi = i & 3;
+                    if (q == oi) z[ri] = z[ri] * rinv[i];
+                    const double zi = __shfl_sync(qmask, z[ri], qbase | oi);
+#pragma unroll
+                    for (int r = 0; r < RW; ++r) {
+                        const int k = q + 4 * r;
+                        if (k > i && k < NU) z[r] = fma(-Ln[k * NU + i], zi, z[r]);
+                    }
+                }
+#pragma unroll
+                for (int i = NU - 1; i >= 0; --i) {
+                    const int ri = i >> 2, oi = i & 3;
+                    if (q == oi) z[ri] = z[ri] * rinv[i];
+                    const double zi = __shfl_sync(qmask, z[ri], qbase | oi);
+#pragma unroll
+                    for (int r = 0; r < RW; ++r) {
+                        const int k = q + 4 * r;
+                        if (k < i) z[r] = fma(-Ln[i * NU + k], zi, z[r]);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < RW; ++r) {
+                    const int k = q + 4 * r;
+                    if (k < NU) Kn[k * NX + j] = -z[r];
+                }
+            }
+            return true;
+        }
         for (int j = tid; j < NX; j += TEAM) {
             for (int i = 0; i < NU; ++i) {
                 double a = Gu[i * NW + NU + j];
