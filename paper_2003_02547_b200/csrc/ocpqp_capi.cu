@@ -227,6 +227,7 @@ struct OcpPlan {
     int* d_sinv = nullptr;       // stage-invariance mask of the broadcast fields (team kernel)
     double* d_ba = nullptr;      // packed [B A] of every stage (team kernel)
     int* d_esc = nullptr;        // [1 + B]: count, QPs the team kernel leaves to the generic one
+    long long* d_esc_meta = nullptr;  // [B, 3]: where each escaped QP resumes
     // generic-kernel shared-memory placement for the modes beyond speed on a
     // shaped-kernel plan (computed on first use)
     bool gen_placed = false;
@@ -689,6 +690,7 @@ int ocpqp_plan_destroy(OcpPlan* P) {
     cudaFree(P->d_sinv);
     cudaFree(P->d_ba);
     cudaFree(P->d_esc);
+    cudaFree(P->d_esc_meta);
     cudaFree(P->d_ws2);
     for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) cudaFree(P->h_field[f]);
     cudaFree(P->hy); cudaFree(P->hpi); cudaFree(P->hlam); cudaFree(P->ht);
@@ -757,9 +759,11 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     if (P->fast && (!ext || team)) {
         if (ext && arg->use_qr_fallback) {
             if (!P->d_esc) CUDA_TRY(cudaMalloc(&P->d_esc, sizeof(int) * (1 + (size_t)P->B)));
+            if (!P->d_esc_meta) CUDA_TRY(cudaMalloc(&P->d_esc_meta, sizeof(long long) * 3 * (size_t)P->B));
             CUDA_TRY(cudaMemsetAsync(P->d_esc, 0, sizeof(int), (cudaStream_t)stream));
             k.esc_count = P->d_esc;
             k.esc_list = P->d_esc + 1;
+            k.esc_meta = P->d_esc_meta;
         }
         fill_defaults(P, k);
         if (P->shape.kind == 0) {
@@ -797,6 +801,7 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
             fill_defaults(P, g);
             g.esc_count = k.esc_count;
             g.esc_list = k.esc_list;
+            g.esc_meta = k.esc_meta;
             // escapes are rare: widest CTAs (the per-QP latency sets their cost)
             e = launch_ipm_solve(g, sp, P->slots, 512, 0, (cudaStream_t)stream);
             if (e != cudaSuccess) return cuda_fail(e, "k_ipm_solve (escapes) launch");

@@ -1895,7 +1895,9 @@ struct Kern {
             for (int i = 0; i < DBG_NUM; ++i) c.ph[i] = 0;
             c.tk = t_start;
         }
+        long long flops_top = 0;   // flops before this iteration (escape resume point)
         while (true) {
+            flops_top = flops;
             res = residuals(c, d, p, y, pi, lam, t);
             const double mu = res.mu;
             if (!isfinite(res.g) || !isfinite(res.b) || !isfinite(res.d) || !isfinite(res.m) || !isfinite(mu))
@@ -2011,9 +2013,22 @@ struct Kern {
         }
         bar<TEAM>();
         if (REF && status == STATUS_ESCAPE) {
-            // left to the generic kernel (launched after this one over the list);
-            // the outputs (and a warm-start guess in them) stay untouched
-            if (tid == 0) p.esc_list[atomicAdd(p.esc_count, 1)] = q;
+            // left to the generic kernel (launched after this one over the list):
+            // it resumes the loop at this iteration from the iterate written here
+            OCPQP_PASS_UNROLL
+            for (int i = tid; i < d.nv; i += TEAM) gy[i] = y[i];
+            OCPQP_PASS_UNROLL
+            for (int i = tid; i < d.ne; i += TEAM) gpi[i] = pi[i];
+            OCPQP_PASS_UNROLL
+            for (int k = tid; k < d.nc; k += TEAM) { glam[k] = lam[k]; gt[k] = t[k]; }
+            if (tid == 0) {
+                long long* m = p.esc_meta + 3ll * q;
+                m[0] = it;
+                m[1] = flops_top;
+                m[2] = __double_as_longlong(alpha_last);
+                __threadfence();
+                p.esc_list[atomicAdd(p.esc_count, 1)] = q;
+            }
             return;
         }
         OCPQP_PASS_UNROLL

@@ -98,6 +98,8 @@ struct KParams {
     long long ba_bs;          //   launch_pack_ba; per-QP stride (0: one copy for the batch)
     int* esc_count;           // shaped kernel, balance mode: QPs left to the generic kernel
     int* esc_list;            //   (count, [B] indices); nullptr = none
+    long long* esc_meta;      //   [B, 3]: iteration, flops, alpha_last bits at the escape;
+                              //   the generic kernel resumes the loop there
     const int* sinv;          // shaped kernels: bit f set = field f (A..r) identical in every
                               // stage it is read at (device word, nullptr = none)
 };

@@ -1391,7 +1391,9 @@ __device__ void ipm_one(Ctx& c, const SolveParams& sp, int q) {
     const bool absf = arg.abs_form != 0, crp = arg.comp_res_pred != 0;
 
     setup_constraints(c);
-    init_iterate(c, arg, y, pi, lam, t);
+    // an escape from the team kernel resumes at its iteration and iterate
+    const long long* meta = p.esc_meta ? p.esc_meta + 3ll * q : nullptr;
+    if (!meta) init_iterate(c, arg, y, pi, lam, t);
     if (absf) {
         // g_full = view.grad(), b_vec = view.b() (solver.py:184-186): the residual
         // operators at the zero point
@@ -1406,9 +1408,9 @@ __device__ void ipm_one(Ctx& c, const SolveParams& sp, int q) {
     const double* rb = absf ? c.w[WS_BF] : r_b;
     const double* rd = absf ? c.w[WS_DVEC] : r_d;
 
-    long long flops = 0;
-    double alpha_last = 1.0;
-    int it = 0;
+    long long flops = meta ? meta[1] : 0;
+    double alpha_last = meta ? __longlong_as_double(meta[2]) : 1.0;
+    int it = meta ? (int)meta[0] : 0;
     int status = -1;
     ResNorms res{qnan(), qnan(), qnan(), qnan(), qnan()};
     while (true) {

@@ -1,6 +1,7 @@
 """GPU-vs-oracle parity report over the five configs (run on a GPU box).
 
-    python tests/parity_report.py [--cfg 1 2 3 4] [--n 64] [--json out.json]
+    python tests/parity_report.py [--cfg 1 2 3 4] [--n 64] [--mode speed|balance|...]
+                                  [--tol T] [--json out.json]
 
 For each config: solve n QPs on the GPU (fused kernel) and with the CPU oracle
 (all host cores), then report status/iteration mismatches and the max
@@ -40,8 +41,11 @@ def main():
     ap.add_argument("--cfg", type=int, nargs="*", default=[0, 1, 2, 3, 4])
     ap.add_argument("--n", type=int, default=64)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--mode", default="speed")
+    ap.add_argument("--tol", type=float, default=None)
     a = ap.parse_args()
-    arg = mode_preset("speed").with_tol(1e-8)
+    tol = a.tol if a.tol is not None else (1e-6 if a.mode in ("balance", "robust") else 1e-8)
+    arg = mode_preset(a.mode).with_tol(tol)
     report = {}
     for cfg in a.cfg:
         n = min(a.n, CONFIGS[cfg].batch)
@@ -77,6 +81,7 @@ def main():
         r["err_res"] = float(np.max(np.abs(res - ref["res"]) / np.maximum(1.0, np.abs(ref["res"]))))
         flo = rep.flops.cpu().numpy()
         r["flops_mismatch"] = int(np.sum(flo != ref["flops"]))
+        r["mode"], r["tol"] = a.mode, tol
         bad = np.flatnonzero((st != ref["status"]) | (its != ref["iters"]))
         r["bad_idx"] = bad[:10].tolist()
         report[cfg] = r
