@@ -439,7 +439,11 @@ void place_fast(OcpPlan* P, long long budget_per_cta) {
     const unsigned long long nosmem = envx ? strtoull(envx, nullptr, 0) : 0ull;
     for (int i = 0; i < np; ++i) {
         const int b = prio[i];
-        const long long bytes = align2(L.ws_size[b]) * 8;
+        long long words = L.ws_size[b];
+        // the team kernel stores P packed (lower triangle) in its first part
+        if (b == WS_P && P->shape.kind == 0 && OCPQP_PPACK && P->shape.nx >= 16)
+            words = (long long)(L.N + 1) * P->shape.nx * (P->shape.nx + 1) / 2;
+        const long long bytes = align2(words) * 8;
         if (bytes == 0 || ((nosmem >> b) & 1ull)) continue;
         if (used + bytes <= budget) {
             P->smem_mask |= 1ull << b;

@@ -554,8 +554,14 @@ struct Shape {
 #define OCPQP_PF_QSR 1
 #endif
     static constexpr bool STAGE_P = OCPQP_STAGE_P != 0;   // sweep staging includes P_{n+1}
+    // factor store of P: the lower triangle, row-major (P is symmetric bit for
+    // bit: 0.5 (T + T')), so the sweeps read ~half the bytes
+    // (measured: config 2 -7 %; config 1, whose store sits in shared memory,
+    // +25 % from the index arithmetic in its latency-bound sweeps -> NX >= 16)
+    static constexpr bool PPACK = OCPQP_PPACK != 0 && NX >= 16;
+    static constexpr int PST = PPACK ? NX * (NX + 1) / 2 : NX * NX;   // per-stage store stride
     static constexpr bool PF_QSR = OCPQP_PF_QSR != 0;     // factor prefetch includes Q, S, R
-    static constexpr int HALF_S = (STAGE_P ? NX * NX : 0) + NX * NW + NU * NX + NU * NU + NU + NX + NW + NU + 4;
+    static constexpr int HALF_S = (STAGE_P ? PST : 0) + NX * NW + NU * NX + NU * NU + NU + NX + NW + NU + 4;
     static constexpr int HALF_F = NX * NW + (PF_QSR ? NX * NX + NU * NX + NU * NU : 0);
     static constexpr int HALF = HALF_S > HALF_F ? HALF_S : HALF_F;
     static constexpr bool STAGE_SOLVE = HALF <= 4096;
@@ -605,6 +611,11 @@ struct Kern {
 
     // ---- field access (uniform-stage formula offsets) ----
     __device__ static __forceinline__ const double* A(const FCtx& c, int n) { return c.f[OCPQP_F_A] + n * c.ss[OCPQP_F_A]; }
+    // element (i, k) of a stored P (full or packed lower triangle)
+    __device__ static __forceinline__ double Pget(const double* P, int i, int k) {
+        if constexpr (S::PPACK) return k <= i ? P[i * (i + 1) / 2 + k] : P[k * (k + 1) / 2 + i];
+        else return P[i * NX + k];
+    }
     // packed [B A] of stage n (kkt_ocp.py:177): row k = (B_k., A_k.)
     __device__ static __forceinline__ const double* BAp(const FCtx& c, int n) { return c.ba + n * c.ba_ss; }
     __device__ static __forceinline__ const double* Bm(const FCtx& c, int n) { return c.f[OCPQP_F_B] + n * c.ss[OCPQP_F_B]; }
@@ -1077,12 +1088,13 @@ struct Kern {
             }
             if (NG > 0 && ng > 0) flops += 2ll * NX * NX * ng;
             bar<TEAM>();
-            double* Pn = Pst + n * NX * NX;
+            double* Pn = Pst + n * S::PST;
             TEAM_FOR(idx, NX * NX)
                 const int i = idx / NX, j = idx - i * NX;
                 const double v = 0.5 * (T1[idx] + T1[j * NX + i]);
                 Pc[idx] = v;
-                Pn[idx] = v;
+                if (!S::PPACK) Pn[idx] = v;
+                else if (j <= i) Pn[i * (i + 1) / 2 + j] = v;
             TEAM_END
             bar<TEAM>();
         }
@@ -1224,12 +1236,13 @@ struct Kern {
                                         [&](int i, int j, double v, double g) { T1[i * NX + j] = v + g; });
             flops += 2ll * NX * NX * NU;
             bar<TEAM>();
-            double* Pn = Pst + n * NX * NX;
+            double* Pn = Pst + n * S::PST;
             TEAM_FOR(idx, NX * NX)
                 const int i = idx / NX, j = idx - i * NX;
                 const double v = 0.5 * (T1[idx] + T1[j * NX + i]);
                 Pc[idx] = v;
-                Pn[idx] = v;
+                if (!S::PPACK) Pn[idx] = v;
+                else if (j <= i) Pn[i * (i + 1) / 2 + j] = v;
             TEAM_END
             bar<TEAM>();
         }
@@ -1393,7 +1406,7 @@ struct Kern {
         const bool gKF = !((sm >> WS_KFF) & 1ull);
         const double* Rst = wsb<WS_RINV>(c, p);
         // half layout offsets
-        constexpr int oP = 0, oBA = S::STAGE_P ? NX * NX : 0, oK = oBA + NX * NW, oL = oK + NU * NX, oR = oL + NU * NU;
+        constexpr int oP = 0, oBA = S::STAGE_P ? S::PST : 0, oK = oBA + NX * NW, oL = oK + NU * NX, oR = oL + NU * NU;
         constexpr int oRB = oR + NU, oRH = oRB + NX, oKF = oRH + NW;
         constexpr bool ss = (S::SSTAGE & 1) != 0;
         auto issue = [&](int n, int h, bool bwd) {
@@ -1405,7 +1418,7 @@ struct Kern {
                 if (gRB) for (int e2 = tid; e2 < NX; e2 += TEAM) cpa8(H + oRB + e2, r_b + n * NX + e2);
                 if (bwd) {
                     if (S::STAGE_P && gP)
-                        for (int e2 = tid; e2 < NX * NX; e2 += TEAM) cpa8(H + oP + e2, Pst + (n + 1) * NX * NX + e2);
+                        for (int e2 = tid; e2 < S::PST; e2 += TEAM) cpa8(H + oP + e2, Pst + (n + 1) * S::PST + e2);
                     if (gL) for (int e2 = tid; e2 < NU * NU; e2 += TEAM) cpa8(H + oL + e2, Lst + n * NU * NU + e2);
                     if (gR) for (int e2 = tid; e2 < NU; e2 += TEAM) cpa8(H + oR + e2, Rst + n * NU + e2);
                     if (gRH) for (int e2 = tid; e2 < NW; e2 += TEAM) cpa8(H + oRH + e2, rhat + n * NW + e2);
@@ -1427,7 +1440,7 @@ struct Kern {
             const int h = n & 1;
             if constexpr (S::L2PF && !ss) {
                 if (n > 0) {  // next stage's operands toward L2 while this one computes
-                    if (gP) team_pf_l2<TEAM>(Pst + n * NX * NX, NX * NX);
+                    if (gP) team_pf_l2<TEAM>(Pst + n * S::PST, S::PST);
                     team_pf_l2<TEAM>(BAp(c, n - 1), NX * NW);
                     if (gK) team_pf_l2<TEAM>(Kst + (n - 1) * NU * NX, NU * NX);
                 }
@@ -1439,7 +1452,7 @@ struct Kern {
             }
             const double* H = SB + h * S::HALF;
             const bool st = ss;
-            const double* Pn = (st && S::STAGE_P && gP) ? H + oP : Pst + (n + 1) * NX * NX;
+            const double* Pn = (st && S::STAGE_P && gP) ? H + oP : Pst + (n + 1) * S::PST;
             const double* rb = (st && gRB) ? H + oRB : r_b + n * NX;
             const double* Kn = (st && gK) ? H + oK : Kst + n * NU * NX;
             const double* Ln = (st && gL) ? H + oL : Lst + n * NU * NU;
@@ -1447,7 +1460,7 @@ struct Kern {
             const double* rh = (st && gRH) ? H + oRH : rhat + n * NW;
             const double* BAn = BAp(c, n);
             auto BA = [&](int k, int j) -> double { return ss ? H[oBA + k * NW + j] : BAn[k * NW + j]; };
-            MV<NX, NX, TEAM>::run([&](int i, int k) { return Pn[i * NX + k]; },
+            MV<NX, NX, TEAM>::run([&](int i, int k) { return Pget(Pn, i, k); },
                                   [&](int k) { return rb[k]; },
                                   [&](int i, double v) { e[i] = v + pvs[i]; });
             bar<TEAM>();
@@ -1550,11 +1563,11 @@ struct Kern {
         for (int e2 = tid; e2 < d.ne; e2 += TEAM) {
             const int n = e2 / NX;
             const int i = e2 - n * NX;
-            const double* Pn = Pst + (n + 1) * NX * NX + i * NX;
+            const double* Pn = Pst + (n + 1) * S::PST;
             const double* xn = dy + (n + 1) * NW + (n + 1 < N ? NU : 0);
             double a = 0.0;
 #pragma unroll 8
-            for (int k = 0; k < NX; ++k) a = fma(Pn[k], xn[k], a);
+            for (int k = 0; k < NX; ++k) a = fma(Pget(Pn, i, k), xn[k], a);
             const double v = a + pv[(n + 1) * NX + i];
             dpi[e2] = v;
             if (!isfinite(v)) nonfinite = 1;

@@ -6,6 +6,11 @@
 
 #include "../../include/ocpqp_b200.h"
 
+// team kernel: factor store of P as the packed lower triangle (see Shape::PPACK)
+#ifndef OCPQP_PPACK
+#define OCPQP_PPACK 1
+#endif
+
 namespace ocpqp {
 
 // Per-stage layout record, computed once per plan on the host.  The offsets
