@@ -638,6 +638,8 @@ int ocpqp_plan_create(const OcpQpDimC* dim, int32_t batch, OcpPlan** out) {
         }
     }
     if (occ == 0) { delete P; return fail(OCPQP_E_CUDA, "kernel does not fit on an SM"); }
+    // experiments: cap the resident CTAs per SM (working set vs latency hiding)
+    if (const char* envc = getenv("OCPQP_CTAS_PER_SM")) occ = std::max(1, std::min(occ, atoi(envc)));
     if (P->fast) {
         const int teams = fast_teams_per_cta(P->shape);
         const int ctas = std::max(1, std::min((std::max(1, batch) + teams - 1) / teams, occ * P->num_sms));
