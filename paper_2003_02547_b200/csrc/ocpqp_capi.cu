@@ -566,7 +566,12 @@ void place_generic_on_fast(OcpPlan* P) {
 // refinement of the combined direction (speed, balance); the QR rungs of the
 // balance ladder are left to the generic kernel per QP (escape list).
 bool team_supports(const OcpIpmArgC* a) {
-    return !a->abs_form && a->comp_res_pred && !a->use_qr_always && a->riccati_variant == 0 &&
+    // delta form with residuals every iteration, or the speed_abs combination
+    // (absolute form, residuals only at exit, no refinement / QR)
+    const bool delta = !a->abs_form && a->comp_res_pred;
+    const bool abs_speed = a->abs_form && !a->comp_res_pred && a->itref_corr_max <= 0 &&
+                           !a->use_qr_fallback;
+    return (delta || abs_speed) && !a->use_qr_always && a->riccati_variant == 0 &&
            a->itref_pred_max <= 0;
 }
 

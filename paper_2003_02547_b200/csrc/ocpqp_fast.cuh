@@ -1316,10 +1316,14 @@ struct Kern {
 
     // ---------------- Riccati solve (kkt_ocp.py:254-320) ----------------
     // r_m(k) = act ? (lam t - tau) + [dlam_a dt_a] : 0, or rm_ext (masked)
+    // absm: absolute formulation (speed_abs): 1 affine rhs -lam t, 2 combined
+    // rhs minus 2 lam t (solver.py:210-246); 0 (a literal at every speed-mode
+    // call site) is the delta form
     OCPQP_BIGFN static int solve(FCtx& c, const RD& d, const KParams& p, double* stg,
                                 const double* lam, const double* t, const double* rm_ext,
                                 double tau, const double* dla, const double* dta, double* dy,
-                                double* dpi, double* dlam, double* dt, long long& flops) {
+                                double* dpi, double* dlam, double* dt, long long& flops,
+                                int absm = 0) {
         const int tid = threadIdx.x;
         const double* act = c.w[WS_DVEC];  // NaN = inactive
         const double* gam = c.w[WS_GAM];
@@ -1346,9 +1350,13 @@ struct Kern {
                 double rmk;
                 if (rm_ext) {
                     rmk = rm_ext[k];
+                } else if (absm == 1) {
+                    rmk = -(lam[k] * t[k]);
                 } else {
-                    rmk = lam[k] * t[k] - tau;
+                    const double comp = lam[k] * t[k];
+                    rmk = comp - tau;
                     if (dla) rmk = rmk + dla[k] * dta[k];
+                    if (absm == 2) rmk = rmk - 2.0 * comp;
                 }
                 w = (lam[k] * r_d[k] - rmk) * tinv[k];
             }
@@ -1909,19 +1917,57 @@ struct Kern {
             c.tk = t_start;
         }
         long long flops_top = 0;   // flops before this iteration (escape resume point)
+        // speed_abs (absolute formulation, no per-iteration residuals): the
+        // solves take g, b, d (solver.py:184-186, 209-211), evaluated once as
+        // the residual operators at the zero point into the solve's rhs buffers
+        const bool absf = REF && arg.abs_form;
+        if (absf) {
+            for (int i = tid; i < d.nv; i += TEAM) dy[i] = 0.0;
+            for (int i = tid; i < d.ne; i += TEAM) dpi[i] = 0.0;
+            for (int k = tid; k < d.nc; k += TEAM) { alam[k] = 0.0; at[k] = 0.0; }
+            bar<TEAM>();
+            residuals(c, d, p, dy, dpi, alam, at);
+            bar<TEAM>();
+        }
         while (true) {
             flops_top = flops;
-            res = residuals(c, d, p, y, pi, lam, t);
-            const double mu = res.mu;
-            if (!isfinite(res.g) || !isfinite(res.b) || !isfinite(res.d) || !isfinite(res.m) || !isfinite(mu))
-                status = OCPQP_STATUS_NAN;
-            else if (alpha_last < arg.alpha_min)
-                status = OCPQP_STATUS_MINSTEP;
-            else if (mu <= arg.tol_comp && res.g <= arg.tol_stat && res.b <= arg.tol_eq &&
-                     res.d <= arg.tol_ineq && res.m <= arg.tol_comp)
-                status = OCPQP_STATUS_SUCCESS;
-            else if (it >= arg.iter_max)
-                status = OCPQP_STATUS_MAXITER;
+            double mu;
+            if (!absf) {
+                res = residuals(c, d, p, y, pi, lam, t);
+                mu = res.mu;
+                if (!isfinite(res.g) || !isfinite(res.b) || !isfinite(res.d) || !isfinite(res.m) || !isfinite(mu))
+                    status = OCPQP_STATUS_NAN;
+                else if (alpha_last < arg.alpha_min)
+                    status = OCPQP_STATUS_MINSTEP;
+                else if (mu <= arg.tol_comp && res.g <= arg.tol_stat && res.b <= arg.tol_eq &&
+                         res.d <= arg.tol_ineq && res.m <= arg.tol_comp)
+                    status = OCPQP_STATUS_SUCCESS;
+                else if (it >= arg.iter_max)
+                    status = OCPQP_STATUS_MAXITER;
+            } else {
+                // duality measure and iterate finiteness (solver.py:191-199);
+                // exit on mu only (ipm_core.py:296-304)
+                const double* act = c.w[WS_DVEC];
+                double sm = 0.0;
+                int bad = 0;
+                for (int k = tid; k < d.nc; k += TEAM) {
+                    if (!isnan(act[k])) sm += lam[k] * t[k];
+                    bad |= !isfinite(lam[k]) || !isfinite(t[k]);
+                }
+                for (int i = tid; i < d.nv; i += TEAM) bad |= !isfinite(y[i]);
+                for (int i = tid; i < d.ne; i += TEAM) bad |= !isfinite(pi[i]);
+                sm = tsum<TEAM>(sm, c.red);
+                bad = any_of<TEAM>(bad);
+                mu = c.n_act > 0.0 ? sm / c.n_act : 0.0;
+                if (bad || !isfinite(mu))
+                    status = OCPQP_STATUS_NAN;
+                else if (alpha_last < arg.alpha_min)
+                    status = OCPQP_STATUS_MINSTEP;
+                else if (mu <= arg.tol_comp)
+                    status = OCPQP_STATUS_SUCCESS;
+                else if (it >= arg.iter_max)
+                    status = OCPQP_STATUS_MAXITER;
+            }
             OCPQP_TICK(c, DBG_RES);
             if (status >= 0) break;
             bar<TEAM>();
@@ -1934,9 +1980,27 @@ struct Kern {
             if (fs >= 0) { status = OCPQP_STATUS_FAILURE; break; }
             OCPQP_TICK(c, DBG_FACTOR);
             // the affine dy / dpi are scratch (only dlam_aff, dt_aff are used later)
-            if (solve(c, d, p, stg, lam, t, nullptr, 0.0, nullptr, nullptr, dy, dpi, alam, at, flops)) {
-                status = OCPQP_STATUS_NAN;
-                break;
+            // the absolute form's solution minus the iterate is the step
+            // (recover_step_absolute, ipm_core.py:275-283)
+            auto to_step = [&](double* sy, double* spi, double* sl, double* st) -> int {
+                int bad = 0;
+                for (int i = tid; i < d.nv; i += TEAM) { sy[i] = sy[i] - y[i]; bad |= !isfinite(sy[i]); }
+                for (int i = tid; i < d.ne; i += TEAM) { spi[i] = spi[i] - pi[i]; bad |= !isfinite(spi[i]); }
+                for (int k = tid; k < d.nc; k += TEAM) {
+                    sl[k] = sl[k] - lam[k];
+                    st[k] = st[k] - t[k];
+                    bad |= !isfinite(sl[k]) || !isfinite(st[k]);
+                }
+                return any_of<TEAM>(bad);
+            };
+            {
+                int nfa = solve(c, d, p, stg, lam, t, nullptr, 0.0, nullptr, nullptr, dy, dpi, alam,
+                                at, flops, absf ? 1 : 0);
+                if (absf) { bar<TEAM>(); nfa = to_step(dy, dpi, alam, at); }
+                if (nfa) {
+                    status = OCPQP_STATUS_NAN;
+                    break;
+                }
             }
             bar<TEAM>();
             OCPQP_TICK(c, DBG_SOLVE_AFF);
@@ -1946,16 +2010,19 @@ struct Kern {
             if (mu > 0.0) sigma = fmin(1.0, fmax(0.0, pow(mu_aff / mu, 3.0)));
             const double tau = sigma * mu;
             int nf = solve(c, d, p, stg, lam, t, nullptr, tau, arg.pred_corr ? alam : nullptr,
-                           arg.pred_corr ? at : nullptr, dy, dpi, dlam, dt, flops);
+                           arg.pred_corr ? at : nullptr, dy, dpi, dlam, dt, flops, absf ? 2 : 0);
             bar<TEAM>();
+            if (absf) { nf = to_step(dy, dpi, dlam, dt); bar<TEAM>(); }
             bool rejected = false;
             if (arg.pred_corr && arg.cond_pred_corr) {
                 const double a_t = max_step(c, d, lam, t, dlam, dt, 1.0);
                 const double mu_t = trial_mu(c, d, lam, t, dlam, dt, a_t);
                 if (!(mu_t <= arg.corr_ratio * mu_aff)) {
                     rejected = true;
-                    nf = solve(c, d, p, stg, lam, t, nullptr, tau, nullptr, nullptr, dy, dpi, dlam, dt, flops);
+                    nf = solve(c, d, p, stg, lam, t, nullptr, tau, nullptr, nullptr, dy, dpi, dlam, dt,
+                               flops, absf ? 2 : 0);
                     bar<TEAM>();
+                    if (absf) { nf = to_step(dy, dpi, dlam, dt); bar<TEAM>(); }
                 }
             }
             if (REF && arg.itref_corr_max > 0) {
@@ -2017,7 +2084,8 @@ struct Kern {
             if (trace && tid == 0 && it < arg.iter_max) {
                 double* tr = trace + (long long)it * 8;
                 tr[0] = alpha_aff; tr[1] = alpha; tr[2] = mu; tr[3] = sigma;
-                tr[4] = res.g; tr[5] = res.b; tr[6] = res.d; tr[7] = res.m;
+                tr[4] = absf ? qnan() : res.g; tr[5] = absf ? qnan() : res.b;
+                tr[6] = absf ? qnan() : res.d; tr[7] = absf ? qnan() : res.m;
             }
             bar<TEAM>();
             alpha_last = alpha;
@@ -2043,6 +2111,10 @@ struct Kern {
                 p.esc_list[atomicAdd(p.esc_count, 1)] = q;
             }
             return;
+        }
+        if (absf) {  // final residuals (solver.py:300), computed once in speed_abs
+            res = residuals(c, d, p, y, pi, lam, t);
+            bar<TEAM>();
         }
         OCPQP_PASS_UNROLL
         for (int i = tid; i < d.nv; i += TEAM) gy[i] = y[i];
@@ -2109,7 +2181,7 @@ int stage_doubles() { return S::STAGE; }
 
 template <class S>
 cudaError_t launch(const KParams& p, const SolveParams& sp, int grid, size_t smem, cudaStream_t st) {
-    const bool ref = sp.arg.itref_corr_max > 0 || sp.arg.use_qr_fallback;
+    const bool ref = sp.arg.itref_corr_max > 0 || sp.arg.use_qr_fallback || sp.arg.abs_form;
     cudaError_t e = cudaFuncSetAttribute(ref ? k_fast_solve<S, true> : k_fast_solve<S, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
