@@ -270,10 +270,10 @@ def main():
             torch.cuda.synchronize()
     torch.cuda.synchronize()
     plan_info = get_plan(dev).info()
-    from paper_2003_02547_b200.ipm import is_speed_classical
+    from paper_2003_02547_b200.ipm import team_supports
 
-    if not is_speed_classical(arg):
-        plan_info["kernel"] = "generic"   # modes beyond speed run on k_ipm_solve
+    if plan_info.get("kernel") == "team" and not team_supports(arg):
+        plan_info["kernel"] = "generic"   # square-root / robust run on k_ipm_solve
 
     peak_dfma, peak_dmma = fp64_peak()
     torch.cuda.synchronize()
@@ -352,11 +352,18 @@ def main():
         except (ValueError, OSError):
             pass
 
+    # our kernels per solve (ocpqp_solve): the team kernel path launches the
+    # stage-invariance check, the [B A] pack and the solve, plus the generic
+    # kernel over the escape list in balance mode; the generic path one kernel
+    if plan_info.get("kernel") == "team":
+        launches_per_solve = 3 + (1 if arg.use_qr_fallback else 0)
+    else:
+        launches_per_solve = 1
     line = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world,
             "steps": a.steps, "warmup": w, "ms_per_step": t_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, BASELINE configs)", "config": config,
-            "roofline": roof, "clocks": clocks, "gpu_launches": a.steps,
+            "roofline": roof, "clocks": clocks, "gpu_launches": a.steps * launches_per_solve,
             "plan": plan_info,
             "iterations": {"min": int(iters.min()), "mean": float(iters.mean()),
                            "max": int(iters.max())},
