@@ -1279,7 +1279,7 @@ struct Kern {
     template <int NN>
     __device__ static __forceinline__ void warp_cho_solve(const double* L, const double* rv, const double* xin,
                                           double* out, double sgn) {
-        const int lane = threadIdx.x;
+        const int lane = threadIdx.x & 31;   // any one whole warp
         if constexpr (NN <= 32) {
             double z = lane < NN ? xin[lane] : 0.0;
             const double rii = lane < NN ? rv[lane] : 1.0;
@@ -1477,14 +1477,26 @@ struct Kern {
                                   [&](int j, double v) { win[j] = rh[j] + v; });
             bar<TEAM>();
             double* pvc = pv + n * NX;
-            MV<NX, NU, TEAM>::run([&](int i, int k) { return Kn[k * NX + i]; },
-                                  [&](int k) { return win[k]; },
-                                  [&](int i, double v) {
-                                      const double r = win[NU + i] + v;
-                                      pvc[i] = r;
-                                      pvs[i] = r;
-                                  });
-            if constexpr (S::SMALL && TEAM > 32) {
+            auto p_out = [&](int i, double v) {
+                const double r = win[NU + i] + v;
+                pvc[i] = r;
+                pvs[i] = r;
+            };
+            if constexpr (!S::SMALL && TEAM >= 64 && NU <= 32) {
+                // p_n on all warps but the last, k_n = -G_uu^{-1} rr on the last
+                // warp at the same time (the warp solve used to follow the
+                // mat-vec on warp 0 while the others waited at the barrier)
+                if (tid >= TEAM - 32)
+                    warp_cho_solve<NU>(Ln, Rn, win, kff + n * NU, -1.0);
+                else
+                    MV<NX, NU, TEAM - 32>::run([&](int i, int k) { return Kn[k * NX + i]; },
+                                               [&](int k) { return win[k]; }, p_out);
+            } else {
+                MV<NX, NU, TEAM>::run([&](int i, int k) { return Kn[k * NX + i]; },
+                                      [&](int k) { return win[k]; }, p_out);
+            }
+            if constexpr (!S::SMALL && TEAM >= 64 && NU <= 32) {
+            } else if constexpr (S::SMALL && TEAM > 32) {
                 // k_n = -G_uu^{-1} rr in one thread of the second warp, in
                 // registers, concurrent with p_n on the first warp
                 if (tid == 32) {
