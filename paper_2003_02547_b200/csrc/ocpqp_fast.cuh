@@ -392,13 +392,14 @@ struct NoPre {
     __device__ __forceinline__ double operator()(int, int) const { return 0.0; }
 };
 
-template <int M, int N, int K, int TEAM, class FA, class FB, class FP, class FE>
+// OFF: the GEMM runs on threads OFF .. OFF + TEAM - 1 of the CTA
+template <int M, int N, int K, int TEAM, int OFF = 0, class FA, class FB, class FP, class FE>
 __device__ __forceinline__ void tile_gemm(FA a, FB b, FP pre, FE epi) {
     constexpr int PK = gemm_pick(M, N, TEAM);
     constexpr int TM = PK / 8, TN = PK % 8;
     constexpr int MT = (M + TM - 1) / TM, NT = (N + TN - 1) / TN, TILES = MT * NT;
     constexpr bool HASPRE = !std::is_same<FP, NoPre>::value;
-    for (int t = threadIdx.x; t < TILES; t += TEAM) {
+    for (int t = (int)threadIdx.x - OFF; t < TILES; t += TEAM) {
         const int r0 = (t / NT) * TM, c0 = (t % NT) * TN;
         double acc[TM][TN], pv[TM][TN];
 #pragma unroll
@@ -444,7 +445,7 @@ __device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, doubl
 #ifndef OCPQP_MMA_NBW
 #define OCPQP_MMA_NBW 2
 #endif
-template <int M, int N, int K, int TEAM, class FA, class FB, class FP, class FE>
+template <int M, int N, int K, int TEAM, int OFF = 0, class FA, class FB, class FP, class FE>
 __device__ __forceinline__ void tile_mma(FA a, FB b, FP pre, FE epi) {
     constexpr bool HASPRE = !std::is_same<FP, NoPre>::value;
     constexpr int NWARP = TEAM / 32;
@@ -452,7 +453,7 @@ __device__ __forceinline__ void tile_mma(FA a, FB b, FP pre, FE epi) {
     constexpr int NBW0 = OCPQP_MMA_NBW;
     constexpr int NBW = (N + 7) / 8 < NBW0 ? (N + 7) / 8 : NBW0;
     constexpr int MB = (M + 7) / 8, NB = (N + 8 * NBW - 1) / (8 * NBW), KS = (K + 3) / 4;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = ((int)threadIdx.x - OFF) >> 5;
     const int gr = lane >> 2, tg = lane & 3;
     for (int t = warp; t < MB * NB; t += NWARP) {
         const int r0 = (t / NB) * 8, c0 = (t % NB) * (8 * NBW);
@@ -495,10 +496,10 @@ __device__ __forceinline__ void tile_mma(FA a, FB b, FP pre, FE epi) {
 }
 
 // stage GEMM: DMMA tiles on the large shapes, register-tiled DFMA otherwise
-template <bool MMA, int M, int N, int K, int TEAM, class FA, class FB, class FP, class FE>
+template <bool MMA, int M, int N, int K, int TEAM, int OFF = 0, class FA, class FB, class FP, class FE>
 __device__ __forceinline__ void stage_gemm(FA a, FB b, FP pre, FE epi) {
-    if constexpr (MMA) tile_mma<M, N, K, TEAM>(a, b, pre, epi);
-    else tile_gemm<M, N, K, TEAM>(a, b, pre, epi);
+    if constexpr (MMA) tile_mma<M, N, K, TEAM, OFF>(a, b, pre, epi);
+    else tile_gemm<M, N, K, TEAM, OFF>(a, b, pre, epi);
 }
 
 // accumulate the cycles since the previous tick into phase `slot` (thread 0)
@@ -870,26 +871,32 @@ struct Kern {
     // and K = -L'^{-1} L^{-1} G_ux, one column per thread (kkt_ocp.py:237-243).
     // false on a pivot that is not > 0.  Kept out of line so that its NU-long
     // register arrays do not spill inside the factor.
+    // warp 0: L_uu = chol(G_uu) with the rows in registers; c.flag = success
+    __device__ __noinline__ static void warp0_chol(FCtx& c, const double* Gu, double* Ln,
+                                                   double* Rinv_n, double* rinv) {
+        const int tid = threadIdx.x;
+        double row[NU];
+        double rin = 0.0;
+#pragma unroll
+        for (int j = 0; j < NU; ++j) row[j] = (tid < NU && j <= tid) ? Gu[tid * NW + j] : 0.0;
+        const bool ok = warp_chol<NU>(row, tid, rin);
+        if (tid == 0) c.flag = ok;
+        if (ok && tid < NU) {
+#pragma unroll
+            for (int j = 0; j < NU; ++j) Ln[tid * NU + j] = j <= tid ? row[j] : 0.0;
+            rinv[tid] = rin;
+            Rinv_n[tid] = rin;
+        }
+    }
+
+    // chol_done: warp 0 already factored G_uu (concurrently with G_xx)
     __device__ __noinline__ static bool chol_k(FCtx& c, const long long* dbg, const double* Gu,
                                                double* Ln, double* Rinv_n, double* rinv,
-                                               double* Kn, double* Z) {
+                                               double* Kn, double* Z, bool chol_done = false) {
         struct { const long long* dbg; } p{dbg};  // OCPQP_TICK reads p.dbg
         const int tid = threadIdx.x;
         if constexpr (NU <= 32) {
-            if (tid < 32) {
-                double row[NU];
-                double rin = 0.0;
-#pragma unroll
-                for (int j = 0; j < NU; ++j) row[j] = (tid < NU && j <= tid) ? Gu[tid * NW + j] : 0.0;
-                const bool ok = warp_chol<NU>(row, tid, rin);
-                if (tid == 0) c.flag = ok;
-                if (ok && tid < NU) {
-#pragma unroll
-                    for (int j = 0; j < NU; ++j) Ln[tid * NU + j] = j <= tid ? row[j] : 0.0;
-                    rinv[tid] = rin;
-                    Rinv_n[tid] = rin;
-                }
-            }
+            if (!chol_done && tid < 32) warp0_chol(c, Gu, Ln, Rinv_n, rinv);
             bar<TEAM>();
             if (!c.flag) return false;
         } else {
@@ -1169,22 +1176,36 @@ struct Kern {
                 return h;
             };
             // M~ entries are fetched before the k loops (their loads overlap the GEMMs)
+            double* Ln = Lst + n * NU * NU;
+            double* Rinv_n = wsb<WS_RINV>(c, p) + n * NU;
+            double* Kn = Kst + n * NU * NX;
             stage_gemm<S::DMMA, NU, NW, NX, TEAM>([&](int i, int k) { return BA(k, i); },
                                         [&](int k, int j) { return T1[k * NW + j]; },
                                         [&](int i, int j) { return Mt(i, j); },
                                         [&](int i, int j, double v, double m) { Gu[i * NW + j] = v + m; });
-            stage_gemm<S::DMMA, NX, NX, NX, TEAM>([&](int i, int k) { return BA(k, NU + i); },
-                                        [&](int k, int j) { return T1[k * NW + NU + j]; },
-                                        [&](int i, int j) { return Mt(NU + i, NU + j); },
-                                        [&](int i, int j, double v, double m) { Pc[i * NX + j] = v + m; });
+            // non-small NU: warp 0 factors G_uu while the other warps form G_xx
+            constexpr bool OVL = !S::SMALL && TEAM >= 64 && NU <= 32;
+            if constexpr (OVL) {
+                bar<TEAM>();
+                if (tid < 32)
+                    warp0_chol(c, Gu, Ln, Rinv_n, vec);
+                else
+                    stage_gemm<S::DMMA, NX, NX, NX, TEAM - 32, 32>(
+                        [&](int i, int k) { return BA(k, NU + i); },
+                        [&](int k, int j) { return T1[k * NW + NU + j]; },
+                        [&](int i, int j) { return Mt(NU + i, NU + j); },
+                        [&](int i, int j, double v, double m) { Pc[i * NX + j] = v + m; });
+            } else {
+                stage_gemm<S::DMMA, NX, NX, NX, TEAM>([&](int i, int k) { return BA(k, NU + i); },
+                                            [&](int k, int j) { return T1[k * NW + NU + j]; },
+                                            [&](int i, int j) { return Mt(NU + i, NU + j); },
+                                            [&](int i, int j, double v, double m) { Pc[i * NX + j] = v + m; });
+            }
             if (NG > 0) flops += 2ll * NW * NW * NG;
             flops += 2ll * NX * NW * NX + 2ll * NW * NW * NX;
             bar<TEAM>();
             OCPQP_TICK(c, DBG_F_G);
             // L_uu = chol(G_uu)
-            double* Ln = Lst + n * NU * NU;
-            double* Rinv_n = wsb<WS_RINV>(c, p) + n * NU;
-            double* Kn = Kst + n * NU * NX;
             if constexpr (S::SMALL) {
                 // every thread factors G_uu in registers (measured faster than
                 // factoring in the K threads only and broadcasting the pivot
@@ -1221,7 +1242,7 @@ struct Kern {
             double* rinv = vec;  // NU
             flops += (long long)NU * NU * NU / 3;
             // out of line: its row / column registers spill inside the factor
-            if (!chol_k(c, p.dbg, Gu, Ln, Rinv_n, rinv, Kn, T1)) {
+            if (!chol_k(c, p.dbg, Gu, Ln, Rinv_n, rinv, Kn, T1, OVL)) {
                 if (fpf) cpa_wait<0>();
                 return n;
             }
