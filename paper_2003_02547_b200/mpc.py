@@ -157,16 +157,20 @@ def _x0_rows(batch):
 
 
 def run_closed_loop_batch(cfg, x0s, steps, arg=None, warm_start="primal_dual",
-                          compare_cold=False, strict=True, device="cuda"):
+                          compare_cold=False, strict=True, device="cuda", graph=True):
     """Closed-loop MPC of B independent chains (same model, own initial states).
 
     Per step: impose every plant's state through the stage-0 box rows, solve
     the whole batch (warm started from the shifted previous solutions after
     the first step), apply each first input to its exact discrete plant, shift
-    the solutions on the device.  Returns a list of ClosedLoopResult, one per
+    the solutions on the device.  Every buffer is preallocated, so with
+    ``graph`` the warm steps are one captured CUDA graph replayed per step
+    (the step is launch-bound: the index writes, the solve's kernels, the
+    shift and the plant update); the first (cold) step and the capture's
+    warm-up step run eagerly.  Returns a list of ClosedLoopResult, one per
     plant.  With ``strict`` a non-Success controller solve raises
-    ClosedLoopFailed (the reference's behaviour, mass_spring.py:256-260);
-    otherwise failed plants keep running and their records carry the status.
+    ClosedLoopFailed for the first failing step (the reference's behaviour,
+    mass_spring.py:256-260); otherwise the records carry the statuses.
     """
     torch = _torch()
     cfg.validate()
@@ -175,7 +179,7 @@ def run_closed_loop_batch(cfg, x0s, steps, arg=None, warm_start="primal_dual",
     arg = arg or mode_preset("balance").with_tol(1e-6)
     x0s = np.atleast_2d(np.asarray(x0s, dtype=float))
     Bn = x0s.shape[0]
-    M, N = cfg.masses, cfg.horizon
+    M = cfg.masses
     nx, nu = 2 * M, M - 1
     A, Bm = mass_spring_dynamics(M, cfg.ts)
     host = OcpQpBatch.from_qps([gen_mass_spring(replace(cfg, x0=x0s[0]))])
@@ -185,59 +189,112 @@ def run_closed_loop_batch(cfg, x0s, steps, arg=None, warm_start="primal_dual",
         batch.alloc(name, per_qp, 0.0)
         batch.fields[name][:] = arr
     dev = batch.to(device)
+    lay = batch.layout
     rows, comps = _x0_rows(batch)
-    off = int(batch.layout.stage_slice("lb", 0).start)
+    off = int(lay.stage_slice("lb", 0).start)
     cols = torch.as_tensor(off + rows, device=device)
     comps_t = torch.as_tensor(comps, device=device)
     f64 = dict(dtype=torch.float64, device=device)
     At = torch.as_tensor(A.T.copy(), **f64)
     Bt = torch.as_tensor(Bm.T.copy(), **f64)
-    x = torch.as_tensor(x0s, **f64)
-    states = [x.clone()]
-    inputs = []
-    stats = []
-    cold_stats = []
-    guess = None
-    u_off0 = int(batch.layout.u_off[0])
-    for k in range(steps):
+    x = torch.as_tensor(x0s, **f64).clone()
+    u_off0 = int(lay.u_off[0])
+
+    def buffers():
+        return dict(y=torch.empty((Bn, lay.ny), **f64), pi=torch.empty((Bn, lay.ne), **f64),
+                    lam=torch.empty((Bn, lay.nc), **f64), t=torch.empty((Bn, lay.nc), **f64),
+                    status=torch.empty(Bn, dtype=torch.int32, device=device),
+                    iters=torch.empty(Bn, dtype=torch.int32, device=device),
+                    res=torch.empty((Bn, 5), **f64),
+                    flops=torch.empty(Bn, dtype=torch.int64, device=device), trace=None)
+
+    out = buffers()
+    cold = buffers() if compare_cold else None
+    guess = tuple(torch.zeros_like(out[k]) for k in ("y", "pi", "lam", "t"))
+    hist_x = torch.empty((steps + 1, Bn, nx), **f64)
+    hist_u = torch.empty((steps, Bn, nu), **f64)
+    hist_st = torch.empty((steps, Bn), dtype=torch.int32, device=device)
+    hist_it = torch.empty((steps, Bn), dtype=torch.int32, device=device)
+    hist_cold = torch.empty((steps, Bn), dtype=torch.int32, device=device) if compare_cold else None
+    hist_x[0].copy_(x)
+    cold_arg = replace(arg, warm_start="none")
+    warm_arg = replace(arg, warm_start=warm_start)
+
+    def step(first):
+        s = torch.cuda.current_stream()
         xs = x[:, comps_t]
         dev.fields["lb"][:, cols] = xs
         dev.fields["ub"][:, cols] = xs
-        step_arg = replace(arg, warm_start=warm_start if guess is not None else "none")
-        rep = solve_ocp_qp_batch(dev, step_arg, guess=guess, trace=False)
+        solve_ocp_qp_batch(dev, cold_arg if first else warm_arg, guess=None if first else guess,
+                           trace=False, out=out, stream=s)
         if compare_cold:
-            crep = solve_ocp_qp_batch(dev, replace(arg, warm_start="none"), trace=False)
-            cold_stats.append(crep.iterations.clone())
-        stats.append((rep.status_code.clone(), rep.iterations.clone()))
-        if strict:
-            bad = torch.nonzero(rep.status_code != 0)
-            if bad.numel():
-                i = int(bad[0, 0])
-                code = int(rep.status_code[i])
-                raise ClosedLoopFailed(
-                    f"controller solve failed at step {k} (plant {i}) with status "
-                    f"{rep.statuses()[i].value if code <= 4 else code}", step=k)
-        u0 = rep.y[:, u_off0:u_off0 + nu]
-        inputs.append(u0.clone())
-        x = x @ At + u0 @ Bt
-        states.append(x.clone())
-        guess = shift_guess(dev, (rep.y, rep.pi, rep.lam, rep.t))
+            solve_ocp_qp_batch(dev, cold_arg, trace=False, out=cold, stream=s)
+        u0 = out["y"][:, u_off0:u_off0 + nu]
+        x.copy_(x @ At + u0 @ Bt)
+        shift_guess(dev, (out["y"], out["pi"], out["lam"], out["t"]), out=guess, stream=s)
+
+    def record(k):
+        hist_u[k].copy_(out["y"][:, u_off0:u_off0 + nu])
+        hist_x[k + 1].copy_(x)
+        hist_st[k].copy_(out["status"])
+        hist_it[k].copy_(out["iters"])
+        if compare_cold:
+            hist_cold[k].copy_(cold["iters"])
+
+    step(True)
+    record(0)
+    k = 1
+    if graph and steps > 2:
+        try:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):   # warm-up of the warm step (a real step)
+                step(False)
+                record(1)
+            torch.cuda.current_stream().wait_stream(side)
+            k = 2
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step(False)
+            while k < steps:
+                g.replay()
+                record(k)
+                k += 1
+        except RuntimeError as exc:   # capture unsupported here: the rest runs eagerly
+            import warnings
+
+            warnings.warn(f"closed loop: CUDA graph capture failed ({exc}); running eagerly")
+            torch.cuda.synchronize()
+    while k < steps:
+        step(False)
+        record(k)
+        k += 1
     torch.cuda.synchronize()
-    S = torch.stack(states, 1).cpu().numpy()
-    U = torch.stack(inputs, 1).cpu().numpy()
-    st = [(a.cpu().numpy(), b.cpu().numpy()) for a, b in stats]
-    cs = [c.cpu().numpy() for c in cold_stats]
+    st = hist_st.cpu().numpy()
+    its = hist_it.cpu().numpy()
+    if strict:
+        bad = np.argwhere(st != 0)
+        if bad.size:
+            kk, i = (int(v) for v in bad[np.argmin(bad[:, 0])])
+            code = int(st[kk, i])
+            names = ["Success", "MaxIter", "MinStep", "NaNDetected", "Failure"]
+            raise ClosedLoopFailed(
+                f"controller solve failed at step {kk} (plant {i}) with status "
+                f"{names[code] if 0 <= code < 5 else code}", step=kk)
+    S = hist_x.permute(1, 0, 2).cpu().numpy()
+    U = hist_u.permute(1, 0, 2).cpu().numpy()
+    cs = hist_cold.cpu().numpy() if compare_cold else None
     names = {int(c): s.value for c, s in zip(range(5), (Status.Success, Status.MaxIter,
                                                          Status.MinStep, Status.NaNDetected,
                                                          Status.Failure))}
-    out = []
+    results = []
     for i in range(Bn):
-        recs = [StepRecord(step=k, status=names.get(int(st[k][0][i]), str(int(st[k][0][i]))),
-                           iterations=int(st[k][1][i]),
-                           cold_iterations=int(cs[k][i]) if compare_cold else None)
-                for k in range(steps)]
-        out.append(ClosedLoopResult(records=recs, states=S[i], inputs=U[i]))
-    return out
+        recs = [StepRecord(step=k2, status=names.get(int(st[k2, i]), str(int(st[k2, i]))),
+                           iterations=int(its[k2, i]),
+                           cold_iterations=int(cs[k2, i]) if compare_cold else None)
+                for k2 in range(steps)]
+        results.append(ClosedLoopResult(records=recs, states=S[i], inputs=U[i]))
+    return results
 
 
 def run_closed_loop(cfg, steps, arg=None, warm_start="primal_dual", compare_cold=False):

@@ -36,18 +36,20 @@ def main():
     ap.add_argument("--mode", default="balance")
     ap.add_argument("--tol", type=float, default=1e-6)
     ap.add_argument("--no-cold", action="store_true", help="warm solves only")
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph for the warm steps")
     a = ap.parse_args()
     cfg = MassSpringConfig(masses=a.masses, horizon=a.horizon)
     rng = np.random.default_rng(0)
     M = a.masses
     x0s = np.concatenate([rng.uniform(-1.0, 1.0, (a.plants, M)), np.zeros((a.plants, M))], 1)
     arg = mode_preset(a.mode).with_tol(a.tol)
-    run_closed_loop_batch(cfg, x0s, 2, arg=arg)          # warm-up (plans, kernels)
+    run_closed_loop_batch(cfg, x0s, 3, arg=arg, graph=not a.eager)   # warm-up (plans, kernels)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     e0.record()
-    res = run_closed_loop_batch(cfg, x0s, a.steps, arg=arg, compare_cold=not a.no_cold)
+    res = run_closed_loop_batch(cfg, x0s, a.steps, arg=arg, compare_cold=not a.no_cold,
+                                graph=not a.eager)
     e1.record()
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
@@ -59,6 +61,7 @@ def main():
         "workload": f"{a.plants} spring chains M={a.masses}, N={a.horizon}, {a.steps} steps, "
                     f"{a.mode} tol {a.tol:g}, warm primal_dual + paired cold solves",
         "ms_per_step": ms / a.steps, "wall_s": wall, "includes_cold_solves": not a.no_cold,
+        "cuda_graph": not a.eager,
         "plant_steps_per_s": a.plants * a.steps / (ms * 1e-3),
         "warm_iterations": warm, "cold_iterations": cold,
         "warm_over_cold": warm / cold if cold else None, "all_success": ok}))
