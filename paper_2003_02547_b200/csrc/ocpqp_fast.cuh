@@ -573,7 +573,10 @@ struct Shape {
     // measured to pay only where the stage operands are large (config 3); on
     // the small shapes the bigger tile costs more occupancy than it saves
     static constexpr int SSTAGE = (STAGE_SOLVE && NX * NW >= 1000) ? 3 : 0;
-    static constexpr int STAGE = STAGE0 + (SSTAGE ? (BA_BUF > SOLVE_BUF ? BA_BUF : SOLVE_BUF) : BA_BUF);
+    // general rows: the stage's Jg = [D C] and gamma-scaled copy, staged for the
+    // reduced-Hessian term Jg' diag(gamma) Jg of M~ (kkt_common.py:100-115)
+    static constexpr int JGB = NG > 0 ? 2 * NG * NW : 0;
+    static constexpr int STAGE = STAGE0 + (SSTAGE ? (BA_BUF > SOLVE_BUF ? BA_BUF : SOLVE_BUF) : BA_BUF) + JGB;
     // resident CTAs per SM the register allocation must allow (latency hiding
     // across QPs): 512 threads per SM
     static constexpr int MINB = TEAM >= OCPQP_MINB_THREADS ? 1 : OCPQP_MINB_THREADS / TEAM;
@@ -1140,6 +1143,19 @@ struct Kern {
                 if constexpr (S::STAGE_BA) return BAs[k * NW + j];
                 else return BAn[k * NW + j];
             };
+            // general rows of the stage into shared memory (read by M~ after the
+            // T1 barrier): JgT = [D C], JgS = diag(gamma_lo + gamma_up) [D C]
+            double* JgT = stg + (S::STAGE - S::JGB);
+            double* JgS = JgT + NG * NW;
+            if constexpr (NG > 0) {
+                const double* cfn = coef + n * d.M + d.NB;
+                for (int e = tid; e < NG * NW; e += TEAM) {
+                    const int r = e / NW, j = e - r * NW;
+                    const double v = Jg(c, n, NU, r, j);
+                    JgT[e] = v;
+                    JgS[e] = cfn[r] * v;
+                }
+            }
             // T1 = P_{n+1} [B A]   (kkt_ocp.py:232)
             stage_gemm<S::DMMA, NX, NW, NX, TEAM>([&](int i, int k) { return Pc[i * NX + k]; },
                                         [&](int k, int j) { return BA(k, j); }, NoPre(),
@@ -1168,8 +1184,7 @@ struct Kern {
                 if (NG > 0) {
                     double sg = 0.0;
 #pragma unroll 4
-                    for (int r = 0; r < NG; ++r)
-                        sg = fma(Jg(c, n, NU, r, i), cf[d.NB + r] * Jg(c, n, NU, r, j), sg);
+                    for (int r = 0; r < NG; ++r) sg = fma(JgT[r * NW + i], JgS[r * NW + j], sg);
                     h = sg + h;
                 }
                 if (i == j && reg != 0.0) h += reg;
