@@ -272,7 +272,8 @@ def main():
     plan_info = get_plan(dev).info()
     from paper_2003_02547_b200.ipm import team_supports
 
-    if plan_info.get("kernel") == "team" and not team_supports(arg):
+    if plan_info.get("kernel") == "team" and not team_supports(
+            arg, int(batch.dim.nx[0]) + int(batch.dim.nu[0])):
         plan_info["kernel"] = "generic"   # square-root / robust run on k_ipm_solve
 
     peak_dfma, peak_dmma = fp64_peak()

@@ -565,14 +565,15 @@ void place_generic_on_fast(OcpPlan* P) {
 // The team kernel runs the classical-Riccati delta-form loop with optional
 // refinement of the combined direction (speed, balance); the QR rungs of the
 // balance ladder are left to the generic kernel per QP (escape list).
-bool team_supports(const OcpIpmArgC* a) {
+bool team_supports(const OcpIpmArgC* a, int nw) {
     // delta form with residuals every iteration, or the speed_abs combination
     // (absolute form, residuals only at exit, no refinement / QR)
     const bool delta = !a->abs_form && a->comp_res_pred;
     const bool abs_speed = a->abs_form && !a->comp_res_pred && a->itref_corr_max <= 0 &&
                            !a->use_qr_fallback;
-    return (delta || abs_speed) && !a->use_qr_always && a->riccati_variant == 0 &&
-           a->itref_pred_max <= 0;
+    // square-root variant: warp Cholesky of the whole stage block (nw <= 32)
+    const bool variant_ok = a->riccati_variant == 0 || (a->riccati_variant == 1 && nw <= 32);
+    return (delta || abs_speed) && !a->use_qr_always && variant_ok && a->itref_pred_max <= 0;
 }
 
 // modes beyond the classical speed loop need the extended workspace
@@ -745,7 +746,8 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     if (P->B == 0) return OCPQP_OK;
     const bool ext = needs_ext(arg);
     if (ext && (rc = ensure_ext(P))) return rc;
-    const bool team = P->fast && P->shape.kind == 0 && team_supports(arg) && !getenv("OCPQP_EXT_GENERIC");
+    const bool team = P->fast && P->shape.kind == 0 &&
+                      team_supports(arg, P->shape.nx + P->shape.nu) && !getenv("OCPQP_EXT_GENERIC");
     KParams k;
     fill_kparams(P, k, data, !(ext && P->fast) || team);
     size_t gen_smem = P->smem_bytes;

@@ -1003,6 +1003,212 @@ struct Kern {
         return true;
     }
 
+    // ---------------- square-root Riccati factor (NW <= 32) ----------------
+    // kkt_ocp.py:206-230 without QR: W = L_{n+1}' [B A], G = W'W + M~, L_G =
+    // chol(G) (warp 0, rows in registers), split into L_uu, K = -L_uu^{-T}
+    // L_xu', L_P (_split_stage_factor :83-91).  The factor store holds L_P in
+    // P's place (lower triangle); the sweeps apply L_P L_P'.  Returns -1 ok,
+    // the failing stage, -2 non-positive iterate.
+    struct FacOut {
+        int fs;
+        long long flops;
+    };
+    __device__ __noinline__ static FacOut factor_sqrt(FCtx& c, const RD& d, const KParams& p,
+                                                      double* stg, const double* lam,
+                                                      const double* t, double reg) {
+        long long flops = 0;
+        const int tid = threadIdx.x;
+        const double* act = c.w[WS_DVEC];
+        double* gam = c.w[WS_GAM];
+        double* coef = c.w[WS_COEF];
+        double* Pst = wsb<WS_P>(c, p);
+        double* Kst = wsb<WS_K>(c, p);
+        double* Lst = wsb<WS_L>(c, p);
+        double* Rst = wsb<WS_RINV>(c, p);
+        double* Lc = stg;                       // NX*NX: L_{n+1} (full, upper zero)
+        double* W = Lc + NX * NX;               // NX*NW
+        double* Lxu = W + S::T1N;               // NX*NU scratch (fits the NU*NW tile)
+        double* tinv = c.w[WS_TINV];
+        int bad = 0;
+        for (int k = tid; k < d.nc; k += TEAM) {
+            double g = 0.0, ti = 0.0;
+            if (!isnan(act[k])) {
+                if (lam[k] <= 0.0 || t[k] <= 0.0) bad = 1;
+                ti = 1.0 / t[k];
+                g = lam[k] * ti;
+            }
+            gam[k] = g;
+            tinv[k] = ti;
+        }
+        if (any_of<TEAM>(bad)) return FacOut{-2, 0};
+        if constexpr (TEAM == 32) bar<TEAM>();
+        if constexpr (NG > 0) {
+            for (int r = tid; r < d.msum; r += TEAM) {
+                const int n = d.row_stage(r);
+                const int i = r - n * d.M;
+                const int m = n < d.N ? d.M : d.MN;
+                const int k = n * 2 * d.M + i;
+                coef[r] = gam[k] + gam[k + m];
+            }
+            bar<TEAM>();
+        }
+        auto cfv = [&](int n, int kb) -> double {
+            if constexpr (NG > 0) {
+                return coef[n * d.M + kb];
+            } else {
+                const int k = n * 2 * d.M + kb;
+                return gam[k] + gam[k + (n < d.N ? d.M : d.MN)];
+            }
+        };
+        const int N = d.N;
+        // stores L_P of stage n (lane row i of L_P, lanes NU.. of warp 0)
+        auto store_lp = [&](int n, int i, const double* row, int off) {
+            double* Ps = Pst + n * S::PST;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) {
+                const double v = j <= i ? row[off + j] : 0.0;
+                Lc[i * NX + j] = v;
+                if (j <= i) {
+                    if constexpr (S::PPACK) Ps[i * (i + 1) / 2 + j] = v;
+                    else Ps[i * NX + j] = v;
+                } else if constexpr (!S::PPACK) {
+                    Ps[i * NX + j] = 0.0;
+                }
+            }
+        };
+        // ---- terminal stage: L_P(N) = chol(M~_N) ----
+        if constexpr (NW <= 32) {
+            const int n = N;
+            const double* Qn = Q(c, n);
+            const double* cf = coef + n * d.M;
+            const int ng = d.NGN;
+            if (tid < 32) {
+                const int i = tid;
+                double row[NX];
+#pragma unroll
+                for (int j = 0; j < NX; ++j) {
+                    double h = 0.0;
+                    if (i < NX && j <= i) {
+                        h = 0.5 * (Qn[i * NX + j] + Qn[j * NX + i]);
+                        if (i == j) {
+                            const int kb = p.var_box[n * NW + i];
+                            if (kb >= 0) h += cfv(n, kb);
+                        }
+                        if (NG > 0 && ng > 0) {
+                            const double* Cn = Cm(c, n);
+                            double a = 0.0;
+                            for (int r = 0; r < ng; ++r) a = fma(Cn[r * NX + i], cf[d.NBN + r] * Cn[r * NX + j], a);
+                            h = a + h;
+                        }
+                        if (i == j && reg != 0.0) h += reg;
+                    }
+                    row[j] = h;
+                }
+                double rin = 0.0;
+                const bool ok = warp_chol<NX>(row, i, rin);
+                if (tid == 0) c.flag = ok;
+                if (ok && i < NX) {
+                    store_lp(n, i, row, 0);
+                    if (N == 0) Rst[i] = rin;
+                }
+            }
+            if (NG > 0 && ng > 0) flops += 2ll * NX * NX * ng;
+            flops += (long long)NX * NX * NX / 3;
+            bar<TEAM>();
+            if (!c.flag) return FacOut{n, flops};
+            // ---- stages N-1 .. 0 ----
+            for (int n = N - 1; n >= 0; --n) {
+                const double* BAn = BAp(c, n);
+                // W = L_{n+1}' [B A] (all threads)
+                stage_gemm<S::DMMA, NX, NW, NX, TEAM>(
+                    [&](int i, int k) { return k >= i ? Lc[k * NX + i] : 0.0; },
+                    [&](int k, int j) { return BAn[k * NW + j]; }, NoPre(),
+                    [&](int i, int j, double v, double) { W[i * NW + j] = v; });
+                flops += 2ll * NX * NW * NX + 2ll * NW * NW * NX;
+                bar<TEAM>();
+                const double* Qn = Q(c, n);
+                const double* Rn = R(c, n);
+                const double* Sn = Sm(c, n);
+                const double* cf = coef + n * d.M;
+                const bool full_box = d.NB == NW;
+                if (tid < 32) {
+                    // lane i: row i of G = W'W + M~ (j <= i), then the warp Cholesky
+                    const int i = tid;
+                    double row[NW];
+#pragma unroll
+                    for (int j = 0; j < NW; ++j) {
+                        double h = 0.0;
+                        if (i < NW && j <= i) {
+                            double a = 0.0;
+                            for (int k = 0; k < NX; ++k) a = fma(W[k * NW + i], W[k * NW + j], a);
+                            double mij, mji;
+                            if (i < NU && j < NU) { mij = Rn[i * NU + j]; mji = Rn[j * NU + i]; }
+                            else if (i < NU) { mij = Sn[i * NX + (j - NU)]; mji = mij; }
+                            else if (j < NU) { mij = Sn[j * NX + (i - NU)]; mji = mij; }
+                            else { mij = Qn[(i - NU) * NX + (j - NU)]; mji = Qn[(j - NU) * NX + (i - NU)]; }
+                            double m = 0.5 * (mij + mji);
+                            if (i == j) {
+                                const int kb = full_box ? i : p.var_box[n * NW + i];
+                                if (kb >= 0) m += cfv(n, kb);
+                            }
+                            if (NG > 0) {
+                                double sg = 0.0;
+                                for (int r = 0; r < NG; ++r)
+                                    sg = fma(Jg(c, n, NU, r, i), cf[d.NB + r] * Jg(c, n, NU, r, j), sg);
+                                m = sg + m;
+                            }
+                            if (i == j && reg != 0.0) m += reg;
+                            h = a + m;
+                        }
+                        row[j] = h;
+                    }
+                    double rin = 0.0;
+                    const bool ok = warp_chol<NW>(row, i, rin);
+                    if (tid == 0) c.flag = ok;
+                    if (ok) {
+                        if (i < NU) {
+#pragma unroll
+                            for (int j = 0; j < NU; ++j) Lst[n * NU * NU + i * NU + j] = j <= i ? row[j] : 0.0;
+                            Rst[n * NU + i] = rin;
+                        } else if (i < NW) {
+#pragma unroll
+                            for (int j = 0; j < NU; ++j) Lxu[(i - NU) * NU + j] = row[j];
+                            store_lp(n, i - NU, row, NU);
+                            if (n == 0) Rst[N * NU + (i - NU)] = rin;   // 1 / L_P0 diagonal
+                        }
+                    }
+                }
+                if (NG > 0) flops += 2ll * NW * NW * NG;
+                flops += (long long)NW * NW * NW / 3;
+                bar<TEAM>();
+                if (!c.flag) return FacOut{n, flops};
+                // K = -L_uu^{-T} L_xu' : column j from row j of L_xu (back substitution)
+                const double* Ln = Lst + n * NU * NU;
+                const double* rv = Rst + n * NU;
+                double* Kn = Kst + n * NU * NX;
+                for (int j = tid; j < NX; j += TEAM) {
+                    double z[NU];
+#pragma unroll
+                    for (int ii = NU - 1; ii >= 0; --ii) {
+                        double a = Lxu[j * NU + ii];
+#pragma unroll
+                        for (int k = ii + 1; k < NU; ++k) a = fma(-Ln[k * NU + ii], z[k], a);
+                        z[ii] = a * rv[ii];
+                    }
+#pragma unroll
+                    for (int ii = 0; ii < NU; ++ii) Kn[ii * NX + j] = -z[ii];
+                }
+                flops += (long long)NU * NU * NX;
+                bar<TEAM>();
+            }
+            // L_P0 = L_P(0) for the x0 step of the sweeps
+            double* LP0 = wsb<WS_LP0>(c, p);
+            for (int idx = tid; idx < NX * NX; idx += TEAM) LP0[idx] = Lc[idx];
+            bar<TEAM>();
+        }
+        return FacOut{-1, flops};
+    }
+
     // ---------------- classical Riccati factor ----------------
     // returns -1 ok, failing stage, -2 non-positive iterate
     OCPQP_BIGFN static int factor(FCtx& c, const RD& d, const KParams& p, double* stg,
@@ -1359,7 +1565,7 @@ struct Kern {
                                 const double* lam, const double* t, const double* rm_ext,
                                 double tau, const double* dla, const double* dta, double* dy,
                                 double* dpi, double* dlam, double* dt, long long& flops,
-                                int absm = 0) {
+                                int absm = 0, bool lp = false) {
         const int tid = threadIdx.x;
         const double* act = c.w[WS_DVEC];  // NaN = inactive
         const double* gam = c.w[WS_GAM];
@@ -1504,9 +1710,20 @@ struct Kern {
             const double* rh = (st && gRH) ? H + oRH : rhat + n * NW;
             const double* BAn = BAp(c, n);
             auto BA = [&](int k, int j) -> double { return ss ? H[oBA + k * NW + j] : BAn[k * NW + j]; };
-            MV<NX, NX, TEAM>::run([&](int i, int k) { return Pget(Pn, i, k); },
-                                  [&](int k) { return rb[k]; },
-                                  [&](int i, double v) { e[i] = v + pvs[i]; });
+            if (lp) {
+                // square-root factor: P r_b = L_P (L_P' r_b) (kkt_ocp.py:110-113)
+                MV<NX, NX, TEAM>::run([&](int i, int k) { return k >= i ? Pget(Pn, k, i) : 0.0; },
+                                      [&](int k) { return rb[k]; },
+                                      [&](int i, double v) { xv[i] = v; });
+                bar<TEAM>();
+                MV<NX, NX, TEAM>::run([&](int i, int k) { return k <= i ? Pget(Pn, i, k) : 0.0; },
+                                      [&](int k) { return xv[k]; },
+                                      [&](int i, double v) { e[i] = v + pvs[i]; });
+            } else {
+                MV<NX, NX, TEAM>::run([&](int i, int k) { return Pget(Pn, i, k); },
+                                      [&](int k) { return rb[k]; },
+                                      [&](int i, double v) { e[i] = v + pvs[i]; });
+            }
             bar<TEAM>();
             MV<NW, NX, TEAM>::run([&](int j, int k) { return BA(k, j); },
                                   [&](int k) { return e[k]; },
@@ -1615,6 +1832,19 @@ struct Kern {
         }
         OCPQP_TICK(c, DBG_S_FWD);
         // dpi_n = P_{n+1} x_{n+1} + pv_{n+1}, all stages in parallel
+        double* zt = lp ? c.x[WS_ZT - WS_EXT0] : nullptr;
+        if (lp) {   // z = L_P' x of every stage first
+            for (int e2 = tid; e2 < d.ne; e2 += TEAM) {
+                const int n = e2 / NX;
+                const int i = e2 - n * NX;
+                const double* Pn = Pst + (n + 1) * S::PST;
+                const double* xn = dy + (n + 1) * NW + (n + 1 < N ? NU : 0);
+                double a = 0.0;
+                for (int k = i; k < NX; ++k) a = fma(Pget(Pn, k, i), xn[k], a);
+                zt[e2] = a;
+            }
+            bar<TEAM>();
+        }
         OCPQP_PASS_UNROLL
         for (int e2 = tid; e2 < d.ne; e2 += TEAM) {
             const int n = e2 / NX;
@@ -1622,8 +1852,13 @@ struct Kern {
             const double* Pn = Pst + (n + 1) * S::PST;
             const double* xn = dy + (n + 1) * NW + (n + 1 < N ? NU : 0);
             double a = 0.0;
+            if (lp) {
+                const double* zz = zt + n * NX;
+                for (int k = 0; k <= i; ++k) a = fma(Pget(Pn, i, k), zz[k], a);
+            } else {
 #pragma unroll 8
-            for (int k = 0; k < NX; ++k) a = fma(Pget(Pn, i, k), xn[k], a);
+                for (int k = 0; k < NX; ++k) a = fma(Pget(Pn, i, k), xn[k], a);
+            }
             const double v = a + pv[(n + 1) * NX + i];
             dpi[e2] = v;
             if (!isfinite(v)) nonfinite = 1;
@@ -1821,7 +2056,7 @@ struct Kern {
     __device__ __noinline__ static RefOut refine(FCtx& c, const RD& d, const KParams& p,
                                                  double* stg, const double* lam, const double* t,
                                                  double* dy, double* dpi, double* dl, double* dt,
-                                                 int max_steps, double stop_ratio) {
+                                                 int max_steps, double stop_ratio, bool lp) {
         long long flops = 0;
         const double* act = c.w[WS_DVEC];
         const double* hg = c.x[WS_GF - WS_EXT0];
@@ -1857,7 +2092,7 @@ struct Kern {
         double norm = best;
         int grew = 0;
         for (int st = 0; st < max_steps; ++st) {
-            solve(c, d, p, stg, lam, t, om, 0.0, nullptr, nullptr, cy, cpi, cl, ct, flops);
+            solve(c, d, p, stg, lam, t, om, 0.0, nullptr, nullptr, cy, cpi, cl, ct, flops, 0, lp);
             bar<TEAM>();
             for (int i = threadIdx.x; i < d.nv; i += TEAM) dy[i] = dy[i] + cy[i];
             for (int i = threadIdx.x; i < d.ne; i += TEAM) dpi[i] = dpi[i] + cpi[i];
@@ -2019,11 +2254,23 @@ struct Kern {
             OCPQP_TICK(c, DBG_RES);
             if (status >= 0) break;
             bar<TEAM>();
-            int fs = factor(c, d, p, stg, lam, t, arg.reg_prim, flops);
+            // square-root variant (REF instantiation, NW <= 32): factor_sqrt
+            const bool sqv = REF && arg.riccati_variant != 0;
+            auto do_factor = [&](double rg) -> int {
+                if constexpr (REF && NW <= 32) {
+                    if (sqv) {
+                        const FacOut fo = factor_sqrt(c, d, p, stg, lam, t, rg);
+                        flops += fo.flops;
+                        return fo.fs;
+                    }
+                }
+                return factor(c, d, p, stg, lam, t, rg, flops);
+            };
+            int fs = do_factor(arg.reg_prim);
             // the balance-mode ladder continues with the QR array algorithm
             // (solver.py:145-164): the generic kernel re-solves this QP
             if (REF && fs >= 0 && arg.use_qr_fallback) { status = STATUS_ESCAPE; break; }
-            if (fs >= 0) { bar<TEAM>(); fs = factor(c, d, p, stg, lam, t, reg2, flops); }
+            if (fs >= 0) { bar<TEAM>(); fs = do_factor(reg2); }
             if (fs == -2) { status = OCPQP_STATUS_NONPOSITIVE_ITERATE; break; }
             if (fs >= 0) { status = OCPQP_STATUS_FAILURE; break; }
             OCPQP_TICK(c, DBG_FACTOR);
@@ -2043,7 +2290,7 @@ struct Kern {
             };
             {
                 int nfa = solve(c, d, p, stg, lam, t, nullptr, 0.0, nullptr, nullptr, dy, dpi, alam,
-                                at, flops, absf ? 1 : 0);
+                                at, flops, absf ? 1 : 0, sqv);
                 if (absf) { bar<TEAM>(); nfa = to_step(dy, dpi, alam, at); }
                 if (nfa) {
                     status = OCPQP_STATUS_NAN;
@@ -2058,7 +2305,7 @@ struct Kern {
             if (mu > 0.0) sigma = fmin(1.0, fmax(0.0, pow(mu_aff / mu, 3.0)));
             const double tau = sigma * mu;
             int nf = solve(c, d, p, stg, lam, t, nullptr, tau, arg.pred_corr ? alam : nullptr,
-                           arg.pred_corr ? at : nullptr, dy, dpi, dlam, dt, flops, absf ? 2 : 0);
+                           arg.pred_corr ? at : nullptr, dy, dpi, dlam, dt, flops, absf ? 2 : 0, sqv);
             bar<TEAM>();
             if (absf) { nf = to_step(dy, dpi, dlam, dt); bar<TEAM>(); }
             bool rejected = false;
@@ -2068,7 +2315,7 @@ struct Kern {
                 if (!(mu_t <= arg.corr_ratio * mu_aff)) {
                     rejected = true;
                     nf = solve(c, d, p, stg, lam, t, nullptr, tau, nullptr, nullptr, dy, dpi, dlam, dt,
-                               flops, absf ? 2 : 0);
+                               flops, absf ? 2 : 0, sqv);
                     bar<TEAM>();
                     if (absf) { nf = to_step(dy, dpi, dlam, dt); bar<TEAM>(); }
                 }
@@ -2098,7 +2345,7 @@ struct Kern {
                 }
                 bar<TEAM>();
                 const RefOut ro = refine(c, d, p, stg, lam, t, dy, dpi, dlam, dt,
-                                         arg.itref_corr_max, arg.itref_stop_ratio);
+                                         arg.itref_corr_max, arg.itref_stop_ratio, sqv);
                 flops += ro.flops;
                 if (arg.use_qr_fallback && ro.best > arg.qr_fallback_ratio * ro.rhs) {
                     status = STATUS_ESCAPE;   // QR refactorization: generic kernel
@@ -2229,7 +2476,8 @@ int stage_doubles() { return S::STAGE; }
 
 template <class S>
 cudaError_t launch(const KParams& p, const SolveParams& sp, int grid, size_t smem, cudaStream_t st) {
-    const bool ref = sp.arg.itref_corr_max > 0 || sp.arg.use_qr_fallback || sp.arg.abs_form;
+    const bool ref = sp.arg.itref_corr_max > 0 || sp.arg.use_qr_fallback || sp.arg.abs_form ||
+                     sp.arg.riccati_variant != 0;
     cudaError_t e = cudaFuncSetAttribute(ref ? k_fast_solve<S, true> : k_fast_solve<S, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
