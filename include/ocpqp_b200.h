@@ -55,6 +55,7 @@ extern "C" {
 #define OCPQP_E_UNSUPPORTED (-3)      /* option outside the implemented modes */
 #define OCPQP_E_CUDA (-4)             /* CUDA runtime error */
 #define OCPQP_E_ARG (-5)              /* bad argument / NULL pointer */
+#define OCPQP_E_CONDENSE (-6)         /* CondenseError (errors.py; condensing.py:180-185) */
 
 /* per-QP status words; values 0..4 mirror ipm_core.Status (ipm_core.py:56-63) */
 #define OCPQP_STATUS_SUCCESS 0
@@ -272,6 +273,20 @@ int ocpqp_pc_condense(OcpPcPlan* plan, int32_t B, const OcpQpDataC* in, OcpQpDat
  * condensing.py:553-619); device pointers. */
 int ocpqp_pc_expand(OcpPcPlan* plan, int32_t B, const OcpQpDataC* in, const OcpIterC* short_sol,
                     OcpIterC* full_sol, void* stream);
+
+/* ---- full condensing (reference condense / expand_solution,
+ * condensing.py:160-429) ----
+ * The plan of condense(qp, keep_x0): one block over stages 0..N (terminal
+ * included).  keep_x0 = 0 drops x0: every component must be fixed by a
+ * stage-0 box row (fix_row[j] fixes component fix_comp[j], nfix entries, as
+ * _detect_fixed_x0 finds them, condensing.py:97-118), else OCPQP_E_CONDENSE.
+ * The dense QP (ne = 0) is produced as a single-stage OCP-QP with N = 0,
+ * nx = 0, nu = nv: R = H, r = g, D = C, idxb = dense idxb -- the IPM kernels
+ * solve that form exactly like the reference's dense backend
+ * (solve_dense_qp, solver.py:98-100).  ocpqp_pc_dims / _condense / _expand /
+ * _destroy take this plan too (N2 = 0; expansion = expand_solution). */
+int ocpqp_fc_create(const OcpQpDimC* dim, int32_t keep_x0, int32_t nfix, const int32_t* fix_row,
+                    const int32_t* fix_comp, OcpPcPlan** out);
 
 const char* ocpqp_pc_last_error(void);
 

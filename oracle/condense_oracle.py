@@ -204,3 +204,198 @@ def partial_expand(qp, blocks, short):
     lam[lay.c_off[N]: lay.c_off[N] + ncN] = short["lam"][sl.c_off[Np]: sl.c_off[Np] + ncN]
     t[lay.c_off[N]: lay.c_off[N] + ncN] = short["t"][sl.c_off[Np]: sl.c_off[Np] + ncN]
     return y, pi, lam, t
+
+
+# ---------------------------------------------------------------------------
+# full condensing (condensing.py:160-340) and expand_solution (:343-429)
+# ---------------------------------------------------------------------------
+
+def detect_fixed_x0(qp):
+    """(all_fixed, x0hat, fix_rows) from stage-0 equal-bound rows (condensing.py:97-118)."""
+    s = qp._stages[0]
+    nu0, nx0 = int(qp.dim.nu[0]), int(qp.dim.nx[0])
+    x0hat = np.full(nx0, np.nan)
+    fix = []
+    for i, k in enumerate(s["idxb"]):
+        if k < nu0:
+            continue
+        c = int(k) - nu0
+        lo, up = s["lb"][i], s["ub"][i]
+        if lo == up and np.isfinite(lo) and s["maskl"][i] != 0.0 and s["masku"][i] != 0.0:
+            x0hat[c] = lo
+            fix.append((i, c))
+    return (not np.any(np.isnan(x0hat))) if nx0 else True, x0hat, fix
+
+
+def full_condense(qp, keep_x0=None):
+    """Dense QP fields (H, g, idxb, lb, ub, C, lg, ug, maskl, masku) + map.
+
+    Classical cost recursion (condensing.py:148-157) with P[N] = sym(Q_N);
+    z = [x0 (kept) | u_0 | ... | u_N]; x-box rows past stage 0 and all general
+    rows become dense general rows in stage order; box rows sorted by z.
+    """
+    d = qp.dim
+    N = int(d.N)
+    all_fixed, x0hat, fix = detect_fixed_x0(qp)
+    if keep_x0 is None:
+        keep_x0 = not all_fixed
+    if not keep_x0 and not all_fixed:
+        raise ValueError("keep_x0=False requires every initial-state component fixed")
+    nx0 = int(d.nx[0])
+    zx = nx0 if keep_x0 else 0
+    u_off, off = [], zx
+    for n in range(N + 1):
+        nu = int(d.nu[n])
+        u_off.append(off if nu else None)
+        off += nu
+    nv = off
+    pred = [np.zeros((int(d.nx[n]), nv)) for n in range(N + 1)]
+    gamma = [np.zeros(nx0) if keep_x0 else x0hat.copy()]
+    if keep_x0:
+        pred[0][:, :nx0] = np.eye(nx0)
+    for n in range(N):
+        A, B, b = qp._dyn[n]["A"], qp._dyn[n]["B"], qp._dyn[n]["b"]
+        pred[n + 1] = A @ pred[n]
+        if u_off[n] is not None:
+            pred[n + 1][:, u_off[n]: u_off[n] + B.shape[1]] += B
+        gamma.append(A @ gamma[n] + b)
+    st = qp._stages
+    P = [None] * (N + 1)
+    Y = [None] * N
+    P[N] = 0.5 * (st[N]["Q"] + st[N]["Q"].T)
+    for n in range(N - 1, -1, -1):
+        A, B = qp._dyn[n]["A"], qp._dyn[n]["B"]
+        Y[n] = A.T @ (P[n + 1] @ B) + st[n]["S"].T
+        Pn = A.T @ (P[n + 1] @ A) + st[n]["Q"]
+        P[n] = 0.5 * (Pn + Pn.T)
+    beta = [None] * (N + 1)
+    beta[N] = st[N]["q"] + st[N]["Q"] @ gamma[N]
+    for n in range(N - 1, -1, -1):
+        beta[n] = st[n]["q"] + st[n]["Q"] @ gamma[n] + qp._dyn[n]["A"].T @ beta[n + 1]
+    H = np.zeros((nv, nv))
+    g = np.zeros(nv)
+    if keep_x0:
+        H[:nx0, :nx0] = P[0]
+        g[:nx0] = beta[0]
+    for j in range(N + 1):
+        nu = int(d.nu[j])
+        if not nu:
+            continue
+        o = u_off[j]
+        if j < N:
+            Bj = qp._dyn[j]["B"]
+            H[o: o + nu, o: o + nu] = st[j]["R"] + Bj.T @ (P[j + 1] @ Bj)
+            cross = Y[j]
+            g[o: o + nu] = st[j]["r"] + st[j]["S"] @ gamma[j] + Bj.T @ beta[j + 1]
+        else:
+            H[o: o + nu, o: o + nu] = st[j]["R"]
+            cross = st[j]["S"].T
+            g[o: o + nu] = st[j]["r"] + st[j]["S"] @ gamma[j]
+        cols = pred[j].T @ cross
+        H[:, o: o + nu] += cols
+        H[o: o + nu, :] += cols.T
+    H = 0.5 * (H + H.T)
+    box, gen = [], []
+    for n in range(N + 1):
+        s = st[n]
+        nu = int(d.nu[n])
+        for r, k in enumerate(s["idxb"]):
+            if k < nu:
+                box.append((u_off[n] + int(k), n, r))
+            elif n == 0 and keep_x0:
+                box.append((int(k) - nu, n, r))
+            elif n == 0:
+                continue
+            else:
+                c = int(k) - nu
+                gen.append((pred[n][c].copy(), s["lb"][r] - gamma[n][c], s["ub"][r] - gamma[n][c],
+                            n, r))
+        for gi in range(int(d.ng[n])):
+            row = np.zeros(nv)
+            if nu:
+                row[u_off[n]: u_off[n] + nu] = s["D"][gi]
+            row += s["C"][gi] @ pred[n]
+            sh = float(s["C"][gi] @ gamma[n])
+            gen.append((row, s["lg"][gi] - sh, s["ug"][gi] - sh, n, int(d.nb[n]) + gi))
+    box.sort(key=lambda e: e[0])
+    rows = [(e[1], e[2]) for e in box] + [(e[3], e[4]) for e in gen]
+    dense = dict(
+        H=H, g=g, idxb=np.array([e[0] for e in box], dtype=int),
+        lb=np.array([st[e[1]]["lb"][e[2]] for e in box]),
+        ub=np.array([st[e[1]]["ub"][e[2]] for e in box]),
+        C=np.array([e[0] for e in gen]).reshape(len(gen), nv),
+        lg=np.array([e[1] for e in gen]), ug=np.array([e[2] for e in gen]),
+        maskl=np.array([st[n]["maskl"][r] for n, r in rows]),
+        masku=np.array([st[n]["masku"][r] for n, r in rows]))
+    cmap = dict(keep_x0=keep_x0, x0hat=None if keep_x0 else x0hat, nx0=nx0, u_off=u_off, nv=nv,
+                rows=rows, nb=len(box), fix=[] if keep_x0 else fix)
+    return dense, cmap
+
+
+def _ctlam_x(qp, lam, lay, n):
+    """(C' lam)_x of stage n over active multipliers (view.py:145-153, 197-205)."""
+    d = qp.dim
+    s = qp._stages[n]
+    nu, nb, ng = int(d.nu[n]), int(d.nb[n]), int(d.ng[n])
+    mo = nb + ng
+    lm = lam[lay.c_off[n]: lay.c_off[n] + 2 * mo]
+    lo = np.concatenate([s["lb"], s["lg"]])
+    up = np.concatenate([s["ub"], s["ug"]])
+    al = (s["maskl"] != 0) & np.isfinite(lo)
+    au = (s["masku"] != 0) & np.isfinite(up)
+    coef = np.where(al, lm[:mo], 0.0) - np.where(au, lm[mo:], 0.0)
+    ct = np.zeros(nu + int(d.nx[n]))
+    np.add.at(ct, s["idxb"], coef[:nb])
+    if ng:
+        ct += np.hstack([s["D"], s["C"]]).T @ coef[nb:]
+    return ct[nu:]
+
+
+def full_expand(qp, cmap, v, dlam, dt):
+    """Full OCP (y, pi, lam, t) from the dense solution (condensing.py:343-429)."""
+    from paper_2003_02547_b200.layout import OcpLayout
+
+    d = qp.dim
+    N = int(d.N)
+    lay = OcpLayout(d)
+    y = np.zeros(lay.ny)
+    pi = np.zeros(lay.ne)
+    lam = np.zeros(lay.nc)
+    t = np.zeros(lay.nc)
+    x = cmap["x0hat"].copy() if not cmap["keep_x0"] else v[: cmap["nx0"]].copy()
+    xs = [x]
+    for n in range(N + 1):
+        nu = int(d.nu[n])
+        u = v[cmap["u_off"][n]: cmap["u_off"][n] + nu] if nu else np.zeros(0)
+        y[lay.u_off[n]: lay.u_off[n] + nu] = u
+        y[lay.x_off[n]: lay.x_off[n] + int(d.nx[n])] = xs[n]
+        if n < N:
+            dyn = qp._dyn[n]
+            xs.append(dyn["A"] @ xs[n] + dyn["B"] @ u + dyn["b"])
+    mc = len(cmap["rows"])
+    for r, (n, src) in enumerate(cmap["rows"]):
+        mo = int(d.nb[n] + d.ng[n])
+        c0 = lay.c_off[n]
+        lam[c0 + src], lam[c0 + mo + src] = dlam[r], dlam[mc + r]
+        t[c0 + src], t[c0 + mo + src] = dt[r], dt[mc + r]
+    ctx = [_ctlam_x(qp, lam, lay, n) for n in range(N + 1)]
+    for m in range(N, 0, -1):
+        s = qp._stages[m]
+        nu = int(d.nu[m])
+        val = s["Q"] @ xs[m] + s["S"].T @ y[lay.u_off[m]: lay.u_off[m] + nu] + s["q"] - ctx[m]
+        if m < N:
+            val = val + qp._dyn[m]["A"].T @ pi[lay.pi_off[m]: lay.pi_off[m] + int(d.nx[m + 1])]
+        pi[lay.pi_off[m - 1]: lay.pi_off[m - 1] + val.size] = val
+    if cmap["fix"]:
+        s = qp._stages[0]
+        nu = int(d.nu[0])
+        gap = s["Q"] @ xs[0] + s["S"].T @ y[lay.u_off[0]: lay.u_off[0] + nu] + s["q"] - ctx[0]
+        if N >= 1:
+            gap = gap + qp._dyn[0]["A"].T @ pi[lay.pi_off[0]: lay.pi_off[0] + int(d.nx[1])]
+        mo = int(d.nb[0] + d.ng[0])
+        for i, c in cmap["fix"]:
+            if gap[c] >= 0.0:
+                lam[lay.c_off[0] + i] = gap[c]
+            else:
+                lam[lay.c_off[0] + mo + i] = -gap[c]
+    return y, pi, lam, t

@@ -9,7 +9,12 @@ steps of every QP in one launch).  See DESIGN.md.
 
 from .batch import OcpQpBatch
 from .condensing import (
+    CondensingMap,
     PartialCondensingMap,
+    condense,
+    condense_batch,
+    expand_batch,
+    expand_solution,
     partial_condense,
     partial_condense_batch,
     partial_expand,
@@ -33,6 +38,7 @@ from .errors import (
     SingularSlackBlock,
     UnknownField,
 )
+from .dense import DenseQp, dense_to_ocp, ocp_to_dense, solve_dense_qp
 from .ipm import IpmArg, IterRecord, SolverStats, Status, mode_preset
 from .mpc import (
     ClosedLoopResult,
@@ -69,5 +75,7 @@ __all__ = [
     "solve_ocp_qp_host", "PartialCondensingMap", "partial_condense", "partial_condense_batch",
     "partial_expand", "partial_expand_batch", "ClosedLoopResult", "MassSpringConfig",
     "default_x0", "gen_mass_spring", "mass_spring_dynamics", "run_closed_loop",
-    "run_closed_loop_batch", "shift_guess", "__version__",
+    "run_closed_loop_batch", "shift_guess", "CondensingMap", "condense", "condense_batch",
+    "expand_batch", "expand_solution", "DenseQp", "dense_to_ocp", "ocp_to_dense", "solve_dense_qp",
+    "__version__",
 ]

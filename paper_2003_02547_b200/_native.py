@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = (
     "ocpqp_solve_host", "ocpqp_residuals", "ocpqp_newton_step", "ocpqp_factor_export",
     "ocpqp_plan_info", "ocpqp_fp64_peak", "ocpqp_abi_version", "ocpqp_last_error",
     "ocpqp_pc_create", "ocpqp_pc_destroy", "ocpqp_pc_dims", "ocpqp_pc_condense",
-    "ocpqp_pc_expand", "ocpqp_pc_last_error", "ocpqp_shift_guess",
+    "ocpqp_pc_expand", "ocpqp_pc_last_error", "ocpqp_shift_guess", "ocpqp_fc_create",
 )
 
 _i32p = ctypes.POINTER(ctypes.c_int32)

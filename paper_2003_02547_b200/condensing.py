@@ -1,4 +1,5 @@
-"""Batched partial condensing / expansion on the GPU (reference condensing.py:451-619).
+"""Batched partial / full condensing and expansion on the GPU (reference
+condensing.py:160-619).
 
 ``partial_condense_batch(batch, N1)`` turns a batch of OCP-QPs with horizon N
 into the batch of block-condensed QPs with horizon ceil(N / N1) (each block of
@@ -9,6 +10,13 @@ recursion for pi).  The routing tables are built once per structure by the C
 ABI (ocpqp_pc_create); the arithmetic runs in the CUDA kernels of
 csrc/ocpqp_condense.cu.  ``partial_condense`` / ``partial_expand`` are the
 reference's single-QP calls.
+
+``condense_batch(batch, keep_x0)`` is full condensing (condense,
+condensing.py:160-340): every state except (optionally) x0 eliminated, the
+dense QP returned as the single-stage batch (N = 0, nx = 0, nu = nv) that the
+IPM kernels solve exactly like the reference's dense backend (dense.py);
+``expand_batch`` is expand_solution (condensing.py:343-429).  ``condense`` /
+``expand_solution`` are the single-QP drop-ins.
 """
 
 from __future__ import annotations
@@ -19,12 +27,13 @@ import numpy as np
 
 from . import _native as nat
 from .batch import OcpQpBatch, default_fill
-from .errors import InvalidBlockSize, NativeLibraryError
+from .errors import CondenseError, DimensionMismatch, InvalidBlockSize, NativeLibraryError
 from .layout import FIELD_ORDER, QpSolution
 from .qp_data import OcpQp, OcpQpDim
 
 __all__ = ["PartialCondensingMap", "partial_condense_batch", "partial_expand_batch",
-           "partial_condense", "partial_expand"]
+           "partial_condense", "partial_expand", "CondensingMap", "condense_batch", "expand_batch",
+           "condense", "expand_solution", "detect_fixed_x0"]
 
 
 def _lib():
@@ -38,6 +47,9 @@ def _lib():
                                         ctypes.POINTER(nat.OcpQpDataC), vp]
         L.ocpqp_pc_expand.argtypes = [vp, ctypes.c_int32, ctypes.POINTER(nat.OcpQpDataC),
                                       ctypes.POINTER(nat.OcpIterC), ctypes.POINTER(nat.OcpIterC), vp]
+        L.ocpqp_fc_create.argtypes = [ctypes.POINTER(nat.OcpQpDimC), ctypes.c_int32, ctypes.c_int32,
+                                      vp, vp, ctypes.POINTER(vp)]
+        L.ocpqp_fc_create.restype = ctypes.c_int
         L.ocpqp_pc_last_error.restype = ctypes.c_char_p
         for f in ("ocpqp_pc_create", "ocpqp_pc_destroy", "ocpqp_pc_dims", "ocpqp_pc_condense",
                   "ocpqp_pc_expand"):
@@ -56,6 +68,8 @@ def _check(rc):
         raise NotImplementedError(msg)
     if rc == -5:
         raise ValueError(msg)
+    if rc == -6:
+        raise CondenseError(msg)
     raise NativeLibraryError(f"partial condensing error {rc}: {msg}")
 
 
@@ -217,5 +231,208 @@ def partial_expand(sol_p, pmap, qp):
     b = OcpQpBatch.from_qps([qp])
     y, pi, lam, t = partial_expand_batch(
         tuple(np.asarray(a)[None] for a in (sol_p.y, sol_p.pi, sol_p.lam, sol_p.t)), pmap, b)
+    return QpSolution(b.layout, y[0].cpu().numpy(), pi[0].cpu().numpy(), lam[0].cpu().numpy(),
+                      t[0].cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# full condensing (condensing.py:160-429)
+# ---------------------------------------------------------------------------
+
+def _stage0_rows(batch):
+    """Host copies [Bf, nb0] of the stage-0 lb, ub, maskl, masku of a batch."""
+    d = batch.dim
+    nb0 = int(d.nb[0])
+    out = []
+    for name in ("lb", "ub", "maskl", "masku"):
+        arr = batch.fields.get(name)
+        if arr is None:
+            from .batch import default_fill
+            out.append(np.full((1, nb0), default_fill(name)))
+            continue
+        sl = batch.layout.stage_slice(name, 0)
+        a = arr[:, sl]
+        if not isinstance(a, np.ndarray):
+            a = a.detach().cpu().numpy()
+        out.append(np.asarray(a, dtype=np.float64)[:, :nb0])
+    return out
+
+
+def detect_fixed_x0(batch):
+    """(all_fixed, fix_rows) of _detect_fixed_x0 (condensing.py:97-118) for a batch.
+
+    A stage-0 x row fixes its component when lb == ub, finite, both masks set.
+    Every QP of the batch must fix the same rows (CondenseError otherwise).
+    """
+    d = batch.dim
+    nu0, nx0 = int(d.nu[0]), int(d.nx[0])
+    lb, ub, ml, mu = _stage0_rows(batch)
+    fixed = (lb == ub) & np.isfinite(lb) & (ml != 0.0) & (mu != 0.0)
+    B = batch.B
+    fixed = np.broadcast_to(fixed, (B, fixed.shape[1])) if fixed.shape[0] == 1 else fixed
+    idxb = batch.idxb[0]
+    xrow = idxb >= nu0
+    fixed = fixed & xrow[None, :]
+    if B > 1 and not np.all(fixed == fixed[:1]):
+        raise CondenseError("the QPs of the batch fix different initial-state rows; "
+                            "condense them separately")
+    rows = [(int(i), int(idxb[i]) - nu0) for i in np.flatnonzero(fixed[0])]
+    comps = {c for _, c in rows}
+    all_fixed = (len(comps) == nx0) if nx0 else True
+    return all_fixed, rows
+
+
+class CondensingMap:
+    """Full-condensing plan of one batch structure (reference CondensingMap)."""
+
+    def __init__(self, batch, keep_x0=None):
+        d = batch.dim
+        all_fixed, rows = detect_fixed_x0(batch)
+        if keep_x0 is None:
+            keep_x0 = not all_fixed
+        if not keep_x0 and not all_fixed:
+            raise CondenseError("keep_x0=False requires every initial-state component fixed "
+                                "by active equal-bound box rows")
+        self.keep_x0 = bool(keep_x0)
+        self.fix_rows = [] if self.keep_x0 else rows
+        self.dim = d
+        self.N = d.N
+        self.nx0 = int(d.nx[0])
+        self._dimc, self._keep = nat.make_dim_c(d, batch.idxb_concat(), batch.idxs_concat())
+        fr = np.array([r for r, _ in self.fix_rows] or [0], dtype=np.int32)
+        fc = np.array([c for _, c in self.fix_rows] or [0], dtype=np.int32)
+        h = ctypes.c_void_p()
+        _check(_lib().ocpqp_fc_create(ctypes.byref(self._dimc), int(self.keep_x0),
+                                      len(self.fix_rows), fr.ctypes.data, fc.ctypes.data,
+                                      ctypes.byref(h)))
+        self.handle = h
+        arrs = [np.zeros(1, dtype=np.int32) for _ in range(4)]
+        _lib().ocpqp_pc_dims(h, *(a.ctypes.data for a in arrs), None)
+        nx, nu, nb, ng = (int(a[0]) for a in arrs)
+        idxb = np.zeros(max(1, nb), dtype=np.int32)
+        _lib().ocpqp_pc_dims(h, None, None, None, None, idxb.ctypes.data)
+        self.nv = nu
+        self.new_dim = OcpQpDim(0, [0], [nu], [nb], [ng], [0])
+        self.new_idxb = [idxb[:nb].copy()]
+        zx = self.nx0 if self.keep_x0 else 0
+        self.u_off, off = [], zx
+        for n in range(d.N + 1):
+            self.u_off.append(off if int(d.nu[n]) else None)
+            off += int(d.nu[n])
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib().ocpqp_pc_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_FMAPS = {}
+
+
+def _fmap_for(batch, keep_x0):
+    all_fixed, rows = detect_fixed_x0(batch)
+    keep = (not all_fixed) if keep_x0 is None else bool(keep_x0)
+    key = (batch.structure_key(), keep, tuple(rows) if not keep else ())
+    m = _FMAPS.get(key)
+    if m is None:
+        m = CondensingMap(batch, keep)
+        _FMAPS[key] = m
+    return m
+
+
+def condense_batch(batch, keep_x0=None, device="cuda"):
+    """Fully condensed device batch (N = 0, nx = 0, nu = nv) and its map."""
+    import torch
+
+    from .solver import _as_batch
+
+    batch = _as_batch(batch, check=False)
+    cmap = _fmap_for(batch, keep_x0)
+    src = _device_full(batch, device)
+    out = OcpQpBatch(cmap.new_dim, batch.B, cmap.new_idxb, None)
+    lay = out.layout
+    dout = nat.OcpQpDataC()
+    keep = []
+    for i, name in enumerate(FIELD_ORDER):
+        L = lay.field_len[name]
+        buf = torch.zeros((batch.B, max(1, L)), dtype=torch.float64, device=device)
+        keep.append(buf)
+        dout.ptr[i] = buf.data_ptr()
+        dout.batch_stride[i] = max(1, L)
+        if L:
+            out.fields[name] = buf
+    din = _data_c_full(src)
+    s = torch.cuda.current_stream(device)
+    _check(_lib().ocpqp_pc_condense(cmap.handle, batch.B, ctypes.byref(din), ctypes.byref(dout),
+                                    ctypes.c_void_p(s.cuda_stream)))
+    del keep
+    return out, cmap
+
+
+def expand_batch(dense, cmap, batch, device="cuda"):
+    """Full OCP (y, pi, lam, t) device tensors from dense solutions
+    (expand_solution, condensing.py:343-429).  ``dense`` is a BatchReport of
+    the condensed batch or a (y, pi, lam, t) tuple."""
+    import torch
+
+    from .solver import _as_batch
+
+    batch = _as_batch(batch, check=False)
+    src = _device_full(batch, device)
+    parts = (dense.y, dense.pi, dense.lam, dense.t) if hasattr(dense, "lam") else tuple(dense)
+    f64 = dict(dtype=torch.float64, device=device)
+
+    def dev(a):
+        a = torch.as_tensor(a, **f64)
+        if a.numel() == 0:  # pi of the N = 0 form is empty
+            return torch.zeros((batch.B, 1), **f64)
+        return a.reshape(batch.B, -1).contiguous()
+
+    sy, spi, slam, st = (dev(a) for a in parts)
+    if sy.shape[1] < cmap.nv:
+        raise DimensionMismatch("dense solution does not match the map")
+    lay = batch.layout
+    y = torch.zeros((batch.B, lay.ny), **f64)
+    pi = torch.zeros((batch.B, max(1, lay.ne)), **f64)
+    lam = torch.zeros((batch.B, max(1, lay.nc)), **f64)
+    t = torch.zeros((batch.B, max(1, lay.nc)), **f64)
+    din = _data_c_full(src)
+    s_it = nat.OcpIterC(sy.data_ptr(), spi.data_ptr(), slam.data_ptr(), st.data_ptr())
+    f_it = nat.OcpIterC(y.data_ptr(), pi.data_ptr(), lam.data_ptr(), t.data_ptr())
+    s = torch.cuda.current_stream(device)
+    _check(_lib().ocpqp_pc_expand(cmap.handle, batch.B, ctypes.byref(din), ctypes.byref(s_it),
+                                  ctypes.byref(f_it), ctypes.c_void_p(s.cuda_stream)))
+    return y, pi[:, : lay.ne], lam[:, : lay.nc], t[:, : lay.nc]
+
+
+def condense(qp, keep_x0=None, variant="classical"):
+    """Single-QP drop-in: ``(DenseQp, CondensingMap)`` (condensing.py:160)."""
+    from .dense import ocp_to_dense
+
+    if not isinstance(qp, OcpQp):
+        raise TypeError("condense expects an OcpQp")
+    if variant != "classical":
+        raise NotImplementedError("only the classical cost recursion is provided")
+    b = OcpQpBatch.from_qps([qp])
+    cb, cmap = condense_batch(b, keep_x0)
+    return ocp_to_dense(cb.numpy().qp(0)), cmap
+
+
+def expand_solution(dense_sol, cmap, qp, pi_terminal=None):
+    """Single-QP drop-in: full OCP QpSolution (condensing.py:343)."""
+    if pi_terminal is not None:
+        raise NotImplementedError("pi_terminal seeding is used by partial condensing only")
+    if dense_sol.v.shape[0] != cmap.nv:
+        raise DimensionMismatch("dense solution does not match the map")
+    b = OcpQpBatch.from_qps([qp])
+    y, pi, lam, t = expand_batch(
+        tuple(np.asarray(a)[None] for a in (dense_sol.y, dense_sol.pi, dense_sol.lam, dense_sol.t)),
+        cmap, b)
     return QpSolution(b.layout, y[0].cpu().numpy(), pi[0].cpu().numpy(), lam[0].cpu().numpy(),
                       t[0].cpu().numpy())

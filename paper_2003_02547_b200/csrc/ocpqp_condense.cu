@@ -1,6 +1,9 @@
-// Batched partial condensing and expansion (reference condensing.py:451-619,
-// with condense(keep_x0=True) :160-340, _cost_recursion :128-157 and
-// expand_solution :343-429).
+// Batched partial and full condensing and expansion (reference
+// condensing.py:451-619, condense :160-340, _cost_recursion :128-157 and
+// expand_solution :343-429).  Full condensing is the one-block case over the
+// whole horizon, terminal stage included, whose dense QP is emitted as a
+// single-stage OCP-QP (N = 0, nx = 0, nu = nv) -- the form the IPM kernels
+// solve identically to the reference's dense-QP backend when ne = 0.
 //
 // Host side (C++): the block structure and every row routing table are
 // computed once per (dims, idxb, N1) -- they are identical for all QPs of a
@@ -99,12 +102,16 @@ struct Dims {
 // ---------------------------------------------------------------------------
 struct PcBlockDev {
     int n0, L, nx0, nv, nb_new, ng_new;   // block geometry; new stage k = block index
+    int zx;        // x0 columns of z (nx0, or 0 when full condensing drops a fixed x0)
+    int ox;        // leading z columns emitted as the new stage's x part (nx0; 0 for full)
     int row0;      // first entry of this block in the row tables
     int uoff0;     // first entry in the per-block-stage u offset table
 };
 
 struct PcParams {
     int B, nblk, N, N2;
+    int full;               // full condensing: one block 0..N including the terminal stage
+    int nfix; const int* fix_row; const int* fix_c;   // dropped stage-0 fixing rows (full, x0 dropped)
     int nxmax, nvmax, numax, Lmax;
     const PcBlockDev* blk;
     const int* uoff;        // z offset of u for each block stage (-1 when nu = 0)
@@ -149,8 +156,8 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
     const int XM = p.nxmax, VM = p.nvmax, UM = p.numax;
     // workspace carve-up
     double* P = ws;                                 // (L+1) * XM*XM
-    double* Y = P + (long long)(p.Lmax + 1) * XM * XM;   // L * XM*UM
-    double* gam = Y + (long long)p.Lmax * XM * UM;     // (L+1) * XM
+    double* Y = P + (long long)(p.Lmax + 1) * XM * XM;   // (L+1) * XM*UM
+    double* gam = Y + (long long)(p.Lmax + 1) * XM * UM;     // (L+1) * XM
     double* bet = gam + (long long)(p.Lmax + 1) * XM;  // (L+1) * XM
     double* Hc = bet + (long long)(p.Lmax + 1) * XM;   // VM * VM
     double* gc = Hc + (long long)VM * VM;              // VM
@@ -159,7 +166,11 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
     double* T1 = pr1 + (long long)XM * VM;             // XM * max(XM, UM)
     double* T2 = T1 + (long long)XM * (XM > UM ? XM : UM);  // XM * UM
     // gamma forward: gamma[0] = 0, gamma[i+1] = A gamma[i] + b  (condensing.py:199-207)
+    // (full condensing without x0: gamma[0] = x0hat from the fixing rows, :97-118, :197)
     for (int a = tid; a < nx0; a += T) gam[a] = 0.0;
+    __syncthreads();
+    if (tid == 0 && p.full && bk.zx == 0)
+        for (int j = 0; j < p.nfix; ++j) gam[p.fix_c[j]] = fin(p, q, OCPQP_F_lb, 0)[p.fix_row[j]];
     __syncthreads();
     for (int i = 0; i < L; ++i) {
         const int n = n0 + i, nx = p.onx[n], nxn = p.onx[n + 1];
@@ -175,12 +186,52 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
     // zero Hc, gc
     for (int e = tid; e < nv * nv; e += T) Hc[e] = 0.0;
     for (int e = tid; e < nv; e += T) gc[e] = 0.0;
+    __syncthreads();
     // backward cost recursion (condensing.py:148-157) with P[L] = 0, beta[L] = 0 (the
-    // sub-QP's zero-cost terminal placeholder, condensing.py:432-448, 211)
+    // sub-QP's zero-cost terminal placeholder, condensing.py:432-448, 211); full
+    // condensing starts from the real terminal stage: P[N] = sym(Q_N),
+    // beta[N] = q_N + Q_N gamma_N, and its inputs (if any) enter with R_N, S_N'
+    // (condensing.py:151, 209, 238-241)
     {
         const int nxL = p.onx[n0 + L];
-        for (int e = tid; e < nxL * nxL; e += T) P[(long long)L * XM * XM + e] = 0.0;
-        for (int a = tid; a < nxL; a += T) bet[L * XM + a] = 0.0;
+        double* PL = P + (long long)L * XM * XM;
+        if (p.full) {
+            const int nuL = p.onu[n0 + L];
+            const double* Q = fin(p, q, OCPQP_F_Q, n0 + L);
+            const double* S = fin(p, q, OCPQP_F_S, n0 + L);
+            const double* R = fin(p, q, OCPQP_F_R, n0 + L);
+            const double* qv = fin(p, q, OCPQP_F_q, n0 + L);
+            const double* rv = fin(p, q, OCPQP_F_r, n0 + L);
+            for (int e = tid; e < nxL * nxL; e += T) {
+                const int a = e / nxL, c = e - a * nxL;
+                PL[e] = 0.5 * (Q[e] + Q[c * nxL + a]);
+            }
+            for (int a = tid; a < nxL; a += T) {
+                double qg = 0.0;
+                for (int c = 0; c < nxL; ++c) qg = fma(Q[a * nxL + c], gam[L * XM + c], qg);
+                bet[L * XM + a] = qv[a] + qg;
+            }
+            const int ou = uoff[L];
+            if (nuL && ou >= 0) {
+                double* YL = Y + (long long)L * XM * UM;
+                for (int e = tid; e < nxL * nuL; e += T) {
+                    const int a = e / nuL, c = e - a * nuL;
+                    YL[e] = S[c * nxL + a];
+                }
+                for (int e = tid; e < nuL * nuL; e += T) {
+                    const int a = e / nuL, c = e - a * nuL;
+                    Hc[(ou + a) * nv + ou + c] = R[e];
+                }
+                for (int a = tid; a < nuL; a += T) {
+                    double sg = 0.0;
+                    for (int c = 0; c < nxL; ++c) sg = fma(S[a * nxL + c], gam[L * XM + c], sg);
+                    gc[ou + a] = rv[a] + sg;
+                }
+            }
+        } else {
+            for (int e = tid; e < nxL * nxL; e += T) PL[e] = 0.0;
+            for (int a = tid; a < nxL; a += T) bet[L * XM + a] = 0.0;
+        }
     }
     __syncthreads();
     for (int i = L - 1; i >= 0; --i) {
@@ -260,24 +311,25 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
         }
         __syncthreads();
     }
-    // x0 block and gradient (condensing.py:220-222)
-    for (int e = tid; e < nx0 * nx0; e += T) {
-        const int a = e / nx0, c = e - a * nx0;
+    // x0 block and gradient (condensing.py:220-222), when x0 is a variable
+    const int zx = bk.zx, ox = bk.ox;
+    for (int e = tid; e < zx * zx; e += T) {
+        const int a = e / zx, c = e - a * zx;
         Hc[a * nv + c] = P[e];
     }
-    for (int a = tid; a < nx0; a += T) gc[a] = bet[a];
+    for (int a = tid; a < zx; a += T) gc[a] = bet[a];
     __syncthreads();
     // forward pass over the prediction operators (condensing.py:196-207, 242-245)
     double* pr = pr0;
     double* prn = pr1;
     for (int e = tid; e < nx0 * nv; e += T) {
         const int a = e / nv, c = e - a * nv;
-        pr[e] = (c == a) ? 1.0 : 0.0;
+        pr[e] = (c == a && c < zx) ? 1.0 : 0.0;
     }
     __syncthreads();
     for (int i = 0; i <= L; ++i) {
         const int n = n0 + i, nx = p.onx[n];
-        if (i < L) {
+        if (i < L || p.full) {
             const int nu = p.onu[n], ou = uoff[i];
             if (nu && ou >= 0) {
                 // cols = pred_i' Y_i (nv x nu); Hc[:, u_i] += cols; Hc[u_i, :] += cols'
@@ -307,13 +359,13 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
             if (p.row_stage[ridx] != i) continue;
             const int kind = p.row_kind[ridx];
             const int g = r - bk.nb_new;
-            double* Cz = fout(p, q, OCPQP_F_C, k) + (long long)g * nx0;
-            double* Dz = fout(p, q, OCPQP_F_D, k) + (long long)g * (nv - nx0);
+            double* Cz = fout(p, q, OCPQP_F_C, k) + (long long)g * ox;
+            double* Dz = fout(p, q, OCPQP_F_D, k) + (long long)g * (nv - ox);
             if (kind == 2) {
                 const int cc = p.row_aux[ridx];
                 for (int e = tid; e < nv; e += T) {
                     const double v = pr[cc * nv + e];
-                    if (e < nx0) Cz[e] = v; else Dz[e - nx0] = v;
+                    if (e < ox) Cz[e] = v; else Dz[e - ox] = v;
                 }
                 if (tid == 0) {
                     const int src = p.row_src[ridx];
@@ -332,7 +384,7 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
                     double base = 0.0;
                     if (nu && ou >= 0 && e >= ou && e < ou + nu) base = Dg[e - ou];
                     const double v = base + s;
-                    if (e < nx0) Cz[e] = v; else Dz[e - nx0] = v;
+                    if (e < ox) Cz[e] = v; else Dz[e - ox] = v;
                 }
                 if (tid == 0) {
                     double sh = 0.0;
@@ -361,7 +413,7 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
         }
     }
     // new stage dynamics: A = pred_L[:, :nx0], B = pred_L[:, nx0:], b = gamma_L
-    {
+    if (!p.full) {
         const int nxn = p.onx[n0 + L], nun = nv - nx0;
         double* Ao = fout(p, q, OCPQP_F_A, k);
         double* Bo = fout(p, q, OCPQP_F_B, k);
@@ -375,7 +427,7 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
     __syncthreads();
     // Hc = 0.5 (Hc + Hc') and the new stage cost blocks (condensing.py:246, 504-509)
     {
-        const int nun = nv - nx0;
+        const int nun = nv - ox;
         double* Qo = fout(p, q, OCPQP_F_Q, k);
         double* So = fout(p, q, OCPQP_F_S, k);
         double* Ro = fout(p, q, OCPQP_F_R, k);
@@ -384,12 +436,12 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
         for (int e = tid; e < nv * nv; e += T) {
             const int a = e / nv, c = e - a * nv;
             const double v = 0.5 * (Hc[e] + Hc[c * nv + a]);
-            if (a < nx0 && c < nx0) Qo[a * nx0 + c] = v;
-            else if (a >= nx0 && c < nx0) So[(a - nx0) * nx0 + c] = v;
-            else if (a >= nx0 && c >= nx0) Ro[(a - nx0) * nun + (c - nx0)] = v;
+            if (a < ox && c < ox) Qo[a * ox + c] = v;
+            else if (a >= ox && c < ox) So[(a - ox) * ox + c] = v;
+            else if (a >= ox && c >= ox) Ro[(a - ox) * nun + (c - ox)] = v;
         }
         for (int a = tid; a < nv; a += T) {
-            if (a < nx0) qo[a] = gc[a]; else ro[a - nx0] = gc[a];
+            if (a < ox) qo[a] = gc[a]; else ro[a - ox] = gc[a];
         }
     }
     // box rows of the new stage (bounds unshifted) and masks of every row
@@ -436,14 +488,15 @@ __device__ void copy_terminal(const PcParams& p, int q) {
 __global__ void __launch_bounds__(256) k_pc_condense(PcParams p) {
     __shared__ int s_item;
     double* ws = p.ws + (long long)blockIdx.x * p.ws_slot;
-    const int items = p.B * (p.nblk + 1);
+    const int per = p.nblk + (p.full ? 0 : 1);
+    const int items = p.B * per;
     while (true) {
         if (threadIdx.x == 0) s_item = atomicAdd(p.counter, 1);
         __syncthreads();
         const int it = s_item;
         __syncthreads();
         if (it >= items) break;
-        const int q = it / (p.nblk + 1), k = it - q * (p.nblk + 1);
+        const int q = it / per, k = it - q * per;
         if (k < p.nblk) condense_block(p, q, k, ws);
         else copy_terminal(p, q);
         __syncthreads();
@@ -471,15 +524,25 @@ __device__ void expand_block(const PcParams& p, int q, int k, double* ws) {
     double* xs = ws;                           // (L+1) * XM
     double* ctx = xs + (long long)(p.Lmax + 1) * p.nxmax;   // XM
     double* pis = ctx + p.nxmax;               // XM
+    double* gap = pis + p.nxmax;               // XM
     const int XM = p.nxmax;
-    // forward rollout (condensing.py:359-367)
-    for (int a = tid; a < nx0; a += T) xs[a] = xk[a];
+    const int ox = bk.ox;
+    // forward rollout (condensing.py:359-367); full condensing: x0 from z or x0hat
+    if (!p.full) {
+        for (int a = tid; a < nx0; a += T) xs[a] = xk[a];
+    } else if (bk.zx) {
+        for (int a = tid; a < nx0; a += T) xs[a] = uk[a];
+    } else if (tid == 0) {
+        for (int j = 0; j < p.nfix; ++j) xs[p.fix_c[j]] = fin(p, q, OCPQP_F_lb, 0)[p.fix_row[j]];
+    }
     __syncthreads();
-    for (int i = 0; i < L; ++i) {
-        const int n = n0 + i, nx = p.onx[n], nu = p.onu[n], nxn = p.onx[n + 1];
+    for (int i = 0; i < L + (p.full ? 1 : 0); ++i) {
+        const int n = n0 + i, nx = p.onx[n], nu = p.onu[n];
         const int ou = uoff[i];
-        for (int a = tid; a < nu; a += T) fy[p.o_u[n] + a] = (ou >= 0) ? uk[ou - nx0 + a] : 0.0;
+        for (int a = tid; a < nu; a += T) fy[p.o_u[n] + a] = (ou >= 0) ? uk[ou - ox + a] : 0.0;
         for (int a = tid; a < nx; a += T) fy[p.o_x[n] + a] = xs[i * XM + a];
+        if (i == L) break;
+        const int nxn = p.onx[n + 1];
         const double* A = fin(p, q, OCPQP_F_A, n);
         const double* Bm = fin(p, q, OCPQP_F_B, n);
         const double* b = fin(p, q, OCPQP_F_b, n);
@@ -487,7 +550,7 @@ __device__ void expand_block(const PcParams& p, int q, int k, double* ws) {
             double ax = 0.0, bu = 0.0;
             for (int c = 0; c < nx; ++c) ax = fma(A[a * nx + c], xs[i * XM + c], ax);
             if (ou >= 0)
-                for (int c = 0; c < nu; ++c) bu = fma(Bm[a * nu + c], uk[ou - nx0 + c], bu);
+                for (int c = 0; c < nu; ++c) bu = fma(Bm[a * nu + c], uk[ou - ox + c], bu);
             xs[(i + 1) * XM + a] = (ax + bu) + b[a];
         }
         __syncthreads();
@@ -506,13 +569,19 @@ __device__ void expand_block(const PcParams& p, int q, int k, double* ws) {
         ft[cf + mo + src] = sts[cs + mn + r];
     }
     __syncthreads();
-    // costate recursion (condensing.py:397-412) seeded with the short-horizon pi_k
-    for (int a = tid; a < p.onx[n0 + L]; a += T) pis[a] = spi[p.n_pi[k] + a];
-    __syncthreads();
-    if (L >= 1)
-        for (int a = tid; a < p.onx[n0 + L]; a += T) fpi[p.o_pi[n0 + L - 1] + a] = pis[a];
-    for (int m = L - 1; m >= 1; --m) {
-        const int n = n0 + m, nx = p.onx[n], nu = p.onu[n], nxn = p.onx[n + 1];
+    // costate recursion (condensing.py:397-412) seeded with the short-horizon pi_k;
+    // full condensing runs it from the terminal stage (no seed) down to the
+    // stage-0 stationarity gap of the dropped fixing rows (:414-428)
+    if (!p.full) {
+        for (int a = tid; a < p.onx[n0 + L]; a += T) pis[a] = spi[p.n_pi[k] + a];
+        __syncthreads();
+        if (L >= 1)
+            for (int a = tid; a < p.onx[n0 + L]; a += T) fpi[p.o_pi[n0 + L - 1] + a] = pis[a];
+    }
+    const bool want_gap = p.full && bk.zx == 0 && p.nfix > 0;
+    for (int m = p.full ? L : L - 1; m >= (want_gap ? 0 : 1); --m) {
+        const int n = n0 + m, nx = p.onx[n], nu = p.onu[n];
+        const int nxn = (p.full && m == L) ? 0 : p.onx[n + 1];
         const int nb = p.onb[n], ng = p.ong[n], mo = nb + ng;
         const int cf = p.o_c[n];
         // (C' lam)_x of stage n over the masked multipliers (view.py:145-153, 197-205)
@@ -548,11 +617,22 @@ __device__ void expand_block(const PcParams& p, int q, int k, double* ws) {
             for (int c = 0; c < nx; ++c) qx = fma(Q[a * nx + c], xs[m * XM + c], qx);
             for (int c = 0; c < nu; ++c) su = fma(S[c * nx + a], um[c], su);
             for (int c = 0; c < nxn; ++c) ap = fma(A[c * nx + a], pis[c], ap);
-            fpi[p.o_pi[n - 1] + a] = (((qx + su) + qv[a]) - ctx[a]) + ap;
+            const double v = (((qx + su) + qv[a]) - ctx[a]) + ap;
+            if (m >= 1) fpi[p.o_pi[n - 1] + a] = v; else gap[a] = v;
         }
         __syncthreads();
-        for (int a = tid; a < nx; a += T) pis[a] = fpi[p.o_pi[n - 1] + a];
+        if (m >= 1)
+            for (int a = tid; a < nx; a += T) pis[a] = fpi[p.o_pi[n - 1] + a];
         __syncthreads();
+    }
+    if (want_gap && tid == 0) {
+        // net multiplier of each dropped fixing row, split by sign (condensing.py:414-428)
+        const int mo = p.onb[0] + p.ong[0], cf = p.o_c[0];
+        for (int j = 0; j < p.nfix; ++j) {
+            const double g = gap[p.fix_c[j]];
+            if (g >= 0.0) flam[cf + p.fix_row[j]] = g;
+            else flam[cf + mo + p.fix_row[j]] = -g;
+        }
     }
 }
 
@@ -607,6 +687,10 @@ __global__ void __launch_bounds__(256) k_pc_expand_terminal(PcParams p) {
 struct OcpPcPlan {
     Dims od, nd;
     int N1 = 1, nblk = 0;
+    int full = 0;
+    std::vector<int> fix_row, fix_c;
+    int* d_fix_row = nullptr;
+    int* d_fix_c = nullptr;
     std::vector<PcBlockDev> blk;
     std::vector<int> uoff, row_kind, row_stage, row_src, row_aux;
     int nxmax = 1, nvmax = 1, numax = 1, Lmax = 1;
@@ -636,6 +720,16 @@ int upload(T** dst, const std::vector<T>& v) {
     return 0;
 }
 
+// workspace per CTA slot; T1 scratch doubles as the (nv x nu) cross-term buffer
+void pc_size(OcpPcPlan* P) {
+    const long long UM = P->numax, VM = P->nvmax;
+    long long XM = P->nxmax;
+    while (XM * std::max(XM, UM) < VM * UM) ++XM;
+    P->nxmax = (int)XM;
+    P->ws_slot = (P->Lmax + 1) * XM * XM + (long long)(P->Lmax + 1) * XM * UM + 2ll * (P->Lmax + 1) * XM +
+                 VM * VM + VM + 2ll * XM * VM + XM * std::max(XM, UM) + XM * UM + 64;
+}
+
 int pc_prepare(OcpPcPlan* P, int items) {
     if (!P->uploaded) {
         int rc = 0;
@@ -661,6 +755,8 @@ int pc_prepare(OcpPcPlan* P, int items) {
         rc |= upload(&P->d_oidxb, P->od.idxb);
         rc |= upload(&P->d_ofoff, P->od.foff);
         rc |= upload(&P->d_nfoff, P->nd.foff);
+        rc |= upload(&P->d_fix_row, P->fix_row);
+        rc |= upload(&P->d_fix_c, P->fix_c);
         if (cudaMalloc(&P->d_counter, sizeof(int)) != cudaSuccess) rc = -1;
         if (rc) return pc_fail(OCPQP_E_CUDA, "partial condensing: table upload failed");
         P->uploaded = true;
@@ -682,6 +778,8 @@ int pc_prepare(OcpPcPlan* P, int items) {
 void pc_fill(const OcpPcPlan* P, PcParams& k, int B) {
     memset(&k, 0, sizeof(k));
     k.B = B; k.nblk = P->nblk; k.N = P->od.N; k.N2 = P->nd.N;
+    k.full = P->full; k.nfix = (int)P->fix_row.size();
+    k.fix_row = P->d_fix_row; k.fix_c = P->d_fix_c;
     k.nxmax = P->nxmax; k.nvmax = P->nvmax; k.numax = P->numax; k.Lmax = P->Lmax;
     k.blk = P->d_blk; k.uoff = P->d_uoff;
     k.row_kind = P->d_kind; k.row_stage = P->d_stage; k.row_src = P->d_src; k.row_aux = P->d_aux;
@@ -735,6 +833,7 @@ int ocpqp_pc_create(const OcpQpDimC* dim, int32_t N1, OcpPcPlan** out) {
         const int n0 = starts[k], n1 = std::min(n0 + N1, od.N), L = n1 - n0;
         PcBlockDev b{};
         b.n0 = n0; b.L = L; b.nx0 = od.nx[n0];
+        b.zx = b.ox = b.nx0;
         b.uoff0 = (int)P->uoff.size();
         int off = b.nx0;
         for (int i = 0; i < L; ++i) {
@@ -803,13 +902,118 @@ int ocpqp_pc_create(const OcpQpDimC* dim, int32_t N1, OcpPcPlan** out) {
     nd.ng.push_back(od.ng[od.N]); nd.ns.push_back(0);
     for (int r = 0; r < od.nb[od.N]; ++r) nd.idxb.push_back(od.idxb[od.ib_off[od.N] + r]);
     nd.finish();
-    // T1 scratch doubles as the (nv x nu) cross-term buffer
-    const long long UM = P->numax, VM = P->nvmax;
-    long long XM = P->nxmax;
-    while (XM * std::max(XM, UM) < VM * UM) ++XM;
-    P->nxmax = (int)XM;
-    P->ws_slot = (P->Lmax + 1) * XM * XM + (long long)P->Lmax * XM * UM + 2ll * (P->Lmax + 1) * XM +
-                 VM * VM + VM + 2ll * XM * VM + XM * std::max(XM, UM) + XM * UM + 64;
+    pc_size(P);
+    *out = P;
+    return OCPQP_OK;
+}
+
+// Full condensing, condense(qp, keep_x0) (condensing.py:160-340): one block over
+// stages 0..N, terminal included.  With keep_x0 = 0 the stage-0 x rows are
+// dropped and x0hat is read from the fixing rows (fix_row[j] fixes component
+// fix_comp[j]; the caller detects them from the data, condensing.py:97-118).
+// The dense QP comes out as a single-stage OCP-QP: nx = 0, nu = nv, box rows
+// keyed and sorted by z, general rows in stage order.
+int ocpqp_fc_create(const OcpQpDimC* dim, int32_t keep_x0, int32_t nfix, const int32_t* fix_row,
+                    const int32_t* fix_comp, OcpPcPlan** out) {
+    if (!dim || !out || (nfix > 0 && (!fix_row || !fix_comp))) return pc_fail(OCPQP_E_ARG, "NULL argument");
+    *out = nullptr;
+    if (dim->N < 0) return pc_fail(OCPQP_E_INVALID_DIM, "negative horizon");
+    OcpPcPlan* P = new OcpPcPlan();
+    P->full = 1;
+    Dims& od = P->od;
+    od.N = dim->N;
+    const int N = od.N, S = N + 1;
+    od.nx.assign(dim->nx, dim->nx + S); od.nu.assign(dim->nu, dim->nu + S);
+    od.nb.assign(dim->nb, dim->nb + S); od.ng.assign(dim->ng, dim->ng + S);
+    od.ns.assign(dim->ns, dim->ns + S);
+    long long snb = 0;
+    for (int n = 0; n < S; ++n) {
+        snb += od.nb[n];
+        if (od.ns[n]) {
+            delete P;
+            return pc_fail(OCPQP_E_UNSUPPORTED, "soft rows are not supported by the batched condensing");
+        }
+    }
+    od.idxb.assign(dim->idxb, dim->idxb + snb);
+    od.finish();
+    const int nx0 = od.nx[0];
+    if (!keep_x0) {
+        std::vector<int> seen(nx0, 0);
+        for (int j = 0; j < nfix; ++j) {
+            if (fix_comp[j] < 0 || fix_comp[j] >= nx0 || fix_row[j] < 0 || fix_row[j] >= od.nb[0]) {
+                delete P;
+                return pc_fail(OCPQP_E_ARG, "fixing row %d out of range", j);
+            }
+            seen[fix_comp[j]] = 1;
+            P->fix_row.push_back(fix_row[j]);
+            P->fix_c.push_back(fix_comp[j]);
+        }
+        for (int c = 0; c < nx0; ++c)
+            if (!seen[c]) {
+                delete P;
+                return pc_fail(OCPQP_E_CONDENSE, "keep_x0=False requires every initial-state component "
+                                                  "fixed by active equal-bound box rows");
+            }
+    }
+    P->nblk = 1;
+    PcBlockDev b{};
+    b.n0 = 0; b.L = N; b.nx0 = nx0;
+    b.zx = keep_x0 ? nx0 : 0;
+    b.ox = 0;
+    b.uoff0 = 0;
+    int off = b.zx;
+    for (int n = 0; n <= N; ++n) {
+        const int nu = od.nu[n];
+        P->uoff.push_back(nu ? off : -1);
+        off += nu;
+        P->nxmax = std::max(P->nxmax, od.nx[n]);
+        P->numax = std::max(P->numax, nu);
+    }
+    b.nv = off;
+    P->nvmax = std::max(1, b.nv);
+    P->Lmax = std::max(1, N);
+    // routing (condensing.py:251-297): u-box rows and kept-x0 rows are dense box
+    // rows keyed by z; x-box rows past stage 0 and all general rows become dense
+    // general rows in stage order; stage-0 x rows are dropped with x0
+    struct Box { int z, i, r, kind; };
+    struct Gen { int kind, i, r, aux; };
+    std::vector<Box> box;
+    std::vector<Gen> gen;
+    for (int n = 0; n <= N; ++n) {
+        const int nu = od.nu[n];
+        for (int r = 0; r < od.nb[n]; ++r) {
+            const int kk = od.idxb[od.ib_off[n] + r];
+            if (kk < nu) box.push_back({P->uoff[n] + kk, n, r, 0});
+            else if (n == 0 && keep_x0) box.push_back({kk - nu, n, r, 1});
+            else if (n == 0) continue;
+            else gen.push_back({2, n, r, kk - nu});
+        }
+        for (int g = 0; g < od.ng[n]; ++g) gen.push_back({3, n, od.nb[n] + g, g});
+    }
+    std::stable_sort(box.begin(), box.end(), [](const Box& a, const Box& c) { return a.z < c.z; });
+    Dims& nd = P->nd;
+    nd.N = 0;
+    b.row0 = 0;
+    b.nb_new = (int)box.size();
+    b.ng_new = (int)gen.size();
+    for (auto& e : box) {
+        P->row_kind.push_back(e.kind);
+        P->row_stage.push_back(e.i);
+        P->row_src.push_back(e.r);
+        P->row_aux.push_back(e.z);
+        nd.idxb.push_back(e.z);
+    }
+    for (auto& g : gen) {
+        P->row_kind.push_back(g.kind);
+        P->row_stage.push_back(g.i);
+        P->row_src.push_back(g.r);
+        P->row_aux.push_back(g.aux);
+    }
+    P->blk.push_back(b);
+    nd.nx.push_back(0); nd.nu.push_back(b.nv); nd.nb.push_back(b.nb_new);
+    nd.ng.push_back(b.ng_new); nd.ns.push_back(0);
+    nd.finish();
+    pc_size(P);
     *out = P;
     return OCPQP_OK;
 }
@@ -822,6 +1026,7 @@ int ocpqp_pc_destroy(OcpPcPlan* P) {
     cudaFree(P->d_opi); cudaFree(P->d_oc); cudaFree(P->d_nu); cudaFree(P->d_nx);
     cudaFree(P->d_npi); cudaFree(P->d_nc); cudaFree(P->d_oib); cudaFree(P->d_oidxb);
     cudaFree(P->d_ofoff); cudaFree(P->d_nfoff); cudaFree(P->d_counter); cudaFree(P->d_ws);
+    cudaFree(P->d_fix_row); cudaFree(P->d_fix_c);
     delete P;
     return OCPQP_OK;
 }
@@ -848,7 +1053,7 @@ int ocpqp_pc_dims(const OcpPcPlan* P, int32_t* nx, int32_t* nu, int32_t* nb, int
 int ocpqp_pc_condense(OcpPcPlan* P, int32_t B, const OcpQpDataC* in, OcpQpDataC* out, void* stream) {
     if (!P || !in || !out) return pc_fail(OCPQP_E_ARG, "NULL argument");
     if (B <= 0) return OCPQP_OK;
-    const int items = B * (P->nblk + 1);
+    const int items = B * (P->nblk + (P->full ? 0 : 1));
     int rc = pc_prepare(P, items);
     if (rc) return rc;
     PcParams k;
@@ -885,8 +1090,14 @@ int ocpqp_pc_expand(OcpPcPlan* P, int32_t B, const OcpQpDataC* in, const OcpIter
         return pc_fail(OCPQP_E_CUDA, "memset");
     if (cudaMemsetAsync(full_sol->pi, 0, sizeof(double) * (size_t)B * P->od.ne, st) != cudaSuccess)
         return pc_fail(OCPQP_E_CUDA, "memset");
+    if (P->full) {
+        // dropped fixing rows are not routed: their lam / t start from zero
+        if (cudaMemsetAsync(full_sol->lam, 0, sizeof(double) * (size_t)B * P->od.nc, st) != cudaSuccess ||
+            cudaMemsetAsync(full_sol->t, 0, sizeof(double) * (size_t)B * P->od.nc, st) != cudaSuccess)
+            return pc_fail(OCPQP_E_CUDA, "memset");
+    }
     k_pc_expand<<<std::min(P->slots, items), 256, 0, st>>>(k);
-    k_pc_expand_terminal<<<std::min(B, 1024), 256, 0, st>>>(k);
+    if (!P->full) k_pc_expand_terminal<<<std::min(B, 1024), 256, 0, st>>>(k);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return pc_fail(OCPQP_E_CUDA, "k_pc_expand: %s", cudaGetErrorString(e));
     return OCPQP_OK;

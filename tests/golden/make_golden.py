@@ -244,6 +244,41 @@ def pcond():
     np.savez_compressed(HERE / "pcond.npz", **out)
 
 
+# full condensing (condensing.py:160-429) + the dense-QP IPM (solver.py:98-100)
+FCOND_CASES = [
+    ("f21", (21, dict(N=8, nx=3, nu=2, nb=4, ng=1, ns=0, fix_x0=True)), None),
+    ("f23", (23, dict(N=6, nx=3, nu=2, nb=5, ng=2, ns=0, fix_x0=True)), None),
+    ("f25", (25, dict(N=5, nx=3, nu=2, nb=3, ng=1, ns=0, fix_x0=False)), None),
+    ("f26", (26, dict(N=4, nx=4, nu=1, nb=4, ng=0, ns=0, fix_x0=False, mask_last=False)), None),
+    ("f27", (27, dict(N=6, nx=3, nu=2, nb=5, ng=1, ns=0, fix_x0=True)), True),
+    ("c1", ("cfg", 1, None), None),
+    ("c2", ("cfg", 2, 10), None),
+]
+FCOND_FIELDS = ("H", "g", "idxb", "lb", "ub", "C", "lg", "ug", "maskl", "masku")
+
+
+def fcond():
+    out = {}
+    for name, src, keep in FCOND_CASES:
+        qp = pcond_source(src)
+        dq, cmap = mpcqp.condense(qp, keep_x0=keep)
+        out[f"{name}_dims"] = np.array([dq.nv, dq.ne, dq.nb, dq.ng, dq.ns, int(cmap.keep_x0)])
+        for f in FCOND_FIELDS:
+            out[f"{name}_{f}"] = dq.get_field(f)
+        rep = mpcqp.solve_dense_qp(dq, ARG)
+        for k, v in pack_report(rep).items():
+            out[f"{name}_dense_{k}"] = v
+        full = mpcqp.expand_solution(rep.solution, cmap, qp)
+        for k in ("y", "pi", "lam", "t"):
+            out[f"{name}_full_{k}"] = getattr(full, k)
+        direct = mpcqp.solve_ocp_qp(qp, ARG)
+        out[f"{name}_direct_iters"] = direct.iterations
+        out[f"{name}_direct_y"] = direct.solution.y
+        print("fcond", name, dq.nv, dq.ng, cmap.keep_x0, rep.status.value, rep.iterations,
+              direct.iterations, flush=True)
+    np.savez_compressed(HERE / "fcond.npz", **out)
+
+
 # modes beyond speed (ipm_core.py:131-168): (name, preset, tol, overrides)
 MODES = [
     ("balance6", "balance", 1e-6, {}),
@@ -356,7 +391,8 @@ def qp_files():
     subprocess.run([py, "-m", "mpcqp.cli", "gen-mass-spring", "--masses", "3", "--horizon", "6",
                     "--out", str(d / "mass3.qp")], check=True, env=env, cwd=str(d))
     for name, extra in (("mass3_balance", []), ("mass3_speed", ["--mode", "speed", "--tol", "1e-8"]),
-                        ("mass3_partial", ["--path", "partial:2"])):
+                        ("mass3_partial", ["--path", "partial:2"]),
+                        ("mass3_condense", ["--path", "condense"])):
         r = subprocess.run([py, "-m", "mpcqp.cli", "solve", "--qp", "mass3.qp", *extra],
                            env=env, cwd=str(d), capture_output=True, text=True)
         (d / f"{name}.report").write_text(r.stdout)
@@ -365,6 +401,6 @@ def qp_files():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["known", "residuals", "newton", "solve_random", "solve_cfg", "pcond",
-                            "solve_modes", "closed_loop", "qp_files"]
+                            "solve_modes", "closed_loop", "qp_files", "fcond"]
     for w in which:
         globals()[w]()

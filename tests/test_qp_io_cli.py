@@ -107,7 +107,8 @@ def _report(text):
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,extra", [("mass3_balance", []),
                                         ("mass3_speed", ["--mode", "speed", "--tol", "1e-8"]),
-                                        ("mass3_partial", ["--path", "partial:2"])])
+                                        ("mass3_partial", ["--path", "partial:2"]),
+                                        ("mass3_condense", ["--path", "condense"])])
 def test_cli_solve_report_matches_reference(cuda, tmp_path, name, extra):
     import shutil
 
