@@ -452,6 +452,48 @@ __device__ __forceinline__ void warp_cho_solve(const double* L, int n, const dou
     if (lane < n) out[lane] = sgn * z;
 }
 
+// warp_cho_solve for 32 < n <= 128: lane owns x_{lane + 32 q}, q < 4 (dense QPs
+// after full condensing: n = nv up to a few hundred go serial beyond this).
+__device__ __forceinline__ double wsel4(int q, double a, double b, double c, double d) {
+    return q == 0 ? a : q == 1 ? b : q == 2 ? c : d;
+}
+__device__ void warp_cho_solve4(const double* L, int n, const double* xin, double* out,
+                                double sgn) {
+    const int lane = threadIdx.x & 31;
+    double z[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) z[q] = lane + 32 * q < n ? xin[lane + 32 * q] : 0.0;
+    for (int k = 0; k < n; ++k) {
+        const int kq = k >> 5, kl = k & 31;
+        const double dk = L[k * n + k];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (q == kq && lane == kl) z[q] = z[q] / dk;
+        const double zk = __shfl_sync(0xffffffffu, wsel4(kq, z[0], z[1], z[2], z[3]), kl);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = lane + 32 * q;
+            if (i > k && i < n) z[q] = fma(-L[i * n + k], zk, z[q]);
+        }
+    }
+    for (int k = n - 1; k >= 0; --k) {
+        const int kq = k >> 5, kl = k & 31;
+        const double dk = L[k * n + k];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (q == kq && lane == kl) z[q] = z[q] / dk;
+        const double zk = __shfl_sync(0xffffffffu, wsel4(kq, z[0], z[1], z[2], z[3]), kl);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = lane + 32 * q;
+            if (i < k) z[q] = fma(-L[k * n + i], zk, z[q]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (lane + 32 * q < n) out[lane + 32 * q] = sgn * z[q];
+}
+
 // ---------------------------------------------------------------------------
 // Householder QR of the m x n (m >= n) row-major stack S in place (LAPACK
 // dgeqr2 / dlarfg reflectors, the arithmetic of np.linalg.qr(mode="r")), then
@@ -1018,7 +1060,9 @@ __device__ int solve(Ctx& c, const double* lam, const double* t, const double* r
         }
         if (nu && nu <= 32 && tid >= T - 32) {
             warp_cho_solve(Lall + s.L_off, nu, win, kff + s.kff_off, -1.0);
-        } else if (nu > 32 && tid == T - 1) {
+        } else if (nu > 32 && nu <= 128 && tid >= T - 32) {
+            warp_cho_solve4(Lall + s.L_off, nu, win, kff + s.kff_off, -1.0);
+        } else if (nu > 128 && tid == T - 1) {
             const double* L = Lall + s.L_off;
             for (int i = 0; i < nu; ++i) z[i] = win[i];
             cho_solve_serial(L, nu, z);
@@ -1034,6 +1078,8 @@ __device__ int solve(Ctx& c, const double* lam, const double* t, const double* r
         const double* LP0 = (haslp && haslp[0] != 0.0) ? LPs + c.st[0].P_off : c.w[WS_LP0];
         if (nx0 <= 32) {
             if (tid < 32) warp_cho_solve(LP0, nx0, pv + c.st[0].pv_off, dy + c.st[0].x_off, -1.0);
+        } else if (nx0 <= 128) {
+            if (tid < 32) warp_cho_solve4(LP0, nx0, pv + c.st[0].pv_off, dy + c.st[0].x_off, -1.0);
         } else if (tid == 0) {
             for (int i = 0; i < nx0; ++i) z[i] = pv[c.st[0].pv_off + i];
             cho_solve_serial(LP0, nx0, z);
