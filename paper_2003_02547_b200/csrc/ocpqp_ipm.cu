@@ -459,34 +459,62 @@ __device__ __forceinline__ double wsel4(int q, double a, double b, double c, dou
 }
 __device__ void warp_cho_solve4(const double* L, int n, const double* xin, double* out,
                                 double sgn) {
+    // Each lane holds the reciprocal pivots of its rows (computed in parallel,
+    // off the chain) and column k+1 of L is loaded while step k runs: a step
+    // is one multiply, one shuffle and one FMA.
     const int lane = threadIdx.x & 31;
-    double z[4];
+    double z[4], lc[4], rd[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) z[q] = lane + 32 * q < n ? xin[lane + 32 * q] : 0.0;
+    for (int q = 0; q < 4; ++q) {
+        const int i = lane + 32 * q;
+        z[q] = i < n ? xin[i] : 0.0;
+        rd[q] = i < n ? 1.0 / L[i * n + i] : 0.0;
+        lc[q] = (i > 0 && i < n) ? L[i * n] : 0.0;
+    }
     for (int k = 0; k < n; ++k) {
         const int kq = k >> 5, kl = k & 31;
-        const double dk = L[k * n + k];
+        double ln[4];
+        const int k1 = k + 1;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = lane + 32 * q;
+            ln[q] = (i > k1 && i < n) ? L[i * n + k1] : 0.0;
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            if (q == kq && lane == kl) z[q] = z[q] / dk;
+            if (q == kq && lane == kl) z[q] = z[q] * rd[q];
         const double zk = __shfl_sync(0xffffffffu, wsel4(kq, z[0], z[1], z[2], z[3]), kl);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int i = lane + 32 * q;
-            if (i > k && i < n) z[q] = fma(-L[i * n + k], zk, z[q]);
+            if (i > k && i < n) z[q] = fma(-lc[q], zk, z[q]);
+            lc[q] = ln[q];
         }
+    }
+    // backward: row k of L (entries i < k) prefetched one step ahead
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int i = lane + 32 * q;
+        lc[q] = (i < n - 1) ? L[(n - 1) * n + i] : 0.0;
     }
     for (int k = n - 1; k >= 0; --k) {
         const int kq = k >> 5, kl = k & 31;
-        const double dk = L[k * n + k];
+        const int k1 = k - 1;
+        double ln[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = lane + 32 * q;
+            ln[q] = (i < k1) ? L[k1 * n + i] : 0.0;
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            if (q == kq && lane == kl) z[q] = z[q] / dk;
+            if (q == kq && lane == kl) z[q] = z[q] * rd[q];
         const double zk = __shfl_sync(0xffffffffu, wsel4(kq, z[0], z[1], z[2], z[3]), kl);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int i = lane + 32 * q;
-            if (i < k) z[q] = fma(-L[k * n + i], zk, z[q]);
+            if (i < k) z[q] = fma(-lc[q], zk, z[q]);
+            lc[q] = ln[q];
         }
     }
 #pragma unroll
