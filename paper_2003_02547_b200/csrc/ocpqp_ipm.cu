@@ -390,23 +390,32 @@ __device__ ResNorms residuals(Ctx& c, const double* y, const double* pi, const d
 // triangle is zeroed.  Fails (returns false) on a pivot that is not > 0,
 // including NaN, like LAPACK potrf behind linalg.cholesky_factor (linalg.py:81-118).
 __device__ bool team_chol(double* L, int n, int ld, int* flag) {
+    // Two barriers per column: every thread reads the pivot and takes the
+    // (identical) square root itself; the diagonal is written back during the
+    // trailing update, which reads only the scaled column.  The trailing
+    // update walks the lower triangle with an incremental (row, col) carry.
+    (void)flag;
     const int tid = threadIdx.x, T = blockDim.x;
     for (int k = 0; k < n; ++k) {
-        if (tid == 0) {
-            const double d = L[k * ld + k];
-            const int ok = d > 0.0;
-            if (ok) L[k * ld + k] = sqrt(d);
-            *flag = ok;
+        const double d = L[k * ld + k];
+        if (!(d > 0.0)) {
+            tsync();
+            return false;
         }
-        tsync();
-        if (!*flag) return false;
-        const double dk = L[k * ld + k];
+        const double dk = sqrt(d);
         for (int i = k + 1 + tid; i < n; i += T) L[i * ld + k] /= dk;
         tsync();
-        const int rem = n - k - 1;
-        for (int idx = tid; idx < rem * rem; idx += T) {
-            const int i = k + 1 + idx / rem, j = k + 1 + idx % rem;
-            if (j <= i) L[i * ld + j] -= L[i * ld + k] * L[j * ld + k];
+        if (tid == 0) L[k * ld + k] = dk;
+        const int rem = n - k - 1, tot = rem * (rem + 1) / 2;
+        if (tid < tot) {
+            int i = 0, j = tid;
+            while (j > i) { j -= i + 1; ++i; }
+            for (int idx = tid; idx < tot; idx += T) {
+                double* Li = L + (k + 1 + i) * ld;
+                Li[k + 1 + j] -= Li[k] * L[(k + 1 + j) * ld + k];
+                j += T;
+                while (j > i) { j -= i + 1; ++i; }
+            }
         }
         tsync();
     }
