@@ -531,6 +531,96 @@ __device__ void warp_cho_solve4(const double* L, int n, const double* xin, doubl
         if (lane + 32 * q < n) out[lane + 32 * q] = sgn * z[q];
 }
 
+// Jg' diag(coef) Jg added into the symmetric stage matrix Mb (nw x nw; the
+// SYRK of add_reduced_hessian, kkt_common.py:100-115) plus reg on the
+// diagonal.  Kept out of line: the generic kernel is register-bound.
+__device__ __noinline__ void rows_syrk(const Ctx& c, const StageInfo& s, const double* cg,
+                                       double* Mb, int nw, int ng, double reg) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    if (ng >= 32 && nw >= 24) {
+        // Jg' diag(coef) Jg on the FP64 tensor cores (DMMA m8n8k4): one warp
+        // per 8x8 tile of the lower tile triangle, k = general rows in
+        // steps of 4, mirrored in the epilogue.  Fragments: A row = lane/4,
+        // col = lane%4; B row = lane%4, col = lane/4; D row = lane/4, cols
+        // 2*(lane%4)+{0,1}.  (Dense QPs from full condensing: ng >> nw.)
+        const int lane = tid & 31, warp = tid >> 5, nwarp = T >> 5;
+        const int gr = lane >> 2, tg = lane & 3;
+        const int nt = (nw + 7) >> 3, ntile = nt * (nt + 1) / 2;
+        for (int t = warp; t < ntile; t += nwarp) {
+            int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+            while (ti * (ti + 1) / 2 > t) --ti;
+            while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+            const int tj = t - ti * (ti + 1) / 2;
+            const int ia = ti * 8 + gr, jb = tj * 8 + gr;
+            double d0 = 0.0, d1 = 0.0;
+            for (int r0 = 0; r0 < ng; r0 += 4) {
+                const int r = r0 + tg;
+                const bool rin = r < ng;
+                const double av = (rin && ia < nw) ? Jgget(c, s, r, ia) : 0.0;
+                const double bv = (rin && jb < nw) ? cg[r] * Jgget(c, s, r, jb) : 0.0;
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                             : "+d"(d0), "+d"(d1)
+                             : "d"(av), "d"(bv));
+            }
+            const int i = ti * 8 + gr;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int j = tj * 8 + 2 * tg + e;
+                if (i < nw && j <= i) {
+                    double h = (e ? d1 : d0) + Mb[i * nw + j];
+                    if (i == j && reg != 0.0) h += reg;
+                    Mb[i * nw + j] = h;
+                    Mb[j * nw + i] = h;
+                }
+            }
+        }
+    } else {
+        // Jg' diag(coef) Jg over 4x4 register blocks of the lower block
+        // triangle, mirrored (the SYRK of add_reduced_hessian): 8 loads per
+        // 16 FMAs instead of 2 per FMA -- the dominant term of dense QPs
+        // (full condensing: ng >> nw)
+        const int nbk = (nw + 3) >> 2;
+        const int nblk = nbk * (nbk + 1) / 2;
+        for (int b = tid; b < nblk; b += T) {
+            int bi = (int)((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
+            while (bi * (bi + 1) / 2 > b) --bi;
+            while ((bi + 1) * (bi + 2) / 2 <= b) ++bi;
+            const int bj = b - bi * (bi + 1) / 2;
+            const int i0 = bi * 4, j0 = bj * 4;
+            double acc[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[a][e] = 0.0;
+            for (int r = 0; r < ng; ++r) {
+                const double w = cg[r];
+                double ji[4], cj[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    ji[a] = (i0 + a < nw) ? Jgget(c, s, r, i0 + a) : 0.0;
+                    cj[a] = (j0 + a < nw) ? w * Jgget(c, s, r, j0 + a) : 0.0;
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[a][e] = fma(ji[a], cj[e], acc[a][e]);
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int i = i0 + a, j = j0 + e;
+                    if (i < nw && j <= i) {
+                        double h = acc[a][e] + Mb[i * nw + j];
+                        if (i == j && reg != 0.0) h += reg;
+                        Mb[i * nw + j] = h;
+                        Mb[j * nw + i] = h;
+                    }
+                }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Householder QR of the m x n (m >= n) row-major stack S in place (LAPACK
 // dgeqr2 / dlarfg reflectors, the arithmetic of np.linalg.qr(mode="r")), then
@@ -870,50 +960,7 @@ __device__ int factor(Ctx& c, const double* lam, const double* t, double reg, lo
         }
         tsync();
         if (ng) {
-            // Jg' diag(coef) Jg over 4x4 register blocks of the lower block
-            // triangle, mirrored (the SYRK of add_reduced_hessian): 8 loads per
-            // 16 FMAs instead of 2 per FMA -- the dominant term of dense QPs
-            // (full condensing: ng >> nw)
-            const int nbk = (nw + 3) >> 2;
-            const int nblk = nbk * (nbk + 1) / 2;
-            const double* cg = cf + s.nb;
-            for (int b = tid; b < nblk; b += T) {
-                int bi = (int)((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
-                while (bi * (bi + 1) / 2 > b) --bi;
-                while ((bi + 1) * (bi + 2) / 2 <= b) ++bi;
-                const int bj = b - bi * (bi + 1) / 2;
-                const int i0 = bi * 4, j0 = bj * 4;
-                double acc[4][4];
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) acc[a][e] = 0.0;
-                for (int r = 0; r < ng; ++r) {
-                    const double w = cg[r];
-                    double ji[4], cj[4];
-#pragma unroll
-                    for (int a = 0; a < 4; ++a) {
-                        ji[a] = (i0 + a < nw) ? Jgget(c, s, r, i0 + a) : 0.0;
-                        cj[a] = (j0 + a < nw) ? w * Jgget(c, s, r, j0 + a) : 0.0;
-                    }
-#pragma unroll
-                    for (int a = 0; a < 4; ++a)
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) acc[a][e] = fma(ji[a], cj[e], acc[a][e]);
-                }
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int i = i0 + a, j = j0 + e;
-                        if (i < nw && j <= i) {
-                            double h = acc[a][e] + Mb[i * nw + j];
-                            if (i == j && reg != 0.0) h += reg;
-                            Mb[i * nw + j] = h;
-                            Mb[j * nw + i] = h;
-                        }
-                    }
-            }
+            rows_syrk(c, s, cf + s.nb, Mb, nw, ng, reg);
             flops += 2ll * nw * nw * ng;
             tsync();
         }

@@ -10,6 +10,10 @@ for c in 2 3 4; do
   timeout 600 python bench.py --cfg $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_cfg$c.json 2> gpurun_out/bench_cfg$c.err
 done
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_cfg1.json 2>&1
+for m in balance sqrt speed_abs robust; do
+  timeout 300 python bench.py --mode $m --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_mode_$m.json 2> /dev/null
+done
+for c in 1 2; do timeout 300 python tools/fcond_bench.py --cfg $c; done > gpurun_out/fcond_bench.jsonl 2>&1
 # ncu: launch list then one full capture of the solve kernel (same command exited 0 first)
 CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/ncu_plain.log 2>&1 && \
