@@ -251,7 +251,7 @@ int ocpqp_plan_info(const OcpPlan* plan, int64_t* out, int32_t out_len);
 /* ---- partial condensing (reference condensing.py:451-619) ----
  * A partial-condensing plan holds the block structure and the row routing of
  * partial_condense(qp, N1) for one (dims, idxb) structure; the arithmetic is
- * batched on the device.  Soft rows are not supported (OCPQP_E_UNSUPPORTED). */
+ * batched on the device. */
 typedef struct OcpPcPlan OcpPcPlan;
 
 /* partial_condense block structure (condensing.py:451-550). */
@@ -287,6 +287,11 @@ int ocpqp_pc_expand(OcpPcPlan* plan, int32_t B, const OcpQpDataC* in, const OcpI
  * _destroy take this plan too (N2 = 0; expansion = expand_solution). */
 int ocpqp_fc_create(const OcpQpDimC* dim, int32_t keep_x0, int32_t nfix, const int32_t* fix_row,
                     const int32_t* fix_comp, OcpPcPlan** out);
+
+/* Soft rows of the condensed QP (partial or full plan): ns (N2+1 entries)
+ * and the concatenated new idxs when non-NULL; returns sum(ns).  Slack data
+ * (Zl Zu zl zu sl_lb su_lb) travels with its row (condensing.py:289-334). */
+int ocpqp_pc_soft(const OcpPcPlan* plan, int32_t* ns, int32_t* idxs);
 
 const char* ocpqp_pc_last_error(void);
 

@@ -50,6 +50,8 @@ def _lib():
         L.ocpqp_fc_create.argtypes = [ctypes.POINTER(nat.OcpQpDimC), ctypes.c_int32, ctypes.c_int32,
                                       vp, vp, ctypes.POINTER(vp)]
         L.ocpqp_fc_create.restype = ctypes.c_int
+        L.ocpqp_pc_soft.argtypes = [vp, vp, vp]
+        L.ocpqp_pc_soft.restype = ctypes.c_int
         L.ocpqp_pc_last_error.restype = ctypes.c_char_p
         for f in ("ocpqp_pc_create", "ocpqp_pc_destroy", "ocpqp_pc_dims", "ocpqp_pc_condense",
                   "ocpqp_pc_expand"):
@@ -95,8 +97,8 @@ class PartialCondensingMap:
         nx, nu, nb, ng = arrs
         idxb = np.zeros(max(1, int(nb.sum())), dtype=np.int32)
         _lib().ocpqp_pc_dims(h, None, None, None, None, idxb.ctypes.data)
-        self.new_dim = OcpQpDim(N2, nx.tolist(), nu.tolist(), nb.tolist(), ng.tolist(),
-                                [0] * (N2 + 1))
+        ns, self.new_idxs = _soft_of(h, N2)
+        self.new_dim = OcpQpDim(N2, nx.tolist(), nu.tolist(), nb.tolist(), ng.tolist(), ns.tolist())
         self.new_idxb = []
         o = 0
         for k in range(N2 + 1):
@@ -114,6 +116,19 @@ class PartialCondensingMap:
             self.close()
         except Exception:
             pass
+
+
+def _soft_of(h, N2):
+    """(ns per new stage, list of new idxs arrays) of a condensing plan."""
+    ns = np.zeros(N2 + 1, dtype=np.int32)
+    tot = _check(_lib().ocpqp_pc_soft(h, ns.ctypes.data, None))
+    flat = np.zeros(max(1, tot), dtype=np.int32)
+    _lib().ocpqp_pc_soft(h, None, flat.ctypes.data)
+    out, o = [], 0
+    for k in range(N2 + 1):
+        out.append(flat[o: o + int(ns[k])].copy())
+        o += int(ns[k])
+    return ns, out
 
 
 _MAPS = {}
@@ -164,7 +179,7 @@ def partial_condense_batch(batch, N1, device="cuda"):
     batch = _as_batch(batch, check=False)
     pmap = _map_for(batch, N1)
     src = _device_full(batch, device)
-    out = OcpQpBatch(pmap.new_dim, batch.B, pmap.new_idxb, None)
+    out = OcpQpBatch(pmap.new_dim, batch.B, pmap.new_idxb, pmap.new_idxs)
     lay = out.layout
     dout = nat.OcpQpDataC()
     keep = []
@@ -312,7 +327,8 @@ class CondensingMap:
         idxb = np.zeros(max(1, nb), dtype=np.int32)
         _lib().ocpqp_pc_dims(h, None, None, None, None, idxb.ctypes.data)
         self.nv = nu
-        self.new_dim = OcpQpDim(0, [0], [nu], [nb], [ng], [0])
+        ns, self.new_idxs = _soft_of(h, 0)
+        self.new_dim = OcpQpDim(0, [0], [nu], [nb], [ng], [int(ns[0])])
         self.new_idxb = [idxb[:nb].copy()]
         zx = self.nx0 if self.keep_x0 else 0
         self.u_off, off = [], zx
@@ -355,7 +371,7 @@ def condense_batch(batch, keep_x0=None, device="cuda"):
     batch = _as_batch(batch, check=False)
     cmap = _fmap_for(batch, keep_x0)
     src = _device_full(batch, device)
-    out = OcpQpBatch(cmap.new_dim, batch.B, cmap.new_idxb, None)
+    out = OcpQpBatch(cmap.new_dim, batch.B, cmap.new_idxb, cmap.new_idxs)
     lay = out.layout
     dout = nat.OcpQpDataC()
     keep = []

@@ -64,16 +64,21 @@ struct Dims {
     int N;
     std::vector<int> nx, nu, nb, ng, ns;
     std::vector<int> idxb;  // concatenated
-    std::vector<int> ib_off;
+    std::vector<int> idxs;  // concatenated
+    std::vector<int> ib_off, is_off;
     std::vector<long long> foff;  // [(N+1) * NF]
     std::vector<long long> flen;  // [NF]
     // flat solution layout
-    std::vector<int> u_off, x_off, pi_off, c_off;
-    int ny = 0, ne = 0, nc = 0;
+    std::vector<int> u_off, x_off, pi_off, c_off, s_off;
+    int ny = 0, ne = 0, nc = 0, nv = 0, ns_tot = 0;
     void finish() {
         const int S = N + 1;
         ib_off.assign(S, 0);
-        for (int n = 1; n < S; ++n) ib_off[n] = ib_off[n - 1] + nb[n - 1];
+        is_off.assign(S, 0);
+        for (int n = 1; n < S; ++n) {
+            ib_off[n] = ib_off[n - 1] + nb[n - 1];
+            is_off[n] = is_off[n - 1] + ns[n - 1];
+        }
         foff.assign((size_t)S * OCPQP_NUM_FIELDS, 0);
         flen.assign(OCPQP_NUM_FIELDS, 0);
         for (int f = 0; f < OCPQP_NUM_FIELDS; ++f) {
@@ -85,13 +90,15 @@ struct Dims {
             flen[f] = o;
         }
         u_off.assign(S, 0); x_off.assign(S, 0); pi_off.assign(S, 0); c_off.assign(S, 0);
-        int v = 0, p = 0, c = 0;
+        s_off.assign(S, 0);
+        int v = 0, p = 0, c = 0, sl = 0;
         for (int n = 0; n < S; ++n) {
             u_off[n] = v; x_off[n] = v + nu[n]; v += nu[n] + nx[n];
             pi_off[n] = p; if (n < N) p += nx[n + 1];
             c_off[n] = c; c += 2 * (nb[n] + ng[n]) + 2 * ns[n];
+            s_off[n] = sl; sl += ns[n];
         }
-        ny = v; ne = p; nc = c;
+        nv = v; ns_tot = sl; ny = v + 2 * sl; ne = p; nc = c;
     }
 };
 
@@ -106,6 +113,7 @@ struct PcBlockDev {
     int ox;        // leading z columns emitted as the new stage's x part (nx0; 0 for full)
     int row0;      // first entry of this block in the row tables
     int uoff0;     // first entry in the per-block-stage u offset table
+    int s0, ns_new;  // the new stage's slacks: entries s0.. of the slack tables
 };
 
 struct PcParams {
@@ -127,6 +135,11 @@ struct PcParams {
     const int* o_u; const int* o_x; const int* o_pi; const int* o_c;   // original flat layout
     const int* n_u; const int* n_x; const int* n_pi; const int* n_c;   // condensed flat layout
     const int* o_ib;  const int* o_idxb;
+    // soft rows: source (block-local stage, stage slack index) of each new slack,
+    // slack offsets / counts of both layouts
+    const int* slk_stage; const int* slk_j;
+    const int* o_s; const int* n_s; const int* ons; const int* nns;
+    int nv_s, nv_f, nst_s, nst_f;
     // data
     const double* fin[OCPQP_NUM_FIELDS]; long long bin[OCPQP_NUM_FIELDS];
     double* fout[OCPQP_NUM_FIELDS]; long long bout[OCPQP_NUM_FIELDS];
@@ -456,6 +469,14 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
         fout(p, q, OCPQP_F_maskl, k)[r] = fin(p, q, OCPQP_F_maskl, n)[src];
         fout(p, q, OCPQP_F_masku, k)[r] = fin(p, q, OCPQP_F_masku, n)[src];
     }
+    // soft-row data travels with its row (condensing.py:289-334, 523-534)
+    for (int jn = tid; jn < bk.ns_new; jn += T) {
+        const int e = bk.s0 + jn;
+        const int n = n0 + p.slk_stage[e], j = p.slk_j[e];
+        const int sf[6] = {OCPQP_F_Zl, OCPQP_F_Zu, OCPQP_F_zl, OCPQP_F_zu, OCPQP_F_sl_lb, OCPQP_F_su_lb};
+#pragma unroll
+        for (int f = 0; f < 6; ++f) fout(p, q, sf[f], k)[jn] = fin(p, q, sf[f], n)[j];
+    }
 }
 
 // copy the terminal stage verbatim (condensing.py:547-549)
@@ -477,7 +498,7 @@ __device__ void copy_terminal(const PcParams& p, int q) {
             case OCPQP_F_D: sz = (long long)ng * nu; break;
             case OCPQP_F_lg: case OCPQP_F_ug: sz = ng; break;
             case OCPQP_F_maskl: case OCPQP_F_masku: sz = nb + ng; break;
-            default: sz = 0; break;
+            default: sz = p.ons[p.N]; break;   // soft-row fields
         }
         const double* src = p.fin[f] + (long long)q * p.bin[f] + a0;
         double* dst = fout(p, q, f, p.N2);
@@ -568,6 +589,19 @@ __device__ void expand_block(const PcParams& p, int q, int k, double* ws) {
         ft[cf + src] = sts[cs + r];
         ft[cf + mo + src] = sts[cs + mn + r];
     }
+    // slacks and their multipliers (condensing.py:397-405, 592-601)
+    for (int jn = tid; jn < bk.ns_new; jn += T) {
+        const int e = bk.s0 + jn;
+        const int n = n0 + p.slk_stage[e], j = p.slk_j[e];
+        const int mo = p.onb[n] + p.ong[n], ons = p.ons[n], nns = p.nns[k];
+        const int cs = p.n_c[k] + 2 * mn, cf = p.o_c[n] + 2 * mo;
+        fy[p.nv_f + p.o_s[n] + j] = sy[p.nv_s + p.n_s[k] + jn];
+        fy[p.nv_f + p.nst_f + p.o_s[n] + j] = sy[p.nv_s + p.nst_s + p.n_s[k] + jn];
+        flam[cf + j] = slam[cs + jn];
+        flam[cf + ons + j] = slam[cs + nns + jn];
+        ft[cf + j] = sts[cs + jn];
+        ft[cf + ons + j] = sts[cs + nns + jn];
+    }
     __syncthreads();
     // costate recursion (condensing.py:397-412) seeded with the short-horizon pi_k;
     // full condensing runs it from the terminal stage (no seed) down to the
@@ -645,10 +679,14 @@ __device__ void expand_terminal(const PcParams& p, int q) {
     double* flam = p.flam + (long long)q * p.nc_f;
     double* ft = p.ft + (long long)q * p.nc_f;
     const int N = p.N, N2 = p.N2;
-    const int ncN = 2 * (p.onb[N] + p.ong[N]);
+    const int ncN = 2 * (p.onb[N] + p.ong[N]) + 2 * p.ons[N];
     for (int e = tid; e < ncN; e += T) {
         flam[p.o_c[N] + e] = slam[p.n_c[N2] + e];
         ft[p.o_c[N] + e] = sts[p.n_c[N2] + e];
+    }
+    for (int j = tid; j < p.ons[N]; j += T) {
+        fy[p.nv_f + p.o_s[N] + j] = sy[p.nv_s + p.n_s[N2] + j];
+        fy[p.nv_f + p.nst_f + p.o_s[N] + j] = sy[p.nv_s + p.nst_s + p.n_s[N2] + j];
     }
     // boundary states come verbatim from the short-horizon solution (condensing.py:608-610)
     for (int k = 0; k <= N2; ++k) {
@@ -689,6 +727,9 @@ struct OcpPcPlan {
     int N1 = 1, nblk = 0;
     int full = 0;
     std::vector<int> fix_row, fix_c;
+    std::vector<int> slk_stage, slk_j;
+    int *d_slk_stage = nullptr, *d_slk_j = nullptr, *d_os = nullptr, *d_ns = nullptr;
+    int *d_ons = nullptr, *d_nns = nullptr;
     int* d_fix_row = nullptr;
     int* d_fix_c = nullptr;
     std::vector<PcBlockDev> blk;
@@ -718,6 +759,28 @@ int upload(T** dst, const std::vector<T>& v) {
     if (!v.empty() && cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice) != cudaSuccess)
         return -1;
     return 0;
+}
+
+// Soft rows of one new stage: a row keeps its slack, and the new slacks are
+// ordered by new row index (condense's slack_entries sorted by dense row,
+// condensing.py:289-300, then partial_condense's idxs re-ordering through the
+// box permutation, :523-534).  Fills b.s0 / b.ns_new and the new idxs.
+void pc_slacks(OcpPcPlan* P, PcBlockDev& b) {
+    const Dims& od = P->od;
+    b.s0 = (int)P->slk_stage.size();
+    b.ns_new = 0;
+    for (int r = 0; r < b.nb_new + b.ng_new; ++r) {
+        const int e = b.row0 + r;
+        const int i = P->row_stage[e], src = P->row_src[e], n = b.n0 + i;
+        for (int j = 0; j < od.ns[n]; ++j)
+            if (od.idxs[od.is_off[n] + j] == src) {
+                P->slk_stage.push_back(i);
+                P->slk_j.push_back(j);
+                P->nd.idxs.push_back(r);
+                ++b.ns_new;
+                break;
+            }
+    }
 }
 
 // workspace per CTA slot; T1 scratch doubles as the (nv x nu) cross-term buffer
@@ -755,6 +818,12 @@ int pc_prepare(OcpPcPlan* P, int items) {
         rc |= upload(&P->d_oidxb, P->od.idxb);
         rc |= upload(&P->d_ofoff, P->od.foff);
         rc |= upload(&P->d_nfoff, P->nd.foff);
+        rc |= upload(&P->d_slk_stage, P->slk_stage);
+        rc |= upload(&P->d_slk_j, P->slk_j);
+        rc |= upload(&P->d_os, P->od.s_off);
+        rc |= upload(&P->d_ns, P->nd.s_off);
+        rc |= upload(&P->d_ons, P->od.ns);
+        rc |= upload(&P->d_nns, P->nd.ns);
         rc |= upload(&P->d_fix_row, P->fix_row);
         rc |= upload(&P->d_fix_c, P->fix_c);
         if (cudaMalloc(&P->d_counter, sizeof(int)) != cudaSuccess) rc = -1;
@@ -779,6 +848,9 @@ void pc_fill(const OcpPcPlan* P, PcParams& k, int B) {
     memset(&k, 0, sizeof(k));
     k.B = B; k.nblk = P->nblk; k.N = P->od.N; k.N2 = P->nd.N;
     k.full = P->full; k.nfix = (int)P->fix_row.size();
+    k.slk_stage = P->d_slk_stage; k.slk_j = P->d_slk_j;
+    k.o_s = P->d_os; k.n_s = P->d_ns; k.ons = P->d_ons; k.nns = P->d_nns;
+    k.nv_s = P->nd.nv; k.nv_f = P->od.nv; k.nst_s = P->nd.ns_tot; k.nst_f = P->od.ns_tot;
     k.fix_row = P->d_fix_row; k.fix_c = P->d_fix_c;
     k.nxmax = P->nxmax; k.nvmax = P->nvmax; k.numax = P->numax; k.Lmax = P->Lmax;
     k.blk = P->d_blk; k.uoff = P->d_uoff;
@@ -813,15 +885,10 @@ int ocpqp_pc_create(const OcpQpDimC* dim, int32_t N1, OcpPcPlan** out) {
     od.nx.assign(dim->nx, dim->nx + S); od.nu.assign(dim->nu, dim->nu + S);
     od.nb.assign(dim->nb, dim->nb + S); od.ng.assign(dim->ng, dim->ng + S);
     od.ns.assign(dim->ns, dim->ns + S);
-    long long snb = 0;
-    for (int n = 0; n < S; ++n) {
-        snb += od.nb[n];
-        if (od.ns[n]) {
-            delete P;
-            return pc_fail(OCPQP_E_UNSUPPORTED, "soft rows are not supported by the batched partial condensing");
-        }
-    }
+    long long snb = 0, sns = 0;
+    for (int n = 0; n < S; ++n) { snb += od.nb[n]; sns += od.ns[n]; }
     od.idxb.assign(dim->idxb, dim->idxb + snb);
+    if (sns) od.idxs.assign(dim->idxs, dim->idxs + sns);
     od.finish();
     P->N1 = N1;
     std::vector<int> starts;
@@ -893,14 +960,16 @@ int ocpqp_pc_create(const OcpQpDimC* dim, int32_t N1, OcpPcPlan** out) {
             P->row_src.push_back(g.r);
             P->row_aux.push_back(g.aux);
         }
+        pc_slacks(P, b);
         P->blk.push_back(b);
         nd.nx.push_back(b.nx0); nd.nu.push_back(nun); nd.nb.push_back(b.nb_new);
-        nd.ng.push_back(b.ng_new); nd.ns.push_back(0);
+        nd.ng.push_back(b.ng_new); nd.ns.push_back(b.ns_new);
     }
     // the old terminal stage is carried over verbatim
     nd.nx.push_back(od.nx[od.N]); nd.nu.push_back(od.nu[od.N]); nd.nb.push_back(od.nb[od.N]);
-    nd.ng.push_back(od.ng[od.N]); nd.ns.push_back(0);
+    nd.ng.push_back(od.ng[od.N]); nd.ns.push_back(od.ns[od.N]);
     for (int r = 0; r < od.nb[od.N]; ++r) nd.idxb.push_back(od.idxb[od.ib_off[od.N] + r]);
+    for (int j = 0; j < od.ns[od.N]; ++j) nd.idxs.push_back(od.idxs[od.is_off[od.N] + j]);
     nd.finish();
     pc_size(P);
     *out = P;
@@ -926,17 +995,21 @@ int ocpqp_fc_create(const OcpQpDimC* dim, int32_t keep_x0, int32_t nfix, const i
     od.nx.assign(dim->nx, dim->nx + S); od.nu.assign(dim->nu, dim->nu + S);
     od.nb.assign(dim->nb, dim->nb + S); od.ng.assign(dim->ng, dim->ng + S);
     od.ns.assign(dim->ns, dim->ns + S);
-    long long snb = 0;
-    for (int n = 0; n < S; ++n) {
-        snb += od.nb[n];
-        if (od.ns[n]) {
-            delete P;
-            return pc_fail(OCPQP_E_UNSUPPORTED, "soft rows are not supported by the batched condensing");
-        }
-    }
+    long long snb = 0, sns = 0;
+    for (int n = 0; n < S; ++n) { snb += od.nb[n]; sns += od.ns[n]; }
     od.idxb.assign(dim->idxb, dim->idxb + snb);
+    if (sns) od.idxs.assign(dim->idxs, dim->idxs + sns);
     od.finish();
     const int nx0 = od.nx[0];
+    if (!keep_x0)
+        for (int j = 0; j < od.ns[0]; ++j) {
+            const int r = od.idxs[od.is_off[0] + j];
+            if (r < od.nb[0] && od.idxb[od.ib_off[0] + r] >= od.nu[0]) {
+                delete P;
+                return pc_fail(OCPQP_E_CONDENSE, "soft initial-state fixing rows are not supported "
+                                                  "with keep_x0=False");
+            }
+        }
     if (!keep_x0) {
         std::vector<int> seen(nx0, 0);
         for (int j = 0; j < nfix; ++j) {
@@ -1009,9 +1082,10 @@ int ocpqp_fc_create(const OcpQpDimC* dim, int32_t keep_x0, int32_t nfix, const i
         P->row_src.push_back(g.r);
         P->row_aux.push_back(g.aux);
     }
+    pc_slacks(P, b);
     P->blk.push_back(b);
     nd.nx.push_back(0); nd.nu.push_back(b.nv); nd.nb.push_back(b.nb_new);
-    nd.ng.push_back(b.ng_new); nd.ns.push_back(0);
+    nd.ng.push_back(b.ng_new); nd.ns.push_back(b.ns_new);
     nd.finish();
     pc_size(P);
     *out = P;
@@ -1027,6 +1101,8 @@ int ocpqp_pc_destroy(OcpPcPlan* P) {
     cudaFree(P->d_npi); cudaFree(P->d_nc); cudaFree(P->d_oib); cudaFree(P->d_oidxb);
     cudaFree(P->d_ofoff); cudaFree(P->d_nfoff); cudaFree(P->d_counter); cudaFree(P->d_ws);
     cudaFree(P->d_fix_row); cudaFree(P->d_fix_c);
+    cudaFree(P->d_slk_stage); cudaFree(P->d_slk_j); cudaFree(P->d_os); cudaFree(P->d_ns);
+    cudaFree(P->d_ons); cudaFree(P->d_nns);
     delete P;
     return OCPQP_OK;
 }
@@ -1045,6 +1121,17 @@ int ocpqp_pc_dims(const OcpPcPlan* P, int32_t* nx, int32_t* nu, int32_t* nb, int
     if (idxb_out)
         for (size_t i = 0; i < P->nd.idxb.size(); ++i) idxb_out[i] = P->nd.idxb[i];
     return P->nd.N;
+}
+
+// Soft rows of the condensed QP: ns (N2+1 entries) and the concatenated new
+// idxs (sum of ns) when non-NULL; returns sum(ns).
+int ocpqp_pc_soft(const OcpPcPlan* P, int32_t* ns, int32_t* idxs_out) {
+    if (!P) return pc_fail(OCPQP_E_ARG, "NULL plan");
+    if (ns)
+        for (int k = 0; k <= P->nd.N; ++k) ns[k] = P->nd.ns[k];
+    if (idxs_out)
+        for (size_t i = 0; i < P->nd.idxs.size(); ++i) idxs_out[i] = P->nd.idxs[i];
+    return (int)P->nd.idxs.size();
 }
 
 // Batched partial_condense arithmetic: `in` is the packed batch of B QPs

@@ -279,6 +279,51 @@ def fcond():
     np.savez_compressed(HERE / "fcond.npz", **out)
 
 
+# condensing with soft rows (condensing.py:289-334, 523-534, 592-601)
+SOFT_CASES = [
+    ("s31", (31, dict(N=5, nx=3, nu=2, nb=4, ng=1, ns=2, fix_x0=True)), None, 2),
+    ("s32", (32, dict(N=4, nx=3, nu=2, nb=3, ng=2, ns=2)), None, 3),
+    ("s33", (33, dict(N=6, nx=2, nu=2, nb=4, ng=1, ns=3, fix_x0=True)), True, 4),
+    ("s34", (34, dict(N=5, nx=4, nu=1, nb=5, ng=0, ns=2, mask_last=False)), None, 2),
+]
+SOFT_DFIELDS = FCOND_FIELDS + ("idxs", "Zl", "Zu", "zl", "zu", "sl_lb", "su_lb")
+SOFT_PFIELDS = PCOND_FIELDS + ("idxs", "Zl", "Zu", "zl", "zu", "sl_lb", "su_lb")
+
+
+def soft_cond():
+    out = {}
+    for name, src, keep, N1 in SOFT_CASES:
+        qp = pcond_source(src)
+        dq, cmap = mpcqp.condense(qp, keep_x0=keep)
+        out[f"{name}_dims"] = np.array([dq.nv, dq.ne, dq.nb, dq.ng, dq.ns, int(cmap.keep_x0)])
+        for f in SOFT_DFIELDS:
+            out[f"{name}_{f}"] = dq.get_field(f)
+        rep = mpcqp.solve_dense_qp(dq, ARG)
+        for k, v in pack_report(rep).items():
+            out[f"{name}_dense_{k}"] = v
+        full = mpcqp.expand_solution(rep.solution, cmap, qp)
+        for k in ("y", "pi", "lam", "t"):
+            out[f"{name}_full_{k}"] = getattr(full, k)
+        qp2, pmap = mpcqp.partial_condense(qp, N1)
+        d2 = qp2.dim
+        out[f"{name}_p_dims"] = np.array([d2.nx, d2.nu, d2.nb, d2.ng, d2.ns])
+        for n in range(d2.N + 1):
+            for f in SOFT_PFIELDS:
+                out[f"{name}_p_s{n}_{f}"] = qp2.get_field(f, n)
+            if n < d2.N:
+                for f in ("A", "B", "b"):
+                    out[f"{name}_p_s{n}_{f}"] = qp2.get_field(f, n)
+        prep = mpcqp.solve_ocp_qp(qp2, ARG)
+        for k, v in pack_report(prep).items():
+            out[f"{name}_short_{k}"] = v
+        pfull = mpcqp.partial_expand(prep.solution, pmap, qp)
+        for k in ("y", "pi", "lam", "t"):
+            out[f"{name}_pfull_{k}"] = getattr(pfull, k)
+        print("soft", name, dq.nv, dq.ns, cmap.keep_x0, rep.iterations, d2.N, list(d2.ns),
+              prep.iterations, flush=True)
+    np.savez_compressed(HERE / "soft_cond.npz", **out)
+
+
 # modes beyond speed (ipm_core.py:131-168): (name, preset, tol, overrides)
 MODES = [
     ("balance6", "balance", 1e-6, {}),
@@ -401,6 +446,6 @@ def qp_files():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["known", "residuals", "newton", "solve_random", "solve_cfg", "pcond",
-                            "solve_modes", "closed_loop", "qp_files", "fcond"]
+                            "solve_modes", "closed_loop", "qp_files", "fcond", "soft_cond"]
     for w in which:
         globals()[w]()
