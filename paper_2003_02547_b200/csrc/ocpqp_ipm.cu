@@ -392,8 +392,7 @@ __device__ ResNorms residuals(Ctx& c, const double* y, const double* pi, const d
 __device__ bool team_chol(double* L, int n, int ld, int* flag) {
     // Two barriers per column: every thread reads the pivot and takes the
     // (identical) square root itself; the diagonal is written back during the
-    // trailing update, which reads only the scaled column.  The trailing
-    // update walks the lower triangle with an incremental (row, col) carry.
+    // trailing update, which reads only the scaled column.
     (void)flag;
     const int tid = threadIdx.x, T = blockDim.x;
     for (int k = 0; k < n; ++k) {
@@ -406,16 +405,12 @@ __device__ bool team_chol(double* L, int n, int ld, int* flag) {
         for (int i = k + 1 + tid; i < n; i += T) L[i * ld + k] /= dk;
         tsync();
         if (tid == 0) L[k * ld + k] = dk;
-        const int rem = n - k - 1, tot = rem * (rem + 1) / 2;
-        if (tid < tot) {
-            int i = 0, j = tid;
-            while (j > i) { j -= i + 1; ++i; }
-            for (int idx = tid; idx < tot; idx += T) {
-                double* Li = L + (k + 1 + i) * ld;
-                Li[k + 1 + j] -= Li[k] * L[(k + 1 + j) * ld + k];
-                j += T;
-                while (j > i) { j -= i + 1; ++i; }
-            }
+        // rows round-robin over warps, columns j <= i over lanes
+        const int lane = tid & 31, nwarp = (T + 31) >> 5;
+        for (int i = k + 1 + (tid >> 5); i < n; i += nwarp) {
+            double* Li = L + i * ld;
+            const double lik = Li[k];
+            for (int j = k + 1 + lane; j <= i; j += 32) Li[j] -= lik * L[j * ld + k];
         }
         tsync();
     }
