@@ -57,6 +57,9 @@ def parse():
                     help="target duration of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--path", default="ocp", choices=["ocp", "condense"],
+                    help="ocp: the Riccati solve (headline); condense: full condensing -> "
+                         "dense-QP solve -> expand_solution (SURVEY 8(f) row 3)")
     ap.add_argument("--mode", default="speed",
                     choices=["speed", "sqrt", "balance", "robust", "speed_abs"],
                     help="IpmArg preset (sqrt = speed with the square-root Riccati variant); "
@@ -229,6 +232,9 @@ def main():
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
+
+    if a.path == "condense":
+        return main_condense(a, arg, B, config, rank, world, local)
 
     import torch
 
@@ -420,6 +426,141 @@ def main():
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def main_condense(a, arg, B, config, rank, world, local):
+    """Full-condensing path: condense_batch -> dense IPM (N = 0 form) -> expand_batch.
+
+    value: QPs/s through the three device stages, inputs resident; roofline of
+    the dominant kernel (the dense IPM solve): the reference's own counted
+    flops of the dense solve (identical to ours, tests/test_gpu_fcond.py) over
+    its event-timed duration; e2e: the same from pinned host buffers, the
+    expanded (y, pi, lam, t) and status / iterations read back.
+    """
+    import torch
+
+    from paper_2003_02547_b200.condensing import condense_batch, expand_batch
+    from paper_2003_02547_b200.generators import make_batch
+    from paper_2003_02547_b200.solver import get_plan, solve_ocp_qp_batch
+
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    batch = make_batch(a.cfg, batch=B)
+    dev = batch.to(device)
+    stream = torch.cuda.current_stream(device)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+    config = dict(config, workload=config["workload"] + "; full condensing + dense-QP solve + "
+                  "expand_solution")
+
+    def step(src, ev=None):
+        cb, cmap = condense_batch(src)
+        if ev is not None:
+            ev[0].record(stream)
+        rep = solve_ocp_qp_batch(cb, arg, trace=False, stream=stream)
+        if ev is not None:
+            ev[1].record(stream)
+        return cb, rep, expand_batch(rep, cmap, src)
+
+    w = 0
+    t_end = time.perf_counter() + 0.5
+    while w < a.warmup or time.perf_counter() < t_end:
+        step(dev)
+        w += 1
+    torch.cuda.synchronize()
+    peak_dfma, peak_dmma = fp64_peak()
+    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    evs = [(E(), E(), (E(), E())) for _ in range(a.steps)]
+    sampler = ClockSampler(index=local)
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.05)
+    for e0, e1, ek in evs:
+        flush.zero_()
+        e0.record(stream)
+        cb, rep, _ = step(dev, ek)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    times = np.array([e0.elapsed_time(e1) for e0, e1, _ in evs])
+    ktimes = np.array([ek[0].elapsed_time(ek[1]) for _, _, ek in evs])
+    t_step = float(times.mean())
+    t_k = float(ktimes.mean())
+    flops = float(rep.flops.sum().item())
+    iters = rep.iterations.cpu().numpy()
+    status = rep.status_code.cpu().numpy()
+    achieved = flops / (t_k * 1e-3) / 1e12
+    plan_info = get_plan(cb).info()
+    line = {"metric": METRIC, "value": world * B / (t_step * 1e-3), "unit": "solves/s",
+            "n_gpus": world, "steps": a.steps, "warmup": w, "ms_per_step": t_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators, BASELINE configs)", "config": config,
+            "path": "condense",
+            "roofline": {"bound": "tensor", "pipe": "fp64 (DFMA / DMMA)", "achieved": achieved,
+                         "peak": peak_dfma, "unit": "TFLOP/s",
+                         "frac": achieved / peak_dfma if peak_dfma else None, "traffic": None,
+                         "kernel": "k_ipm_solve (dense N = 0 form)",
+                         "work": f"reference-counted flops of the dense solves = {flops:.4g} "
+                                 f"per step over the solve kernel's {t_k:.3f} ms",
+                         "kernel_share_of_step": t_k / t_step},
+            "clocks": clocks, "gpu_launches": a.steps * 3, "plan": plan_info,
+            "stage_ms": {"dense_solve": t_k, "condense_plus_expand": t_step - t_k},
+            "dense": {"nv": int(cb.dim.nu[0]), "nb": int(cb.dim.nb[0]), "ng": int(cb.dim.ng[0])},
+            "iterations": {"min": int(iters.min()), "mean": float(iters.mean()),
+                           "max": int(iters.max())},
+            "status_counts": {str(int(k)): int(v) for k, v in zip(*np.unique(status, return_counts=True))}}
+    if not a.no_e2e:
+        hb = batch.pin_memory()
+        et = []
+        for i in range(max(5, a.steps // 4) + 2):
+            flush.zero_()
+            e0, e1 = E(), E()
+            e0.record(stream)
+            _, r2, (y, pi, lam, t) = step(hb)
+            outs = [x.to("cpu", non_blocking=True) for x in (y, pi, lam, t, r2.status_code,
+                                                            r2.iterations)]
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if i >= 2:
+                et.append(e0.elapsed_time(e1))
+        te = float(np.mean(et))
+        line["e2e"] = {"value": world * B / (te * 1e-3), "unit": "solves/s",
+                       "h2d_bytes_per_step": sum(int(v.numel()) * 8 for v in hb.fields.values()),
+                       "d2h_bytes_per_step": sum(int(x.numel()) * x.element_size() for x in outs),
+                       "ms_per_step": te, "steps": len(et)}
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import condense_oracle as co  # test infrastructure; the cpu_baseline leg only
+        import oracle as orc
+
+        from paper_2003_02547_b200 import OcpQpBatch, dense_to_ocp
+        from paper_2003_02547_b200.dense import DenseQp
+
+        orc.build()
+        n = min(B, 64)
+        qps = [batch.qp(i) for i in range(n)]
+        t0 = time.perf_counter()
+        dqs, maps = [], []
+        for q in qps:
+            dd, m = co.full_condense(q)
+            dq = DenseQp(len(dd["g"]), 0, len(dd["idxb"]), len(dd["lg"]), 0)
+            for f in ("H", "g", "idxb", "lb", "ub", "C", "lg", "ug", "maskl", "masku"):
+                dq.set_field(f, dd[f])
+            dqs.append(dense_to_ocp(dq))
+            maps.append(m)
+        ref = orc.solve(OcpQpBatch.from_qps(dqs), arg, nthreads=os.cpu_count() or 1, trace=False)
+        for i, q in enumerate(qps):
+            co.full_expand(q, maps[i], ref["y"][i], ref["lam"][i], ref["t"][i])
+        tc = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": n / tc, "unit": "solves/s", "cores": os.cpu_count() or 1,
+                                "kind": "port",
+                                "sample": f"{n} QPs of the workload: numpy condense + C-oracle "
+                                          f"dense solve ({os.cpu_count()} threads) + numpy expand, "
+                                          f"{tc:.2f} s"}
+        line["parity_vs_oracle"] = {"qps": n,
+                                    "status_mismatch": int(np.sum(ref["status"] != status[:n])),
+                                    "iteration_mismatch": int(np.sum(ref["iters"] != iters[:n]))}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

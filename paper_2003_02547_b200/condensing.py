@@ -255,22 +255,36 @@ def partial_expand(sol_p, pmap, qp):
 # ---------------------------------------------------------------------------
 
 def _stage0_rows(batch):
-    """Host copies [Bf, nb0] of the stage-0 lb, ub, maskl, masku of a batch."""
+    """Host copies [Bf, nb0] of the stage-0 lb, ub, maskl, masku of a batch
+    (one device-to-host copy for a device batch)."""
+    from .batch import default_fill
+
     d = batch.dim
     nb0 = int(d.nb[0])
-    out = []
-    for name in ("lb", "ub", "maskl", "masku"):
+    names = ("lb", "ub", "maskl", "masku")
+    parts, dev = [], None
+    for name in names:
         arr = batch.fields.get(name)
         if arr is None:
-            from .batch import default_fill
-            out.append(np.full((1, nb0), default_fill(name)))
+            parts.append(None)
             continue
-        sl = batch.layout.stage_slice(name, 0)
-        a = arr[:, sl]
+        a = arr[:, batch.layout.stage_slice(name, 0)][:, :nb0]
         if not isinstance(a, np.ndarray):
-            a = a.detach().cpu().numpy()
-        out.append(np.asarray(a, dtype=np.float64)[:, :nb0])
-    return out
+            dev = a
+        parts.append(a)
+    if dev is not None:
+        import torch
+
+        rows = max(p.shape[0] for p in parts if p is not None)
+        stk = torch.stack([torch.as_tensor(p, dtype=torch.float64, device=dev.device).expand(rows, nb0)
+                           if p is not None else
+                           torch.full((rows, nb0), default_fill(n), dtype=torch.float64,
+                                      device=dev.device)
+                           for p, n in zip(parts, names)])
+        host = stk.cpu().numpy()
+        return [host[i] for i in range(len(names))]
+    return [np.asarray(p, dtype=np.float64) if p is not None else np.full((1, nb0), default_fill(n))
+            for p, n in zip(parts, names)]
 
 
 def detect_fixed_x0(batch):
