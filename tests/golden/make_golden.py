@@ -324,6 +324,56 @@ def soft_cond():
     np.savez_compressed(HERE / "soft_cond.npz", **out)
 
 
+# user-built dense QPs (qp_data.DenseQp, solve_dense_qp: solver.py:98-100)
+DENSE_CASES = [(41, 6, 4, 2, 0), (42, 12, 8, 5, 3), (43, 20, 20, 10, 4), (44, 40, 30, 60, 0),
+               (45, 9, 3, 0, 2)]
+DENSE_MODES = (("speed8", "speed", 1e-8), ("balance6", "balance", 1e-6))
+
+
+def dense_random_qp(lib, seed, nv, nb, ng, ns):
+    """A feasible random dense QP (box, general and soft rows, one masked side)."""
+    rng = np.random.default_rng(seed)
+    F = rng.standard_normal((nv, nv))
+    q = lib.DenseQp(nv, 0, nb, ng, ns)
+    q.set_field("H", F @ F.T + np.eye(nv))
+    q.set_field("g", rng.standard_normal(nv))
+    v0 = rng.uniform(-0.5, 0.5, nv)
+    idxb = np.sort(rng.choice(nv, nb, replace=False)) if nb else np.zeros(0, dtype=int)
+    if nb:
+        q.set_field("idxb", idxb)
+        q.set_field("lb", v0[idxb] - rng.uniform(0.1, 1.0, nb))
+        q.set_field("ub", v0[idxb] + rng.uniform(0.1, 1.0, nb))
+    if ng:
+        C = rng.standard_normal((ng, nv))
+        q.set_field("C", C)
+        q.set_field("lg", C @ v0 - rng.uniform(0.1, 1.0, ng))
+        q.set_field("ug", C @ v0 + rng.uniform(0.1, 1.0, ng))
+    if ns:
+        q.set_field("idxs", np.sort(rng.choice(nb + ng, ns, replace=False)))
+        for f in ("Zl", "Zu"):
+            q.set_field(f, rng.uniform(0.5, 2.0, ns))
+        for f in ("zl", "zu"):
+            q.set_field(f, rng.uniform(0.0, 1.0, ns))
+    if nb + ng:
+        mu = np.ones(nb + ng)
+        mu[rng.integers(nb + ng)] = 0.0
+        q.set_field("masku", mu)
+    return q
+
+
+def dense():
+    out = {}
+    for seed, nv, nb, ng, ns in DENSE_CASES:
+        q = dense_random_qp(mpcqp, seed, nv, nb, ng, ns)
+        for mname, preset, tol in DENSE_MODES:
+            arg = mpcqp.mode_preset(preset).with_tol(tol)
+            rep = mpcqp.solve_dense_qp(q, arg)
+            for k, v in pack_report(rep).items():
+                out[f"d{seed}_{mname}_{k}"] = v
+            print("dense", seed, mname, rep.status.value, rep.iterations, flush=True)
+    np.savez_compressed(HERE / "dense.npz", **out)
+
+
 # modes beyond speed (ipm_core.py:131-168): (name, preset, tol, overrides)
 MODES = [
     ("balance6", "balance", 1e-6, {}),
@@ -446,6 +496,6 @@ def qp_files():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["known", "residuals", "newton", "solve_random", "solve_cfg", "pcond",
-                            "solve_modes", "closed_loop", "qp_files", "fcond", "soft_cond"]
+                            "solve_modes", "closed_loop", "qp_files", "fcond", "soft_cond", "dense"]
     for w in which:
         globals()[w]()
