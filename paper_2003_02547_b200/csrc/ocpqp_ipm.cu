@@ -198,9 +198,12 @@ __device__ void rows_values(const Ctx& c, const double* y, double* rowv) {
             if (i < s.nb) {
                 v = w[p.idxb[s.ib_off + i]];
             } else {
-                const int g = i - s.nb;
+                const int g = i - s.nb, nu = s.nu, nx = s.nx;
+                const double* Dg = fptr(c, OCPQP_F_D, s) + g * nu;
+                const double* Cg = fptr(c, OCPQP_F_C, s) + g * nx;
                 v = 0.0;
-                for (int j = 0; j < s.nw; ++j) v = fma(Jgget(c, s, g, j), w[j], v);
+                for (int j = 0; j < nu; ++j) v = fma(Dg[j], w[j], v);
+                for (int j = 0; j < nx; ++j) v = fma(Cg[j], w[nu + j], v);
             }
             rowv[s.m_off + i] = v;
         }
@@ -212,8 +215,13 @@ __device__ __forceinline__ double rows_t(const Ctx& c, const StageInfo& s, int j
     const int kb = c.p->var_box[s.u_off + j];
     double out = kb >= 0 ? coeff[kb] : 0.0;
     if (s.ng) {
+        // column j of Jg = [D C]: stride nu (j < nu) or nx
+        const bool du = j < s.nu;
+        const double* col = du ? fptr(c, OCPQP_F_D, s) + j : fptr(c, OCPQP_F_C, s) + (j - s.nu);
+        const int ld = du ? s.nu : s.nx;
+        const double* cg = coeff + s.nb;
         double g = 0.0;
-        for (int r = 0; r < s.ng; ++r) g = fma(Jgget(c, s, r, j), coeff[s.nb + r], g);
+        for (int r = 0; r < s.ng; ++r) g = fma(col[r * ld], cg[r], g);
         out += g;
     }
     return out;
@@ -547,12 +555,19 @@ __device__ __noinline__ void rows_syrk(const Ctx& c, const StageInfo& s, const d
             while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
             const int tj = t - ti * (ti + 1) / 2;
             const int ia = ti * 8 + gr, jb = tj * 8 + gr;
+            // this lane's columns of Jg = [D C] (row stride nu or nx)
+            const int nu = s.nu, nx = s.nx;
+            const double* Dp = fptr(c, OCPQP_F_D, s);
+            const double* Cp = fptr(c, OCPQP_F_C, s);
+            const double* ca = ia < nu ? Dp + ia : Cp + (ia - nu);
+            const double* cb = jb < nu ? Dp + jb : Cp + (jb - nu);
+            const int la = ia < nu ? nu : nx, lb = jb < nu ? nu : nx;
             double d0 = 0.0, d1 = 0.0;
             for (int r0 = 0; r0 < ng; r0 += 4) {
                 const int r = r0 + tg;
                 const bool rin = r < ng;
-                const double av = (rin && ia < nw) ? Jgget(c, s, r, ia) : 0.0;
-                const double bv = (rin && jb < nw) ? cg[r] * Jgget(c, s, r, jb) : 0.0;
+                const double av = (rin && ia < nw) ? ca[r * la] : 0.0;
+                const double bv = (rin && jb < nw) ? cg[r] * cb[r * lb] : 0.0;
                 asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                              : "+d"(d0), "+d"(d1)
                              : "d"(av), "d"(bv));
