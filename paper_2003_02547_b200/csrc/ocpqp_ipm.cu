@@ -637,8 +637,45 @@ __device__ __noinline__ void rows_syrk(const Ctx& c, const StageInfo& s, const d
 // qr_cholesky's rank test and row-sign normalisation (linalg.py:152-187).
 // Returns false on RankDeficient.  Column-parallel reflector application.
 // ---------------------------------------------------------------------------
+// The same reflectors by warp 0 alone when the stack fits one warp (m <= 32):
+// lane i owns row i, column sums by shuffles, only __syncwarp between steps
+// (the block-wide version spends its time in barriers at these sizes).
+__device__ void warp_qr_reflectors(double* S, int m, int n) {
+    const int lane = threadIdx.x & 31;
+    const bool own = lane < m;
+    for (int k = 0; k < n; ++k) {
+        const double sk = (own && lane > k) ? S[lane * n + k] : 0.0;
+        double ss = sk * sk;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if (ss == 0.0) continue;    // H = I (tau = 0)
+        const double alpha = S[k * n + k];
+        const double beta = -copysign(hypot(alpha, sqrt(ss)), alpha);
+        const double tau = (beta - alpha) / beta;
+        const double sc = 1.0 / (alpha - beta);
+        const double vk = (own && lane > k) ? sk * sc : 0.0;   // reflector entry of this row
+        if (own && lane > k) S[lane * n + k] = vk;
+        for (int j = k + 1; j < n; ++j) {
+            double w = (own && lane > k) ? vk * S[lane * n + j] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+            w = (S[k * n + j] + w) * tau;
+            __syncwarp();
+            if (own && lane > k) S[lane * n + j] = fma(-w, vk, S[lane * n + j]);
+            if (lane == k) S[k * n + j] -= w;
+            __syncwarp();
+        }
+        if (lane == k) S[k * n + k] = beta;
+        __syncwarp();
+    }
+}
+
 __device__ __noinline__ bool team_qr(Ctx& c, double* S, int m, int n) {
     const int tid = threadIdx.x, T = blockDim.x;
+    if (m <= 32) {
+        if (tid < 32) warp_qr_reflectors(S, m, n);
+        tsync();
+    } else
     for (int k = 0; k < n; ++k) {
         double ss = 0.0;
         for (int i = k + 1 + tid; i < m; i += T) ss = fma(S[i * n + k], S[i * n + k], ss);
@@ -650,12 +687,19 @@ __device__ __noinline__ bool team_qr(Ctx& c, double* S, int m, int n) {
         const double sc = 1.0 / (alpha - beta);
         for (int i = k + 1 + tid; i < m; i += T) S[i * n + k] *= sc;
         tsync();
-        for (int j = k + 1 + tid; j < n; j += T) {
-            double w = S[k * n + j];
-            for (int i = k + 1; i < m; ++i) w = fma(S[i * n + k], S[i * n + j], w);
-            w *= tau;
-            S[k * n + j] -= w;
-            for (int i = k + 1; i < m; ++i) S[i * n + j] = fma(-w, S[i * n + k], S[i * n + j]);
+        // reflector application: one warp per column j, lanes over the rows
+        // (the dot product v'S[:, j] by a shuffle reduction)
+        {
+            const int lane = tid & 31, nwarp = (T + 31) >> 5;
+            for (int j = k + 1 + (tid >> 5); j < n; j += nwarp) {
+                double w = 0.0;
+                for (int i = k + 1 + lane; i < m; i += 32) w = fma(S[i * n + k], S[i * n + j], w);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+                w = (S[k * n + j] + w) * tau;
+                for (int i = k + 1 + lane; i < m; i += 32) S[i * n + j] = fma(-w, S[i * n + k], S[i * n + j]);
+                if (lane == 0) S[k * n + j] -= w;
+            }
         }
         if (tid == 0) S[k * n + k] = beta;
         tsync();
