@@ -410,15 +410,22 @@ __device__ bool team_chol(double* L, int n, int ld, int* flag) {
             return false;
         }
         const double dk = sqrt(d);
-        for (int i = k + 1 + tid; i < n; i += T) L[i * ld + k] /= dk;
+        // the scaled column is mirrored into row k's (unused, finally zeroed)
+        // upper part, so the trailing update reads it contiguously
+        for (int i = k + 1 + tid; i < n; i += T) {
+            const double v = L[i * ld + k] / dk;
+            L[i * ld + k] = v;
+            L[k * ld + i] = v;
+        }
         tsync();
         if (tid == 0) L[k * ld + k] = dk;
         // rows round-robin over warps, columns j <= i over lanes
         const int lane = tid & 31, nwarp = (T + 31) >> 5;
+        const double* ck = L + k * ld;
         for (int i = k + 1 + (tid >> 5); i < n; i += nwarp) {
             double* Li = L + i * ld;
             const double lik = Li[k];
-            for (int j = k + 1 + lane; j <= i; j += 32) Li[j] -= lik * L[j * ld + k];
+            for (int j = k + 1 + lane; j <= i; j += 32) Li[j] -= lik * ck[j];
         }
         tsync();
     }
