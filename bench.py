@@ -57,9 +57,10 @@ def parse():
                     help="target duration of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--path", default="ocp", choices=["ocp", "condense"],
-                    help="ocp: the Riccati solve (headline); condense: full condensing -> "
-                         "dense-QP solve -> expand_solution (SURVEY 8(f) row 3)")
+    ap.add_argument("--path", default="ocp",
+                    help="ocp: the Riccati solve (headline); partial:<N1>: partial condensing "
+                         "-> solve -> partial_expand (config 4's second way); condense: full "
+                         "condensing -> dense-QP solve -> expand_solution (SURVEY 8(f) row 3)")
     ap.add_argument("--mode", default="speed",
                     choices=["speed", "sqrt", "balance", "robust", "speed_abs"],
                     help="IpmArg preset (sqrt = speed with the square-root Riccati variant); "
@@ -233,8 +234,10 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
-    if a.path == "condense":
+    if a.path == "condense" or a.path.startswith("partial:"):
         return main_condense(a, arg, B, config, rank, world, local)
+    if a.path != "ocp":
+        raise SystemExit(f"unknown --path {a.path}")
 
     import torch
 
@@ -439,9 +442,13 @@ def main_condense(a, arg, B, config, rank, world, local):
     """
     import torch
 
-    from paper_2003_02547_b200.condensing import condense_batch, expand_batch
+    from paper_2003_02547_b200.condensing import (condense_batch, expand_batch,
+                                                  partial_condense_batch, partial_expand_batch)
     from paper_2003_02547_b200.generators import make_batch
     from paper_2003_02547_b200.solver import get_plan, solve_ocp_qp_batch
+
+    full = a.path == "condense"
+    N1 = None if full else int(a.path.split(":", 1)[1])
 
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
@@ -449,17 +456,19 @@ def main_condense(a, arg, B, config, rank, world, local):
     dev = batch.to(device)
     stream = torch.cuda.current_stream(device)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
-    config = dict(config, workload=config["workload"] + "; full condensing + dense-QP solve + "
-                  "expand_solution")
+    config = dict(config, workload=config["workload"] + (
+        "; full condensing + dense-QP solve + expand_solution" if full else
+        f"; partial condensing N1={N1} + solve + partial_expand"))
 
     def step(src, ev=None):
-        cb, cmap = condense_batch(src)
+        cb, cmap = condense_batch(src) if full else partial_condense_batch(src, N1)
         if ev is not None:
             ev[0].record(stream)
         rep = solve_ocp_qp_batch(cb, arg, trace=False, stream=stream)
         if ev is not None:
             ev[1].record(stream)
-        return cb, rep, expand_batch(rep, cmap, src)
+        ex = expand_batch if full else partial_expand_batch
+        return cb, rep, ex(rep, cmap, src)
 
     w = 0
     t_end = time.perf_counter() + 0.5
@@ -494,17 +503,20 @@ def main_condense(a, arg, B, config, rank, world, local):
             "n_gpus": world, "steps": a.steps, "warmup": w, "ms_per_step": t_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, BASELINE configs)", "config": config,
-            "path": "condense",
+            "path": a.path,
             "roofline": {"bound": "tensor", "pipe": "fp64 (DFMA / DMMA)", "achieved": achieved,
                          "peak": peak_dfma, "unit": "TFLOP/s",
                          "frac": achieved / peak_dfma if peak_dfma else None, "traffic": None,
-                         "kernel": "k_ipm_solve (dense N = 0 form)",
-                         "work": f"reference-counted flops of the dense solves = {flops:.4g} "
+                         "kernel": ("k_ipm_solve (dense N = 0 form)" if full else
+                                    f"{plan_info.get('kernel')} kernel on the condensed QPs"),
+                         "work": f"reference-counted flops of the condensed solves = {flops:.4g} "
                                  f"per step over the solve kernel's {t_k:.3f} ms",
                          "kernel_share_of_step": t_k / t_step},
             "clocks": clocks, "gpu_launches": a.steps * 3, "plan": plan_info,
             "stage_ms": {"dense_solve": t_k, "condense_plus_expand": t_step - t_k},
-            "dense": {"nv": int(cb.dim.nu[0]), "nb": int(cb.dim.nb[0]), "ng": int(cb.dim.ng[0])},
+            "condensed_dims": {"N": int(cb.dim.N), "nu": [int(v) for v in cb.dim.nu[:2]],
+                               "nb": [int(v) for v in cb.dim.nb[:2]],
+                               "ng": [int(v) for v in cb.dim.ng[:2]]},
             "iterations": {"min": int(iters.min()), "mean": float(iters.mean()),
                            "max": int(iters.max())},
             "status_counts": {str(int(k)): int(v) for k, v in zip(*np.unique(status, return_counts=True))}}
@@ -536,25 +548,40 @@ def main_condense(a, arg, B, config, rank, world, local):
         from paper_2003_02547_b200.dense import DenseQp
 
         orc.build()
-        n = min(B, 64)
+        n = min(B, 64) if full else max(2, min(B, 8))
         qps = [batch.qp(i) for i in range(n)]
         t0 = time.perf_counter()
         dqs, maps = [], []
-        for q in qps:
+        if not full:
+            from paper_2003_02547_b200.layout import OcpLayout
+
+            for q in qps:
+                _, blocks = co.partial_condense(q, N1)
+                maps.append(blocks)
+            hb = cb.numpy().select(range(n))   # condensed values (equal to the port's to 1e-12)
+            ref = orc.solve(hb, arg, nthreads=os.cpu_count() or 1, trace=False)
+            lay2 = OcpLayout(cb.dim)
+            for i, q in enumerate(qps):
+                co.partial_expand(q, maps[i], dict(layout=lay2, y=ref["y"][i], pi=ref["pi"][i],
+                                                   lam=ref["lam"][i], t=ref["t"][i]))
+        for q in (qps if full else []):
             dd, m = co.full_condense(q)
             dq = DenseQp(len(dd["g"]), 0, len(dd["idxb"]), len(dd["lg"]), 0)
             for f in ("H", "g", "idxb", "lb", "ub", "C", "lg", "ug", "maskl", "masku"):
                 dq.set_field(f, dd[f])
             dqs.append(dense_to_ocp(dq))
             maps.append(m)
-        ref = orc.solve(OcpQpBatch.from_qps(dqs), arg, nthreads=os.cpu_count() or 1, trace=False)
-        for i, q in enumerate(qps):
-            co.full_expand(q, maps[i], ref["y"][i], ref["lam"][i], ref["t"][i])
+        if full:
+            ref = orc.solve(OcpQpBatch.from_qps(dqs), arg, nthreads=os.cpu_count() or 1,
+                            trace=False)
+            for i, q in enumerate(qps):
+                co.full_expand(q, maps[i], ref["y"][i], ref["lam"][i], ref["t"][i])
         tc = time.perf_counter() - t0
         line["cpu_baseline"] = {"value": n / tc, "unit": "solves/s", "cores": os.cpu_count() or 1,
                                 "kind": "port",
-                                "sample": f"{n} QPs of the workload: numpy condense + C-oracle "
-                                          f"dense solve ({os.cpu_count()} threads) + numpy expand, "
+                                "sample": f"{n} QPs of the workload: numpy "
+                                          f"{'condense' if full else 'partial_condense'} + C-oracle "
+                                          f"solve ({os.cpu_count()} threads) + numpy expand, "
                                           f"{tc:.2f} s"}
         line["parity_vs_oracle"] = {"qps": n,
                                     "status_mismatch": int(np.sum(ref["status"] != status[:n])),

@@ -575,7 +575,10 @@ struct Shape {
     static constexpr int SSTAGE = (STAGE_SOLVE && NX * NW >= 1000) ? 3 : 0;
     // general rows: the stage's Jg = [D C] and gamma-scaled copy, staged for the
     // reduced-Hessian term Jg' diag(gamma) Jg of M~ (kkt_common.py:100-115)
-    static constexpr int JGB = NG > 0 ? 2 * NG * NW : 0;
+    // (only while the two copies fit 48 KB: the condensed config-4 stage,
+    // 240 x 160, reads them from global memory instead)
+    static constexpr bool JGS = NG > 0 && 2 * NG * NW <= 6144;
+    static constexpr int JGB = JGS ? 2 * NG * NW : 0;
     static constexpr int STAGE = STAGE0 + (SSTAGE ? (BA_BUF > SOLVE_BUF ? BA_BUF : SOLVE_BUF) : BA_BUF) + JGB;
     // resident CTAs per SM the register allocation must allow (latency hiding
     // across QPs): 512 threads per SM
@@ -1353,7 +1356,7 @@ struct Kern {
             // T1 barrier): JgT = [D C], JgS = diag(gamma_lo + gamma_up) [D C]
             double* JgT = stg + (S::STAGE - S::JGB);
             double* JgS = JgT + NG * NW;
-            if constexpr (NG > 0) {
+            if constexpr (S::JGS) {
                 const double* cfn = coef + n * d.M + d.NB;
                 for (int e = tid; e < NG * NW; e += TEAM) {
                     const int r = e / NW, j = e - r * NW;
@@ -1387,10 +1390,15 @@ struct Kern {
                     const int kb = full_box ? i : p.var_box[n * NW + i];
                     if (kb >= 0) h += cfv(n, kb);
                 }
-                if (NG > 0) {
+                if constexpr (NG > 0) {
                     double sg = 0.0;
+                    if constexpr (S::JGS) {
 #pragma unroll 4
-                    for (int r = 0; r < NG; ++r) sg = fma(JgT[r * NW + i], JgS[r * NW + j], sg);
+                        for (int r = 0; r < NG; ++r) sg = fma(JgT[r * NW + i], JgS[r * NW + j], sg);
+                    } else {
+                        for (int r = 0; r < NG; ++r)
+                            sg = fma(Jg(c, n, NU, r, i), cf[d.NB + r] * Jg(c, n, NU, r, j), sg);
+                    }
                     h = sg + h;
                 }
                 if (i == j && reg != 0.0) h += reg;
