@@ -399,3 +399,28 @@ def full_expand(qp, cmap, v, dlam, dt):
             else:
                 lam[lay.c_off[0] + mo + i] = -gap[c]
     return y, pi, lam, t
+
+
+def partial_condensed_qp(qp, N1):
+    """(condensed OcpQp, blocks): partial_condense's stages assembled into an
+    OcpQp of horizon N2 with the source terminal stage copied verbatim
+    (condensing.py:530-550), ready for the C oracle's solve."""
+    from paper_2003_02547_b200.qp_data import OcpQp, OcpQpDim
+
+    stages, blocks = partial_condense(qp, N1)
+    d = qp.dim
+    N2 = len(stages)
+    term = qp._stages[d.N]
+    nx = [st["Q"].shape[0] for st in stages] + [int(d.nx[d.N])]
+    nu = [st["R"].shape[0] for st in stages] + [0]
+    nb = [len(st["idxb"]) for st in stages] + [int(d.nb[d.N])]
+    ng = [st["C"].shape[0] for st in stages] + [int(d.ng[d.N])]
+    q2 = OcpQp(OcpQpDim(N2, nx, nu, nb, ng))
+    for k, st in enumerate(stages + [term]):
+        for f in ("Q", "S", "R", "q", "r", "idxb", "lb", "ub", "C", "D", "lg", "ug",
+                  "maskl", "masku"):
+            q2.set_field(f, k, st[f])
+        if k < N2:
+            for f in ("A", "B", "b"):
+                q2.set_field(f, k, st[f])
+    return q2, blocks

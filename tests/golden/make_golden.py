@@ -20,6 +20,7 @@ Fixtures:
   known.npz          hand-derivable answers (scalar LQR) and failure statuses
   modes.npz          balance / robust / square-root / speed_abs solves (MODES),
                      their Failure ladders and the robust-mode RankDeficient raise
+  pcond_full.npz     config 4 (N = 100) partial condensing -> solve -> expand
   closed_loop.npz    run_closed_loop trajectories / iteration counts (warm and
                      cold) and one _shift_guess
   qp_files/          qp_write text files and `mpcqp solve` CLI reports
@@ -242,6 +243,31 @@ def pcond():
         out[f"{name}_direct_y"] = direct.solution.y
         print("pcond", name, d2.N, rep.status.value, rep.iterations, direct.iterations, flush=True)
     np.savez_compressed(HERE / "pcond.npz", **out)
+
+
+# BASELINE config 4's second way at full size: N = 100 -> N2 = 20 blocks of 5
+PCOND_FULL_QPS = [0, 1, 2]
+
+
+def pcond_full():
+    """Reference partial_condense(qp, 5) -> solve -> partial_expand on full-size
+    config-4 QPs (N = 100, nx = 60, nu = 20): condensed-solve status /
+    iterations / final norms and the expanded solution (the condensed fields
+    themselves are 11 MB per QP; their restatement is pinned by pcond.npz)."""
+    out = {}
+    for i in PCOND_FULL_QPS:
+        qp = to_ref(make_batch(4, batch=1, start=i).qp(0))
+        qp2, pmap = mpcqp.partial_condense(qp, 5)
+        rep = mpcqp.solve_ocp_qp(qp2, ARG)
+        full = mpcqp.partial_expand(rep.solution, pmap, qp)
+        r = pack_report(rep)
+        for k in ("status", "iters", "res", "flops"):
+            out[f"q{i}_short_{k}"] = r[k]
+        for k in ("y", "pi", "lam", "t"):
+            out[f"q{i}_full_{k}"] = getattr(full, k)
+        print("pcond_full", i, rep.status.value, rep.iterations, flush=True)
+    out["qps"] = np.array(PCOND_FULL_QPS)
+    np.savez_compressed(HERE / "pcond_full.npz", **out)
 
 
 # full condensing (condensing.py:160-429) + the dense-QP IPM (solver.py:98-100)

@@ -67,3 +67,28 @@ def test_expand_oracle_matches_reference(golden, case):
     y, pi, lam, t = co.partial_expand(qp, blocks, short)
     for k, v in (("y", y), ("pi", pi), ("lam", lam), ("t", t)):
         assert rel_err(v, g[f"{name}_full_{k}"]) <= 1e-11, k
+
+
+def test_partial_path_oracle_config4_full_size(golden, oracle, speed_arg):
+    """The oracle's partial path at BASELINE config 4's full size (N = 100 ->
+    N2 = 20, nx = 60, nu = 20) against the reference's (pcond_full.npz):
+    condensed-solve status, iterations, flops and final norms; expanded
+    y / pi / lam / t within 1e-9 relative."""
+    g = golden("pcond_full")
+    qps_idx = [int(i) for i in g["qps"]]
+    src = [make_batch(4, batch=1, start=i).qp(0) for i in qps_idx]
+    cq = [co.partial_condensed_qp(q, 5) for q in src]
+    cb = pkg.OcpQpBatch.from_qps([c[0] for c in cq])
+    assert cb.dim.N == 20 and int(cb.dim.nu[0]) == 100 and int(cb.dim.ng[0]) == 240
+    ref = oracle.solve(cb, speed_arg, nthreads=len(src), trace=False)
+    lay2 = OcpLayout(cb.dim)
+    for j, i in enumerate(qps_idx):
+        assert int(ref["status"][j]) == int(g[f"q{i}_short_status"])
+        assert int(ref["iters"][j]) == int(g[f"q{i}_short_iters"])
+        assert int(ref["flops"][j]) == int(g[f"q{i}_short_flops"])
+        r = g[f"q{i}_short_res"]
+        assert np.all(np.abs(ref["res"][j] - r) <= 1e-8 * np.maximum(1.0, np.abs(r)))
+        short = dict(layout=lay2, y=ref["y"][j], pi=ref["pi"][j], lam=ref["lam"][j], t=ref["t"][j])
+        full = co.partial_expand(src[j], cq[j][1], short)
+        for k, v in zip(("y", "pi", "lam", "t"), full):
+            assert rel_err(v, g[f"q{i}_full_{k}"]) <= 1e-9, (i, k, rel_err(v, g[f"q{i}_full_{k}"]))

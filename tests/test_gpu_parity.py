@@ -4,8 +4,10 @@ and against the CPU oracle, plus size-independent properties at full size.
 Parity bar (BASELINE.json north star): same status and IPM iteration count as
 the reference, primal/dual solution within 1e-8 relative
 (||x - x_ref||_inf / max(1, ||x_ref||_inf)), identical nominal flop counts.
-Known-hard row: lam on config 3 may exceed 1e-8 between two
-valid implementations on ~1.5 % of QPs; those tests bound the fraction and the
+Known-hard row: lam on config 3 exceeds 1e-8 between any two
+valid implementations on ~2 % of QPs (the reference vs its C restatement, and
+the reference's classical vs square-root variants, included:
+profiles/r02_cfg3_lambda_threeway.json); those tests bound the fraction and the
 max instead of asserting every QP.
 """
 
@@ -47,7 +49,7 @@ def host(rep):
         "trace": rep.trace.cpu().numpy() if rep.trace is not None else None}
 
 
-def assert_parity(got, ref, lam_tol=1e-8, allow_lam_frac=0.0):
+def assert_parity(got, ref, lam_tol=1e-8, allow_lam_frac=0.0, tol=None):
     assert np.array_equal(got["status"], ref["status"])
     assert np.array_equal(got["iters"], ref["iters"])
     assert np.array_equal(got["flops"], ref["flops"])
@@ -57,6 +59,22 @@ def assert_parity(got, ref, lam_tol=1e-8, allow_lam_frac=0.0):
         assert max(errs) <= 1e-8, (k, max(errs))
     errs = np.array([rel_err(got["lam"][i], ref["lam"][i]) for i in range(n)])
     assert np.mean(errs > lam_tol) <= allow_lam_frac, (errs.max(), np.mean(errs > lam_tol))
+    assert_res_parity(got, ref, tol)
+
+
+def assert_res_parity(got, ref, tol=None):
+    """Final residual norms (res_g, res_b, res_d, res_m, mu): north star "final
+    residual norms within 1e-8"; at convergence they are rounding-level, so the
+    bar is SURVEY §8(d)'s |d| <= 1e-8 max(1, |ref|), and on converged QPs both
+    sides <= the exit tolerance."""
+    g, r = np.asarray(got["res"]), np.asarray(ref["res"])
+    fin = np.isfinite(r)
+    assert np.array_equal(fin, np.isfinite(g))
+    d = np.abs(g[fin] - r[fin]) / np.maximum(1.0, np.abs(r[fin]))
+    assert d.size == 0 or d.max() <= 1e-8, d.max()
+    if tol is not None:
+        ok = np.asarray(ref["status"]) == 0
+        assert np.all(g[ok] <= tol) and np.all(r[ok] <= tol)
 
 
 # ---------------------------------------------------------------- goldens
@@ -74,9 +92,10 @@ def test_gpu_matches_reference_goldens(cuda, speed_arg, golden, cfg, indices, N,
         assert int(got["status"][j]) == int(g[f"{p}_status"])
         assert int(got["iters"][j]) == int(g[f"{p}_iters"])
         assert int(got["flops"][j]) == int(g[f"{p}_flops"])
-        tol = 1e-8 if cfg != 3 else 1e-7
         for k in ("y", "pi", "lam", "t"):
-            assert rel_err(got[k][j], g[f"{p}_{k}"]) <= tol, (p, k)
+            assert rel_err(got[k][j], g[f"{p}_{k}"]) <= 1e-8, (p, k)
+        assert_res_parity({"res": got["res"][j:j + 1]},
+                          {"res": g[f"{p}_res"][None], "status": got["status"][j:j + 1]}, tol=1e-8)
         it = int(g[f"{p}_iters"])
         np.testing.assert_allclose(got["trace"][j, :it, :4], g[f"{p}_trace"][:, :4],
                                    rtol=1e-6, atol=1e-12)
@@ -178,14 +197,16 @@ def test_gpu_kernels_match_oracle(cuda, oracle, speed_arg, kind, cfg, n):
     batch = make_batch(cfg, batch=n)
     got = host(solve_ocp_qp_batch(batch, speed_arg))
     ref = oracle.solve(batch, speed_arg)
-    assert_parity(got, ref, allow_lam_frac=0.1 if cfg == 3 else 0.0)
+    assert_parity(got, ref, allow_lam_frac=0.09 if cfg == 3 else 0.0, tol=1e-8)
+    if cfg == 3:  # known-hard lam row: bounded (test_gpu_config3_lambda_distribution)
+        assert max(rel_err(got["lam"][i], ref["lam"][i]) for i in range(n)) <= 2e-6
 
 
 def test_gpu_config4_matches_oracle(cuda, oracle, speed_arg):
     batch = make_batch(4, batch=3)
     got = host(solve_ocp_qp_batch(batch, speed_arg))
     ref = oracle.solve(batch, speed_arg)
-    assert_parity(got, ref)
+    assert_parity(got, ref, tol=1e-8)
 
 
 def test_gpu_host_buffer_path_matches_device_path(cuda, speed_arg):
@@ -254,14 +275,26 @@ def test_gpu_full_batch_properties(cuda, oracle, speed_arg, cfg):
 
 
 def test_gpu_config3_lambda_distribution(cuda, oracle, speed_arg):
-    """Known-hard row: report the lam parity distribution on config 3."""
-    batch = make_batch(3, batch=48)
-    got = host(solve_ocp_qp_batch(batch, speed_arg))
-    ref = oracle.solve(batch, speed_arg)
-    assert np.array_equal(got["status"], ref["status"])
-    assert np.array_equal(got["iters"], ref["iters"])
-    lam_err = np.array([rel_err(got["lam"][i], ref["lam"][i]) for i in range(48)])
-    assert np.mean(lam_err <= 1e-8) >= 0.9 and lam_err.max() <= 1e-5
+    """Known-hard row: the lam parity distribution on config 3.
+
+    profiles/r02_cfg3_lambda_threeway.json ran the REAL reference on every
+    config-3 QP whose GPU-vs-oracle lam differs by > 1e-9 (28 of 512): the
+    reference and the C oracle differ by > 1e-8 on 11 of them (max 1.8e-7),
+    the reference's own classical and square-root variants on 14 (max 3.0e-6),
+    GPU vs reference on 11 (max 8.0e-7), while y, pi, t agree to <= 1.1e-9
+    everywhere -- lam on these QPs amplifies rounding-level differences of
+    any two implementations.  Measured GPU vs oracle on the full 512: 97.9 %
+    within 1e-8, max 6.2e-7; on the first 256: 97.3 %, max 6.2e-7.  The bar
+    below is that distribution with margin, plus exact status / iterations /
+    flops and 1e-8 on y, pi, t and the final norms."""
+    n = 256
+    batch = make_batch(3, batch=n)
+    got = host(solve_ocp_qp_batch(batch, speed_arg, trace=False))
+    ref = oracle.solve(batch, speed_arg, trace=False)
+    assert_parity(got, ref, allow_lam_frac=0.04, tol=1e-8)
+    lam_err = np.array([rel_err(got["lam"][i], ref["lam"][i]) for i in range(n)])
+    assert np.mean(lam_err <= 1e-8) >= 0.96 and lam_err.max() <= 2e-6, (
+        np.mean(lam_err <= 1e-8), lam_err.max())
 
 
 # ---------------------------------------------------------------- edge cases
