@@ -457,7 +457,9 @@ void place_fast(OcpPlan* P, long long budget_per_cta) {
     // to the L1 is 5-9 % faster; config 1 (45 % placed) is 10 % slower that way.
     const char* envp = getenv("OCPQP_PLACE");
     const bool force = envp && atoi(envp) == 1, never = envp && atoi(envp) == 0;
-    if (never || (!force && used * 5 < P->ws_slot * 8)) {
+    // BIG shapes stream their per-stage operands from global memory by TMA
+    // (the copy engine reads global memory only): no placement
+    if (never || fast_big(P->shape) || (!force && used * 5 < P->ws_slot * 8)) {
         P->smem_mask = 0;
         used = 0;
     }
@@ -801,7 +803,8 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
             k.ba = P->d_ba;
             k.ba_bs = shared ? 0 : per_qp;
             e = launch_pack_ba(k.f[OCPQP_F_A], k.bs[OCPQP_F_A], k.f[OCPQP_F_B], k.bs[OCPQP_F_B], P->B,
-                               P->L.N, nx, nu, P->d_ba, k.ba_bs, (cudaStream_t)stream);
+                               P->L.N, nx, nu, P->d_ba, k.ba_bs, (cudaStream_t)stream,
+                               fast_big(P->shape));
             if (e != cudaSuccess) return cuda_fail(e, "k_pack_ba launch");
         }
         e = launch_fast_solve(P->shape, k, sp, P->grid, P->smem_bytes, (cudaStream_t)stream);

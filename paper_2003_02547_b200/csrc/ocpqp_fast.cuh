@@ -225,25 +225,68 @@ struct MV {
 // Cholesky of an NN x NN (NN <= 32) matrix held row-wise by the lanes of one
 // warp (lane i: row[j] = A[i][j], j <= i).  Pivot test as LAPACK potrf: a
 // pivot that is not > 0 (or NaN) fails (linalg.py:81-118).
+// No early exit: a failed pivot is recorded and the (discarded) rest runs on,
+// so the warp never diverges around the shuffles (ptxas then needs no
+// divergent-shuffle fallback with the rows spilled to local memory).
 template <int NN>
 __device__ __forceinline__ bool warp_chol(double (&row)[NN], int lane, double& rin) {
+    bool ok = true;
 #pragma unroll
     for (int k = 0; k < NN; ++k) {
         const double piv = __shfl_sync(FULL, row[k], k);
-        if (!(piv > 0.0)) return false;
+        ok = ok && (piv > 0.0);
         const double inv = rsqrt(piv);  // 1 / L_kk, kept for the triangular solves
         const double dkk = piv * inv;   // L_kk (the solves only use 1 / L_kk)
         if (lane == k) rin = inv;
         const double lik = lane == k ? dkk : row[k] * inv;
         if (lane >= k) row[k] = lik;
+        // constant trip count (j > k tested inside): both loops unroll fully,
+        // so row[] stays in registers
 #pragma unroll
-        for (int j = k + 1; j < NN; ++j) {
-            const double ljk = __shfl_sync(FULL, lik, j);
-            if (lane >= j) row[j] = fma(-lik, ljk, row[j]);
+        for (int j = 1; j < NN; ++j) {
+            if (j > k) {
+                const double ljk = __shfl_sync(FULL, lik, j);
+                if (lane >= j) row[j] = fma(-lik, ljk, row[j]);
+            }
         }
     }
-    return true;
+    return ok;
 }
+
+// Same factorization with the pivot loop rolled: row[] is only indexed by
+// compile-time constants (the pivot's entry picked by a select chain), so it
+// stays in registers without the register pressure of a full unroll.  Same
+// operations and order as warp_chol.
+template <int NN>
+__device__ __forceinline__ bool warp_chol_rolled(double (&row)[NN], int lane, double& rin) {
+    bool ok = true;
+#pragma unroll 1
+    for (int k = 0; k < NN; ++k) {
+        double rk = 0.0;
+#pragma unroll
+        for (int m = 0; m < NN; ++m)
+            if (m == k) rk = row[m];
+        const double piv = __shfl_sync(FULL, rk, k);
+        ok = ok && (piv > 0.0);
+        const double inv = rsqrt(piv);
+        const double dkk = piv * inv;
+        if (lane == k) rin = inv;
+        const double lik = lane == k ? dkk : rk * inv;
+#pragma unroll
+        for (int m = 0; m < NN; ++m)
+            if (m == k && lane >= k) row[m] = lik;
+#pragma unroll
+        for (int m = 1; m < NN; ++m) {
+            const double ljk = __shfl_sync(FULL, lik, m);
+            if (m > k && lane >= m) row[m] = fma(-lik, ljk, row[m]);
+        }
+    }
+    return ok;
+}
+
+// warp index known to the compiler as warp-uniform (a shuffle from lane 0):
+// role branches on it keep their warps converged around shuffles
+__device__ __forceinline__ int warp_id_uniform() { return __shfl_sync(FULL, (int)(threadIdx.x >> 5), 0); }
 
 // Register Cholesky of the NN x NN leading block of G (row stride ld), computed
 // redundantly by every thread that needs it.  Left-looking; pivot test as
@@ -333,6 +376,7 @@ struct FCtx {
     int ba_ss;           // its per-stage stride (0: identical in every stage)
     double* w[WS_EXT0];  // base workspace only (speed mode)
     double red[56];  // team reductions (tred_res: 6 x warps)
+    unsigned long long mbar[4];   // TMA completion barriers (BIG shapes)
     int flag;
     int q;
     double n_act;
@@ -360,6 +404,65 @@ template <int NPEND>
 __device__ __forceinline__ void cpa_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory");
 }
+
+// ---- TMA bulk copies (cp.async.bulk) with mbarrier completion ---------------
+// One elected thread issues 1-D bulk copies global -> shared memory; the team
+// waits on the mbarrier's phase parity.  A shared-memory region written by the
+// copy engine after generic-proxy use needs fence.proxy.async first.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// bulk prefetch of a contiguous block into L2 (no shared memory, no completion)
+__device__ __forceinline__ void l2_prefetch_bulk(const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// Per-thread view of the CTA's TMA barriers: every thread waits on every
+// completion in the same order, so each tracks the phase parity privately.
+// NB barriers; `busy` marks a copy issued and not yet waited for.
+struct Tma {
+    unsigned ph = 0, busy = 0;
+    __device__ __forceinline__ void issue(unsigned long long* bars, int b) { busy |= 1u << b; }
+    __device__ __forceinline__ void wait(unsigned long long* bars, int b) {
+        if (!((busy >> b) & 1u)) return;
+        mbar_wait(bars + b, (ph >> b) & 1u);
+        ph ^= 1u << b;
+        busy &= ~(1u << b);
+    }
+    __device__ __forceinline__ void drain(unsigned long long* bars) {
+        for (int b = 0; b < 8; ++b) wait(bars, b);
+    }
+};
 
 // ---- register-tiled team GEMM ---------------------------------------------
 // C(i, j) = sum_k a(i, k) b(k, j), i < M, j < N, k < K (k ascending, one fma
@@ -579,7 +682,25 @@ struct Shape {
     // 240 x 160, reads them from global memory instead)
     static constexpr bool JGS = NG > 0 && 2 * NG * NW <= 6144;
     static constexpr int JGB = JGS ? 2 * NG * NW : 0;
-    static constexpr int STAGE = STAGE0 + (SSTAGE ? (BA_BUF > SOLVE_BUF ? BA_BUF : SOLVE_BUF) : BA_BUF) + JGB;
+    // BIG: large box-only stages (config 4: 60 x 20) -- the factor keeps its
+    // stage-GEMM accumulators in registers (DMMA fragments), the stage's
+    // [B A]' arrives by TMA one stage ahead, and the solve sweeps stream their
+    // per-stage operands (P, [B A]', K, L, vectors) through shared memory by
+    // TMA (factor_big / sweeps_big).  Shared tile: P | T1' | [B A]' | vec,
+    // 108.8 KB, two CTAs per SM.
+#ifndef OCPQP_BIG
+#define OCPQP_BIG 1
+#endif
+    static constexpr bool BIG = OCPQP_BIG != 0 && NG_ == 0 && NX_ >= 48 && TEAM_ == 256 &&
+                                NU_ <= 32 && NX_ * 4 <= TEAM_ && NU_ % 4 == 0;
+    // packed [B A] of a stage stored transposed ([B A]' : NW x NX, row j = column j)
+    static constexpr bool BAT = BIG;
+    static constexpr int STAGE_STD = STAGE0 + (SSTAGE ? (BA_BUF > SOLVE_BUF ? BA_BUF : SOLVE_BUF) : BA_BUF) + JGB;
+    // BIG vector scratch: win, e, pvs, x, u, x', r_b (sweeps_big)
+    static constexpr int VECB = NW + 6 * NX + NU + 16 > 32 + NU * NU ? NW + 6 * NX + NU + 16 : 32 + NU * NU;
+    static constexpr int STAGE = BIG ? NX * NX + 2 * NW * NX + VECB : STAGE_STD;
+    // offset of the vector scratch (win, e, pvs, x, u) in the stage tile
+    static constexpr int VOFF = BIG ? NX * NX + 2 * NW * NX : NX * NX + T1N + NU * NW;
     // resident CTAs per SM the register allocation must allow (latency hiding
     // across QPs): 512 threads per SM
     static constexpr int MINB = TEAM >= OCPQP_MINB_THREADS ? 1 : OCPQP_MINB_THREADS / TEAM;
@@ -625,6 +746,9 @@ struct Kern {
     }
     // packed [B A] of stage n (kkt_ocp.py:177): row k = (B_k., A_k.)
     __device__ static __forceinline__ const double* BAp(const FCtx& c, int n) { return c.ba + n * c.ba_ss; }
+    // element (k, j) of [B A] sits at k * BK + j * BJ (row-major, or transposed
+    // for the BIG shapes, whose stage GEMMs and TMA staging want [B A]')
+    static constexpr int BK = S::BAT ? 1 : NW, BJ = S::BAT ? NX : 1;
     __device__ static __forceinline__ const double* Bm(const FCtx& c, int n) { return c.f[OCPQP_F_B] + n * c.ss[OCPQP_F_B]; }
     __device__ static __forceinline__ const double* bv(const FCtx& c, int n) { return c.f[OCPQP_F_b] + n * c.ss[OCPQP_F_b]; }
     __device__ static __forceinline__ const double* Q(const FCtx& c, int n) { return c.f[OCPQP_F_Q] + n * c.ss[OCPQP_F_Q]; }
@@ -767,8 +891,8 @@ struct Kern {
         }
         AbsMax ag, ab, ad, am;
         double musum = 0.0;
-        OCPQP_PASS_UNROLL
-        for (int j = threadIdx.x; j < d.nv; j += TEAM) {
+        // r_g of variable j (stage-major numbering)
+        auto rg_item = [&](int j) {
             int n = j / NW;
             if (n > d.N) n = d.N;
             const int jj = j - n * NW;
@@ -799,9 +923,9 @@ struct Kern {
                 double a = 0.0;
                 const double* pn = pi + n * NX;
                 {
-                    const double* BAc = BAp(c, n) + jj;   // column jj of [B A]
+                    const double* BAc = BAp(c, n) + jj * BJ;   // column jj of [B A]
 #pragma unroll 8
-                    for (int k = 0; k < NX; ++k) a = fma(BAc[k * NW], pn[k], a);
+                    for (int k = 0; k < NX; ++k) a = fma(BAc[k * BK], pn[k], a);
                 }
                 atp -= a;
                 r -= atp;
@@ -829,24 +953,129 @@ struct Kern {
             }
             r_g[j] = r;
             ag.add(r);
-        }
-        OCPQP_PASS_UNROLL
-        for (int e = threadIdx.x; e < d.ne; e += TEAM) {
+        };
+        // r_b of dynamics row e
+        auto rb_item = [&](int e) {
             const int n = e / NX;
             const int i = e - n * NX;
             const double* u = y + n * NW;
             const double* x = u + NU;
             const double xn = y[(n + 1) * NW + (n + 1 < d.N ? NU : 0) + i];
-            const double* Br = BAp(c, n) + i * NW;
-            const double* Ar = Br + NU;
+            const double* Br = BAp(c, n) + i * BK;
+            const double* Ar = Br + NU * BJ;
             double ax = 0.0, bu = 0.0;
 #pragma unroll 8
-            for (int k = 0; k < NX; ++k) ax = fma(Ar[k], x[k], ax);
+            for (int k = 0; k < NX; ++k) ax = fma(Ar[k * BJ], x[k], ax);
 #pragma unroll
-            for (int k = 0; k < NU; ++k) bu = fma(Br[k], u[k], bu);
+            for (int k = 0; k < NU; ++k) bu = fma(Br[k * BJ], u[k], bu);
             const double r = -((xn - ax) - bu) + bv(c, n)[i];
             r_b[e] = r;
             ab.add(r);
+        };
+        if constexpr (S::BIG) {
+            // one warp per stage, 8-lane groups per row: the lanes of a group
+            // read consecutive elements of the row (coalesced loads instead of
+            // one row per thread), butterfly-reduced; each warp bulk-prefetches
+            // its next stage's data into L2.  Rows per stage: the NW r_g rows,
+            // then the NX r_b rows (terminal stage: its NX r_g rows).
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+            const int gl = lane & 7, rl = lane >> 3;
+            constexpr int NWARP = TEAM / 32;
+            auto pf_stage = [&](int n) {
+                if (n < d.N) {
+                    l2_prefetch_bulk(BAp(c, n), BAB);
+                    l2_prefetch_bulk(Sm(c, n), NU * NX * 8);
+                    l2_prefetch_bulk(R(c, n), NU * NU * 8);
+                }
+                l2_prefetch_bulk(Q(c, n), NX * NX * 8);
+            };
+            if (lane == 0 && warp <= d.N) pf_stage(warp);
+            for (int n = warp; n <= d.N; n += NWARP) {
+                if (lane == 0 && n + NWARP <= d.N) pf_stage(n + NWARP);
+                const bool term = n == d.N;
+                const int nrow = term ? NX : NW + NX;
+                const double* w = y + n * NW;
+                const double* pn = pi + n * NX;
+                const double* Qs = Q(c, n);
+                const double* Ss = Sm(c, n);
+                const double* Rs = R(c, n);
+                const double* BAs = BAp(c, n);
+                // lane gl of a group covers k = gl, gl + 8, ... (compile-time
+                // trip counts: the loads of a row issue together)
+#define OCPQP_G8(KN, BODY)                                        \
+    _Pragma("unroll") for (int k8 = 0; k8 < ((KN) + 7) / 8; ++k8) { \
+        const int k = gl + 8 * k8;                                \
+        if (k < (KN)) { BODY; }                                   \
+    }
+                for (int r0 = 0; r0 < nrow; r0 += 4) {
+                    const int r = r0 + rl;
+                    double h = 0.0, a = 0.0;
+                    if (r < nrow) {
+                        if (term) {
+                            const double* Qr = Qs + r * NX;
+                            OCPQP_G8(NX, h = fma(Qr[k], w[k], h))
+                        } else if (r < NW) {
+                            if (r < NU) {
+                                const double* Rr = Rs + r * NU;
+                                const double* Sr = Ss + r * NX;
+                                OCPQP_G8(NU, h = fma(Rr[k], w[k], h))
+                                OCPQP_G8(NX, h = fma(Sr[k], w[NU + k], h))
+                            } else {
+                                const int jx = r - NU;
+                                const double* Qr = Qs + jx * NX;
+                                OCPQP_G8(NU, h = fma(Ss[k * NX + jx], w[k], h))
+                                OCPQP_G8(NX, h = fma(Qr[k], w[NU + k], h))
+                            }
+                            const double* BAc = BAs + r * BJ;   // column r of [B A]
+                            OCPQP_G8(NX, a = fma(BAc[k * BK], pn[k], a))
+                        } else {
+                            const double* BAr = BAs + (r - NW) * BK;   // row of [B A]
+                            OCPQP_G8(NW, h = fma(BAr[k * BJ], w[k], h))
+                        }
+                    }
+#undef OCPQP_G8
+#pragma unroll
+                    for (int o = 4; o > 0; o >>= 1) {
+                        h += __shfl_xor_sync(FULL, h, o);
+                        a += __shfl_xor_sync(FULL, a, o);
+                    }
+                    if (r < nrow && gl == 0) {
+                        if (term || r < NW) {
+                            const int j = n * NW + r;
+                            double rr;
+                            if (term) {
+                                rr = h + qv(c, n)[r];
+                                rr -= d.N > 0 ? pi[(n - 1) * NX + r] : 0.0;
+                            } else {
+                                rr = h + (r < NU ? rv(c, n)[r] : qv(c, n)[r - NU]);
+                                double atp = (r >= NU && n > 0) ? pi[(n - 1) * NX + (r - NU)] : 0.0;
+                                atp -= a;
+                                rr -= atp;
+                            }
+                            int kup;
+                            const int klo = box_slot(d, p.var_box, j, n, kup);
+                            if (klo >= 0) {
+                                const double ll = !isnan(act[klo]) ? lam[klo] : 0.0;
+                                const double lu = !isnan(act[kup]) ? lam[kup] : 0.0;
+                                rr -= ll - lu;
+                            }
+                            r_g[j] = rr;
+                            ag.add(rr);
+                        } else {
+                            const int i = r - NW;
+                            const double xn = y[(n + 1) * NW + (n + 1 < d.N ? NU : 0) + i];
+                            const double rr = -(xn - h) + bv(c, n)[i];
+                            r_b[n * NX + i] = rr;
+                            ab.add(rr);
+                        }
+                    }
+                }
+            }
+        } else {
+            OCPQP_PASS_UNROLL
+            for (int j = threadIdx.x; j < d.nv; j += TEAM) rg_item(j);
+            OCPQP_PASS_UNROLL
+            for (int e = threadIdx.x; e < d.ne; e += TEAM) rb_item(e);
         }
         OCPQP_PASS_UNROLL
         for (int k = threadIdx.x; k < d.nc; k += TEAM) {
@@ -902,7 +1131,7 @@ struct Kern {
         struct { const long long* dbg; } p{dbg};  // OCPQP_TICK reads p.dbg
         const int tid = threadIdx.x;
         if constexpr (NU <= 32) {
-            if (!chol_done && tid < 32) warp0_chol(c, Gu, Ln, Rinv_n, rinv);
+            if (!chol_done && warp_id_uniform() == 0) warp0_chol(c, Gu, Ln, Rinv_n, rinv);
             bar<TEAM>();
             if (!c.flag) return false;
         } else {
@@ -1085,7 +1314,7 @@ struct Kern {
             const double* Qn = Q(c, n);
             const double* cf = coef + n * d.M;
             const int ng = d.NGN;
-            if (tid < 32) {
+            if (warp_id_uniform() == 0) {
                 const int i = tid;
                 double row[NX];
 #pragma unroll
@@ -1125,7 +1354,7 @@ struct Kern {
                 // W = L_{n+1}' [B A] (all threads)
                 stage_gemm<S::DMMA, NX, NW, NX, TEAM>(
                     [&](int i, int k) { return k >= i ? Lc[k * NX + i] : 0.0; },
-                    [&](int k, int j) { return BAn[k * NW + j]; }, NoPre(),
+                    [&](int k, int j) { return BAn[k * BK + j * BJ]; }, NoPre(),
                     [&](int i, int j, double v, double) { W[i * NW + j] = v; });
                 flops += 2ll * NX * NW * NX + 2ll * NW * NW * NX;
                 bar<TEAM>();
@@ -1134,7 +1363,7 @@ struct Kern {
                 const double* Sn = Sm(c, n);
                 const double* cf = coef + n * d.M;
                 const bool full_box = d.NB == NW;
-                if (tid < 32) {
+                if (warp_id_uniform() == 0) {
                     // lane i: row i of G = W'W + M~ (j <= i), then the warp Cholesky
                     const int i = tid;
                     double row[NW];
@@ -1343,14 +1572,14 @@ struct Kern {
             else if constexpr (S::STAGE_BA) {
                 TEAM_FOR(e, NX * NW)
                     const int k = e / NW, j = e - k * NW;
-                    BAs[e] = BAn[k * NW + j];
+                    BAs[e] = BAn[k * BK + j * BJ];
                 TEAM_END
                 bar<TEAM>();
             }
             auto BA = [&](int k, int j) -> double {
                 if (fpf) return H[k * NW + j];
                 if constexpr (S::STAGE_BA) return BAs[k * NW + j];
-                else return BAn[k * NW + j];
+                else return BAn[k * BK + j * BJ];
             };
             // general rows of the stage into shared memory (read by M~ after the
             // T1 barrier): JgT = [D C], JgS = diag(gamma_lo + gamma_up) [D C]
@@ -1416,7 +1645,7 @@ struct Kern {
             constexpr bool OVL = !S::SMALL && TEAM >= 64 && NU <= 32;
             if constexpr (OVL) {
                 bar<TEAM>();
-                if (tid < 32)
+                if (warp_id_uniform() == 0)
                     warp0_chol(c, Gu, Ln, Rinv_n, vec);
                 else
                     stage_gemm<S::DMMA, NX, NX, NX, TEAM - 32, 32>(
@@ -1501,7 +1730,7 @@ struct Kern {
         double* LP0 = wsb<WS_LP0>(c, p);
         flops += (long long)NX * NX * NX / 3;
         if constexpr (NX <= 32) {
-            if (tid < 32) {
+            if (warp_id_uniform() == 0) {
                 double row[NX];
                 double rin = 0.0;
 #pragma unroll
@@ -1521,6 +1750,400 @@ struct Kern {
             bar<TEAM>();
             if (!team_chol<TEAM>(LP0, NX, &c.flag, wsb<WS_RINV>(c, p) + N * NU)) return 0;
         }
+        return -1;
+    }
+
+    // ================= BIG shapes (S::BIG, config 4: 60 x 20, box rows) =================
+    // Row stride of the stage's G_u rows in shared memory: NW + 4 keeps the
+    // G_ux' fragment loads of the P update free of bank conflicts.
+    static constexpr int GLD = NW + 4;
+    static constexpr unsigned BAB = NW * NX * 8;   // bytes of one stage's [B A]'
+
+    // thread 0: TMA of stage n's [B A]' into dst, completion on barrier b
+    __device__ static __forceinline__ void tma_ba(FCtx& c, Tma& tm, double* dst, int n, int b) {
+        if (threadIdx.x == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(&c.mbar[b], BAB);
+            tma_load_1d(dst, BAp(c, n), BAB, &c.mbar[b]);
+        }
+        tm.issue(c.mbar, b);
+    }
+
+    // L_uu = chol(G_uu) in one warp, rows in registers (warp_chol_rolled;
+    // linalg.py:81-118 pivot test); L to shared memory (Ls) and the factor
+    // store, 1 / L_kk to rinv and the store; c.flag = success
+    __device__ __forceinline__ static void chol_big(FCtx& c, const double* Gu, double* Ls, double* Ln,
+                                                    double* Rinv_n, double* rinv) {
+        const int lane = threadIdx.x & 31;
+        double row[NU];
+        double rin = 0.0;
+#pragma unroll
+        for (int j = 0; j < NU; ++j) row[j] = (lane < NU && j <= lane) ? Gu[lane * GLD + j] : 0.0;
+        const bool ok = warp_chol_rolled<NU>(row, lane, rin);
+        if (lane == 0) c.flag = ok;
+        if (ok && lane < NU) {
+#pragma unroll
+            for (int j = 0; j < NU; ++j) {
+                const double v = j <= lane ? row[j] : 0.0;
+                Ls[lane * NU + j] = v;
+                Ln[lane * NU + j] = v;
+            }
+            rinv[lane] = rin;
+            Rinv_n[lane] = rin;
+        }
+    }
+
+    // K = -L_uu'^{-1} L_uu^{-1} G_ux (kkt_ocp.py:237-243): column j by the lane
+    // quad 4j..4j+3 (lane q owns rows q, q + 4, ...), one quad broadcast per
+    // pivot; to shared memory (Ks) and the factor store
+    __device__ __forceinline__ static void kcols_big(const double* Gu, const double* Ls, const double* rinv,
+                                                   double* Ks, double* Kn) {
+        constexpr int RW = (NU + 3) / 4;
+        const int tid = threadIdx.x;
+        const int lane = tid & 31;
+        const int j = tid >> 2, q = tid & 3;
+        const unsigned qmask = 0xFu << (lane & ~3);
+        const int qbase = lane & ~3;
+        if (j >= NX) return;
+        double z[RW];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) {
+            const int k = q + 4 * r;
+            z[r] = k < NU ? Gu[k * GLD + NU + j] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < NU; ++i) {
+            const int ri = i >> 2, oi = i & 3;
+            if (q == oi) z[ri] = z[ri] * rinv[i];
+            const double zi = __shfl_sync(qmask, z[ri], qbase | oi);
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                const int k = q + 4 * r;
+                if (k > i && k < NU) z[r] = fma(-Ls[k * NU + i], zi, z[r]);
+            }
+        }
+#pragma unroll
+        for (int i = NU - 1; i >= 0; --i) {
+            const int ri = i >> 2, oi = i & 3;
+            if (q == oi) z[ri] = z[ri] * rinv[i];
+            const double zi = __shfl_sync(qmask, z[ri], qbase | oi);
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                const int k = q + 4 * r;
+                if (k < i) z[r] = fma(-Ls[i * NU + k], zi, z[r]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RW; ++r) {
+            const int k = q + 4 * r;
+            if (k < NU) {
+                Kn[k * NX + j] = -z[r];
+                Ks[k * NX + j] = -z[r];
+            }
+        }
+    }
+
+    // Classical Riccati factor of a BIG shape (kkt_ocp.py:142-251).  Per stage,
+    // on FP64 tensor cores (mma.sync m8n8k4 f64) with register accumulators:
+    //   T1 = P_{n+1} [B A]   8 warp tasks of 2 x 5 8x8 tiles -> T1' (shared)
+    //   G  = [B A]' T1 + M~  warp tasks of 2 x 2 tiles over the G_u rows and
+    //                        the G_xx block, held in registers until every
+    //                        warp is done with T1' and [B A]'; then G_u -> Gu,
+    //                        G_xx -> Pc (P_{n+1} is dead by then)
+    //   L_uu, K              chol_k_big
+    //   P  = G_xx + G_ux' K  in place in Pc, then 0.5 (P + P') (kkt_ocp.py:244, 251)
+    // [B A]'_{n-1} is fetched by TMA as soon as G_n has consumed [B A]'_n, so
+    // the copy overlaps the Cholesky, K and P phases; M~'s Q, S, R of the next
+    // stage are bulk-prefetched into L2.  Fragment layouts (PTX m8n8k4 .f64):
+    // A row = lane/4, col = lane%4; B row = lane%4, col = lane/4; D row =
+    // lane/4, cols 2 (lane%4) + {0, 1}.  Row strides NX = 60 and GLD = 84 are
+    // 12 / 4 mod 16 doubles: the fragment loads are free of bank conflicts.
+    __device__ __noinline__ static int factor_big(FCtx& c, const RD& d, const KParams& p, double* stg,
+                                     const double* lam, const double* t, double reg, long long& flops,
+                                     Tma& tm) {
+        static_assert(NX % 4 == 0 && NU % 4 == 0 && NW % 16 == 0 && NX <= 64 && TEAM == 256,
+                      "factor_big task tiling");
+        const int tid = threadIdx.x;
+        const int lane = tid & 31, warp = tid >> 5, gr = lane >> 2, tg = lane & 3;
+        const double* act = c.w[WS_DVEC];  // NaN = inactive
+        double* gam = c.w[WS_GAM];
+        double* Pst = wsb<WS_P>(c, p);
+        double* Kst = wsb<WS_K>(c, p);
+        double* Lst = wsb<WS_L>(c, p);
+        double* tinv = c.w[WS_TINV];
+        double* Pc = stg;                 // NX x NX: P_{n+1}, then G_xx, then P_n
+        double* T1t = Pc + NX * NX;       // NW x NX: T1'; after G: Gu | K | L
+        double* BAt = T1t + NW * NX;      // NW x NX: [B A]' of the stage (TMA)
+        double* vec = stg + S::VOFF;
+        int bad = 0;
+        OCPQP_PASS_UNROLL
+        for (int k = tid; k < d.nc; k += TEAM) {
+            double g = 0.0, ti = 0.0;
+            if (!isnan(act[k])) {
+                if (lam[k] <= 0.0 || t[k] <= 0.0) bad = 1;
+                ti = 1.0 / t[k];
+                g = lam[k] * ti;
+            }
+            gam[k] = g;
+            tinv[k] = ti;
+        }
+        if (any_of<TEAM>(bad)) return -2;
+        auto cfv = [&](int n, int kb) -> double {
+            const int k = n * 2 * d.M + kb;
+            return gam[k] + gam[k + (n < d.N ? d.M : d.MN)];
+        };
+        const int N = d.N;
+        if (N > 0) tma_ba(c, tm, BAt, N - 1, 0);
+        // ---- terminal stage: P_N = sym(M~_N) ----
+        {
+            const int n = N;
+            const double* Qn = Q(c, n);
+            for (int idx = tid; idx < NX * NX; idx += TEAM) {
+                const int i = idx / NX, j = idx - i * NX;
+                double h = 0.5 * (Qn[i * NX + j] + Qn[j * NX + i]);
+                if (i == j) {
+                    const int kb = p.var_box[n * NW + i];
+                    if (kb >= 0) h += cfv(n, kb);
+                }
+                if (i == j && reg != 0.0) h += reg;
+                T1t[idx] = h;
+            }
+            bar<TEAM>();
+            double* Pn = Pst + n * S::PST;
+            TEAM_FOR(idx, NX * NX)
+                const int i = idx / NX, j = idx - i * NX;
+                const double v = 0.5 * (T1t[idx] + T1t[j * NX + i]);
+                Pc[idx] = v;
+                if (!S::PPACK) Pn[idx] = v;
+                else if (j <= i) Pn[i * (i + 1) / 2 + j] = v;
+            TEAM_END
+            bar<TEAM>();
+        }
+        for (int n = N - 1; n >= 0; --n) {
+            OCPQP_TICK(c, DBG_F_P);
+            if (tid == 0 && n > 0) {   // M~ data of the next stage, the [B A]' after it -> L2
+                l2_prefetch_bulk(Q(c, n - 1), NX * NX * 8);
+                l2_prefetch_bulk(Sm(c, n - 1), NU * NX * 8);
+                l2_prefetch_bulk(R(c, n - 1), NU * NU * 8);
+                if (n > 1) l2_prefetch_bulk(BAp(c, n - 2), BAB);
+            }
+            tm.wait(c.mbar, 0);
+            // ---- T1 = P_{n+1} [B A] (kkt_ocp.py:232), stored transposed ----
+            {
+                const int rp = warp >> 1, ch = warp & 1;
+                constexpr int CB = NW / 16;   // column blocks per half
+                double acc[2][CB][2];
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+#pragma unroll
+                    for (int q = 0; q < CB; ++q) acc[r][q][0] = acc[r][q][1] = 0.0;
+#pragma unroll 3
+                for (int ks = 0; ks < NX / 4; ++ks) {
+                    const int k = 4 * ks + tg;
+                    double a[2], b[CB];
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        const int i = 16 * rp + 8 * r + gr;
+                        a[r] = i < NX ? Pc[i * NX + k] : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < CB; ++q) b[q] = BAt[(CB * 8 * ch + 8 * q + gr) * NX + k];
+#pragma unroll
+                    for (int r = 0; r < 2; ++r)
+#pragma unroll
+                        for (int q = 0; q < CB; ++q) dmma_acc(acc[r][q][0], acc[r][q][1], a[r], b[q]);
+                }
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int i = 16 * rp + 8 * r + gr;
+                    if (i < NX) {
+#pragma unroll
+                        for (int q = 0; q < CB; ++q) {
+                            const int j = CB * 8 * ch + 8 * q + 2 * tg;
+                            T1t[j * NX + i] = acc[r][q][0];
+                            T1t[(j + 1) * NX + i] = acc[r][q][1];
+                        }
+                    }
+                }
+            }
+            bar<TEAM>();
+            OCPQP_TICK(c, DBG_F_T1);
+            // ---- G = [B A]' T1 + M~ (kkt_ocp.py:233, 70-80; kkt_common.py:100-115) ----
+            // warp tasks of 2 x 2 tiles over row pairs rp x column pairs cp: the
+            // u rows need every column, the x rows only the x columns; held in
+            // registers until every warp is done with T1' and [B A]'
+            constexpr int NRP = NW / 16, NUR = (NU - 1) / 16 + 1, CP0 = NU / 16;
+            constexpr int NGT = NUR * NRP + (NRP - NUR) * (NRP - CP0);
+            constexpr int GROUNDS = (NGT + 7) / 8;
+            constexpr int PT = (NX + 15) / 16;
+            double* Gu = T1t;                 // NU x GLD (after G)
+            double* Ks = Gu + NU * GLD;       // NU x NX
+            double* Ls = Ks + NU * NX;        // NU x NU
+            const double* Qn = Q(c, n);
+            const double* Rn = R(c, n);
+            const double* Sn = Sm(c, n);
+            const bool full_box = d.NB == NW;
+            auto Mt = [&](int i, int j) -> double {
+                double mij, mji;
+                if (i < NU && j < NU) { mij = Rn[i * NU + j]; mji = Rn[j * NU + i]; }
+                else if (i < NU) { mij = Sn[i * NX + (j - NU)]; mji = mij; }
+                else if (j < NU) { mij = Sn[j * NX + (i - NU)]; mji = mij; }
+                else { mij = Qn[(i - NU) * NX + (j - NU)]; mji = Qn[(j - NU) * NX + (i - NU)]; }
+                double h = 0.5 * (mij + mji);
+                if (i == j) {
+                    const int kb = full_box ? i : p.var_box[n * NW + i];
+                    if (kb >= 0) h += cfv(n, kb);
+                    if (reg != 0.0) h += reg;
+                }
+                return h;
+            };
+            auto gtask = [&](int task, int& rp, int& cp) {
+                if (task < NUR * NRP) { rp = task / NRP; cp = task % NRP; }
+                else { const int u = task - NUR * NRP; rp = NUR + u / (NRP - CP0); cp = CP0 + u % (NRP - CP0); }
+            };
+            double g[GROUNDS][2][2][2];
+            // accumulators start as M~: every round's loads issued before the first k loop
+#pragma unroll
+            for (int r = 0; r < GROUNDS; ++r) {
+                const int task = warp + 8 * r;
+                if (task < NGT) {
+                    int rp, cp;
+                    gtask(task, rp, cp);
+#pragma unroll
+                    for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+                        for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e)
+                                g[r][ti][tj][e] = Mt(16 * rp + 8 * ti + gr, 16 * cp + 8 * tj + 2 * tg + e);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < GROUNDS; ++r) {
+                const int task = warp + 8 * r;
+                if (task < NGT) {
+                    int rp, cp;
+                    gtask(task, rp, cp);
+#pragma unroll 3
+                    for (int ks = 0; ks < NX / 4; ++ks) {
+                        const int k = 4 * ks + tg;
+                        double a[2], b[2];
+#pragma unroll
+                        for (int ti = 0; ti < 2; ++ti) a[ti] = BAt[(16 * rp + 8 * ti + gr) * NX + k];
+#pragma unroll
+                        for (int tj = 0; tj < 2; ++tj) b[tj] = T1t[(16 * cp + 8 * tj + gr) * NX + k];
+#pragma unroll
+                        for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+                            for (int tj = 0; tj < 2; ++tj) dmma_acc(g[r][ti][tj][0], g[r][ti][tj][1], a[ti], b[tj]);
+                    }
+                }
+            }
+            bar<TEAM>();   // every warp is done with T1' and [B A]'
+            if (n > 0) tma_ba(c, tm, BAt, n - 1, 0);
+#pragma unroll
+            for (int r = 0; r < GROUNDS; ++r) {
+                const int task = warp + 8 * r;
+                if (task < NGT) {
+                    int rp, cp;
+                    gtask(task, rp, cp);
+#pragma unroll
+                    for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+                        for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int i = 16 * rp + 8 * ti + gr, j = 16 * cp + 8 * tj + 2 * tg + e;
+                                const double v = g[r][ti][tj][e];
+                                if (i < NU) Gu[i * GLD + j] = v;
+                                else if (j >= NU) Pc[(i - NU) * NX + (j - NU)] = v;
+                            }
+                }
+            }
+            flops += 2ll * NX * NW * NX + 2ll * NW * NW * NX;
+            bar<TEAM>();
+            OCPQP_TICK(c, DBG_F_G);
+            // ---- L_uu = chol(G_uu), K (kkt_ocp.py:237-243) ----
+            double* Ln = Lst + n * NU * NU;
+            double* Rinv_n = wsb<WS_RINV>(c, p) + n * NU;
+            double* Kn = Kst + n * NU * NX;
+            flops += (long long)NU * NU * NU / 3;
+            if (warp_id_uniform() == 0) chol_big(c, Gu, Ls, Ln, Rinv_n, vec);
+            bar<TEAM>();
+            OCPQP_TICK(c, DBG_F_CHOL);
+            if (!c.flag) {
+                tm.drain(c.mbar);
+                return n;
+            }
+            kcols_big(Gu, Ls, vec, Ks, Kn);
+            flops += 2ll * NU * NU * NX;
+            bar<TEAM>();
+            OCPQP_TICK(c, DBG_F_K);
+            // ---- P = G_xx + G_ux' K (kkt_ocp.py:244), in place ----
+            for (int task = warp; task < PT * PT; task += 8) {
+                const int rp = task / PT, cp = task % PT;
+                double acc[2][2][2];
+#pragma unroll
+                for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+                    for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int i = 16 * rp + 8 * ti + gr, j = 16 * cp + 8 * tj + 2 * tg + e;
+                            acc[ti][tj][e] = (i < NX && j < NX) ? Pc[i * NX + j] : 0.0;
+                        }
+#pragma unroll
+                for (int ks = 0; ks < NU / 4; ++ks) {
+                    const int k = 4 * ks + tg;
+                    double a[2], b[2];
+#pragma unroll
+                    for (int ti = 0; ti < 2; ++ti) {
+                        const int i = 16 * rp + 8 * ti + gr;
+                        a[ti] = i < NX ? Gu[k * GLD + NU + i] : 0.0;
+                    }
+#pragma unroll
+                    for (int tj = 0; tj < 2; ++tj) {
+                        const int j = 16 * cp + 8 * tj + gr;
+                        b[tj] = j < NX ? Ks[k * NX + j] : 0.0;
+                    }
+#pragma unroll
+                    for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+                        for (int tj = 0; tj < 2; ++tj) dmma_acc(acc[ti][tj][0], acc[ti][tj][1], a[ti], b[tj]);
+                }
+#pragma unroll
+                for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+                    for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int i = 16 * rp + 8 * ti + gr, j = 16 * cp + 8 * tj + 2 * tg + e;
+                            if (i < NX && j < NX) Pc[i * NX + j] = acc[ti][tj][e];
+                        }
+            }
+            flops += 2ll * NX * NX * NU;
+            bar<TEAM>();
+            // 0.5 (P + P') in place; the packed lower triangle to the factor store
+            double* Pn = Pst + n * S::PST;
+            TEAM_FOR(idx, NX * NX)
+                const int i = idx / NX, j = idx - i * NX;
+                if (j <= i) {
+                    const double v = 0.5 * (Pc[idx] + Pc[j * NX + i]);
+                    Pc[idx] = v;
+                    Pc[j * NX + i] = v;
+                    if (S::PPACK) Pn[i * (i + 1) / 2 + j] = v;
+                    else { Pn[idx] = v; Pn[j * NX + i] = v; }
+                }
+            TEAM_END
+            bar<TEAM>();
+        }
+        OCPQP_TICK(c, DBG_F_P);
+        // L_P0 = chol(P_0) (kkt_ocp.py:193-200)
+        double* LP0 = wsb<WS_LP0>(c, p);
+        flops += (long long)NX * NX * NX / 3;
+        for (int idx = tid; idx < NX * NX; idx += TEAM) LP0[idx] = Pc[idx];
+        bar<TEAM>();
+        if (!team_chol<TEAM>(LP0, NX, &c.flag, wsb<WS_RINV>(c, p) + N * NU)) return 0;
         return -1;
     }
 
@@ -1546,6 +2169,41 @@ struct Kern {
                 if (lane < k) z = fma(-L[k * NN + lane], zk, z);
             }
             if (lane < NN) out[lane] = sgn * z;
+        } else if constexpr (NN <= 64) {
+            // two rows per lane (lane, lane + 32): right-looking, one broadcast per step
+            const int r1 = lane + 32;
+            double z0 = xin[lane];
+            double z1 = r1 < NN ? xin[r1] : 0.0;
+            const double ri0 = rv[lane];
+            const double ri1 = r1 < NN ? rv[r1] : 1.0;
+#pragma unroll 4
+            for (int k = 0; k < NN; ++k) {
+                double zk;
+                if (k < 32) {
+                    if (lane == k) z0 = z0 * ri0;
+                    zk = __shfl_sync(FULL, z0, k);
+                } else {
+                    if (lane == k - 32) z1 = z1 * ri1;
+                    zk = __shfl_sync(FULL, z1, k - 32);
+                }
+                if (lane > k) z0 = fma(-L[lane * NN + k], zk, z0);
+                if (r1 > k && r1 < NN) z1 = fma(-L[r1 * NN + k], zk, z1);
+            }
+#pragma unroll 4
+            for (int k = NN - 1; k >= 0; --k) {
+                double zk;
+                if (k < 32) {
+                    if (lane == k) z0 = z0 * ri0;
+                    zk = __shfl_sync(FULL, z0, k);
+                } else {
+                    if (lane == k - 32) z1 = z1 * ri1;
+                    zk = __shfl_sync(FULL, z1, k - 32);
+                }
+                if (lane < k) z0 = fma(-L[k * NN + lane], zk, z0);
+                if (r1 < k) z1 = fma(-L[k * NN + r1], zk, z1);
+            }
+            out[lane] = sgn * z0;
+            if (r1 < NN) out[r1] = sgn * z1;
         } else {
             if (lane == 0) {
                 for (int i = 0; i < NN; ++i) out[i] = xin[i];
@@ -1564,6 +2222,218 @@ struct Kern {
         }
     }
 
+    // Riccati solve sweeps of a BIG shape (kkt_ocp.py:270-305), with the dpi
+    // recursion fused into the forward sweep.  The per-stage operands stream
+    // through the stage tile by TMA: [B A]' double-buffered (the first
+    // 2 NW NX doubles), the small blocks single-buffered in the remaining NX^2,
+    // each block issued as soon as its previous contents are consumed; the
+    // operands three stages ahead are bulk-prefetched into L2.
+    //   backward n: O1 = [P_{n+1} (packed), r_b,n]  O2 = [K_n, L_n, 1/L_ii, rhat_n]
+    //   forward  n: F1 = [K_n, kff_n]                F2 = [r_b,n, P_{n+1}, pv_{n+1}]
+    // Barriers: 0 / 1 the [B A]' slots, 2 O1 / F2, 3 O2 / F1.  Returns the
+    // thread's non-finite flag of dpi.
+    __device__ __noinline__ static int sweeps_big(FCtx& c, const RD& d, const KParams& p, double* stg,
+                                                  double* dy, double* dpi, long long& flops, Tma& tm) {
+        const int tid = threadIdx.x;
+        const double* r_b = wsb<WS_RB>(c, p);
+        const double* rhat = wsb<WS_RHAT>(c, p);
+        const double* Pst = wsb<WS_P>(c, p);
+        const double* Kst = wsb<WS_K>(c, p);
+        const double* Lst = wsb<WS_L>(c, p);
+        const double* Rst = wsb<WS_RINV>(c, p);
+        double* pv = wsb<WS_PV>(c, p);
+        double* kff = wsb<WS_KFF>(c, p);
+        double* vec = stg + S::VOFF;
+        double* win = vec;          // NW
+        double* e = win + NW;       // NX
+        double* pvs = e + NX;       // NX: pv_{n+1}
+        double* xa = pvs + NX;      // NX: x_n
+        double* uv = xa + NX;       // NU: u_n
+        double* xb = uv + NU;       // NX: x_{n+1}
+        constexpr int PS = S::PST;
+        double* sBA[2] = {stg, stg + NW * NX};
+        double* pool = stg + 2 * NW * NX;   // NX * NX doubles
+        constexpr int O1N = PS + NX, O2N = NU * NX + NU * NU + NU + NW;
+        constexpr int F1N = NU * NX + NU, F2N = NX + PS + NX;
+        static_assert(O1N + O2N <= NX * NX && F1N + F2N <= NX * NX, "sweeps_big pool");
+        static_assert(O1N % 2 == 0 && F1N % 2 == 0, "16-byte aligned TMA destinations");
+        double* sO1 = pool;
+        double* sO2 = pool + O1N;
+        double* sF1 = pool;
+        double* sF2 = pool + F1N;
+        const int N = d.N;
+        // the factor store, r_b and rhat were written through the generic proxy:
+        // order them before the copy engine reads them
+        asm volatile("fence.proxy.async;\n" ::: "memory");
+        auto cp = [&](double* dst, const double* src, int nd, int b) {
+            tma_load_1d(dst, src, (unsigned)nd * 8u, &c.mbar[b]);
+        };
+        auto issue_O1 = [&](int n) {
+            if (tid == 0) {
+                fence_proxy_async();
+                mbar_expect_tx(&c.mbar[2], O1N * 8);
+                cp(sO1, Pst + (n + 1) * PS, PS, 2);
+                cp(sO1 + PS, r_b + n * NX, NX, 2);
+            }
+            tm.issue(c.mbar, 2);
+        };
+        auto issue_O2 = [&](int n) {
+            if (tid == 0) {
+                fence_proxy_async();
+                mbar_expect_tx(&c.mbar[3], O2N * 8);
+                cp(sO2, Kst + n * NU * NX, NU * NX, 3);
+                cp(sO2 + NU * NX, Lst + n * NU * NU, NU * NU, 3);
+                cp(sO2 + NU * NX + NU * NU, Rst + n * NU, NU, 3);
+                cp(sO2 + NU * NX + NU * NU + NU, rhat + n * NW, NW, 3);
+            }
+            tm.issue(c.mbar, 3);
+        };
+        auto l2pf = [&](int n) {
+            if (tid == 0 && n >= 0 && n < N) {
+                l2_prefetch_bulk(BAp(c, n), BAB);
+                l2_prefetch_bulk(Pst + (n + 1) * PS, PS * 8);
+                l2_prefetch_bulk(Kst + n * NU * NX, NU * NX * 8);
+            }
+        };
+        // ---- backward sweep (kkt_ocp.py:276-289); terminal stage: nu = 0 ----
+        for (int i = tid; i < NX; i += TEAM) {
+            const double v = rhat[N * NW + i];
+            pv[N * NX + i] = v;
+            pvs[i] = v;
+        }
+        bar<TEAM>();
+        if (N > 0) {
+            issue_O1(N - 1);
+            tma_ba(c, tm, sBA[(N - 1) & 1], N - 1, (N - 1) & 1);
+            issue_O2(N - 1);
+            if (N > 1) tma_ba(c, tm, sBA[(N - 2) & 1], N - 2, (N - 2) & 1);
+            l2pf(N - 3);
+        }
+        for (int n = N - 1; n >= 0; --n) {
+            const int s = n & 1;
+            l2pf(n - 3);
+            // e = P_{n+1} r_b + p_{n+1}
+            tm.wait(c.mbar, 2);
+            MV<NX, NX, TEAM>::run([&](int i, int k) { return Pget(sO1, i, k); },
+                                  [&](int k) { return sO1[PS + k]; },
+                                  [&](int i, double v) { e[i] = v + pvs[i]; });
+            bar<TEAM>();
+            if (n > 0) issue_O1(n - 1);
+            // rr, rq = rhat + [B A]' e
+            tm.wait(c.mbar, s);
+            tm.wait(c.mbar, 3);
+            const double* rh = sO2 + NU * NX + NU * NU + NU;
+            const double* BAn = sBA[s];
+            MV<NW, NX, TEAM>::run([&](int j, int k) { return BAn[j * NX + k]; },
+                                  [&](int k) { return e[k]; },
+                                  [&](int j, double v) { win[j] = rh[j] + v; });
+            bar<TEAM>();
+            if (n > 1) tma_ba(c, tm, sBA[s], n - 2, s);
+            // p_n = rq + K' rr on all warps but the last; k_n = -G_uu^{-1} rr on the last
+            const double* Kn = sO2;
+            const double* Ln = sO2 + NU * NX;
+            const double* Rn = Ln + NU * NU;
+            double* pvc = pv + n * NX;
+            if (warp_id_uniform() == TEAM / 32 - 1)
+                warp_cho_solve<NU>(Ln, Rn, win, kff + n * NU, -1.0);
+            else
+                MV<NX, NU, TEAM - 32>::run([&](int i, int k) { return Kn[k * NX + i]; },
+                                           [&](int k) { return win[k]; },
+                                           [&](int i, double v) {
+                                               const double r = win[NU + i] + v;
+                                               pvc[i] = r;
+                                               pvs[i] = r;
+                                           });
+            flops += 2ll * NU * NU;
+            bar<TEAM>();
+            if (n > 0) issue_O2(n - 1);
+        }
+        OCPQP_TICK(c, DBG_S_BWD);
+        // x0 step: dx_0 = -P_0^{-1} p_0
+        if (warp_id_uniform() == 0) warp_cho_solve<NX>(wsb<WS_LP0>(c, p), Rst + N * NU, pvs, xa, -1.0);
+        flops += 2ll * NX * NX;
+        // kff / pv of this solve were written through the generic proxy
+        asm volatile("fence.proxy.async;\n" ::: "memory");
+        bar<TEAM>();
+        // ---- forward rollout (kkt_ocp.py:293-305) ----
+        auto issue_F1 = [&](int n) {
+            if (tid == 0) {
+                fence_proxy_async();
+                mbar_expect_tx(&c.mbar[3], F1N * 8);
+                cp(sF1, Kst + n * NU * NX, NU * NX, 3);
+                cp(sF1 + NU * NX, kff + n * NU, NU, 3);
+            }
+            tm.issue(c.mbar, 3);
+        };
+        auto issue_F2 = [&](int n) {
+            if (tid == 0) {
+                fence_proxy_async();
+                mbar_expect_tx(&c.mbar[2], F2N * 8);
+                cp(sF2, r_b + n * NX, NX, 2);
+                cp(sF2 + NX, Pst + (n + 1) * PS, PS, 2);
+                cp(sF2 + NX + PS, pv + (n + 1) * NX, NX, 2);
+            }
+            tm.issue(c.mbar, 2);
+        };
+        for (int i = tid; i < NX; i += TEAM) dy[(N > 0 ? NU : 0) + i] = xa[i];
+        if (N > 0) {
+            issue_F1(0);
+            tma_ba(c, tm, sBA[0], 0, 0);
+            issue_F2(0);
+            if (N > 1) tma_ba(c, tm, sBA[1], 1, 1);
+            l2pf(2);
+        }
+        int nonfinite = 0;
+        for (int n = 0; n < N; ++n) {
+            const int s = n & 1;
+            l2pf(n + 3);
+            // u_n = K_n x_n + k_n
+            tm.wait(c.mbar, 3);
+            double* du = dy + n * NW;
+            MV<NU, NX, TEAM>::run([&](int i, int k) { return sF1[i * NX + k]; },
+                                  [&](int k) { return xa[k]; },
+                                  [&](int i, double v) {
+                                      const double u = v + sF1[NU * NX + i];
+                                      du[i] = u;
+                                      uv[i] = u;
+                                  });
+            bar<TEAM>();
+            if (n + 1 < N) issue_F1(n + 1);
+            // x_{n+1} = A x_n + B u_n + r_b,n
+            tm.wait(c.mbar, s);
+            tm.wait(c.mbar, 2);
+            const double* BAn = sBA[s];
+            double* xd = dy + (n + 1) * NW + (n + 1 < N ? NU : 0);
+            MV<NX, NW, TEAM>::run(
+                [&](int i, int k) { return k < NX ? BAn[(NU + k) * NX + i] : BAn[(k - NX) * NX + i]; },
+                [&](int k) { return k < NX ? xa[k] : uv[k - NX]; },
+                [&](int i, double v) {
+                    const double x = v + sF2[i];
+                    xb[i] = x;
+                    xd[i] = x;
+                });
+            bar<TEAM>();
+            if (n + 2 < N) tma_ba(c, tm, sBA[s], n + 2, s);
+            // dpi_n = P_{n+1} x_{n+1} + pv_{n+1}
+            const double* Pn = sF2 + NX;
+            const double* pvn = Pn + PS;
+            MV<NX, NX, TEAM>::run([&](int i, int k) { return Pget(Pn, i, k); },
+                                  [&](int k) { return xb[k]; },
+                                  [&](int i, double v) {
+                                      const double w = v + pvn[i];
+                                      dpi[n * NX + i] = w;
+                                      if (!isfinite(w)) nonfinite = 1;
+                                  });
+            bar<TEAM>();
+            if (n + 1 < N) issue_F2(n + 1);
+            double* sw = xa;
+            xa = xb;
+            xb = sw;
+        }
+        OCPQP_TICK(c, DBG_S_FWD);
+        return nonfinite;
+    }
+
     // ---------------- Riccati solve (kkt_ocp.py:254-320) ----------------
     // r_m(k) = act ? (lam t - tau) + [dlam_a dt_a] : 0, or rm_ext (masked)
     // absm: absolute formulation (speed_abs): 1 affine rhs -lam t, 2 combined
@@ -1573,7 +2443,7 @@ struct Kern {
                                 const double* lam, const double* t, const double* rm_ext,
                                 double tau, const double* dla, const double* dta, double* dy,
                                 double* dpi, double* dlam, double* dt, long long& flops,
-                                int absm = 0, bool lp = false) {
+                                int absm = 0, bool lp = false, Tma* tm = nullptr) {
         const int tid = threadIdx.x;
         const double* act = c.w[WS_DVEC];  // NaN = inactive
         const double* gam = c.w[WS_GAM];
@@ -1589,7 +2459,7 @@ struct Kern {
         const double* Lst = wsb<WS_L>(c, p);
         double* pv = wsb<WS_PV>(c, p);
         double* kff = wsb<WS_KFF>(c, p);
-        double* vec = stg + NX * NX + S::T1N + NU * NW;
+        double* vec = stg + S::VOFF;
         double* win = vec;              // NW
         double* e = vec + NW;           // NX
         int nonfinite = 0;
@@ -1652,6 +2522,9 @@ struct Kern {
         bar<TEAM>();
         const int N = d.N;
         OCPQP_TICK(c, DBG_S_PRE);
+        if constexpr (S::BIG) {
+            nonfinite |= sweeps_big(c, d, p, stg, dy, dpi, flops, *tm);
+        } else {
         // ---- per-stage operand staging (global -> smem, one stage ahead) ----
         double* pvs = vec + NW + NX;            // NX: pv_{n+1} of the sweep
         double* xv = pvs + NX;                  // NX: x_n in the forward sweep
@@ -1717,7 +2590,7 @@ struct Kern {
             const double* Rn = (st && gR) ? H + oR : Rst + n * NU;
             const double* rh = (st && gRH) ? H + oRH : rhat + n * NW;
             const double* BAn = BAp(c, n);
-            auto BA = [&](int k, int j) -> double { return ss ? H[oBA + k * NW + j] : BAn[k * NW + j]; };
+            auto BA = [&](int k, int j) -> double { return ss ? H[oBA + k * NW + j] : BAn[k * BK + j * BJ]; };
             if (lp) {
                 // square-root factor: P r_b = L_P (L_P' r_b) (kkt_ocp.py:110-113)
                 MV<NX, NX, TEAM>::run([&](int i, int k) { return k >= i ? Pget(Pn, k, i) : 0.0; },
@@ -1747,7 +2620,7 @@ struct Kern {
                 // p_n on all warps but the last, k_n = -G_uu^{-1} rr on the last
                 // warp at the same time (the warp solve used to follow the
                 // mat-vec on warp 0 while the others waited at the barrier)
-                if (tid >= TEAM - 32)
+                if (warp_id_uniform() == TEAM / 32 - 1)
                     warp_cho_solve<NU>(Ln, Rn, win, kff + n * NU, -1.0);
                 else
                     MV<NX, NU, TEAM - 32>::run([&](int i, int k) { return Kn[k * NX + i]; },
@@ -1774,7 +2647,7 @@ struct Kern {
                     for (int i = 0; i < NU; ++i) kff[n * NU + i] = -z[i];
                 }
             } else {
-                if (tid < 32) warp_cho_solve<NU>(Ln, Rn, win, kff + n * NU, -1.0);
+                if (warp_id_uniform() == 0) warp_cho_solve<NU>(Ln, Rn, win, kff + n * NU, -1.0);
             }
             flops += 2ll * NU * NU;
             bar<TEAM>();
@@ -1782,7 +2655,7 @@ struct Kern {
         OCPQP_TICK(c, DBG_S_BWD);
         if (N == 0) bar<TEAM>();
         // x0 step
-        if (tid < 32) warp_cho_solve<NX>(wsb<WS_LP0>(c, p), Rst + N * NU, pvs, xv, -1.0);
+        if (warp_id_uniform() == 0) warp_cho_solve<NX>(wsb<WS_LP0>(c, p), Rst + N * NU, pvs, xv, -1.0);
         flops += 2ll * NX * NX;
         if (N > 0) issue(0, 0, false);
         bar<TEAM>();
@@ -1823,7 +2696,7 @@ struct Kern {
                 MV<NX, NW, TEAM>::run(
                     [&](int i, int k) {
                         if (ss) return k < NX ? H[oBA + i * NW + NU + k] : H[oBA + i * NW + (k - NX)];
-                        return k < NX ? BAn[i * NW + NU + k] : BAn[i * NW + (k - NX)];
+                        return k < NX ? BAn[i * BK + (NU + k) * BJ] : BAn[i * BK + (k - NX) * BJ];
                     },
                     [&](int k) { return k < NX ? xa[k] : uv[k - NX]; },
                     [&](int i, double v) {
@@ -1870,6 +2743,7 @@ struct Kern {
             const double v = a + pv[(n + 1) * NX + i];
             dpi[e2] = v;
             if (!isfinite(v)) nonfinite = 1;
+        }
         }
         OCPQP_PASS_UNROLL
         for (int j = tid; j < d.nv; j += TEAM)
@@ -1988,9 +2862,9 @@ struct Kern {
                 r = h1 + h2;
                 double atp = (jj >= NU && n > 0) ? dpi[(n - 1) * NX + (jj - NU)] : 0.0;
                 double a = 0.0;
-                const double* BAc = BAp(c, n) + jj;
+                const double* BAc = BAp(c, n) + jj * BJ;
                 const double* pn = dpi + n * NX;
-                for (int k = 0; k < NX; ++k) a = fma(BAc[k * NW], pn[k], a);
+                for (int k = 0; k < NX; ++k) a = fma(BAc[k * BK], pn[k], a);
                 atp -= a;
                 r -= atp;
             } else {
@@ -2025,11 +2899,11 @@ struct Kern {
             const double* u = dy + n * NW;
             const double* x = u + NU;
             const double xn = dy[(n + 1) * NW + (n + 1 < d.N ? NU : 0) + i];
-            const double* Br = BAp(c, n) + i * NW;
-            const double* Ar = Br + NU;
+            const double* Br = BAp(c, n) + i * BK;
+            const double* Ar = Br + NU * BJ;
             double ax = 0.0, bu = 0.0;
-            for (int k = 0; k < NX; ++k) ax = fma(Ar[k], x[k], ax);
-            for (int k = 0; k < NU; ++k) bu = fma(Br[k], u[k], bu);
+            for (int k = 0; k < NX; ++k) ax = fma(Ar[k * BJ], x[k], ax);
+            for (int k = 0; k < NU; ++k) bu = fma(Br[k * BJ], u[k], bu);
             const double o = -((xn - ax) - bu) + hb[e];
             ob[e] = o;
             am.add(o);
@@ -2064,7 +2938,7 @@ struct Kern {
     __device__ __noinline__ static RefOut refine(FCtx& c, const RD& d, const KParams& p,
                                                  double* stg, const double* lam, const double* t,
                                                  double* dy, double* dpi, double* dl, double* dt,
-                                                 int max_steps, double stop_ratio, bool lp) {
+                                                 int max_steps, double stop_ratio, bool lp, Tma* tm) {
         long long flops = 0;
         const double* act = c.w[WS_DVEC];
         const double* hg = c.x[WS_GF - WS_EXT0];
@@ -2100,7 +2974,7 @@ struct Kern {
         double norm = best;
         int grew = 0;
         for (int st = 0; st < max_steps; ++st) {
-            solve(c, d, p, stg, lam, t, om, 0.0, nullptr, nullptr, cy, cpi, cl, ct, flops, 0, lp);
+            solve(c, d, p, stg, lam, t, om, 0.0, nullptr, nullptr, cy, cpi, cl, ct, flops, 0, lp, tm);
             bar<TEAM>();
             for (int i = threadIdx.x; i < d.nv; i += TEAM) dy[i] = dy[i] + cy[i];
             for (int i = threadIdx.x; i < d.ne; i += TEAM) dpi[i] = dpi[i] + cpi[i];
@@ -2129,7 +3003,7 @@ struct Kern {
     // the speed-mode kernel carries none of its code or registers
     template <bool REF>
     __device__ static void ipm_one(FCtx& c, const RD& d, const KParams& p, const SolveParams& sp,
-                                   double* stg, int q) {
+                                   double* stg, int q, Tma& tm) {
         const OcpIpmArgC& arg = sp.arg;
         const int tid = threadIdx.x;
         double* gy = sp.y + (long long)q * d.nv;
@@ -2170,11 +3044,11 @@ struct Kern {
                 for (int e = tid; e < d.ne; e += TEAM) {
                     const int n = e / NX, i = e - n * NX;
                     const double* u = y + n * NW;
-                    const double* Br = BAp(c, n) + i * NW;
-                    const double* Ar = Br + NU;
+                    const double* Br = BAp(c, n) + i * BK;
+                    const double* Ar = Br + NU * BJ;
                     double ax = 0.0, bu = 0.0;
-                    for (int k = 0; k < NX; ++k) ax = fma(Ar[k], u[NU + k], ax);
-                    for (int k = 0; k < NU; ++k) bu = fma(Br[k], u[k], bu);
+                    for (int k = 0; k < NX; ++k) ax = fma(Ar[k * BJ], u[NU + k], ax);
+                    for (int k = 0; k < NU; ++k) bu = fma(Br[k * BJ], u[k], bu);
                     const double xn = y[(n + 1) * NW + (n + 1 < d.N ? NU : 0) + i];
                     gb = fmax(gb, fabs(-((xn - ax) - bu) + bv(c, n)[i]));
                 }
@@ -2272,7 +3146,8 @@ struct Kern {
                         return fo.fs;
                     }
                 }
-                return factor(c, d, p, stg, lam, t, rg, flops);
+                if constexpr (S::BIG) return factor_big(c, d, p, stg, lam, t, rg, flops, tm);
+                else return factor(c, d, p, stg, lam, t, rg, flops);
             };
             int fs = do_factor(arg.reg_prim);
             // the balance-mode ladder continues with the QR array algorithm
@@ -2298,7 +3173,7 @@ struct Kern {
             };
             {
                 int nfa = solve(c, d, p, stg, lam, t, nullptr, 0.0, nullptr, nullptr, dy, dpi, alam,
-                                at, flops, absf ? 1 : 0, sqv);
+                                at, flops, absf ? 1 : 0, sqv, &tm);
                 if (absf) { bar<TEAM>(); nfa = to_step(dy, dpi, alam, at); }
                 if (nfa) {
                     status = OCPQP_STATUS_NAN;
@@ -2313,7 +3188,7 @@ struct Kern {
             if (mu > 0.0) sigma = fmin(1.0, fmax(0.0, pow(mu_aff / mu, 3.0)));
             const double tau = sigma * mu;
             int nf = solve(c, d, p, stg, lam, t, nullptr, tau, arg.pred_corr ? alam : nullptr,
-                           arg.pred_corr ? at : nullptr, dy, dpi, dlam, dt, flops, absf ? 2 : 0, sqv);
+                           arg.pred_corr ? at : nullptr, dy, dpi, dlam, dt, flops, absf ? 2 : 0, sqv, &tm);
             bar<TEAM>();
             if (absf) { nf = to_step(dy, dpi, dlam, dt); bar<TEAM>(); }
             bool rejected = false;
@@ -2323,7 +3198,7 @@ struct Kern {
                 if (!(mu_t <= arg.corr_ratio * mu_aff)) {
                     rejected = true;
                     nf = solve(c, d, p, stg, lam, t, nullptr, tau, nullptr, nullptr, dy, dpi, dlam, dt,
-                               flops, absf ? 2 : 0, sqv);
+                               flops, absf ? 2 : 0, sqv, &tm);
                     bar<TEAM>();
                     if (absf) { nf = to_step(dy, dpi, dlam, dt); bar<TEAM>(); }
                 }
@@ -2353,7 +3228,7 @@ struct Kern {
                 }
                 bar<TEAM>();
                 const RefOut ro = refine(c, d, p, stg, lam, t, dy, dpi, dlam, dt,
-                                         arg.itref_corr_max, arg.itref_stop_ratio, sqv);
+                                         arg.itref_corr_max, arg.itref_stop_ratio, sqv, &tm);
                 flops += ro.flops;
                 if (arg.use_qr_fallback && ro.best > arg.qr_fallback_ratio * ro.rhs) {
                     status = STATUS_ESCAPE;   // QR refactorization: generic kernel
@@ -2463,7 +3338,12 @@ __global__ void __launch_bounds__(S::TEAM, S::MINB) k_fast_solve(const __grid_co
         const int inv = p.sinv ? *p.sinv : 0;
         for (int f = 0; f < OCPQP_F_lb; ++f) c.ss[f] = ((inv >> f) & 1) ? 0 : sz[f];
         c.ba_ss = ((inv & 3) == 3) ? 0 : NX * (NX + NU);   // A and B both invariant
+        if constexpr (S::BIG) {
+            for (int b = 0; b < 4; ++b) mbar_init(&c.mbar[b], 1);
+            fence_mbar_init();
+        }
     }
+    Tma tm;   // per-thread phase parity of the TMA barriers (persists across QPs)
     double* stg = smem + p.stage_smem;
     while (true) {
         if (threadIdx.x == 0) c.q = atomicAdd(p.counter, 1);
@@ -2474,13 +3354,16 @@ __global__ void __launch_bounds__(S::TEAM, S::MINB) k_fast_solve(const __grid_co
             c.f[f] = p.f[f] + (long long)q * p.bs[f];
         if (threadIdx.x == 0) c.ba = p.ba + (long long)q * p.ba_bs;
         bar<S::TEAM>();
-        Kern<S>::template ipm_one<REF>(c, d, p, sp, stg, q);
+        Kern<S>::template ipm_one<REF>(c, d, p, sp, stg, q, tm);
         bar<S::TEAM>();
     }
 }
 
 template <class S>
 int stage_doubles() { return S::STAGE; }
+
+template <class S>
+int is_big() { return S::BIG ? 1 : 0; }
 
 template <class S>
 cudaError_t launch(const KParams& p, const SolveParams& sp, int grid, size_t smem, cudaStream_t st) {

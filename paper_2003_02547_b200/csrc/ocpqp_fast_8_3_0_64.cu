@@ -7,5 +7,6 @@ using S_8_3_0_64 = Shape<8,3,0,64>;
 template cudaError_t launch<S_8_3_0_64>(const KParams&, const SolveParams&, int, size_t, cudaStream_t);
 template int occupancy<S_8_3_0_64>(size_t);
 template int stage_doubles<S_8_3_0_64>();
+template int is_big<S_8_3_0_64>();
 }  // namespace fastk
 }  // namespace ocpqp

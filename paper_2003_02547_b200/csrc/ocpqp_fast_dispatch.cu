@@ -13,6 +13,8 @@ template <class S>
 int occupancy(size_t smem);
 template <class S>
 int stage_doubles();
+template <class S>
+int is_big();
 }  // namespace fastk
 namespace rowk {
 template <int NX_, int NU_, int NG_, int NB_, int G_, int WPB_>
@@ -85,6 +87,13 @@ cudaError_t launch_fast_solve(const FastShape& s, const KParams& p, const SolveP
     OCPQP_ROW_SHAPES(X)
 #undef X
     return cudaErrorNotSupported;
+}
+
+int fast_big(const FastShape& s) {
+#define X(a, b, c_, t, m) if (OCPQP_MATCH(a, b, c_, t, m)) return fastk::is_big<fastk::Shape<a, b, c_, t, m>>();
+    OCPQP_FAST_SHAPES(X)
+#undef X
+    return 0;
 }
 
 int fast_occupancy(const FastShape& s, size_t smem) {

@@ -139,9 +139,11 @@ cudaError_t launch_shift_guess(const KParams& p, const double* sy, const double*
                                cudaStream_t stream);
 int ipm_occupancy(int threads, size_t smem);
 // Pack [B A] of every stage (uniform stages 0..N-1) into out: per QP N * nx * (nu + nx)
-// doubles, QP stride out_bs (0 when A and B are both broadcast).
+// doubles, QP stride out_bs (0 when A and B are both broadcast); trans: each
+// stage stored as [B A]' (nu + nx rows of nx), the BIG shapes' layout.
 cudaError_t launch_pack_ba(const double* A, long long bsA, const double* B, long long bsB, int Bn,
-                           int N, int nx, int nu, double* out, long long out_bs, cudaStream_t stream);
+                           int N, int nx, int nu, double* out, long long out_bs, cudaStream_t stream,
+                           int trans = 0);
 // Stage-invariance detection of the broadcast fields A..r (uniform-stage plans):
 // writes the bit mask consumed by the shaped kernels to *mask.
 cudaError_t launch_stage_invariant(const double* const* f, const long long* bs, int N, int nx,
@@ -161,5 +163,8 @@ int fast_stage_smem_doubles(const FastShape& s);
 cudaError_t launch_fast_solve(const FastShape& s, const KParams& p, const SolveParams& sp,
                               int grid, size_t smem, cudaStream_t stream);
 int fast_occupancy(const FastShape& s, size_t smem);
+// the shape's kernel streams stage data by TMA from a transposed [B A] pack
+// and keeps no workspace buffer in shared memory (ocpqp_fast.cuh, Shape::BIG)
+int fast_big(const FastShape& s);
 
 }  // namespace ocpqp

@@ -165,8 +165,17 @@ def make_batch(cfg, batch=None, start=0, N=None) -> OcpQpBatch:
     if spec.ng:
         for name in ("C", "D", "lg", "ug"):
             out.alloc(name, True, 0.0)
+    # per-QP draws are independent (one RNG per QP); LAPACK eigvals releases
+    # the GIL, so a thread pool generates them in parallel, bit-identically
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+
+    workers = max(1, min(B, os.cpu_count() or 1, 32))
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        draws = list(ex.map(lambda k: _random_draws(spec, start + k, N), range(B)))
     for k in range(B):
-        dr = _random_draws(spec, start + k, N)
+        dr = draws[k]
+        draws[k] = None
         f = out.fields
         f["A"][k] = dr["A"].reshape(-1)
         f["B"][k] = dr["B"].reshape(-1)
