@@ -50,6 +50,7 @@ struct Layout {
     long long flen[OCPQP_NUM_FIELDS] = {0};
     std::vector<int> var_box, row_slack;
     long long ws_size[WS_NUM] = {0};
+    int box_ident = 1;        // every stage's idxb is 0, 1, ..., nb - 1
 };
 
 long long field_stage_size(int f, const Layout& L, int n) {
@@ -161,7 +162,10 @@ int build_layout(const OcpQpDimC* d, Layout& L) {
     L.row_slack.assign(std::max(1, L.msum), -1);
     for (int n = 0; n < S; ++n) {
         const StageInfo& si = L.st[n];
-        for (int i = 0; i < si.nb; ++i) L.var_box[si.u_off + L.idxb[si.ib_off + i]] = i;
+        for (int i = 0; i < si.nb; ++i) {
+            L.var_box[si.u_off + L.idxb[si.ib_off + i]] = i;
+            if (L.idxb[si.ib_off + i] != i) L.box_ident = 0;
+        }
         for (int j = 0; j < si.ns; ++j) L.row_slack[si.m_off + L.idxs[si.is_off + j]] = j;
     }
     long long* w = L.ws_size;
@@ -326,6 +330,7 @@ void fill_kparams(const OcpPlan* P, KParams& k, const OcpQpDataC* data, bool use
     k.smem_mask = use_smem ? P->smem_mask : 0ull;
     k.counter = P->d_counter;
     k.NB = P->NB; k.NBN = P->NBN; k.NGN = P->NGN;
+    k.box_ident = L.box_ident;
     k.stage_smem = P->stage_smem;
     k.team_stride = P->team_stride;
     k.dbg = P->dbg;
@@ -367,7 +372,7 @@ bool detect_fast(OcpPlan* P) {
     const int want_kind = envk ? atoi(envk) : -1;
     FastShape pick{-1, 0, 0, 0, 0, 0, 0};
     // row kernel: only on request (measured slower than the team kernel on configs 1-4)
-    if (want_kind == 1) {
+    if (want_kind == 1 && L.box_ident) {   // the row kernel maps box row i to variable i
         const int gdef = (NX <= 8 && NU <= 8) ? 8 : (NX <= 16 && NU <= 16) ? 16 : 32;
         const int g = envt && want_kind == 1 ? atoi(envt) : gdef;
         const int wpbs[] = {envw ? atoi(envw) : 1, 1, 2, 4};

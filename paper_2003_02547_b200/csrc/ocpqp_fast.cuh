@@ -45,7 +45,8 @@
 #endif
 #define OCPQP_STR2(x) #x
 #define OCPQP_STR(x) OCPQP_STR2(x)
-#define OCPQP_PASS_UNROLL _Pragma(OCPQP_STR(unroll OCPQP_PASS_UNROLL_N))
+// per shape (Shape::PU): the team-strided vector passes (used inside Kern<S>)
+#define OCPQP_PASS_UNROLL _Pragma("unroll (S::PU)")
 
 namespace ocpqp {
 namespace fastk {
@@ -205,6 +206,34 @@ struct MV {
     template <class FA, class FX, class FO>
     __device__ __forceinline__ static void run(FA a, FX x, FO out) {
         const int tid = threadIdx.x;
+        const int g = tid % GS;
+        const int r0 = tid / GS;
+#pragma unroll
+        for (int i0 = 0; i0 < R; i0 += RPP) {
+            const int i = i0 + r0;
+            double acc = 0.0;
+            if (i < R) {
+                _Pragma(OCPQP_STR(unroll OCPQP_K_UNROLL_N))
+                for (int k = g; k < KD; k += GS) acc = fma(a(i, k), x(k), acc);
+            }
+#pragma unroll
+            for (int o = GS / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+            if (i < R && g == 0) out(i, acc);
+        }
+    }
+};
+
+// MV on the T threads OFF .. OFF + T - 1 of the CTA (whole warps): the other
+// warps run other work in the same phase
+template <int R, int KD, int T, int OFF>
+struct MVo {
+    static constexpr int cap = T / (R > 0 ? R : 1);
+    static constexpr int GS0 = cap >= 8 ? 8 : cap >= 4 ? 4 : cap >= 2 ? 2 : 1;
+    static constexpr int GS = (KD >= 8 ? GS0 : (KD >= 4 ? (GS0 < 4 ? GS0 : 4) : (KD >= 2 ? (GS0 < 2 ? GS0 : 2) : 1)));
+    static constexpr int RPP = T / GS;
+    template <class FA, class FX, class FO>
+    __device__ __forceinline__ static void run(FA a, FX x, FO out) {
+        const int tid = (int)threadIdx.x - OFF;
         const int g = tid % GS;
         const int r0 = tid / GS;
 #pragma unroll
@@ -618,6 +647,7 @@ __device__ __forceinline__ void stage_gemm(FA a, FB b, FP pre, FE epi) {
 // runtime structure (uniform stages)
 struct RD {
     int N, NB, M, NBN, NGN, MN, nc, nv, ne, msum;
+    int fullb;            // every variable of every stage has its own box row i = j (idxb = 0..nw-1)
     float inv_m, inv_2m;  // 1/M, 1/(2M): stage decode by float multiply (exact for k < 2^20)
     __device__ __forceinline__ int slot_stage(int k) const {
         if (M == 0) return N;
@@ -697,10 +727,14 @@ struct Shape {
     static constexpr bool BAT = BIG;
     static constexpr int STAGE_STD = STAGE0 + (SSTAGE ? (BA_BUF > SOLVE_BUF ? BA_BUF : SOLVE_BUF) : BA_BUF) + JGB;
     // BIG vector scratch: win, e, pvs, x, u, x', r_b (sweeps_big)
-    static constexpr int VECB = NW + 6 * NX + NU + 16 > 32 + NU * NU ? NW + 6 * NX + NU + 16 : 32 + NU * NU;
+    static constexpr int VECB = 2 * NW + 6 * NX + NU + 16 > 32 + NU * NU ? 2 * NW + 6 * NX + NU + 16 : 32 + NU * NU;
     static constexpr int STAGE = BIG ? NX * NX + 2 * NW * NX + VECB : STAGE_STD;
     // offset of the vector scratch (win, e, pvs, x, u) in the stage tile
     static constexpr int VOFF = BIG ? NX * NX + 2 * NW * NX : NX * NX + T1N + NU * NW;
+    // unroll of the team-strided vector passes: BIG stages have long vectors
+    // (nv = 8060, nc = 16120) read from L2, where four iterations' loads in
+    // flight pay; the small shapes measured best at OCPQP_PASS_UNROLL_N (1)
+    static constexpr int PU = BIG ? 4 : OCPQP_PASS_UNROLL_N;
     // resident CTAs per SM the register allocation must allow (latency hiding
     // across QPs): 512 threads per SM
     static constexpr int MINB = TEAM >= OCPQP_MINB_THREADS ? 1 : OCPQP_MINB_THREADS / TEAM;
@@ -843,7 +877,7 @@ struct Kern {
     // materialised row vector (saves a pass and a barrier each time) ----
     // slot pair (lower, upper) of variable j's box row, or -1
     __device__ static __forceinline__ int box_slot(const RD& d, const int* var_box, int j, int n, int& kup) {
-        const int kb = var_box[j];
+        const int kb = (NG == 0 && d.fullb) ? j - n * NW : var_box[j];
         if (kb < 0) return -1;
         const int k = n * 2 * d.M + kb;
         kup = k + (n < d.N ? d.M : d.MN);
@@ -856,7 +890,7 @@ struct Kern {
         const int kk = k - n * 2 * d.M;
         const bool lo = kk < m;
         const int i = lo ? kk : kk - m;
-        const double v = y[n * NW + idxb[n * d.NB + i]];
+        const double v = y[n * NW + ((NG == 0 && d.fullb) ? i : idxb[n * d.NB + i])];
         return lo ? v : -v;
     }
 
@@ -867,7 +901,8 @@ struct Kern {
 
     // ---------------- residuals (view.py:272-288) ----------------
     __device__ static Res residuals(FCtx& c, const RD& d, const KParams& p, const double* y,
-                                    const double* pi, const double* lam, const double* t) {
+                                    const double* pi, const double* lam, const double* t,
+                                    double* stg = nullptr, Tma* tm = nullptr) {
         const double* act = c.w[WS_DVEC];  // NaN = inactive
         const double* dvec = c.w[WS_DVEC];
         double* rowv = c.w[WS_ROWV];
@@ -973,103 +1008,172 @@ struct Kern {
             ab.add(r);
         };
         if constexpr (S::BIG) {
-            // one warp per stage, 8-lane groups per row: the lanes of a group
-            // read consecutive elements of the row (coalesced loads instead of
-            // one row per thread), butterfly-reduced; each warp bulk-prefetches
-            // its next stage's data into L2.  Rows per stage: the NW r_g rows,
-            // then the NX r_b rows (terminal stage: its NX r_g rows).
-            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-            const int gl = lane & 7, rl = lane >> 3;
-            constexpr int NWARP = TEAM / 32;
-            auto pf_stage = [&](int n) {
-                if (n < d.N) {
-                    l2_prefetch_bulk(BAp(c, n), BAB);
-                    l2_prefetch_bulk(Sm(c, n), NU * NX * 8);
-                    l2_prefetch_bulk(R(c, n), NU * NU * 8);
-                }
-                l2_prefetch_bulk(Q(c, n), NX * NX * 8);
+            // Two stage-sequential passes over shared-memory copies of each
+            // stage's data AND iterate blocks, double-buffered by TMA (the
+            // stage tile is free between factor / solve calls), one row per
+            // thread with the same operations and order as rg_item / rb_item:
+            //   A: [B A]'_n, w_n, x_{n+1}, pi_n, b_n -> r_b rows, and
+            //      a_j = ([B A]' pi_n)_j into r_g as a partial;
+            //   B: Q_n, S_n, R_n, w_n, pi_{n-1}, lam_n, act_n, q_n, r_n ->
+            //      r_g = (h1 + h2) + g - (atp - a) - (lam_lo - lam_up)
+            const int tid = threadIdx.x;
+            const int N = d.N;
+            const bool full_box = p.box_ident && d.NB == NW && d.NBN == NX && d.NGN == 0;
+            constexpr int AW = NW * NX, AX = AW + NW, AP = AX + NX, AB = AP + NX, ASZ = AB + NX;
+            constexpr int BS = NX * NX, BR = BS + NU * NX, BW = BR + NU * NU, BP = BW + NW,
+                          BL = BP + NX, BA_ = BL + 2 * NW, BQ = BA_ + 2 * NW, BRV = BQ + NX,
+                          BSZ = BRV + NU;
+            static_assert(2 * ASZ <= NX * NX + 2 * NW * NX && 2 * BSZ <= NX * NX + 2 * NW * NX,
+                          "residual buffers");
+            static_assert(ASZ % 2 == 0 && BSZ % 2 == 0 && AW % 2 == 0 && BW % 2 == 0 && BP % 2 == 0 &&
+                          BL % 2 == 0 && BA_ % 2 == 0 && BQ % 2 == 0 && BRV % 2 == 0, "16-byte slots");
+            const double* act_g = c.w[WS_DVEC];
+            // the iterate was written through the generic proxy
+            asm volatile("fence.proxy.async;\n" ::: "memory");
+            bar<TEAM>();
+            auto cp = [&](double* dst, const double* src, int nd, int b) {
+                tma_load_1d(dst, src, (unsigned)nd * 8u, &c.mbar[b]);
             };
-            if (lane == 0 && warp <= d.N) pf_stage(warp);
-            for (int n = warp; n <= d.N; n += NWARP) {
-                if (lane == 0 && n + NWARP <= d.N) pf_stage(n + NWARP);
-                const bool term = n == d.N;
-                const int nrow = term ? NX : NW + NX;
-                const double* w = y + n * NW;
-                const double* pn = pi + n * NX;
-                const double* Qs = Q(c, n);
-                const double* Ss = Sm(c, n);
-                const double* Rs = R(c, n);
-                const double* BAs = BAp(c, n);
-                // lane gl of a group covers k = gl, gl + 8, ... (compile-time
-                // trip counts: the loads of a row issue together)
-#define OCPQP_G8(KN, BODY)                                        \
-    _Pragma("unroll") for (int k8 = 0; k8 < ((KN) + 7) / 8; ++k8) { \
-        const int k = gl + 8 * k8;                                \
-        if (k < (KN)) { BODY; }                                   \
-    }
-                for (int r0 = 0; r0 < nrow; r0 += 4) {
-                    const int r = r0 + rl;
-                    double h = 0.0, a = 0.0;
-                    if (r < nrow) {
-                        if (term) {
-                            const double* Qr = Qs + r * NX;
-                            OCPQP_G8(NX, h = fma(Qr[k], w[k], h))
-                        } else if (r < NW) {
-                            if (r < NU) {
-                                const double* Rr = Rs + r * NU;
-                                const double* Sr = Ss + r * NX;
-                                OCPQP_G8(NU, h = fma(Rr[k], w[k], h))
-                                OCPQP_G8(NX, h = fma(Sr[k], w[NU + k], h))
-                            } else {
-                                const int jx = r - NU;
-                                const double* Qr = Qs + jx * NX;
-                                OCPQP_G8(NU, h = fma(Ss[k * NX + jx], w[k], h))
-                                OCPQP_G8(NX, h = fma(Qr[k], w[NU + k], h))
-                            }
-                            const double* BAc = BAs + r * BJ;   // column r of [B A]
-                            OCPQP_G8(NX, a = fma(BAc[k * BK], pn[k], a))
-                        } else {
-                            const double* BAr = BAs + (r - NW) * BK;   // row of [B A]
-                            OCPQP_G8(NW, h = fma(BAr[k * BJ], w[k], h))
-                        }
+            auto issue_A = [&](int n) {
+                const int b = n & 1;
+                if (tid == 0) {
+                    double* dst = stg + b * ASZ;
+                    fence_proxy_async();
+                    mbar_expect_tx(&c.mbar[b], (AW + NW + 3 * NX) * 8);
+                    cp(dst, BAp(c, n), AW, b);
+                    cp(dst + AW, y + n * NW, NW, b);
+                    cp(dst + AX, y + (n + 1) * NW + (n + 1 < N ? NU : 0), NX, b);
+                    cp(dst + AP, pi + n * NX, NX, b);
+                    cp(dst + AB, bv(c, n), NX, b);
+                }
+                tm->issue(c.mbar, b);
+            };
+            auto issue_B = [&](int n) {
+                const int b = n & 1;
+                if (tid == 0) {
+                    double* dst = stg + b * BSZ;
+                    const int m2 = n < N ? 2 * d.M : 2 * d.MN;
+                    const int nw = n < N ? NW : NX;
+                    unsigned bytes = (BS + nw + NX) * 8;
+                    if (n < N) bytes += (NU * NX + NU * NU + NU) * 8;
+                    if (n > 0) bytes += NX * 8;
+                    if (full_box) bytes += 2 * m2 * 8;
+                    fence_proxy_async();
+                    mbar_expect_tx(&c.mbar[b], bytes);
+                    cp(dst, Q(c, n), BS, b);
+                    cp(dst + BW, y + n * NW, nw, b);
+                    cp(dst + BQ, qv(c, n), NX, b);
+                    if (n < N) {
+                        cp(dst + BS, Sm(c, n), NU * NX, b);
+                        cp(dst + BR, R(c, n), NU * NU, b);
+                        cp(dst + BRV, rv(c, n), NU, b);
                     }
-#undef OCPQP_G8
-#pragma unroll
-                    for (int o = 4; o > 0; o >>= 1) {
-                        h += __shfl_xor_sync(FULL, h, o);
-                        a += __shfl_xor_sync(FULL, a, o);
-                    }
-                    if (r < nrow && gl == 0) {
-                        if (term || r < NW) {
-                            const int j = n * NW + r;
-                            double rr;
-                            if (term) {
-                                rr = h + qv(c, n)[r];
-                                rr -= d.N > 0 ? pi[(n - 1) * NX + r] : 0.0;
-                            } else {
-                                rr = h + (r < NU ? rv(c, n)[r] : qv(c, n)[r - NU]);
-                                double atp = (r >= NU && n > 0) ? pi[(n - 1) * NX + (r - NU)] : 0.0;
-                                atp -= a;
-                                rr -= atp;
-                            }
-                            int kup;
-                            const int klo = box_slot(d, p.var_box, j, n, kup);
-                            if (klo >= 0) {
-                                const double ll = !isnan(act[klo]) ? lam[klo] : 0.0;
-                                const double lu = !isnan(act[kup]) ? lam[kup] : 0.0;
-                                rr -= ll - lu;
-                            }
-                            r_g[j] = rr;
-                            ag.add(rr);
-                        } else {
-                            const int i = r - NW;
-                            const double xn = y[(n + 1) * NW + (n + 1 < d.N ? NU : 0) + i];
-                            const double rr = -(xn - h) + bv(c, n)[i];
-                            r_b[n * NX + i] = rr;
-                            ab.add(rr);
-                        }
+                    if (n > 0) cp(dst + BP, pi + (n - 1) * NX, NX, b);
+                    if (full_box) {
+                        cp(dst + BL, lam + n * 2 * d.M, m2, b);
+                        cp(dst + BA_, act_g + n * 2 * d.M, m2, b);
                     }
                 }
+                tm->issue(c.mbar, b);
+            };
+            // ---- pass A: dynamics rows and the E' pi products ----
+            if (N > 0) issue_A(0);
+            if (N > 1) issue_A(1);
+            for (int n = 0; n < N; ++n) {
+                tm->wait(c.mbar, n & 1);
+                const double* sl = stg + (n & 1) * ASZ;
+                const double* Bt = sl;
+                const double* w = sl + AW;
+                if (tid < NX) {
+                    const int i = tid;
+                    const double* u = w;
+                    const double* x = w + NU;
+                    double ax = 0.0, bu = 0.0;
+#pragma unroll 10
+                    for (int k = 0; k < NX; ++k) ax = fma(Bt[(NU + k) * NX + i], x[k], ax);
+#pragma unroll
+                    for (int k = 0; k < NU; ++k) bu = fma(Bt[k * NX + i], u[k], bu);
+                    const double rr = -((sl[AX + i] - ax) - bu) + sl[AB + i];
+                    r_b[n * NX + i] = rr;
+                    ab.add(rr);
+                } else if (tid >= 64 && tid < 64 + NW) {
+                    const int j = tid - 64;
+                    const double* pn = sl + AP;
+                    const double* row = Bt + j * NX;
+                    double a = 0.0;
+#pragma unroll 10
+                    for (int k = 0; k < NX; ++k) a = fma(row[k], pn[k], a);
+                    r_g[n * NW + j] = a;
+                }
+                bar<TEAM>();
+                if (n + 2 < N) issue_A(n + 2);
+            }
+            // ---- pass B: the cost rows ----
+            issue_B(0);
+            if (N > 0) issue_B(1);
+            for (int n = 0; n <= N; ++n) {
+                tm->wait(c.mbar, n & 1);
+                const double* sl = stg + (n & 1) * BSZ;
+                const double* Qs = sl;
+                const double* Ss = sl + BS;
+                const double* Rs = sl + BR;
+                const double* w = sl + BW;
+                const int nr = n < N ? NW : NX;
+                if (tid < nr) {
+                    const int jj = tid, j = n * NW + jj;
+                    double rr;
+                    if (n < N) {
+                        double h1 = 0.0, h2 = 0.0, g;
+                        if (jj < NU) {
+                            const double* Rr = Rs + jj * NU;
+                            const double* Sr = Ss + jj * NX;
+#pragma unroll
+                            for (int k = 0; k < NU; ++k) h1 = fma(Rr[k], w[k], h1);
+#pragma unroll 10
+                            for (int k = 0; k < NX; ++k) h2 = fma(Sr[k], w[NU + k], h2);
+                            g = sl[BRV + jj];
+                        } else {
+                            const int jx = jj - NU;
+                            const double* Qr = Qs + jx * NX;
+#pragma unroll
+                            for (int k = 0; k < NU; ++k) h1 = fma(Ss[k * NX + jx], w[k], h1);
+#pragma unroll 10
+                            for (int k = 0; k < NX; ++k) h2 = fma(Qr[k], w[NU + k], h2);
+                            g = sl[BQ + jx];
+                        }
+                        rr = (h1 + h2) + g;
+                        double atp = (jj >= NU && n > 0) ? sl[BP + (jj - NU)] : 0.0;
+                        atp -= r_g[j];
+                        rr -= atp;
+                    } else {
+                        const double* Qr = Qs + jj * NX;
+                        double h2 = 0.0;
+#pragma unroll 10
+                        for (int k = 0; k < NX; ++k) h2 = fma(Qr[k], w[k], h2);
+                        rr = (0.0 + h2) + sl[BQ + jj];
+                        rr -= N > 0 ? sl[BP + jj] : 0.0;
+                    }
+                    double rt = 0.0;
+                    if (full_box) {
+                        const int m = n < N ? d.M : d.MN;
+                        const double ll = !isnan(sl[BA_ + jj]) ? sl[BL + jj] : 0.0;
+                        const double lu = !isnan(sl[BA_ + m + jj]) ? sl[BL + m + jj] : 0.0;
+                        rt = ll - lu;
+                    } else {
+                        int kup;
+                        const int klo = box_slot(d, p.var_box, j, n, kup);
+                        if (klo >= 0) {
+                            const double ll = !isnan(act[klo]) ? lam[klo] : 0.0;
+                            const double lu = !isnan(act[kup]) ? lam[kup] : 0.0;
+                            rt = ll - lu;
+                        }
+                    }
+                    rr -= rt;
+                    r_g[j] = rr;
+                    ag.add(rr);
+                }
+                bar<TEAM>();
+                if (n + 2 <= N) issue_B(n + 2);
             }
         } else {
             OCPQP_PASS_UNROLL
@@ -1362,7 +1466,7 @@ struct Kern {
                 const double* Rn = R(c, n);
                 const double* Sn = Sm(c, n);
                 const double* cf = coef + n * d.M;
-                const bool full_box = d.NB == NW;
+                const bool full_box = p.box_ident && d.NB == NW;
                 if (warp_id_uniform() == 0) {
                     // lane i: row i of G = W'W + M~ (j <= i), then the warp Cholesky
                     const int i = tid;
@@ -1607,7 +1711,7 @@ struct Kern {
             const double* Rn = pq ? H + fR : R(c, n);
             const double* Sn = pq ? H + fS : Sm(c, n);
             const double* cf = coef + n * d.M;
-            const bool full_box = d.NB == NW;
+            const bool full_box = p.box_ident && d.NB == NW;
             auto Mt = [&](int i, int j) -> double {
                 double mij, mji;
                 if (i < NU && j < NU) { mij = Rn[i * NU + j]; mji = Rn[j * NU + i]; }
@@ -1769,27 +1873,48 @@ struct Kern {
         tm.issue(c.mbar, b);
     }
 
-    // L_uu = chol(G_uu) in one warp, rows in registers (warp_chol_rolled;
-    // linalg.py:81-118 pivot test); L to shared memory (Ls) and the factor
-    // store, 1 / L_kk to rinv and the store; c.flag = success
+    // L_uu = chol(G_uu) by one warp with the rows in registers as a shift
+    // register: at pivot k, r[m] holds A(lane, k + m), so every register index
+    // is a compile-time constant while the pivot loop stays rolled (no
+    // dynamically indexed array, no full unroll).  The next pivot's diagonal
+    // update is lane-local; the other updates take one shuffle each.  Same
+    // operations and order as warp_chol (linalg.py:81-118 pivot test); L (lower,
+    // zero upper) to shared memory (Ls) and the factor store, 1 / L_kk to rinv
+    // and the store; c.flag = success.
     __device__ __forceinline__ static void chol_big(FCtx& c, const double* Gu, double* Ls, double* Ln,
                                                     double* Rinv_n, double* rinv) {
         const int lane = threadIdx.x & 31;
-        double row[NU];
-        double rin = 0.0;
+        double r[NU];
 #pragma unroll
-        for (int j = 0; j < NU; ++j) row[j] = (lane < NU && j <= lane) ? Gu[lane * GLD + j] : 0.0;
-        const bool ok = warp_chol_rolled<NU>(row, lane, rin);
+        for (int m = 0; m < NU; ++m) r[m] = (lane < NU && m <= lane) ? Gu[lane * GLD + m] : 0.0;
+        bool ok = true;
+#pragma unroll 1
+        for (int k = 0; k < NU; ++k) {
+            const double piv = __shfl_sync(FULL, r[0], k);
+            ok = ok && (piv > 0.0);
+            const double inv = rsqrt(piv);
+            const double lik = lane == k ? piv * inv : r[0] * inv;
+            if (lane == k) rinv[k] = inv;
+            if (lane >= k && lane < NU) Ls[lane * NU + k] = lik;
+            // unconditional update: for lane < k + m the entry (lane, k + m) is
+            // in the upper triangle, never read by a later pivot or stored
+#pragma unroll
+            for (int m = 1; m < NU; ++m) {
+                const int src = k + m < 32 ? k + m : 31;
+                r[m - 1] = fma(-lik, __shfl_sync(FULL, lik, src), r[m]);
+            }
+            r[NU - 1] = 0.0;
+        }
         if (lane == 0) c.flag = ok;
+        __syncwarp();
         if (ok && lane < NU) {
 #pragma unroll
-            for (int j = 0; j < NU; ++j) {
-                const double v = j <= lane ? row[j] : 0.0;
-                Ls[lane * NU + j] = v;
-                Ln[lane * NU + j] = v;
+            for (int m = 0; m < NU; ++m) {
+                const double v = m <= lane ? Ls[lane * NU + m] : 0.0;
+                Ls[lane * NU + m] = v;
+                Ln[lane * NU + m] = v;
             }
-            rinv[lane] = rin;
-            Rinv_n[lane] = rin;
+            Rinv_n[lane] = rinv[lane];
         }
     }
 
@@ -1982,7 +2107,7 @@ struct Kern {
             const double* Qn = Q(c, n);
             const double* Rn = R(c, n);
             const double* Sn = Sm(c, n);
-            const bool full_box = d.NB == NW;
+            const bool full_box = p.box_ident && d.NB == NW;
             auto Mt = [&](int i, int j) -> double {
                 double mij, mji;
                 if (i < NU && j < NU) { mij = Rn[i * NU + j]; mji = Rn[j * NU + i]; }
@@ -2001,23 +2126,20 @@ struct Kern {
                 if (task < NUR * NRP) { rp = task / NRP; cp = task % NRP; }
                 else { const int u = task - NUR * NRP; rp = NUR + u / (NRP - CP0); cp = CP0 + u % (NRP - CP0); }
             };
-            double g[GROUNDS][2][2][2];
-            // accumulators start as M~: every round's loads issued before the first k loop
-#pragma unroll
-            for (int r = 0; r < GROUNDS; ++r) {
-                const int task = warp + 8 * r;
-                if (task < NGT) {
-                    int rp, cp;
-                    gtask(task, rp, cp);
-#pragma unroll
-                    for (int ti = 0; ti < 2; ++ti)
-#pragma unroll
-                        for (int tj = 0; tj < 2; ++tj)
-#pragma unroll
-                            for (int e = 0; e < 2; ++e)
-                                g[r][ti][tj][e] = Mt(16 * rp + 8 * ti + gr, 16 * cp + 8 * tj + 2 * tg + e);
-                }
+            // Q_n of M~ into P_{n+1}'s area (dead after T1) by TMA while the k loops run
+            if (tid == 0) {
+                fence_proxy_async();
+                mbar_expect_tx(&c.mbar[1], NX * NX * 8);
+                tma_load_1d(Pc, Qn, NX * NX * 8, &c.mbar[1]);
             }
+            tm.issue(c.mbar, 1);
+            double g[GROUNDS][2][2][2];
+#pragma unroll
+            for (int r = 0; r < GROUNDS; ++r)
+#pragma unroll
+                for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+                    for (int tj = 0; tj < 2; ++tj) g[r][ti][tj][0] = g[r][ti][tj][1] = 0.0;
 #pragma unroll
             for (int r = 0; r < GROUNDS; ++r) {
                 const int task = warp + 8 * r;
@@ -2037,6 +2159,36 @@ struct Kern {
 #pragma unroll
                             for (int tj = 0; tj < 2; ++tj) dmma_acc(g[r][ti][tj][0], g[r][ti][tj][1], a[ti], b[tj]);
                     }
+                }
+            }
+            // G = ([B A]' T1) + M~ (the reference's matmul_acc order): Q from
+            // shared memory, R and S (L2-prefetched) from global memory
+            tm.wait(c.mbar, 1);
+            auto Mts = [&](int i, int j) -> double {
+                if (i >= NU && j >= NU) {
+                    double h = 0.5 * (Pc[(i - NU) * NX + (j - NU)] + Pc[(j - NU) * NX + (i - NU)]);
+                    if (i == j) {
+                        const int kb = full_box ? i : p.var_box[n * NW + i];
+                        if (kb >= 0) h += cfv(n, kb);
+                        if (reg != 0.0) h += reg;
+                    }
+                    return h;
+                }
+                return Mt(i, j);
+            };
+#pragma unroll
+            for (int r = 0; r < GROUNDS; ++r) {
+                const int task = warp + 8 * r;
+                if (task < NGT) {
+                    int rp, cp;
+                    gtask(task, rp, cp);
+#pragma unroll
+                    for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+                        for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e)
+                                g[r][ti][tj][e] += Mts(16 * rp + 8 * ti + gr, 16 * cp + 8 * tj + 2 * tg + e);
                 }
             }
             bar<TEAM>();   // every warp is done with T1' and [B A]'
@@ -2222,19 +2374,28 @@ struct Kern {
         }
     }
 
-    // Riccati solve sweeps of a BIG shape (kkt_ocp.py:270-305), with the dpi
-    // recursion fused into the forward sweep.  The per-stage operands stream
-    // through the stage tile by TMA: [B A]' double-buffered (the first
-    // 2 NW NX doubles), the small blocks single-buffered in the remaining NX^2,
-    // each block issued as soon as its previous contents are consumed; the
+    // Riccati solve sweeps of a BIG shape (kkt_ocp.py:270-305) in two team
+    // phases per stage, with the dpi recursion fused into the forward sweep.
+    // Backward stage n:
+    //   A: win = rhat_n + [B A]' (q_n + p_{n+1})      (q_n = P_{n+1} r_b,n from B of n+1)
+    //   B: p_n = rq + K' rr (warps 4-6) | k_n = -G_uu^{-1} rr (warp 7) |
+    //      q_{n-1} = P_n r_b,n-1 (warps 0-3): the P r_b product of the next
+    //      stage does not depend on p_n (kkt_ocp.py:282 split as P r_b + p)
+    // Forward stage n:
+    //   A: u_n = K_n x_n + k_n  and  dpi_{n-1} = P_n x_n + pv_n  (one MV)
+    //   B: x_{n+1} = A x_n + B u_n + r_b,n
+    // Operands stream through the stage tile by TMA: [B A]' double-buffered
+    // (2 NW NX doubles), the per-stage block single-buffered in the remaining
+    // NX^2, each issued as soon as its previous contents are consumed; the
     // operands three stages ahead are bulk-prefetched into L2.
-    //   backward n: O1 = [P_{n+1} (packed), r_b,n]  O2 = [K_n, L_n, 1/L_ii, rhat_n]
-    //   forward  n: F1 = [K_n, kff_n]                F2 = [r_b,n, P_{n+1}, pv_{n+1}]
-    // Barriers: 0 / 1 the [B A]' slots, 2 O1 / F2, 3 O2 / F1.  Returns the
-    // thread's non-finite flag of dpi.
+    //   backward Y_n = [K_n, L_n, 1/L_ii, P_n (packed), r_b,n-1, rhat_{n-1}]
+    //   forward  F_n = [K_n, kff_n, r_b,n, P_n (packed), pv_n]
+    // Barriers: 0 / 1 the [B A]' slots, 2 the block.  Returns the thread's
+    // non-finite flag of dpi.
     __device__ __noinline__ static int sweeps_big(FCtx& c, const RD& d, const KParams& p, double* stg,
                                                   double* dy, double* dpi, long long& flops, Tma& tm) {
         const int tid = threadIdx.x;
+        const int warp = warp_id_uniform();
         const double* r_b = wsb<WS_RB>(c, p);
         const double* rhat = wsb<WS_RHAT>(c, p);
         const double* Pst = wsb<WS_P>(c, p);
@@ -2245,48 +2406,42 @@ struct Kern {
         double* kff = wsb<WS_KFF>(c, p);
         double* vec = stg + S::VOFF;
         double* win = vec;          // NW
-        double* e = win + NW;       // NX
-        double* pvs = e + NX;       // NX: pv_{n+1}
+        double* qv = win + NW;      // NX: q = P r_b of the stage
+        double* pvs = qv + NX;      // NX: p_{n+1}
         double* xa = pvs + NX;      // NX: x_n
         double* uv = xa + NX;       // NU: u_n
         double* xb = uv + NU;       // NX: x_{n+1}
+        double* rhs = xb + NX;      // NW: rhat of the stage / r_b of the stage
         constexpr int PS = S::PST;
         double* sBA[2] = {stg, stg + NW * NX};
-        double* pool = stg + 2 * NW * NX;   // NX * NX doubles
-        constexpr int O1N = PS + NX, O2N = NU * NX + NU * NU + NU + NW;
-        constexpr int F1N = NU * NX + NU, F2N = NX + PS + NX;
-        static_assert(O1N + O2N <= NX * NX && F1N + F2N <= NX * NX, "sweeps_big pool");
-        static_assert(O1N % 2 == 0 && F1N % 2 == 0, "16-byte aligned TMA destinations");
-        double* sO1 = pool;
-        double* sO2 = pool + O1N;
-        double* sF1 = pool;
-        double* sF2 = pool + F1N;
+        double* blk = stg + 2 * NW * NX;   // NX * NX doubles
+        constexpr int YK = 0, YL = NU * NX, YR = YL + NU * NU, YP = YR + NU, YB = YP + PS, YH = YB + NX,
+                      YN = YH + NW;
+        constexpr int FK = 0, FF = NU * NX, FB = FF + NU, FP = FB + NX, FV = FP + PS, FN = FV + NX;
+        static_assert(YN <= NX * NX && FN <= NX * NX, "sweeps_big block");
+        static_assert(YL % 2 == 0 && YR % 2 == 0 && YP % 2 == 0 && YB % 2 == 0 && YH % 2 == 0 &&
+                      FF % 2 == 0 && FB % 2 == 0 && FP % 2 == 0 && FV % 2 == 0, "16-byte block offsets");
+        static_assert(NW + 4 * NX + NU + NW <= S::VECB, "sweeps_big vectors");
         const int N = d.N;
-        // the factor store, r_b and rhat were written through the generic proxy:
-        // order them before the copy engine reads them
+        // the factor store, r_b and rhat were written through the generic proxy
         asm volatile("fence.proxy.async;\n" ::: "memory");
-        auto cp = [&](double* dst, const double* src, int nd, int b) {
-            tma_load_1d(dst, src, (unsigned)nd * 8u, &c.mbar[b]);
+        auto cp = [&](double* dst, const double* src, int nd) {
+            tma_load_1d(dst, src, (unsigned)nd * 8u, &c.mbar[2]);
         };
-        auto issue_O1 = [&](int n) {
+        auto issue_Y = [&](int n) {   // K_n, L_n, 1/L_ii, and for n > 0: P_n, r_b,n-1, rhat_{n-1}
             if (tid == 0) {
                 fence_proxy_async();
-                mbar_expect_tx(&c.mbar[2], O1N * 8);
-                cp(sO1, Pst + (n + 1) * PS, PS, 2);
-                cp(sO1 + PS, r_b + n * NX, NX, 2);
+                mbar_expect_tx(&c.mbar[2], (n > 0 ? YN : YP) * 8);
+                cp(blk + YK, Kst + n * NU * NX, NU * NX);
+                cp(blk + YL, Lst + n * NU * NU, NU * NU);
+                cp(blk + YR, Rst + n * NU, NU);
+                if (n > 0) {
+                    cp(blk + YP, Pst + n * PS, PS);
+                    cp(blk + YB, r_b + (n - 1) * NX, NX);
+                    cp(blk + YH, rhat + (n - 1) * NW, NW);
+                }
             }
             tm.issue(c.mbar, 2);
-        };
-        auto issue_O2 = [&](int n) {
-            if (tid == 0) {
-                fence_proxy_async();
-                mbar_expect_tx(&c.mbar[3], O2N * 8);
-                cp(sO2, Kst + n * NU * NX, NU * NX, 3);
-                cp(sO2 + NU * NX, Lst + n * NU * NU, NU * NU, 3);
-                cp(sO2 + NU * NX + NU * NU, Rst + n * NU, NU, 3);
-                cp(sO2 + NU * NX + NU * NU + NU, rhat + n * NW, NW, 3);
-            }
-            tm.issue(c.mbar, 3);
         };
         auto l2pf = [&](int n) {
             if (tid == 0 && n >= 0 && n < N) {
@@ -2301,85 +2456,81 @@ struct Kern {
             pv[N * NX + i] = v;
             pvs[i] = v;
         }
-        bar<TEAM>();
         if (N > 0) {
-            issue_O1(N - 1);
             tma_ba(c, tm, sBA[(N - 1) & 1], N - 1, (N - 1) & 1);
-            issue_O2(N - 1);
+            issue_Y(N - 1);
             if (N > 1) tma_ba(c, tm, sBA[(N - 2) & 1], N - 2, (N - 2) & 1);
             l2pf(N - 3);
+            // q_{N-1} = P_N r_b,N-1 and rhat_{N-1} from global memory
+            const double* PN = Pst + N * PS;
+            const double* rbN = r_b + (N - 1) * NX;
+            MV<NX, NX, TEAM>::run([&](int i, int k) { return Pget(PN, i, k); },
+                                  [&](int k) { return rbN[k]; }, [&](int i, double v) { qv[i] = v; });
+            for (int i = tid; i < NW; i += TEAM) rhs[i] = rhat[(N - 1) * NW + i];
         }
+        bar<TEAM>();
         for (int n = N - 1; n >= 0; --n) {
             const int s = n & 1;
             l2pf(n - 3);
-            // e = P_{n+1} r_b + p_{n+1}
-            tm.wait(c.mbar, 2);
-            MV<NX, NX, TEAM>::run([&](int i, int k) { return Pget(sO1, i, k); },
-                                  [&](int k) { return sO1[PS + k]; },
-                                  [&](int i, double v) { e[i] = v + pvs[i]; });
-            bar<TEAM>();
-            if (n > 0) issue_O1(n - 1);
-            // rr, rq = rhat + [B A]' e
+            // A: rr, rq = rhat + [B A]' (P_{n+1} r_b + p_{n+1})
             tm.wait(c.mbar, s);
-            tm.wait(c.mbar, 3);
-            const double* rh = sO2 + NU * NX + NU * NU + NU;
             const double* BAn = sBA[s];
             MV<NW, NX, TEAM>::run([&](int j, int k) { return BAn[j * NX + k]; },
-                                  [&](int k) { return e[k]; },
-                                  [&](int j, double v) { win[j] = rh[j] + v; });
+                                  [&](int k) { return qv[k] + pvs[k]; },
+                                  [&](int j, double v) { win[j] = rhs[j] + v; });
             bar<TEAM>();
             if (n > 1) tma_ba(c, tm, sBA[s], n - 2, s);
-            // p_n = rq + K' rr on all warps but the last; k_n = -G_uu^{-1} rr on the last
-            const double* Kn = sO2;
-            const double* Ln = sO2 + NU * NX;
-            const double* Rn = Ln + NU * NU;
+            // B: p_n, k_n, and q_{n-1} for the next stage
+            tm.wait(c.mbar, 2);
+            const double* Kn = blk + YK;
+            const double* Ln = blk + YL;
+            const double* Rn = blk + YR;
             double* pvc = pv + n * NX;
-            if (warp_id_uniform() == TEAM / 32 - 1)
+            if (warp == TEAM / 32 - 1) {
                 warp_cho_solve<NU>(Ln, Rn, win, kff + n * NU, -1.0);
-            else
-                MV<NX, NU, TEAM - 32>::run([&](int i, int k) { return Kn[k * NX + i]; },
-                                           [&](int k) { return win[k]; },
-                                           [&](int i, double v) {
-                                               const double r = win[NU + i] + v;
-                                               pvc[i] = r;
-                                               pvs[i] = r;
-                                           });
+            } else if (warp >= 4) {
+                MVo<NX, NU, TEAM - 160, 128>::run([&](int i, int k) { return Kn[k * NX + i]; },
+                                                  [&](int k) { return win[k]; },
+                                                  [&](int i, double v) {
+                                                      const double r = win[NU + i] + v;
+                                                      pvc[i] = r;
+                                                      pvs[i] = r;
+                                                  });
+            } else if (n > 0) {
+                const double* Pn = blk + YP;
+                const double* rbm = blk + YB;
+                MVo<NX, NX, 128, 0>::run([&](int i, int k) { return Pget(Pn, i, k); },
+                                         [&](int k) { return rbm[k]; }, [&](int i, double v) { qv[i] = v; });
+                for (int i = tid; i < NW; i += 128) rhs[i] = blk[YH + i];
+            }
             flops += 2ll * NU * NU;
             bar<TEAM>();
-            if (n > 0) issue_O2(n - 1);
+            if (n > 0) issue_Y(n - 1);
         }
         OCPQP_TICK(c, DBG_S_BWD);
         // x0 step: dx_0 = -P_0^{-1} p_0
-        if (warp_id_uniform() == 0) warp_cho_solve<NX>(wsb<WS_LP0>(c, p), Rst + N * NU, pvs, xa, -1.0);
+        if (warp == 0) warp_cho_solve<NX>(wsb<WS_LP0>(c, p), Rst + N * NU, pvs, xa, -1.0);
         flops += 2ll * NX * NX;
         // kff / pv of this solve were written through the generic proxy
         asm volatile("fence.proxy.async;\n" ::: "memory");
         bar<TEAM>();
         // ---- forward rollout (kkt_ocp.py:293-305) ----
-        auto issue_F1 = [&](int n) {
+        auto issue_F = [&](int n) {   // K_n, kff_n, r_b,n, P_n, pv_n
             if (tid == 0) {
                 fence_proxy_async();
-                mbar_expect_tx(&c.mbar[3], F1N * 8);
-                cp(sF1, Kst + n * NU * NX, NU * NX, 3);
-                cp(sF1 + NU * NX, kff + n * NU, NU, 3);
-            }
-            tm.issue(c.mbar, 3);
-        };
-        auto issue_F2 = [&](int n) {
-            if (tid == 0) {
-                fence_proxy_async();
-                mbar_expect_tx(&c.mbar[2], F2N * 8);
-                cp(sF2, r_b + n * NX, NX, 2);
-                cp(sF2 + NX, Pst + (n + 1) * PS, PS, 2);
-                cp(sF2 + NX + PS, pv + (n + 1) * NX, NX, 2);
+                mbar_expect_tx(&c.mbar[2], FN * 8);
+                cp(blk + FK, Kst + n * NU * NX, NU * NX);
+                cp(blk + FF, kff + n * NU, NU);
+                cp(blk + FB, r_b + n * NX, NX);
+                cp(blk + FP, Pst + n * PS, PS);
+                cp(blk + FV, pv + n * NX, NX);
             }
             tm.issue(c.mbar, 2);
         };
         for (int i = tid; i < NX; i += TEAM) dy[(N > 0 ? NU : 0) + i] = xa[i];
         if (N > 0) {
-            issue_F1(0);
+            issue_F(0);
             tma_ba(c, tm, sBA[0], 0, 0);
-            issue_F2(0);
             if (N > 1) tma_ba(c, tm, sBA[1], 1, 1);
             l2pf(2);
         }
@@ -2387,48 +2538,69 @@ struct Kern {
         for (int n = 0; n < N; ++n) {
             const int s = n & 1;
             l2pf(n + 3);
-            // u_n = K_n x_n + k_n
-            tm.wait(c.mbar, 3);
-            double* du = dy + n * NW;
-            MV<NU, NX, TEAM>::run([&](int i, int k) { return sF1[i * NX + k]; },
-                                  [&](int k) { return xa[k]; },
-                                  [&](int i, double v) {
-                                      const double u = v + sF1[NU * NX + i];
-                                      du[i] = u;
-                                      uv[i] = u;
-                                  });
-            bar<TEAM>();
-            if (n + 1 < N) issue_F1(n + 1);
-            // x_{n+1} = A x_n + B u_n + r_b,n
-            tm.wait(c.mbar, s);
+            // A: u_n = K_n x_n + k_n; dpi_{n-1} = P_n x_n + pv_n (kkt_ocp.py:296-304)
             tm.wait(c.mbar, 2);
+            double* du = dy + n * NW;
+            const double* Kn = blk + FK;
+            const double* kf = blk + FF;
+            const double* Pn = blk + FP;
+            const double* pvn = blk + FV;
+            if (n > 0) {
+                MV<NU + NX, NX, TEAM>::run(
+                    [&](int i, int k) { return i < NU ? Kn[i * NX + k] : Pget(Pn, i - NU, k); },
+                    [&](int k) { return xa[k]; },
+                    [&](int i, double v) {
+                        if (i < NU) {
+                            const double u = v + kf[i];
+                            du[i] = u;
+                            uv[i] = u;
+                        } else {
+                            const double w = v + pvn[i - NU];
+                            dpi[(n - 1) * NX + (i - NU)] = w;
+                            if (!isfinite(w)) nonfinite = 1;
+                        }
+                    });
+            } else {
+                MV<NU, NX, TEAM>::run([&](int i, int k) { return Kn[i * NX + k]; },
+                                      [&](int k) { return xa[k]; },
+                                      [&](int i, double v) {
+                                          const double u = v + kf[i];
+                                          du[i] = u;
+                                          uv[i] = u;
+                                      });
+            }
+            for (int i = tid; i < NX; i += TEAM) rhs[i] = blk[FB + i];
+            bar<TEAM>();
+            if (n + 1 < N) issue_F(n + 1);
+            // B: x_{n+1} = A x_n + B u_n + r_b,n
+            tm.wait(c.mbar, s);
             const double* BAn = sBA[s];
             double* xd = dy + (n + 1) * NW + (n + 1 < N ? NU : 0);
             MV<NX, NW, TEAM>::run(
                 [&](int i, int k) { return k < NX ? BAn[(NU + k) * NX + i] : BAn[(k - NX) * NX + i]; },
                 [&](int k) { return k < NX ? xa[k] : uv[k - NX]; },
                 [&](int i, double v) {
-                    const double x = v + sF2[i];
+                    const double x = v + rhs[i];
                     xb[i] = x;
                     xd[i] = x;
                 });
             bar<TEAM>();
             if (n + 2 < N) tma_ba(c, tm, sBA[s], n + 2, s);
-            // dpi_n = P_{n+1} x_{n+1} + pv_{n+1}
-            const double* Pn = sF2 + NX;
-            const double* pvn = Pn + PS;
-            MV<NX, NX, TEAM>::run([&](int i, int k) { return Pget(Pn, i, k); },
-                                  [&](int k) { return xb[k]; },
-                                  [&](int i, double v) {
-                                      const double w = v + pvn[i];
-                                      dpi[n * NX + i] = w;
-                                      if (!isfinite(w)) nonfinite = 1;
-                                  });
-            bar<TEAM>();
-            if (n + 1 < N) issue_F2(n + 1);
             double* sw = xa;
             xa = xb;
             xb = sw;
+        }
+        // dpi_{N-1} = P_N x_N + pv_N
+        if (N > 0) {
+            const double* PN = Pst + N * PS;
+            const double* pvN = pv + N * NX;
+            MV<NX, NX, TEAM>::run([&](int i, int k) { return Pget(PN, i, k); },
+                                  [&](int k) { return xa[k]; },
+                                  [&](int i, double v) {
+                                      const double w = v + pvN[i];
+                                      dpi[(N - 1) * NX + i] = w;
+                                      if (!isfinite(w)) nonfinite = 1;
+                                  });
         }
         OCPQP_TICK(c, DBG_S_FWD);
         return nonfinite;
@@ -3091,14 +3263,14 @@ struct Kern {
             for (int i = tid; i < d.ne; i += TEAM) dpi[i] = 0.0;
             for (int k = tid; k < d.nc; k += TEAM) { alam[k] = 0.0; at[k] = 0.0; }
             bar<TEAM>();
-            residuals(c, d, p, dy, dpi, alam, at);
+            residuals(c, d, p, dy, dpi, alam, at, stg, &tm);
             bar<TEAM>();
         }
         while (true) {
             flops_top = flops;
             double mu;
             if (!absf) {
-                res = residuals(c, d, p, y, pi, lam, t);
+                res = residuals(c, d, p, y, pi, lam, t, stg, &tm);
                 mu = res.mu;
                 if (!isfinite(res.g) || !isfinite(res.b) || !isfinite(res.d) || !isfinite(res.m) || !isfinite(mu))
                     status = OCPQP_STATUS_NAN;
@@ -3291,7 +3463,7 @@ struct Kern {
             return;
         }
         if (absf) {  // final residuals (solver.py:300), computed once in speed_abs
-            res = residuals(c, d, p, y, pi, lam, t);
+            res = residuals(c, d, p, y, pi, lam, t, stg, &tm);
             bar<TEAM>();
         }
         OCPQP_PASS_UNROLL
@@ -3324,6 +3496,7 @@ __global__ void __launch_bounds__(S::TEAM, S::MINB) k_fast_solve(const __grid_co
     RD d;
     d.N = p.N; d.NB = p.NB; d.M = p.NB + S::NG; d.NBN = p.NBN; d.NGN = p.NGN;
     d.MN = p.NBN + p.NGN; d.nc = p.nc; d.nv = p.nv; d.ne = p.ne; d.msum = p.msum;
+    d.fullb = p.box_ident && p.NB == S::NW && p.NBN == S::NX && p.NGN == 0;
     d.inv_m = d.M ? 1.0f / (float)d.M : 0.0f;
     d.inv_2m = d.M ? 0.5f / (float)d.M : 0.0f;
     for (int b = threadIdx.x; b < WS_EXT0; b += S::TEAM)

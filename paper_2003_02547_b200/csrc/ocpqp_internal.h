@@ -96,6 +96,7 @@ struct KParams {
     int* counter;             // dynamic QP scheduler
     // shaped-kernel structure (uniform stages 0..N-1, terminal stage N)
     int NB, NBN, NGN;         // box rows (n < N), box / general rows at N
+    int box_ident;            // 1: every stage's idxb is 0..nb-1 (box row i bounds variable i)
     int stage_smem;           // doubles: offset of the per-stage scratch / per-team tile
     int team_stride;          // doubles of shared memory per team (row kernel)
     long long* dbg;           // optional [B, 8] phase-cycle counters (nullptr = off)

@@ -382,3 +382,4 @@ def test_gpu_shaped_kernel_random_structure(cuda, oracle, speed_arg, nx, nu, ng,
                   res_bar=2.5e-7 if ng else 1e-8)
     if ng:  # lam: bounded like the config-3 known-hard row
         assert rel_err(got["lam"][0], ref["lam"][0]) <= 1e-6
+

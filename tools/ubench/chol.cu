@@ -9,6 +9,47 @@
 using namespace ocpqp::fastk;
 constexpr int NN = 20;
 
+// the shift-register variant of Kern::chol_big (ocpqp_fast.cuh), rows from smem
+__device__ __forceinline__ bool chol_shift(const double* Gu, double* Ls, double* rinv) {
+    const int lane = threadIdx.x & 31;
+    double r[NN];
+#pragma unroll
+    for (int m = 0; m < NN; ++m) r[m] = (lane < NN && m <= lane) ? Gu[lane * NN + m] : 0.0;
+    bool ok = true;
+#pragma unroll 1
+    for (int k = 0; k < NN; ++k) {
+        const double piv = __shfl_sync(0xffffffffu, r[0], k);
+        ok = ok && (piv > 0.0);
+        const double inv = rsqrt(piv);
+        const double lik = lane == k ? piv * inv : r[0] * inv;
+        if (lane == k) rinv[k] = inv;
+        if (lane >= k && lane < NN) Ls[lane * NN + k] = lik;
+#pragma unroll
+        for (int m = 1; m < NN; ++m) {
+            const int src = k + m < 32 ? k + m : 31;
+            r[m - 1] = fma(-lik, __shfl_sync(0xffffffffu, lik, src), r[m]);
+        }
+        r[NN - 1] = 0.0;
+    }
+    return ok;
+}
+
+__global__ void kshift(const double* G, double* out, long long* t, int reps) {
+    __shared__ double Gs[NN * NN], Ls[NN * NN], rv[32];
+    for (int i = threadIdx.x; i < NN * NN; i += 32) Gs[i] = G[i];
+    __syncwarp();
+    double acc = 0.0;
+    long long c0 = 0;
+    for (int r = -1; r < reps; ++r) {
+        if (r == 0) c0 = clock64();
+        acc += chol_shift(Gs, Ls, rv) ? Ls[(threadIdx.x % NN) * NN] : 1.0;
+        __syncwarp();
+    }
+    const long long c1 = clock64();
+    out[threadIdx.x] = acc;
+    if (threadIdx.x == 0) t[5] = (c1 - c0) / reps;
+}
+
 template <int V>
 __global__ void kchol(const double* G, double* out, long long* t, int reps) {
     const int lane = threadIdx.x & 31;
@@ -60,11 +101,13 @@ int main() {
     kchol<0><<<1, 32>>>(G, out, t, 64);
     kchol<1><<<1, 32>>>(G, out, t, 64);
     kops<<<1, 32>>>(out, t, 1024);
+    kshift<<<1, 32>>>(G, out, t, 64);
     cudaDeviceSynchronize();
-    long long r[5];
+    long long r[6];
     cudaMemcpy(r, t, sizeof(r), cudaMemcpyDeviceToHost);
     printf("warp_chol<20> unrolled: %lld cycles\nwarp_chol_rolled<20>: %lld cycles\n", r[0], r[1]);
     printf("dfma dep: %lld  rsqrt(double)+add dep: %lld  shfl.f64 dep: %lld cycles\n", r[2], r[3], r[4]);
+    printf("chol_big shift-register variant: %lld cycles\n", r[5]);
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
