@@ -10,8 +10,13 @@
  * Conventions
  *   - plain pointers and sizes only; no torch / C++ types cross the boundary;
  *   - all arithmetic is fp64; integers are int32 (indices) / int64 (strides);
- *   - a "plan" is created once per (dims, idxb, idxs, batch) and owns the device
- *     workspace (no allocation inside a solve);
+ *   - a "plan" is created once per (dims, idxb, idxs, batch) on the current
+ *     CUDA device and owns the device workspace; its calls run on that device
+ *     whatever the caller's current device.  A speed-mode solve never
+ *     allocates; the first solve in another mode (refinement, QR, square-root,
+ *     absolute form) allocates the plan's extended workspace once.  One solve
+ *     per plan may be in flight: solves on one plan are ordered on their
+ *     streams by the caller (use one plan per concurrent stream);
  *   - functions return 0 on success and a negative OCPQP_E_* code on misuse or
  *     CUDA error (ocpqp_last_error() gives the message).  Numerical trouble is
  *     never an error: it is a per-QP status word, as in the reference
@@ -191,7 +196,10 @@ int ocpqp_plan_destroy(OcpPlan* plan);
 /* Batched `solve_ocp_qp(qp, arg, guess)` (solver.py:103-105, loop
  * solver.py:180-308) over device-resident data.  `iter` holds the warm-start
  * guess on entry when arg->warm_start != 0 and the solution on exit.
- * Stream-ordered on `stream` (a cudaStream_t; NULL = legacy default stream). */
+ * Stream-ordered on `stream` (a cudaStream_t; NULL = legacy default stream).
+ * Stage shapes whose kernel streams stage data by TMA (nx >= 48, box rows
+ * only, ocpqp_plan_info) need Q, S, R, q, r, b 16-byte aligned with even batch
+ * strides (cudaMalloc'd / torch buffers are); misaligned data is OCPQP_E_ARG. */
 int ocpqp_solve(OcpPlan* plan, const OcpQpDataC* data, const OcpIpmArgC* arg,
                 OcpIterC* iter, OcpStatsC* stats, void* stream);
 

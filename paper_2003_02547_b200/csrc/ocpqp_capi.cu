@@ -684,6 +684,17 @@ int ocpqp_plan_create(const OcpQpDimC* dim, int32_t batch, OcpPlan** out) {
         e = cudaMemcpy(P->d_defaults, dflt.data(), sizeof(double) * dflt.size(), cudaMemcpyHostToDevice);
     }
     if (e == cudaSuccess) e = cudaMalloc(&P->d_ws, sizeof(double) * (size_t)P->ws_slot * P->slots);
+    // per-solve buffers sized for the worst case here, so that a solve never
+    // allocates (the extended workspace of the non-speed modes excepted, see
+    // the header): the escape list of balance mode and the packed [B A]
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_esc, sizeof(int) * (1 + (size_t)std::max(1, P->B)));
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_esc_meta, sizeof(long long) * 3 * (size_t)std::max(1, P->B));
+    if (e == cudaSuccess && P->fast && P->shape.kind == 0) {
+        const long long need = std::max(1ll, (long long)L.N * P->shape.nx * (P->shape.nx + P->shape.nu) *
+                                                  std::max(1, P->B));
+        e = cudaMalloc(&P->d_ba, sizeof(double) * need);
+        if (e == cudaSuccess) P->ba_cap = need;
+    }
     if (e == cudaSuccess) e = cudaMemcpy(P->d_st, L.st.data(), sizeof(StageInfo) * S, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !L.idxb.empty())
         e = cudaMemcpy(P->d_idxb, L.idxb.data(), sizeof(int) * L.idxb.size(), cudaMemcpyHostToDevice);
@@ -740,11 +751,38 @@ int ocpqp_plan_info(const OcpPlan* P, int64_t* out, int32_t out_len) {
     return OCPQP_OK;
 }
 
+// Runs a plan's work on the device it was created on (restoring the caller's
+// current device afterwards): a plan's buffers live on that device.
+struct DeviceGuard {
+    int prev = -1, dev;
+    explicit DeviceGuard(int d) : dev(d) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+    }
+};
+
+// The BIG shapes read stage data by TMA bulk copies: 16-byte aligned blocks.
+static int check_tma_alignment(const OcpPlan* P, const OcpQpDataC* data) {
+    if (!(P->fast && P->shape.kind == 0 && fast_big(P->shape)) || !data) return OCPQP_OK;
+    static const int fs[] = {OCPQP_F_Q, OCPQP_F_S, OCPQP_F_R, OCPQP_F_q, OCPQP_F_r, OCPQP_F_b};
+    for (int f : fs) {
+        if (!data->ptr[f] || P->L.flen[f] == 0) continue;
+        if (((uintptr_t)data->ptr[f] & 15u) || (data->batch_stride[f] & 1))
+            return fail(OCPQP_E_ARG, "this stage shape streams Q, S, R, q, r, b by TMA: their device "
+                                     "pointers must be 16-byte aligned and batch strides even");
+    }
+    return OCPQP_OK;
+}
+
 int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIterC* iter,
                 OcpStatsC* stats, void* stream) {
     if (!P) return fail(OCPQP_E_ARG, "plan is NULL");
     int rc = check_arg(arg);
     if (rc) return rc;
+    if ((rc = check_tma_alignment(P, data))) return rc;
+    DeviceGuard dg(P->device);
     // zero-length vectors (e.g. nc = 0 for an unconstrained QP) may be NULL
     const Layout& Ly = P->L;
     if (!iter || !stats || (Ly.ny && !iter->y) || (Ly.ne && !iter->pi) || (Ly.nc && !iter->lam) ||
@@ -778,8 +816,6 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     cudaError_t e;
     if (P->fast && (!ext || team)) {
         if (ext && arg->use_qr_fallback) {
-            if (!P->d_esc) CUDA_TRY(cudaMalloc(&P->d_esc, sizeof(int) * (1 + (size_t)P->B)));
-            if (!P->d_esc_meta) CUDA_TRY(cudaMalloc(&P->d_esc_meta, sizeof(long long) * 3 * (size_t)P->B));
             CUDA_TRY(cudaMemsetAsync(P->d_esc, 0, sizeof(int), (cudaStream_t)stream));
             k.esc_count = P->d_esc;
             k.esc_list = P->d_esc + 1;
@@ -798,18 +834,20 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
             const long long per_qp = (long long)P->L.N * nx * (nx + nu);
             const bool shared = k.bs[OCPQP_F_A] == 0 && k.bs[OCPQP_F_B] == 0;
             const long long need = std::max(1ll, per_qp * (shared ? 1 : P->B));
-            if (P->ba_cap < need) {
-                cudaFree(P->d_ba);
-                P->d_ba = nullptr;
-                P->ba_cap = 0;
-                CUDA_TRY(cudaMalloc(&P->d_ba, sizeof(double) * need));
-                P->ba_cap = need;
-            }
+            if (P->ba_cap < need) return fail(OCPQP_E_CUDA, "packed [B A] buffer smaller than the batch");
             k.ba = P->d_ba;
             k.ba_bs = shared ? 0 : per_qp;
+            // OCPQP_BA_STAGE_MAJOR=1: batch-interleaved [N][B][stage] packing
+            // (layout experiment; QP-major is the default, profiles/r02_layout_*)
+            const char* envl = getenv("OCPQP_BA_STAGE_MAJOR");
+            const int smaj = (!shared && envl && atoi(envl) == 1) ? 1 : 0;
+            if (smaj) {
+                k.ba_bs = (long long)nx * (nx + nu);
+                k.ba_ns = (long long)P->B * nx * (nx + nu);
+            }
             e = launch_pack_ba(k.f[OCPQP_F_A], k.bs[OCPQP_F_A], k.f[OCPQP_F_B], k.bs[OCPQP_F_B], P->B,
-                               P->L.N, nx, nu, P->d_ba, k.ba_bs, (cudaStream_t)stream,
-                               fast_big(P->shape));
+                               P->L.N, nx, nu, P->d_ba, shared ? 0 : per_qp, (cudaStream_t)stream,
+                               fast_big(P->shape), smaj);
             if (e != cudaSuccess) return cuda_fail(e, "k_pack_ba launch");
         }
         e = launch_fast_solve(P->shape, k, sp, P->grid, P->smem_bytes, (cudaStream_t)stream);
@@ -857,6 +895,7 @@ static void* mapped_host(void* p) {
 int ocpqp_solve_host(OcpPlan* P, const OcpQpDataC* hd, const OcpIpmArgC* arg, OcpIterC* hit,
                      OcpStatsC* hst, void* stream_) {
     if (!P || !hd || !hit || !hst) return fail(OCPQP_E_ARG, "NULL argument");
+    DeviceGuard dg(P->device);
     int rc = check_arg(arg);
     if (rc) return rc;
     cudaStream_t stream = (cudaStream_t)stream_;
@@ -945,6 +984,7 @@ int ocpqp_solve_host(OcpPlan* P, const OcpQpDataC* hd, const OcpIpmArgC* arg, Oc
 int ocpqp_residuals(OcpPlan* P, const OcpQpDataC* data, const OcpIterC* pt, double* r_g,
                     double* r_b, double* r_d, double* r_m, double* norms, void* stream) {
     if (!P || !pt || !norms) return fail(OCPQP_E_ARG, "NULL argument");
+    DeviceGuard dg(P->device);
     if (P->B == 0) return OCPQP_OK;
     KParams k;
     fill_kparams(P, k, data, false);
@@ -960,6 +1000,7 @@ int ocpqp_newton_step(OcpPlan* P, const OcpQpDataC* data, double reg, const OcpI
                       OcpIterC* step, int32_t* fail_stage, void* stream) {
     if (!P || !it || !step || !r_g || !r_b || !r_d || !r_m || !fail_stage)
         return fail(OCPQP_E_ARG, "NULL argument");
+    DeviceGuard dg(P->device);
     if (P->B == 0) return OCPQP_OK;
     KParams k;
     fill_kparams(P, k, data, false);
@@ -974,6 +1015,7 @@ int ocpqp_newton_step(OcpPlan* P, const OcpQpDataC* data, double reg, const OcpI
 int ocpqp_shift_guess(OcpPlan* P, const OcpQpDataC* data, const OcpIterC* sol, OcpIterC* guess,
                       void* stream) {
     if (!P || !sol || !guess) return fail(OCPQP_E_ARG, "NULL argument");
+    DeviceGuard dg(P->device);
     const Layout& L = P->L;
     if ((L.ny && (!sol->y || !guess->y)) || (L.ne && (!sol->pi || !guess->pi)) ||
         (L.nc && (!sol->lam || !sol->t || !guess->lam || !guess->t)))
@@ -995,6 +1037,7 @@ int ocpqp_shift_guess(OcpPlan* P, const OcpQpDataC* data, const OcpIterC* sol, O
 
 int ocpqp_factor_export(OcpPlan* P, int32_t qp, double* P_out, double* K_out) {
     if (!P || qp < 0 || qp >= P->B) return fail(OCPQP_E_ARG, "bad plan or qp index");
+    DeviceGuard dg(P->device);
     if (P->B > P->slots)
         return fail(OCPQP_E_UNSUPPORTED, "factor export needs batch <= slots (%d)", P->slots);
     const double* slot = P->d_ws + (long long)qp * P->ws_slot;

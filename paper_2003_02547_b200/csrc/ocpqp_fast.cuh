@@ -402,7 +402,7 @@ struct FCtx {
     int ss[OCPQP_F_lb];  // per-stage element stride of A..r (0: identical in every stage)
     double* x[WS_NUM - WS_EXT0];  // extended workspace (refinement), nullptr without it
     const double* ba;    // this QP's packed [B A] (NX x NW per stage, KParams::ba)
-    int ba_ss;           // its per-stage stride (0: identical in every stage)
+    long long ba_ss;     // its per-stage stride (0: identical in every stage)
     double* w[WS_EXT0];  // base workspace only (speed mode)
     double red[56];  // team reductions (tred_res: 6 x warps)
     unsigned long long mbar[4];   // TMA completion barriers (BIG shapes)
@@ -3510,7 +3510,7 @@ __global__ void __launch_bounds__(S::TEAM, S::MINB) k_fast_solve(const __grid_co
         const int sz[OCPQP_F_lb] = {NX * NX, NX * NU, NX, NX * NX, NU * NX, NU * NU, NX, NU};
         const int inv = p.sinv ? *p.sinv : 0;
         for (int f = 0; f < OCPQP_F_lb; ++f) c.ss[f] = ((inv >> f) & 1) ? 0 : sz[f];
-        c.ba_ss = ((inv & 3) == 3) ? 0 : NX * (NX + NU);   // A and B both invariant
+        c.ba_ss = ((inv & 3) == 3) ? 0 : (p.ba_ns ? p.ba_ns : (long long)NX * (NX + NU));   // A and B both invariant
         if constexpr (S::BIG) {
             for (int b = 0; b < 4; ++b) mbar_init(&c.mbar[b], 1);
             fence_mbar_init();

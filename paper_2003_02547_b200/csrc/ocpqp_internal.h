@@ -102,6 +102,7 @@ struct KParams {
     long long* dbg;           // optional [B, 8] phase-cycle counters (nullptr = off)
     const double* ba;         // shaped kernels: packed [B A] per stage (NX x NW), see
     long long ba_bs;          //   launch_pack_ba; per-QP stride (0: one copy for the batch)
+    long long ba_ns;          //   per-stage stride (0: the kernel's default, QP-major packing)
     int* esc_count;           // shaped kernel, balance mode: QPs left to the generic kernel
     int* esc_list;            //   (count, [B] indices); nullptr = none
     long long* esc_meta;      //   [B, 3]: iteration, flops, alpha_last bits at the escape;
@@ -144,7 +145,7 @@ int ipm_occupancy(int threads, size_t smem);
 // stage stored as [B A]' (nu + nx rows of nx), the BIG shapes' layout.
 cudaError_t launch_pack_ba(const double* A, long long bsA, const double* B, long long bsB, int Bn,
                            int N, int nx, int nu, double* out, long long out_bs, cudaStream_t stream,
-                           int trans = 0);
+                           int trans = 0, int stage_major = 0);
 // Stage-invariance detection of the broadcast fields A..r (uniform-stage plans):
 // writes the bit mask consumed by the shaped kernels to *mask.
 cudaError_t launch_stage_invariant(const double* const* f, const long long* bs, int N, int nx,

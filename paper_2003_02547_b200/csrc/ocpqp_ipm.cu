@@ -2008,7 +2008,8 @@ __global__ void k_stage_invariant(StageFields sf, int N, int nx, int nu, int* ma
 }
 
 __global__ void k_pack_ba(const double* A, long long bsA, const double* B, long long bsB, int N,
-                          int nx, int nu, double* out, long long out_bs, long long total, int trans) {
+                          int nx, int nu, double* out, long long out_bs, long long total, int trans,
+                          long long copies, int stage_major) {
     const int nw = nx + nu;
     const long long per_qp = (long long)N * nx * nw;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -2020,20 +2021,23 @@ __global__ void k_pack_ba(const double* A, long long bsA, const double* B, long 
         int k, j;   // element (k, j) of [B A]: row-major (k, j) or transposed (j, k)
         if (trans) { j = rem / nx; k = rem - j * nx; }
         else { k = rem / nw; j = rem - k * nw; }
-        out[q * out_bs + r] = j < nu ? B[q * bsB + ((long long)n * nx + k) * nu + j]
-                                     : A[q * bsA + ((long long)n * nx + k) * nx + (j - nu)];
+        // QP-major [copies][N][stage] or stage-major [N][copies][stage]
+        const long long o = stage_major ? ((long long)n * copies + q) * nx * nw + rem : q * out_bs + r;
+        out[o] = j < nu ? B[q * bsB + ((long long)n * nx + k) * nu + j]
+                        : A[q * bsA + ((long long)n * nx + k) * nx + (j - nu)];
     }
 }
 
 cudaError_t launch_pack_ba(const double* A, long long bsA, const double* B, long long bsB, int Bn,
                            int N, int nx, int nu, double* out, long long out_bs, cudaStream_t stream,
-                           int trans) {
+                           int trans, int stage_major) {
     const long long copies = out_bs == 0 ? 1 : Bn;
     const long long total = copies * N * (long long)nx * (nx + nu);
     if (total == 0) return cudaSuccess;
     const int threads = 256;
     const long long blocks = std::min<long long>((total + threads - 1) / threads, 148ll * 16);
-    k_pack_ba<<<(int)blocks, threads, 0, stream>>>(A, bsA, B, bsB, N, nx, nu, out, out_bs, total, trans);
+    k_pack_ba<<<(int)blocks, threads, 0, stream>>>(A, bsA, B, bsB, N, nx, nu, out, out_bs, total, trans,
+                                                   copies, stage_major);
     return cudaGetLastError();
 }
 

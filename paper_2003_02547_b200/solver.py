@@ -34,15 +34,43 @@ __all__ = ["SolveReport", "BatchReport", "solve_ocp_qp", "solve_ocp_qp_batch",
            "solve_ocp_qp_host", "newton_step", "compute_residuals", "get_plan"]
 
 _PLANS = {}
+_MAX_PLANS = 8   # least-recently-used plans beyond this are released
 
 
-def get_plan(batch: OcpQpBatch):
-    """Cached plan for the batch's structure and size."""
-    key = (batch.structure_key(), batch.B)
-    plan = _PLANS.get(key)
+def _device_index(batch, device=None):
+    for arr in batch.fields.values():
+        dev = getattr(arr, "device", None)
+        if dev is not None and getattr(dev, "type", "") == "cuda":
+            return dev.index if dev.index is not None else 0
+    if device is not None:
+        import torch
+
+        d = torch.device(device)
+        if d.type == "cuda":
+            return d.index if d.index is not None else torch.cuda.current_device()
+    import torch
+
+    return torch.cuda.current_device()
+
+
+def get_plan(batch: OcpQpBatch, device=None):
+    """Cached plan for the batch's structure, size and CUDA device.
+
+    A plan owns one workspace: solves on it are stream-ordered (one solve in
+    flight per plan, the C ABI's contract).  The plan is created on, and its
+    solves run on, the device that holds the batch."""
+    import torch
+
+    dev = _device_index(batch, device)
+    key = (batch.structure_key(), batch.B, dev)
+    plan = _PLANS.pop(key, None)
     if plan is None:
-        plan = nat.Plan(batch, batch.B)
-        _PLANS[key] = plan
+        with torch.cuda.device(dev):
+            plan = nat.Plan(batch, batch.B)
+        while len(_PLANS) >= _MAX_PLANS:
+            old = _PLANS.pop(next(iter(_PLANS)))
+            old.close()
+    _PLANS[key] = plan   # most recently used last
     return plan
 
 
@@ -209,12 +237,15 @@ def solve_ocp_qp_batch(batch, arg=None, guess=None, device="cuda", trace=True,
             flops=torch.empty(B, dtype=torch.int64, device=device),
             trace=torch.zeros((B, max(1, arg.iter_max), 8), **f64) if trace else None,
         )
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     if arg.warm_start != "none" and guess is not None:
-        gy, gpi, glam, _ = _guess_arrays(guess, batch, torch, device)
-        out["y"].copy_(gy)
-        if arg.warm_start == "primal_dual":
-            out["pi"].copy_(gpi)
-            out["lam"].copy_(glam)
+        # the guess lands in the output buffers on the solve's stream
+        with torch.cuda.stream(s):
+            gy, gpi, glam, _ = _guess_arrays(guess, batch, torch, device)
+            out["y"].copy_(gy)
+            if arg.warm_start == "primal_dual":
+                out["pi"].copy_(gpi)
+                out["lam"].copy_(glam)
         carg = nat.arg_to_c(arg)
     else:
         from dataclasses import replace
@@ -225,7 +256,6 @@ def solve_ocp_qp_batch(batch, arg=None, guess=None, device="cuda", trace=True,
     st = nat.OcpStatsC(out["status"].data_ptr(), out["iters"].data_ptr(), out["res"].data_ptr(),
                        out["flops"].data_ptr(),
                        out["trace"].data_ptr() if out["trace"] is not None else None)
-    s = stream if stream is not None else torch.cuda.current_stream(device)
     if phase_debug is not None or getattr(plan, "_dbg_on", False):
         L = nat.lib()
         L.ocpqp_debug_phases.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
