@@ -256,6 +256,37 @@ int ocpqp_shift_guess(OcpPlan* plan, const OcpQpDataC* data, const OcpIterC* sol
  * keeps its factor store at fixed shared-memory offsets. */
 int ocpqp_plan_info(const OcpPlan* plan, int64_t* out, int32_t out_len);
 
+/* ---- dense QPs with equality constraints (reference DenseQp,
+ * qp_data.py:426-500; solve_dense_qp, solver.py:98-100; kkt_dense.py:117-256) ----
+ * min 1/2 v'Hv + g'v s.t. A v = b, lb <= v[idxb] <= ub, lg <= C v <= ug.
+ * Dense QPs without equality rows run through ocpqp_solve as the N = 0
+ * OCP-QP (see ocpqp_fc_create); these entry points handle ne > 0 with the
+ * reference's two equality methods: kkt_method 0 = "schur" (Schur complement
+ * A Hred^-1 A' + reg_dual I), 1 = "null_space" (Householder QR of A',
+ * reduced Hessian on the null-space basis).  Speed-mode loop (predictor-
+ * corrector, regularised factor retry); no soft rows. */
+typedef struct OcpDensePlan OcpDensePlan;
+typedef struct {
+    int32_t nv, ne, nb, ng, ns;   /* ns must be 0 */
+    const int32_t* idxb;          /* [nb] host, strictly increasing (NULL: 0..nb-1) */
+} OcpDenseDimC;
+typedef struct {
+    /* device pointers, per QP: H nv*nv, g nv, A ne*nv, b ne, lb ub nb, C ng*nv,
+     * lg ug ng, maskl masku nb+ng (row-major); NULL = the reference's zero-
+     * initialised value (0, -inf / +inf bounds, all-one masks) */
+    const double* H; const double* g; const double* A; const double* b;
+    const double* lb; const double* ub; const double* C; const double* lg; const double* ug;
+    const double* maskl; const double* masku;
+    int64_t batch_stride[11];     /* same order; 0 broadcasts one copy */
+} OcpDenseDataC;
+int ocpqp_dense_plan_create(const OcpDenseDimC* dim, int32_t batch, int32_t kkt_method,
+                            OcpDensePlan** out);
+int ocpqp_dense_plan_destroy(OcpDensePlan* plan);
+/* iter: y = v [B, nv], pi [B, ne], lam / t [B, 2 (nb + ng)] (lower rows, then
+ * upper rows); stats as ocpqp_solve; reg_dual = IpmArg.reg_dual (Schur path). */
+int ocpqp_dense_solve(OcpDensePlan* plan, const OcpDenseDataC* data, const OcpIpmArgC* arg,
+                      double reg_dual, OcpIterC* iter, OcpStatsC* stats, void* stream);
+
 /* ---- partial condensing (reference condensing.py:451-619) ----
  * A partial-condensing plan holds the block structure and the row routing of
  * partial_condense(qp, N1) for one (dims, idxb) structure; the arithmetic is

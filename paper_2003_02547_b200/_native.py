@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = (
     "ocpqp_plan_info", "ocpqp_fp64_peak", "ocpqp_abi_version", "ocpqp_last_error",
     "ocpqp_pc_create", "ocpqp_pc_destroy", "ocpqp_pc_dims", "ocpqp_pc_condense",
     "ocpqp_pc_expand", "ocpqp_pc_last_error", "ocpqp_shift_guess", "ocpqp_fc_create",
-    "ocpqp_pc_soft",
+    "ocpqp_pc_soft", "ocpqp_dense_plan_create", "ocpqp_dense_plan_destroy", "ocpqp_dense_solve",
 )
 
 _i32p = ctypes.POINTER(ctypes.c_int32)
@@ -62,6 +62,19 @@ class OcpIpmArgC(ctypes.Structure):
                 ("riccati_variant", ctypes.c_int32), ("abs_form", ctypes.c_int32),
                 ("comp_res_pred", ctypes.c_int32), ("mu_only_exit", ctypes.c_int32),
                 ("itref_stop_ratio", ctypes.c_double), ("qr_fallback_ratio", ctypes.c_double)]
+
+
+class OcpDenseDimC(ctypes.Structure):
+    _fields_ = [("nv", ctypes.c_int32), ("ne", ctypes.c_int32), ("nb", ctypes.c_int32),
+                ("ng", ctypes.c_int32), ("ns", ctypes.c_int32), ("idxb", _i32p)]
+
+
+DENSE_FIELDS = ("H", "g", "A", "b", "lb", "ub", "C", "lg", "ug", "maskl", "masku")
+
+
+class OcpDenseDataC(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in DENSE_FIELDS] + [
+        ("batch_stride", ctypes.c_int64 * len(DENSE_FIELDS))]
 
 
 class OcpIterC(ctypes.Structure):
@@ -108,6 +121,12 @@ def lib():
     L.ocpqp_factor_export.argtypes = [vp, ctypes.c_int32, vp, vp]
     L.ocpqp_shift_guess.argtypes = [vp, ctypes.POINTER(OcpQpDataC), ctypes.POINTER(OcpIterC),
                                     ctypes.POINTER(OcpIterC), vp]
+    L.ocpqp_dense_plan_create.argtypes = [ctypes.POINTER(OcpDenseDimC), ctypes.c_int32,
+                                          ctypes.c_int32, ctypes.POINTER(vp)]
+    L.ocpqp_dense_plan_destroy.argtypes = [vp]
+    L.ocpqp_dense_solve.argtypes = [vp, ctypes.POINTER(OcpDenseDataC), ctypes.POINTER(OcpIpmArgC),
+                                    ctypes.c_double, ctypes.POINTER(OcpIterC),
+                                    ctypes.POINTER(OcpStatsC), vp]
     L.ocpqp_abi_version.argtypes = []
     L.ocpqp_last_error.argtypes = []
     L.ocpqp_last_error.restype = ctypes.c_char_p

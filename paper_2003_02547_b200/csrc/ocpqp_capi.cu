@@ -199,6 +199,10 @@ inline long long align2(long long x) { return (x + 1) & ~1ll; }
 
 }  // namespace
 
+namespace ocpqp {
+void set_last_error(const char* msg) { g_last_error = msg; }
+}  // namespace ocpqp
+
 struct OcpPlan {
     Layout L;
     int B = 0;

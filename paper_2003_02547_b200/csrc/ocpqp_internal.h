@@ -168,5 +168,7 @@ int fast_occupancy(const FastShape& s, size_t smem);
 // the shape's kernel streams stage data by TMA from a transposed [B A] pack
 // and keeps no workspace buffer in shared memory (ocpqp_fast.cuh, Shape::BIG)
 int fast_big(const FastShape& s);
+// message of the calling thread's last error (ocpqp_last_error)
+void set_last_error(const char* msg);
 
 }  // namespace ocpqp

@@ -21,6 +21,7 @@ Fixtures:
   modes.npz          balance / robust / square-root / speed_abs solves (MODES),
                      their Failure ladders and the robust-mode RankDeficient raise
   pcond_full.npz     config 4 (N = 100) partial condensing -> solve -> expand
+  dense_eq.npz       dense QPs with equality constraints (Schur / null-space)
   closed_loop.npz    run_closed_loop trajectories / iteration counts (warm and
                      cold) and one _shift_guess
   qp_files/          qp_write text files and `mpcqp solve` CLI reports
@@ -400,6 +401,65 @@ def dense():
     np.savez_compressed(HERE / "dense.npz", **out)
 
 
+# dense QPs with equality constraints (kkt_dense.py:117-231): (seed, nv, ne, nb, ng,
+# kkt_method, rank_deficient); speed mode, tol 1e-8
+DENSE_EQ_CASES = [
+    (61, 8, 2, 4, 2, "schur", False),
+    (62, 12, 4, 6, 3, "schur", False),
+    (63, 10, 3, 0, 4, "null_space", False),
+    (64, 16, 5, 8, 0, "null_space", False),
+    (65, 6, 6, 3, 1, "null_space", False),
+    (66, 20, 8, 10, 5, "schur", False),
+    (67, 20, 8, 10, 5, "null_space", False),
+    (68, 9, 3, 4, 2, "schur", True),
+    (69, 9, 3, 4, 2, "null_space", True),
+]
+
+
+def dense_eq_qp(lib, seed, nv, ne, nb, ng, rank_deficient=False):
+    """A feasible random dense QP with ne equality rows A v = b (b = A v0)."""
+    rng = np.random.default_rng(seed)
+    F = rng.standard_normal((nv, nv))
+    q = lib.DenseQp(nv, ne, nb, ng, 0)
+    q.set_field("H", F @ F.T + np.eye(nv))
+    q.set_field("g", rng.standard_normal(nv))
+    v0 = rng.uniform(-0.5, 0.5, nv)
+    A = rng.standard_normal((ne, nv))
+    if rank_deficient:
+        A[-1] = 0.0   # an all-zero equality row: exactly singular for both methods
+    q.set_field("A", A)
+    q.set_field("b", A @ v0)
+    if nb:
+        idxb = np.sort(rng.choice(nv, nb, replace=False))
+        q.set_field("idxb", idxb)
+        q.set_field("lb", v0[idxb] - rng.uniform(0.1, 1.0, nb))
+        q.set_field("ub", v0[idxb] + rng.uniform(0.1, 1.0, nb))
+    if ng:
+        C = rng.standard_normal((ng, nv))
+        q.set_field("C", C)
+        q.set_field("lg", C @ v0 - rng.uniform(0.1, 1.0, ng))
+        q.set_field("ug", C @ v0 + rng.uniform(0.1, 1.0, ng))
+    if nb + ng:
+        mu = np.ones(nb + ng)
+        mu[rng.integers(nb + ng)] = 0.0
+        q.set_field("masku", mu)
+    return q
+
+
+def dense_eq():
+    from dataclasses import replace
+
+    out = {}
+    for seed, nv, ne, nb, ng, method, rd in DENSE_EQ_CASES:
+        q = dense_eq_qp(mpcqp, seed, nv, ne, nb, ng, rd)
+        arg = replace(mpcqp.mode_preset("speed").with_tol(1e-8), kkt_method=method)
+        rep = mpcqp.solve_dense_qp(q, arg)
+        for k, v in pack_report(rep).items():
+            out[f"e{seed}_{k}"] = v
+        print("dense_eq", seed, method, rep.status.value, rep.iterations, rep.stats.flops, flush=True)
+    np.savez_compressed(HERE / "dense_eq.npz", **out)
+
+
 # modes beyond speed (ipm_core.py:131-168): (name, preset, tol, overrides)
 MODES = [
     ("balance6", "balance", 1e-6, {}),
@@ -522,6 +582,7 @@ def qp_files():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["known", "residuals", "newton", "solve_random", "solve_cfg", "pcond",
-                            "solve_modes", "closed_loop", "qp_files", "fcond", "soft_cond", "dense"]
+                            "solve_modes", "closed_loop", "qp_files", "fcond", "soft_cond", "dense",
+                            "pcond_full", "dense_eq"]
     for w in which:
         globals()[w]()

@@ -86,3 +86,39 @@ def test_no_cpu_fallback_without_gpu():
 
     with pytest.raises(pkg.NativeLibraryError):
         pkg.solve_ocp_qp_batch(make_batch(0), pkg.mode_preset("speed"))
+
+
+def test_dense_plan_rejects_bad_structure_without_gpu_work(lib):
+    """ocpqp_dense_plan_create validates before touching the device."""
+    dim = nat.OcpDenseDimC(4, 5, 0, 0, 0, None)       # ne > nv
+    h = ctypes.c_void_p()
+    assert lib.ocpqp_dense_plan_create(ctypes.byref(dim), 1, 0, ctypes.byref(h)) == -1
+    ib = (ctypes.c_int32 * 2)(1, 0)
+    dim = nat.OcpDenseDimC(4, 1, 2, 0, 0, ib)           # idxb not increasing
+    assert lib.ocpqp_dense_plan_create(ctypes.byref(dim), 1, 0, ctypes.byref(h)) == -2
+    dim = nat.OcpDenseDimC(4, 1, 0, 0, 1, None)         # soft rows
+    assert lib.ocpqp_dense_plan_create(ctypes.byref(dim), 1, 0, ctypes.byref(h)) == -3
+    assert b"soft rows" in lib.ocpqp_last_error()
+
+
+def test_dense_eq_residual_assembly_at_reference_solution(golden):
+    """Host-side report assembly (dense.py _dense_residuals, view.py:272-288 on
+    the DenseView) reproduces the reference's final residual norms at the
+    reference's own solutions."""
+    import sys
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from test_gpu_dense_eq import build, cases
+
+    from paper_2003_02547_b200.dense import _dense_residuals
+
+    g = golden("dense_eq")
+    for seed, nv, ne, nb, ng, method, rd in cases():
+        p = f"e{seed}"
+        if int(g[f"{p}_status"]) != 0:
+            continue
+        q = build(seed, nv, ne, nb, ng, rd)
+        r = _dense_residuals(q, g[f"{p}_y"], g[f"{p}_pi"], g[f"{p}_lam"], g[f"{p}_t"])
+        got = np.array([r.res_g, r.res_b, r.res_d, r.res_m, r.mu])
+        ref = g[f"{p}_res"]
+        assert np.all(np.abs(got - ref) <= 1e-12 * np.maximum(1.0, np.abs(ref))), (seed, got, ref)

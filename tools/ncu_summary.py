@@ -68,8 +68,13 @@ def main():
             tr = json.load(open(a.traffic))
         except (OSError, ValueError):
             tr = {}
+        sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+        from bench import kernel_source_hash   # ties the record to the kernel sources
+
         tr[a.key] = {"dram_bytes_per_launch": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"),
-                     "source": a.report.split("/")[-1]}
+                     "duration_ms": num("gpu__time_duration.sum") / 1e6 if d["gpu__time_duration.sum"][1] == "ns"
+                     else float(d["gpu__time_duration.sum"][0].replace(",", "")),
+                     "source": a.report.split("/")[-1], "src_hash": kernel_source_hash()}
         json.dump(tr, open(a.traffic, "w"), indent=1)
     print(json.dumps(out)[:400])
 
