@@ -369,7 +369,7 @@ def bench_ocp(cx, cfg, B, arg, steps, warmup, *, e2e=True, cpu=True, cpu_seconds
     # sweeps are the Riccati phases, the rest are the IPM vector passes
     if plan_info.get("kernel") == "team":
         try:
-            dbg = torch.zeros((B, 16), dtype=torch.int64, device=cx.device)
+            dbg = torch.zeros((B, 24), dtype=torch.int64, device=cx.device)
             solve_ocp_qp_batch(dev, arg, trace=False, phase_debug=dbg, stream=stream)
             torch.cuda.synchronize()
             solve_ocp_qp_batch(dev, arg, trace=False, stream=stream)  # instrumentation off

@@ -450,6 +450,12 @@ __device__ __forceinline__ void fence_mbar_init() {
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
+// before a TMA *load* into a region last touched through the generic proxy (experiment switch)
+__device__ __forceinline__ void fence_proxy_async_ld() {
+#ifndef OCPQP_NOFENCE_LD
+    fence_proxy_async();
+#endif
+}
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
@@ -644,6 +650,13 @@ __device__ __forceinline__ void stage_gemm(FA a, FB b, FP pre, FE epi) {
         }                                                         \
     } while (0)
 
+// finer ticks into the free slots, only in -DOCPQP_XDIAG builds
+#ifdef OCPQP_XDIAG
+#define OCPQP_XTICK(c, slot) OCPQP_TICK(c, slot)
+#else
+#define OCPQP_XTICK(c, slot) do { } while (0)
+#endif
+
 // runtime structure (uniform stages)
 struct RD {
     int N, NB, M, NBN, NGN, MN, nc, nv, ne, msum;
@@ -693,7 +706,11 @@ struct Shape {
     // (measured: config 2 -7 %; config 1, whose store sits in shared memory,
     // +25 % from the index arithmetic in its latency-bound sweeps -> NX >= 16)
     static constexpr bool PPACK = OCPQP_PPACK != 0 && NX >= 16;
-    static constexpr int PST = PPACK ? NX * (NX + 1) / 2 : NX * NX;   // per-stage store stride
+    // BIG shapes pad every packed row to an even length (row i starts at
+    // (i + 1)^2 / 2): 16-byte aligned rows, written by TMA bulk stores
+    static constexpr bool PPAD = PPACK && NG_ == 0 && NX_ >= 48 && TEAM_ == 256 && NX_ % 2 == 0;
+    static constexpr int PST = PPACK ? (PPAD ? NX * (NX + 2) / 2 : NX * (NX + 1) / 2) : NX * NX;   // per-stage store stride
+    __host__ __device__ static constexpr int prow(int i) { return PPAD ? ((i + 1) * (i + 1)) >> 1 : i * (i + 1) / 2; }
     static constexpr bool PF_QSR = OCPQP_PF_QSR != 0;     // factor prefetch includes Q, S, R
     static constexpr int HALF_S = (STAGE_P ? PST : 0) + NX * NW + NU * NX + NU * NU + NU + NX + NW + NU + 4;
     static constexpr int HALF_F = NX * NW + (PF_QSR ? NX * NX + NU * NX + NU * NU : 0);
@@ -727,7 +744,9 @@ struct Shape {
     static constexpr bool BAT = BIG;
     static constexpr int STAGE_STD = STAGE0 + (SSTAGE ? (BA_BUF > SOLVE_BUF ? BA_BUF : SOLVE_BUF) : BA_BUF) + JGB;
     // BIG vector scratch: win, e, pvs, x, u, x', r_b (sweeps_big)
-    static constexpr int VECB = 2 * NW + 6 * NX + NU + 16 > 32 + NU * NU ? 2 * NW + 6 * NX + NU + 16 : 32 + NU * NU;
+    // (sweeps_big) / R_n, G_uu, the box diagonal and 1 / L_kk (factor_big)
+    static constexpr int VECB_S = 2 * NW + 6 * NX + NU + 16, VECB_F = 2 * NU * NU + NW + NU + 4;
+    static constexpr int VECB = VECB_S > VECB_F ? VECB_S : VECB_F;
     static constexpr int STAGE = BIG ? NX * NX + 2 * NW * NX + VECB : STAGE_STD;
     // offset of the vector scratch (win, e, pvs, x, u) in the stage tile
     static constexpr int VOFF = BIG ? NX * NX + 2 * NW * NX : NX * NX + T1N + NU * NW;
@@ -775,7 +794,7 @@ struct Kern {
     __device__ static __forceinline__ const double* A(const FCtx& c, int n) { return c.f[OCPQP_F_A] + n * c.ss[OCPQP_F_A]; }
     // element (i, k) of a stored P (full or packed lower triangle)
     __device__ static __forceinline__ double Pget(const double* P, int i, int k) {
-        if constexpr (S::PPACK) return k <= i ? P[i * (i + 1) / 2 + k] : P[k * (k + 1) / 2 + i];
+        if constexpr (S::PPACK) return k <= i ? P[S::prow(i) + k] : P[S::prow(k) + i];
         else return P[i * NX + k];
     }
     // packed [B A] of stage n (kkt_ocp.py:177): row k = (B_k., A_k.)
@@ -1038,7 +1057,7 @@ struct Kern {
                 const int b = n & 1;
                 if (tid == 0) {
                     double* dst = stg + b * ASZ;
-                    fence_proxy_async();
+                    fence_proxy_async_ld();
                     mbar_expect_tx(&c.mbar[b], (AW + NW + 3 * NX) * 8);
                     cp(dst, BAp(c, n), AW, b);
                     cp(dst + AW, y + n * NW, NW, b);
@@ -1058,7 +1077,7 @@ struct Kern {
                     if (n < N) bytes += (NU * NX + NU * NU + NU) * 8;
                     if (n > 0) bytes += NX * 8;
                     if (full_box) bytes += 2 * m2 * 8;
-                    fence_proxy_async();
+                    fence_proxy_async_ld();
                     mbar_expect_tx(&c.mbar[b], bytes);
                     cp(dst, Q(c, n), BS, b);
                     cp(dst + BW, y + n * NW, nw, b);
@@ -1405,7 +1424,7 @@ struct Kern {
                 const double v = j <= i ? row[off + j] : 0.0;
                 Lc[i * NX + j] = v;
                 if (j <= i) {
-                    if constexpr (S::PPACK) Ps[i * (i + 1) / 2 + j] = v;
+                    if constexpr (S::PPACK) Ps[S::prow(i) + j] = v;
                     else Ps[i * NX + j] = v;
                 } else if constexpr (!S::PPACK) {
                     Ps[i * NX + j] = 0.0;
@@ -1646,7 +1665,7 @@ struct Kern {
                 const double v = 0.5 * (T1[idx] + T1[j * NX + i]);
                 Pc[idx] = v;
                 if (!S::PPACK) Pn[idx] = v;
-                else if (j <= i) Pn[i * (i + 1) / 2 + j] = v;
+                else if (j <= i) Pn[S::prow(i) + j] = v;
             TEAM_END
             bar<TEAM>();
         }
@@ -1825,7 +1844,7 @@ struct Kern {
                 const double v = 0.5 * (T1[idx] + T1[j * NX + i]);
                 Pc[idx] = v;
                 if (!S::PPACK) Pn[idx] = v;
-                else if (j <= i) Pn[i * (i + 1) / 2 + j] = v;
+                else if (j <= i) Pn[S::prow(i) + j] = v;
             TEAM_END
             bar<TEAM>();
         }
@@ -1863,109 +1882,123 @@ struct Kern {
     static constexpr int GLD = NW + 4;
     static constexpr unsigned BAB = NW * NX * 8;   // bytes of one stage's [B A]'
 
-    // thread 0: TMA of stage n's [B A]' into dst, completion on barrier b
+    // The thread that issues the TMA copies and L2 prefetches of the BIG paths.
+    // Each copy is preceded by fence.proxy.async, which waits for the issuing
+    // thread's own outstanding stores, global ones included: lane 31 of warp 0
+    // is an odd thread (the MV helpers store from even threads only) outside
+    // the Cholesky rows and the K columns, so it never has stores in flight.
+    static constexpr int TMA_THR = 31;
+    // TMA_THR: TMA of stage n's [B A]' into dst, completion on barrier b
     __device__ static __forceinline__ void tma_ba(FCtx& c, Tma& tm, double* dst, int n, int b) {
-        if (threadIdx.x == 0) {
-            fence_proxy_async();
+        if (threadIdx.x == TMA_THR) {
+            fence_proxy_async_ld();
             mbar_expect_tx(&c.mbar[b], BAB);
             tma_load_1d(dst, BAp(c, n), BAB, &c.mbar[b]);
         }
         tm.issue(c.mbar, b);
     }
 
-    // L_uu = chol(G_uu) by one warp with the rows in registers as a shift
-    // register: at pivot k, r[m] holds A(lane, k + m), so every register index
-    // is a compile-time constant while the pivot loop stays rolled (no
-    // dynamically indexed array, no full unroll).  The next pivot's diagonal
-    // update is lane-local; the other updates take one shuffle each.  Same
-    // operations and order as warp_chol (linalg.py:81-118 pivot test); L (lower,
-    // zero upper) to shared memory (Ls) and the factor store, 1 / L_kk to rinv
-    // and the store; c.flag = success.
-    __device__ __forceinline__ static void chol_big(FCtx& c, const double* Gu, double* Ls, double* Ln,
-                                                    double* Rinv_n, double* rinv) {
+    // L_uu = chol(G_uu) by one warp, lane i holding row i in registers
+    // (warp_chol: linalg.py:81-118 pivot test); in place in shared memory
+    // (Guu: L lower, L' mirrored above) and to the factor store (zero upper), 1 / L_kk to rinv and
+    // the store; c.flag = success.
+    __device__ __forceinline__ static void chol_uu(FCtx& c, double* Guu, double* Ln, double* Rinv_n,
+                                                   double* rinv) {
         const int lane = threadIdx.x & 31;
-        double r[NU];
+        double row[NU];
 #pragma unroll
-        for (int m = 0; m < NU; ++m) r[m] = (lane < NU && m <= lane) ? Gu[lane * GLD + m] : 0.0;
-        bool ok = true;
-#pragma unroll 1
-        for (int k = 0; k < NU; ++k) {
-            const double piv = __shfl_sync(FULL, r[0], k);
-            ok = ok && (piv > 0.0);
-            const double inv = rsqrt(piv);
-            const double lik = lane == k ? piv * inv : r[0] * inv;
-            if (lane == k) rinv[k] = inv;
-            if (lane >= k && lane < NU) Ls[lane * NU + k] = lik;
-            // unconditional update: for lane < k + m the entry (lane, k + m) is
-            // in the upper triangle, never read by a later pivot or stored
-#pragma unroll
-            for (int m = 1; m < NU; ++m) {
-                const int src = k + m < 32 ? k + m : 31;
-                r[m - 1] = fma(-lik, __shfl_sync(FULL, lik, src), r[m]);
-            }
-            r[NU - 1] = 0.0;
-        }
+        for (int m = 0; m < NU; ++m) row[m] = (lane < NU && m <= lane) ? Guu[lane * NU + m] : 0.0;
+        double rin = 0.0;
+        const bool ok = warp_chol<NU>(row, lane, rin);
         if (lane == 0) c.flag = ok;
-        __syncwarp();
-        if (ok && lane < NU) {
+        if (lane < NU) {
 #pragma unroll
             for (int m = 0; m < NU; ++m) {
-                const double v = m <= lane ? Ls[lane * NU + m] : 0.0;
-                Ls[lane * NU + m] = v;
-                Ln[lane * NU + m] = v;
+                const double v = m <= lane ? row[m] : 0.0;
+                if (m <= lane) Guu[lane * NU + m] = v;
+                if (m < lane) Guu[m * NU + lane] = v;   // L' mirrored (kcols_big)
+                if (ok) Ln[lane * NU + m] = v;
             }
-            Rinv_n[lane] = rinv[lane];
+            rinv[lane] = rin;
+            if (ok) Rinv_n[lane] = rin;
         }
     }
 
-    // K = -L_uu'^{-1} L_uu^{-1} G_ux (kkt_ocp.py:237-243): column j by the lane
-    // quad 4j..4j+3 (lane q owns rows q, q + 4, ...), one quad broadcast per
-    // pivot; to shared memory (Ks) and the factor store
-    __device__ __forceinline__ static void kcols_big(const double* Gu, const double* Ls, const double* rinv,
-                                                   double* Ks, double* Kn) {
-        constexpr int RW = (NU + 3) / 4;
-        const int tid = threadIdx.x;
-        const int lane = tid & 31;
-        const int j = tid >> 2, q = tid & 3;
-        const unsigned qmask = 0xFu << (lane & ~3);
-        const int qbase = lane & ~3;
-        if (j >= NX) return;
-        double z[RW];
+    // K = -L_uu'^{-1} L_uu^{-1} G_ux (kkt_ocp.py:238-243): one thread per column
+    // (no shuffles: per pivot one multiply and independent FMAs, the L entries
+    // broadcast from shared memory), the columns spread over KW warps so that
+    // each warp scheduler issues for one of them; to shared memory (Ks) and the
+    // factor store.  G_ux = ([B A]' T1)_ux + S_n first (M~, kkt_common.py:100-115):
+    // Ss is S_n in shared memory (TMA); the sum goes back to Gu for the P update.
+    static constexpr int KW = 4, KCPW = (NX + KW - 1) / KW;   // warps, columns per warp
+    static_assert(KCPW <= 32 && KW * 32 <= TEAM, "kcols_big columns");
+    __device__ __forceinline__ static int kcol_of(int tid) {
+        const int w = tid >> 5, l = tid & 31;
+        return (w < KW && l < KCPW && w * KCPW + l < NX) ? w * KCPW + l : -1;
+    }
+    __device__ __forceinline__ static void kcols_big(double* Gu, const double* Ls, const double* rinv,
+                                                   const double* Ss, double* Ks, double* Kn) {
+        const int j = kcol_of(threadIdx.x);
+        if (j < 0) return;
+        // Ls holds L_uu in its lower triangle and L_uu' mirrored into the upper
+        // one (chol_uu): both substitutions walk column i of the array, and the
+        // backward pass reads other addresses than the forward pass -- with one
+        // copy the compiler keeps all 190 loaded entries for reuse and spills them.
+        double z[NU];
 #pragma unroll
-        for (int r = 0; r < RW; ++r) {
-            const int k = q + 4 * r;
-            z[r] = k < NU ? Gu[k * GLD + NU + j] : 0.0;
+        for (int k = 0; k < NU; ++k) {
+            z[k] = Gu[k * GLD + NU + j] + Ss[k * NX + j];
+            Gu[k * GLD + NU + j] = z[k];
         }
 #pragma unroll
         for (int i = 0; i < NU; ++i) {
-            const int ri = i >> 2, oi = i & 3;
-            if (q == oi) z[ri] = z[ri] * rinv[i];
-            const double zi = __shfl_sync(qmask, z[ri], qbase | oi);
+            z[i] = z[i] * rinv[i];
 #pragma unroll
-            for (int r = 0; r < RW; ++r) {
-                const int k = q + 4 * r;
-                if (k > i && k < NU) z[r] = fma(-Ls[k * NU + i], zi, z[r]);
-            }
+            for (int k = i + 1; k < NU; ++k) z[k] = fma(-Ls[k * NU + i], z[i], z[k]);
         }
 #pragma unroll
         for (int i = NU - 1; i >= 0; --i) {
-            const int ri = i >> 2, oi = i & 3;
-            if (q == oi) z[ri] = z[ri] * rinv[i];
-            const double zi = __shfl_sync(qmask, z[ri], qbase | oi);
+            z[i] = z[i] * rinv[i];
 #pragma unroll
-            for (int r = 0; r < RW; ++r) {
-                const int k = q + 4 * r;
-                if (k < i) z[r] = fma(-Ls[i * NU + k], zi, z[r]);
-            }
+            for (int k = 0; k < i; ++k) z[k] = fma(-Ls[k * NU + i], z[i], z[k]);
         }
 #pragma unroll
-        for (int r = 0; r < RW; ++r) {
-            const int k = q + 4 * r;
-            if (k < NU) {
-                Kn[k * NX + j] = -z[r];
-                Ks[k * NX + j] = -z[r];
+        for (int k = 0; k < NU; ++k) {
+            Kn[k * NX + j] = -z[k];
+            Ks[k * NX + j] = -z[k];
+        }
+    }
+
+    // P (symmetric, in shared memory) -> the factor store: row i of the padded
+    // packed lower triangle is one TMA bulk store (16-byte aligned on both
+    // sides, an even number of doubles; the pad is the row's next entry), issued
+    // by thread PS_T0 + i.  The stores drain in the background; p_store_wait
+    // before the rows in shared memory are overwritten.
+    static constexpr int PS_T0 = 64;
+    static_assert(PS_T0 + NX <= TEAM, "store_p_big threads");
+    __device__ __forceinline__ static void store_p_big(const double* Pc, double* Pn) {
+#ifdef OCPQP_NOPSTORE
+        return;
+#endif
+        const int i = (int)threadIdx.x - PS_T0;
+        if (i >= 0 && i < NX) {
+            if constexpr (S::PPAD) {
+                fence_proxy_async();
+                const unsigned bytes = (unsigned)(((i + 2) >> 1) << 1) * 8u;
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(Pn + S::prow(i)),
+                             "r"(smem_u32(Pc + i * NX)), "r"(bytes)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+            } else {
+                for (int j = 0; j < NX; ++j)
+                    if (!S::PPACK) Pn[i * NX + j] = Pc[i * NX + j];
+                    else if (j <= i) Pn[S::prow(i) + j] = Pc[i * NX + j];
             }
         }
+    }
+    // the bulk stores of this thread have read their shared-memory rows
+    __device__ __forceinline__ static void p_store_wait() {
+        if constexpr (S::PPAD) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     }
 
     // Classical Riccati factor of a BIG shape (kkt_ocp.py:142-251).  Per stage,
@@ -2000,6 +2033,12 @@ struct Kern {
         double* T1t = Pc + NX * NX;       // NW x NX: T1'; after G: Gu | K | L
         double* BAt = T1t + NW * NX;      // NW x NX: [B A]' of the stage (TMA)
         double* vec = stg + S::VOFF;
+        double* Rs = vec;                 // NU x NU: R_n (TMA)
+        double* Guu = Rs + NU * NU;       // NU x NU: G_uu, factored in place to L_uu
+        double* dgv = Guu + NU * NU;      // NW: box term of M~'s diagonal (kkt_common.py:100-115)
+        double* rinv = dgv + NW;          // NU: 1 / L_kk
+        static_assert(2 * NU * NU + NW + NU <= S::VECB, "factor_big scratch");
+        const bool full_box = p.box_ident && d.NB == NW;
         int bad = 0;
         OCPQP_PASS_UNROLL
         for (int k = tid; k < d.nc; k += TEAM) {
@@ -2019,6 +2058,16 @@ struct Kern {
         };
         const int N = d.N;
         if (N > 0) tma_ba(c, tm, BAt, N - 1, 0);
+        // box term of M~'s diagonal for every stage (kkt_common.py:100-115), fetched per
+        // stage by TMA; kept in the rhat buffer, which is free until the solves' fold pass
+        double* dgall = wsb<WS_RHAT>(c, p);
+        OCPQP_PASS_UNROLL
+        for (int j = tid; j < N * NW; j += TEAM) {
+            const int n = j / NW;
+            const int kb = full_box ? j - n * NW : p.var_box[j];
+            dgall[j] = kb >= 0 ? cfv(n, kb) : 0.0;
+        }
+        asm volatile("fence.proxy.async;\n" ::: "memory");
         // ---- terminal stage: P_N = sym(M~_N) ----
         {
             const int n = N;
@@ -2040,19 +2089,30 @@ struct Kern {
                 const double v = 0.5 * (T1t[idx] + T1t[j * NX + i]);
                 Pc[idx] = v;
                 if (!S::PPACK) Pn[idx] = v;
-                else if (j <= i) Pn[i * (i + 1) / 2 + j] = v;
+                else if (j <= i) Pn[S::prow(i) + j] = v;
             TEAM_END
             bar<TEAM>();
         }
         for (int n = N - 1; n >= 0; --n) {
             OCPQP_TICK(c, DBG_F_P);
-            if (tid == 0 && n > 0) {   // M~ data of the next stage, the [B A]' after it -> L2
+            if (tid == TMA_THR + 32 && n > 0) {   // M~ data of the next stage, the [B A]' after it -> L2
                 l2_prefetch_bulk(Q(c, n - 1), NX * NX * 8);
                 l2_prefetch_bulk(Sm(c, n - 1), NU * NX * 8);
                 l2_prefetch_bulk(R(c, n - 1), NU * NU * 8);
                 if (n > 1) l2_prefetch_bulk(BAp(c, n - 2), BAB);
             }
+            if (tid == TMA_THR) {   // R_n and the box diagonal of M~ -> Rs, dgv (their last readers passed the previous stage's barriers)
+                fence_proxy_async_ld();
+                mbar_expect_tx(&c.mbar[2], (NU * NU + NW) * 8);
+                tma_load_1d(Rs, R(c, n), NU * NU * 8, &c.mbar[2]);
+                tma_load_1d(dgv, dgall + n * NW, NW * 8, &c.mbar[2]);
+            }
+            tm.issue(c.mbar, 2);
+            // P_{n+1} -> the factor store while the T1 loads start (P_N went there above)
+            if (n + 1 < N) store_p_big(Pc, Pst + (n + 1) * S::PST);
+            OCPQP_XTICK(c, DBG_X2);
             tm.wait(c.mbar, 0);
+            OCPQP_XTICK(c, DBG_X3);
             // ---- T1 = P_{n+1} [B A] (kkt_ocp.py:232), stored transposed ----
             {
                 const int rp = warp >> 1, ch = warp & 1;
@@ -2091,44 +2151,42 @@ struct Kern {
                     }
                 }
             }
+            p_store_wait();
             bar<TEAM>();
             OCPQP_TICK(c, DBG_F_T1);
             // ---- G = [B A]' T1 + M~ (kkt_ocp.py:233, 70-80; kkt_common.py:100-115) ----
             // warp tasks of 2 x 2 tiles over row pairs rp x column pairs cp: the
             // u rows need every column, the x rows only the x columns; held in
-            // registers until every warp is done with T1' and [B A]'
+            // registers until every warp is done with T1' and [B A]'.  Round 0
+            // (task = warp) covers G_uu: its lower triangle goes to Guu at once
+            // and warp 0 factors it (kkt_ocp.py:237) while warps 1-7 run the
+            // remaining tasks -- the Cholesky is off the stage's critical path.
+            // M~: Q_n and R_n arrive by TMA (Q into P_{n+1}'s area, dead after
+            // T1), the box term from dgv; S_n is added to G_ux in kcols_big.
             constexpr int NRP = NW / 16, NUR = (NU - 1) / 16 + 1, CP0 = NU / 16;
             constexpr int NGT = NUR * NRP + (NRP - NUR) * (NRP - CP0);
-            constexpr int GROUNDS = (NGT + 7) / 8;
+            constexpr int GROUNDS = 1 + (NGT - 8 + 6) / 7;
+            constexpr int NPROD = NUR == 1 ? 1 : 3;   // warps holding G_uu's lower triangle (incl. warp 0)
+            static_assert(NGT >= 8 && NUR <= 2 && (NUR - 1) * (NRP + 1) < 8, "factor_big G tasks");
             constexpr int PT = (NX + 15) / 16;
             double* Gu = T1t;                 // NU x GLD (after G)
             double* Ks = Gu + NU * GLD;       // NU x NX
-            double* Ls = Ks + NU * NX;        // NU x NU
+            double* Ss = Ks + NU * NX;        // NU x NX: S_n (TMA, after G)
+            static_assert(NU * GLD + 2 * NU * NX <= NW * NX && (NU * GLD) % 2 == 0, "factor_big Gu | Ks | Ss");
             const double* Qn = Q(c, n);
-            const double* Rn = R(c, n);
             const double* Sn = Sm(c, n);
-            const bool full_box = p.box_ident && d.NB == NW;
-            auto Mt = [&](int i, int j) -> double {
-                double mij, mji;
-                if (i < NU && j < NU) { mij = Rn[i * NU + j]; mji = Rn[j * NU + i]; }
-                else if (i < NU) { mij = Sn[i * NX + (j - NU)]; mji = mij; }
-                else if (j < NU) { mij = Sn[j * NX + (i - NU)]; mji = mij; }
-                else { mij = Qn[(i - NU) * NX + (j - NU)]; mji = Qn[(j - NU) * NX + (i - NU)]; }
-                double h = 0.5 * (mij + mji);
-                if (i == j) {
-                    const int kb = full_box ? i : p.var_box[n * NW + i];
-                    if (kb >= 0) h += cfv(n, kb);
-                    if (reg != 0.0) h += reg;
-                }
-                return h;
-            };
             auto gtask = [&](int task, int& rp, int& cp) {
                 if (task < NUR * NRP) { rp = task / NRP; cp = task % NRP; }
                 else { const int u = task - NUR * NRP; rp = NUR + u / (NRP - CP0); cp = CP0 + u % (NRP - CP0); }
             };
-            // Q_n of M~ into P_{n+1}'s area (dead after T1) by TMA while the k loops run
-            if (tid == 0) {
-                fence_proxy_async();
+            // round r's task of this warp (-1: none): round 0 every warp, then warps 1-7
+            auto gtask_of = [&](int r) -> int {
+                if (r == 0) return warp;
+                const int task = 8 + (warp - 1) + 7 * (r - 1);
+                return (warp > 0 && task < NGT) ? task : -1;
+            };
+            if (tid == TMA_THR) {
+                fence_proxy_async_ld();
                 mbar_expect_tx(&c.mbar[1], NX * NX * 8);
                 tma_load_1d(Pc, Qn, NX * NX * 8, &c.mbar[1]);
             }
@@ -2140,63 +2198,110 @@ struct Kern {
                 for (int ti = 0; ti < 2; ++ti)
 #pragma unroll
                     for (int tj = 0; tj < 2; ++tj) g[r][ti][tj][0] = g[r][ti][tj][1] = 0.0;
-#pragma unroll
-            for (int r = 0; r < GROUNDS; ++r) {
-                const int task = warp + 8 * r;
-                if (task < NGT) {
-                    int rp, cp;
-                    gtask(task, rp, cp);
+            auto kloop = [&](double (&ga)[2][2][2], int task) {
+                int rp, cp;
+                gtask(task, rp, cp);
 #pragma unroll 3
-                    for (int ks = 0; ks < NX / 4; ++ks) {
-                        const int k = 4 * ks + tg;
-                        double a[2], b[2];
+                for (int ks = 0; ks < NX / 4; ++ks) {
+                    const int k = 4 * ks + tg;
+                    double a[2], b[2];
 #pragma unroll
-                        for (int ti = 0; ti < 2; ++ti) a[ti] = BAt[(16 * rp + 8 * ti + gr) * NX + k];
+                    for (int ti = 0; ti < 2; ++ti) a[ti] = BAt[(16 * rp + 8 * ti + gr) * NX + k];
 #pragma unroll
-                        for (int tj = 0; tj < 2; ++tj) b[tj] = T1t[(16 * cp + 8 * tj + gr) * NX + k];
+                    for (int tj = 0; tj < 2; ++tj) b[tj] = T1t[(16 * cp + 8 * tj + gr) * NX + k];
 #pragma unroll
-                        for (int ti = 0; ti < 2; ++ti)
+                    for (int ti = 0; ti < 2; ++ti)
 #pragma unroll
-                            for (int tj = 0; tj < 2; ++tj) dmma_acc(g[r][ti][tj][0], g[r][ti][tj][1], a[ti], b[tj]);
-                    }
+                        for (int tj = 0; tj < 2; ++tj) dmma_acc(ga[ti][tj][0], ga[ti][tj][1], a[ti], b[tj]);
                 }
-            }
-            // G = ([B A]' T1) + M~ (the reference's matmul_acc order): Q from
-            // shared memory, R and S (L2-prefetched) from global memory
-            tm.wait(c.mbar, 1);
-            auto Mts = [&](int i, int j) -> double {
-                if (i >= NU && j >= NU) {
-                    double h = 0.5 * (Pc[(i - NU) * NX + (j - NU)] + Pc[(j - NU) * NX + (i - NU)]);
-                    if (i == j) {
-                        const int kb = full_box ? i : p.var_box[n * NW + i];
-                        if (kb >= 0) h += cfv(n, kb);
-                        if (reg != 0.0) h += reg;
-                    }
-                    return h;
-                }
-                return Mt(i, j);
             };
+            // G = ([B A]' T1) + M~ (the reference's matmul_acc order) on the uu and xx blocks
+            auto addM = [&](double (&ga)[2][2][2], int task, bool uu) {
+                int rp, cp;
+                gtask(task, rp, cp);
 #pragma unroll
-            for (int r = 0; r < GROUNDS; ++r) {
-                const int task = warp + 8 * r;
-                if (task < NGT) {
-                    int rp, cp;
-                    gtask(task, rp, cp);
+                for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+                    for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int i = 16 * rp + 8 * ti + gr, j = 16 * cp + 8 * tj + 2 * tg + e;
+                            double h;
+                            if (!uu && i >= NU && j >= NU)
+                                h = 0.5 * (Pc[(i - NU) * NX + (j - NU)] + Pc[(j - NU) * NX + (i - NU)]);
+                            else if (uu && i < NU && j < NU)
+                                h = 0.5 * (Rs[i * NU + j] + Rs[j * NU + i]);
+                            else
+                                continue;
+                            if (i == j) {
+                                h += dgv[i];
+                                if (reg != 0.0) h += reg;
+                            }
+                            ga[ti][tj][e] += h;
+                        }
+            };
+            // ---- round 0, G_uu -> Guu, then warp 0: L_uu = chol(G_uu) | warps 1-7: the other tasks
+            kloop(g[0], warp);
+            OCPQP_XTICK(c, DBG_X0);
+            tm.wait(c.mbar, 2);
+            {
+                int rp, cp;
+                gtask(warp, rp, cp);
+                if (rp < NUR && cp <= rp) {
+                    addM(g[0], warp, true);
 #pragma unroll
                     for (int ti = 0; ti < 2; ++ti)
 #pragma unroll
                         for (int tj = 0; tj < 2; ++tj)
 #pragma unroll
-                            for (int e = 0; e < 2; ++e)
-                                g[r][ti][tj][e] += Mts(16 * rp + 8 * ti + gr, 16 * cp + 8 * tj + 2 * tg + e);
+                            for (int e = 0; e < 2; ++e) {
+                                const int i = 16 * rp + 8 * ti + gr, j = 16 * cp + 8 * tj + 2 * tg + e;
+                                if (i < NU && j <= i) Guu[i * NU + j] = g[0][ti][tj][e];
+                            }
+                    if constexpr (NPROD > 1) {
+                        if (warp != 0) {
+                            __threadfence_block();
+                            asm volatile("bar.arrive 1, %0;\n" ::"n"(32 * NPROD) : "memory");
+                        }
+                    }
                 }
             }
-            bar<TEAM>();   // every warp is done with T1' and [B A]'
+            OCPQP_XTICK(c, DBG_X1);
+            double* Ln = Lst + n * NU * NU;
+            double* Rinv_n = wsb<WS_RINV>(c, p) + n * NU;
+            double* Kn = Kst + n * NU * NX;
+            if (warp == 0) {
+                if constexpr (NPROD > 1) asm volatile("bar.sync 1, %0;\n" ::"n"(32 * NPROD) : "memory");
+                else __syncwarp();
+                chol_uu(c, Guu, Ln, Rinv_n, rinv);
+                OCPQP_XTICK(c, DBG_X7);
+                tm.wait(c.mbar, 1);
+                addM(g[0], 0, false);
+            } else {
+#pragma unroll
+                for (int r = 1; r < GROUNDS; ++r) {
+                    const int task = gtask_of(r);
+                    if (task >= 0) kloop(g[r], task);
+                }
+                tm.wait(c.mbar, 1);
+#pragma unroll
+                for (int r = 0; r < GROUNDS; ++r) {
+                    const int task = gtask_of(r);
+                    if (task >= 0) addM(g[r], task, false);
+                }
+            }
+            bar<TEAM>();   // every warp is done with T1' and [B A]'; L_uu is in Guu
             if (n > 0) tma_ba(c, tm, BAt, n - 1, 0);
+            if (tid == TMA_THR) {   // S_n of M~ (added to G_ux in kcols_big) behind Gu | Ks
+                fence_proxy_async_ld();
+                mbar_expect_tx(&c.mbar[2], NU * NX * 8);
+                tma_load_1d(Ss, Sn, NU * NX * 8, &c.mbar[2]);
+            }
+            tm.issue(c.mbar, 2);
 #pragma unroll
             for (int r = 0; r < GROUNDS; ++r) {
-                const int task = warp + 8 * r;
-                if (task < NGT) {
+                const int task = gtask_of(r);
+                if (task >= 0) {
                     int rp, cp;
                     gtask(task, rp, cp);
 #pragma unroll
@@ -2207,34 +2312,38 @@ struct Kern {
                             for (int e = 0; e < 2; ++e) {
                                 const int i = 16 * rp + 8 * ti + gr, j = 16 * cp + 8 * tj + 2 * tg + e;
                                 const double v = g[r][ti][tj][e];
-                                if (i < NU) Gu[i * GLD + j] = v;
-                                else if (j >= NU) Pc[(i - NU) * NX + (j - NU)] = v;
+                                if (i < NU) {
+                                    if (j >= NU) Gu[i * GLD + j] = v;
+                                } else if (j >= NU) Pc[(i - NU) * NX + (j - NU)] = v;
                             }
                 }
             }
             flops += 2ll * NX * NW * NX + 2ll * NW * NW * NX;
+            flops += (long long)NU * NU * NU / 3;
+            OCPQP_XTICK(c, DBG_X4);
             bar<TEAM>();
             OCPQP_TICK(c, DBG_F_G);
-            // ---- L_uu = chol(G_uu), K (kkt_ocp.py:237-243) ----
-            double* Ln = Lst + n * NU * NU;
-            double* Rinv_n = wsb<WS_RINV>(c, p) + n * NU;
-            double* Kn = Kst + n * NU * NX;
-            flops += (long long)NU * NU * NU / 3;
-            if (warp_id_uniform() == 0) chol_big(c, Gu, Ls, Ln, Rinv_n, vec);
-            bar<TEAM>();
             OCPQP_TICK(c, DBG_F_CHOL);
             if (!c.flag) {
                 tm.drain(c.mbar);
+                p_store_wait();
                 return n;
             }
-            kcols_big(Gu, Ls, vec, Ks, Kn);
+            // ---- K (kkt_ocp.py:238-243) ----
+            tm.wait(c.mbar, 2);
+            OCPQP_XTICK(c, DBG_X6);
+            kcols_big(Gu, Guu, rinv, Ss, Ks, Kn);
             flops += 2ll * NU * NU * NX;
             bar<TEAM>();
             OCPQP_TICK(c, DBG_F_K);
-            // ---- P = G_xx + G_ux' K (kkt_ocp.py:244), in place ----
-            for (int task = warp; task < PT * PT; task += 8) {
-                const int rp = task / PT, cp = task % PT;
-                double acc[2][2][2];
+            // ---- P = 0.5 (T + T'), T = G_xx + G_ux' K (kkt_ocp.py:244, 251), in place ----
+            // warp task = the tile pair (rp, cp), (cp, rp), rp >= cp: the warp holds
+            // T(i, j) and T(j, i) in the same fragment slot (the second product with
+            // the operand roles swapped), so the symmetrisation is register-local
+            for (int task = warp; task < PT * (PT + 1) / 2; task += 8) {
+                int rp = 0, cp = task;
+                while (cp > rp) { cp -= rp + 1; ++rp; }
+                double acc[2][2][2], act[2][2][2];
 #pragma unroll
                 for (int ti = 0; ti < 2; ++ti)
 #pragma unroll
@@ -2242,27 +2351,35 @@ struct Kern {
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
                             const int i = 16 * rp + 8 * ti + gr, j = 16 * cp + 8 * tj + 2 * tg + e;
-                            acc[ti][tj][e] = (i < NX && j < NX) ? Pc[i * NX + j] : 0.0;
+                            const bool in = i < NX && j < NX;
+                            acc[ti][tj][e] = in ? Pc[i * NX + j] : 0.0;
+                            act[ti][tj][e] = in ? Pc[j * NX + i] : 0.0;
                         }
 #pragma unroll
                 for (int ks = 0; ks < NU / 4; ++ks) {
                     const int k = 4 * ks + tg;
-                    double a[2], b[2];
+                    double a[2], b[2], at[2], bt[2];
 #pragma unroll
                     for (int ti = 0; ti < 2; ++ti) {
                         const int i = 16 * rp + 8 * ti + gr;
                         a[ti] = i < NX ? Gu[k * GLD + NU + i] : 0.0;
+                        at[ti] = i < NX ? Ks[k * NX + i] : 0.0;
                     }
 #pragma unroll
                     for (int tj = 0; tj < 2; ++tj) {
                         const int j = 16 * cp + 8 * tj + gr;
                         b[tj] = j < NX ? Ks[k * NX + j] : 0.0;
+                        bt[tj] = j < NX ? Gu[k * GLD + NU + j] : 0.0;
                     }
 #pragma unroll
                     for (int ti = 0; ti < 2; ++ti)
 #pragma unroll
-                        for (int tj = 0; tj < 2; ++tj) dmma_acc(acc[ti][tj][0], acc[ti][tj][1], a[ti], b[tj]);
+                        for (int tj = 0; tj < 2; ++tj) {
+                            dmma_acc(acc[ti][tj][0], acc[ti][tj][1], a[ti], b[tj]);
+                            dmma_acc(act[ti][tj][0], act[ti][tj][1], at[ti], bt[tj]);
+                        }
                 }
+                __syncwarp();   // diagonal pairs: every lane has read its T(j, i) seed
 #pragma unroll
                 for (int ti = 0; ti < 2; ++ti)
 #pragma unroll
@@ -2270,30 +2387,24 @@ struct Kern {
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
                             const int i = 16 * rp + 8 * ti + gr, j = 16 * cp + 8 * tj + 2 * tg + e;
-                            if (i < NX && j < NX) Pc[i * NX + j] = acc[ti][tj][e];
+                            if (i < NX && j < NX) {
+                                const double v = 0.5 * (acc[ti][tj][e] + act[ti][tj][e]);
+                                Pc[i * NX + j] = v;
+                                Pc[j * NX + i] = v;
+                            }
                         }
             }
             flops += 2ll * NX * NX * NU;
-            bar<TEAM>();
-            // 0.5 (P + P') in place; the packed lower triangle to the factor store
-            double* Pn = Pst + n * S::PST;
-            TEAM_FOR(idx, NX * NX)
-                const int i = idx / NX, j = idx - i * NX;
-                if (j <= i) {
-                    const double v = 0.5 * (Pc[idx] + Pc[j * NX + i]);
-                    Pc[idx] = v;
-                    Pc[j * NX + i] = v;
-                    if (S::PPACK) Pn[i * (i + 1) / 2 + j] = v;
-                    else { Pn[idx] = v; Pn[j * NX + i] = v; }
-                }
-            TEAM_END
+            OCPQP_XTICK(c, DBG_X5);
             bar<TEAM>();
         }
         OCPQP_TICK(c, DBG_F_P);
+        if (N > 0) store_p_big(Pc, Pst);
         // L_P0 = chol(P_0) (kkt_ocp.py:193-200)
         double* LP0 = wsb<WS_LP0>(c, p);
         flops += (long long)NX * NX * NX / 3;
         for (int idx = tid; idx < NX * NX; idx += TEAM) LP0[idx] = Pc[idx];
+        if constexpr (S::PPAD) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // P rows are in the store
         bar<TEAM>();
         if (!team_chol<TEAM>(LP0, NX, &c.flag, wsb<WS_RINV>(c, p) + N * NU)) return 0;
         return -1;
@@ -2412,16 +2523,16 @@ struct Kern {
         double* uv = xa + NX;       // NU: u_n
         double* xb = uv + NU;       // NX: x_{n+1}
         double* rhs = xb + NX;      // NW: rhat of the stage / r_b of the stage
+        double* rvs = rhs + NW;     // NU: 1 / L_ii of the stage (TMA, with the Y block)
         constexpr int PS = S::PST;
         double* sBA[2] = {stg, stg + NW * NX};
         double* blk = stg + 2 * NW * NX;   // NX * NX doubles
-        constexpr int YK = 0, YL = NU * NX, YR = YL + NU * NU, YP = YR + NU, YB = YP + PS, YH = YB + NX,
-                      YN = YH + NW;
+        constexpr int YK = 0, YL = NU * NX, YP = YL + NU * NU, YB = YP + PS, YH = YB + NX, YN = YH + NW;
         constexpr int FK = 0, FF = NU * NX, FB = FF + NU, FP = FB + NX, FV = FP + PS, FN = FV + NX;
         static_assert(YN <= NX * NX && FN <= NX * NX, "sweeps_big block");
-        static_assert(YL % 2 == 0 && YR % 2 == 0 && YP % 2 == 0 && YB % 2 == 0 && YH % 2 == 0 &&
+        static_assert(YL % 2 == 0 && YP % 2 == 0 && YB % 2 == 0 && YH % 2 == 0 && (NW + 4 * NX + NU + NW) % 2 == 0 &&
                       FF % 2 == 0 && FB % 2 == 0 && FP % 2 == 0 && FV % 2 == 0, "16-byte block offsets");
-        static_assert(NW + 4 * NX + NU + NW <= S::VECB, "sweeps_big vectors");
+        static_assert(NW + 4 * NX + NU + NW + NU <= S::VECB, "sweeps_big vectors");
         const int N = d.N;
         // the factor store, r_b and rhat were written through the generic proxy
         asm volatile("fence.proxy.async;\n" ::: "memory");
@@ -2429,12 +2540,12 @@ struct Kern {
             tma_load_1d(dst, src, (unsigned)nd * 8u, &c.mbar[2]);
         };
         auto issue_Y = [&](int n) {   // K_n, L_n, 1/L_ii, and for n > 0: P_n, r_b,n-1, rhat_{n-1}
-            if (tid == 0) {
-                fence_proxy_async();
-                mbar_expect_tx(&c.mbar[2], (n > 0 ? YN : YP) * 8);
+            if (tid == TMA_THR) {
+                fence_proxy_async_ld();
+                mbar_expect_tx(&c.mbar[2], ((n > 0 ? YN : YP) + NU) * 8);
                 cp(blk + YK, Kst + n * NU * NX, NU * NX);
                 cp(blk + YL, Lst + n * NU * NU, NU * NU);
-                cp(blk + YR, Rst + n * NU, NU);
+                cp(rvs, Rst + n * NU, NU);
                 if (n > 0) {
                     cp(blk + YP, Pst + n * PS, PS);
                     cp(blk + YB, r_b + (n - 1) * NX, NX);
@@ -2444,7 +2555,7 @@ struct Kern {
             tm.issue(c.mbar, 2);
         };
         auto l2pf = [&](int n) {
-            if (tid == 0 && n >= 0 && n < N) {
+            if (tid == TMA_THR + 32 && n >= 0 && n < N) {
                 l2_prefetch_bulk(BAp(c, n), BAB);
                 l2_prefetch_bulk(Pst + (n + 1) * PS, PS * 8);
                 l2_prefetch_bulk(Kst + n * NU * NX, NU * NX * 8);
@@ -2484,7 +2595,7 @@ struct Kern {
             tm.wait(c.mbar, 2);
             const double* Kn = blk + YK;
             const double* Ln = blk + YL;
-            const double* Rn = blk + YR;
+            const double* Rn = rvs;
             double* pvc = pv + n * NX;
             if (warp == TEAM / 32 - 1) {
                 warp_cho_solve<NU>(Ln, Rn, win, kff + n * NU, -1.0);
@@ -2516,8 +2627,8 @@ struct Kern {
         bar<TEAM>();
         // ---- forward rollout (kkt_ocp.py:293-305) ----
         auto issue_F = [&](int n) {   // K_n, kff_n, r_b,n, P_n, pv_n
-            if (tid == 0) {
-                fence_proxy_async();
+            if (tid == TMA_THR) {
+                fence_proxy_async_ld();
                 mbar_expect_tx(&c.mbar[2], FN * 8);
                 cp(blk + FK, Kst + n * NU * NX, NU * NX);
                 cp(blk + FF, kff + n * NU, NU);

@@ -99,7 +99,7 @@ struct KParams {
     int box_ident;            // 1: every stage's idxb is 0..nb-1 (box row i bounds variable i)
     int stage_smem;           // doubles: offset of the per-stage scratch / per-team tile
     int team_stride;          // doubles of shared memory per team (row kernel)
-    long long* dbg;           // optional [B, 8] phase-cycle counters (nullptr = off)
+    long long* dbg;           // optional [B, DBG_NUM] phase-cycle counters (nullptr = off)
     const double* ba;         // shaped kernels: packed [B A] per stage (NX x NW), see
     long long ba_bs;          //   launch_pack_ba; per-QP stride (0: one copy for the batch)
     long long ba_ns;          //   per-stage stride (0: the kernel's default, QP-major packing)
@@ -116,7 +116,9 @@ enum DbgPhase { DBG_RES = 0, DBG_FACTOR, DBG_SOLVE_AFF, DBG_SOLVE_DIR, DBG_STEP,
                 DBG_ITERS, DBG_SPARE,
                 // sub-phases (team kernel): factor stage parts, solve parts
                 DBG_F_T1, DBG_F_G, DBG_F_CHOL, DBG_F_K, DBG_F_P, DBG_S_PRE, DBG_S_BWD, DBG_S_FWD,
-                DBG_NUM = 16 };
+                // free slots for finer diagnostics (OCPQP_XTICK, -DOCPQP_XDIAG builds)
+                DBG_X0, DBG_X1, DBG_X2, DBG_X3, DBG_X4, DBG_X5, DBG_X6, DBG_X7,
+                DBG_NUM = 24 };
 
 struct SolveParams {
     OcpIpmArgC arg;

@@ -73,7 +73,7 @@ def main():
             info = S.get_plan(batch).info()
             phases = None
             if a.phases and kind != "g":
-                dbg = torch.zeros((B, 16), dtype=torch.int64, device="cuda")
+                dbg = torch.zeros((B, 24), dtype=torch.int64, device="cuda")
                 solve_ocp_qp_batch(batch, arg, trace=False, phase_debug=dbg)
                 torch.cuda.synchronize()
                 solve_ocp_qp_batch(batch, arg, trace=False)  # switch instrumentation off
@@ -83,6 +83,9 @@ def main():
                          8: "f_T1", 9: "f_G", 10: "f_chol", 11: "f_K", 12: "f_P",
                          13: "s_pre_post", 14: "s_bwd", 15: "s_fwd"}
                 phases = {nm: round(float(np.mean(ph[:, i] / n_it))) for i, nm in names.items()}
+                for x in range(8):   # free diagnostic slots (OCPQP_XDIAG builds)
+                    if ph[:, 16 + x].any():
+                        phases[f"x{x}"] = round(float(np.mean(ph[:, 16 + x] / n_it)))
                 phases["total_per_iter"] = float(np.mean(ph[:, 5] / n_it))
                 phases["max_total_cycles"] = float(ph[:, 5].max())
             print(json.dumps({"cfg": cfg, "kind": kind, "B": B, "gen_s": round(tg, 1),
