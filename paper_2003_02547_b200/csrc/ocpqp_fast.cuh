@@ -410,6 +410,7 @@ struct FCtx {
     int q;
     double n_act;
     long long ph[DBG_NUM];  // clock64 phase accumulators (KParams::dbg)
+    long long tk1;          // OCPQP_XTICK1: previous tick of thread 32
     long long tk;
 };
 
@@ -653,8 +654,18 @@ __device__ __forceinline__ void stage_gemm(FA a, FB b, FP pre, FE epi) {
 // finer ticks into the free slots, only in -DOCPQP_XDIAG builds
 #ifdef OCPQP_XDIAG
 #define OCPQP_XTICK(c, slot) OCPQP_TICK(c, slot)
+// the same from thread 32 (warp 1); slot < 0 only restarts its clock
+#define OCPQP_XTICK1(c, slot)                                     \
+    do {                                                          \
+        if (p.dbg && threadIdx.x == 32) {                         \
+            const long long n_ = clock64();                       \
+            if ((slot) >= 0) (c).ph[(slot) < 0 ? 0 : (slot)] += n_ - (c).tk1; \
+            (c).tk1 = n_;                                         \
+        }                                                         \
+    } while (0)
 #else
 #define OCPQP_XTICK(c, slot) do { } while (0)
+#define OCPQP_XTICK1(c, slot) do { } while (0)
 #endif
 
 // runtime structure (uniform stages)
@@ -2110,9 +2121,7 @@ struct Kern {
             tm.issue(c.mbar, 2);
             // P_{n+1} -> the factor store while the T1 loads start (P_N went there above)
             if (n + 1 < N) store_p_big(Pc, Pst + (n + 1) * S::PST);
-            OCPQP_XTICK(c, DBG_X2);
             tm.wait(c.mbar, 0);
-            OCPQP_XTICK(c, DBG_X3);
             // ---- T1 = P_{n+1} [B A] (kkt_ocp.py:232), stored transposed ----
             {
                 const int rp = warp >> 1, ch = warp & 1;
@@ -2157,17 +2166,18 @@ struct Kern {
             // ---- G = [B A]' T1 + M~ (kkt_ocp.py:233, 70-80; kkt_common.py:100-115) ----
             // warp tasks of 2 x 2 tiles over row pairs rp x column pairs cp: the
             // u rows need every column, the x rows only the x columns; held in
-            // registers until every warp is done with T1' and [B A]'.  Round 0
-            // (task = warp) covers G_uu: its lower triangle goes to Guu at once
-            // and warp 0 factors it (kkt_ocp.py:237) while warps 1-7 run the
-            // remaining tasks -- the Cholesky is off the stage's critical path.
-            // M~: Q_n and R_n arrive by TMA (Q into P_{n+1}'s area, dead after
-            // T1), the box term from dgv; S_n is added to G_ux in kcols_big.
-            constexpr int NRP = NW / 16, NUR = (NU - 1) / 16 + 1, CP0 = NU / 16;
-            constexpr int NGT = NUR * NRP + (NRP - NUR) * (NRP - CP0);
-            constexpr int GROUNDS = 1 + (NGT - 8 + 6) / 7;
-            constexpr int NPROD = NUR == 1 ? 1 : 3;   // warps holding G_uu's lower triangle (incl. warp 0)
-            static_assert(NGT >= 8 && NUR <= 2 && (NUR - 1) * (NRP + 1) < 8, "factor_big G tasks");
+            // registers until every warp is done with T1' and [B A]'.  G_uu comes
+            // first: warps 1.. each take 8 x 8 tiles of its lower triangle, add
+            // M~ and put them in Guu; warp 0 then factors it (kkt_ocp.py:237)
+            // while warps 1-7 run the G_ux / G_xx tasks -- the Cholesky is off
+            // the stage's critical path.  M~: Q_n and R_n arrive by TMA (Q into
+            // P_{n+1}'s area, dead after T1), the box term from dgv; S_n is
+            // added to G_ux in kcols_big.
+            constexpr int NRP = NW / 16, CP0 = NU / 16;   // column pairs below CP0 hold u columns only
+            constexpr int NGT = NRP * (NRP - CP0);
+            constexpr int GROUNDS = (NGT + 6) / 7;
+            constexpr int TU = (NU + 7) / 8, NUT = TU * (TU + 1) / 2;   // 8 x 8 tiles of G_uu's lower triangle
+            constexpr int NPROD = NUT < 7 ? NUT : 7;                    // warps 1..NPROD produce them
             constexpr int PT = (NX + 15) / 16;
             double* Gu = T1t;                 // NU x GLD (after G)
             double* Ks = Gu + NU * GLD;       // NU x NX
@@ -2176,13 +2186,12 @@ struct Kern {
             const double* Qn = Q(c, n);
             const double* Sn = Sm(c, n);
             auto gtask = [&](int task, int& rp, int& cp) {
-                if (task < NUR * NRP) { rp = task / NRP; cp = task % NRP; }
-                else { const int u = task - NUR * NRP; rp = NUR + u / (NRP - CP0); cp = CP0 + u % (NRP - CP0); }
+                rp = task / (NRP - CP0);
+                cp = CP0 + task % (NRP - CP0);
             };
-            // round r's task of this warp (-1: none): round 0 every warp, then warps 1-7
+            // round r's task of this warp (-1: none): warps 1-7
             auto gtask_of = [&](int r) -> int {
-                if (r == 0) return warp;
-                const int task = 8 + (warp - 1) + 7 * (r - 1);
+                const int task = (warp - 1) + 7 * r;
                 return (warp > 0 && task < NGT) ? task : -1;
             };
             if (tid == TMA_THR) {
@@ -2191,6 +2200,38 @@ struct Kern {
                 tma_load_1d(Pc, Qn, NX * NX * 8, &c.mbar[1]);
             }
             tm.issue(c.mbar, 1);
+            OCPQP_XTICK1(c, -1);
+            tm.wait(c.mbar, 2);   // R_n, dgv (issued at the top of the stage)
+            OCPQP_XTICK1(c, DBG_X0);
+            // ---- G_uu (lower 8 x 8 tiles) + M~ -> Guu ----
+            if (warp >= 1 && warp <= NPROD) {
+                for (int q = warp - 1; q < NUT; q += 7) {
+                    int t = 0, sc = q;
+                    while (sc > t) { sc -= t + 1; ++t; }
+                    double u0 = 0.0, u1 = 0.0;
+#pragma unroll 5
+                    for (int ks = 0; ks < NX / 4; ++ks) {
+                        const int k = 4 * ks + tg;
+                        dmma_acc(u0, u1, BAt[(8 * t + gr) * NX + k], T1t[(8 * sc + gr) * NX + k]);
+                    }
+                    const int i = 8 * t + gr;
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int j = 8 * sc + 2 * tg + e;
+                        if (i < NU && j <= i) {
+                            double h = 0.5 * (Rs[i * NU + j] + Rs[j * NU + i]);
+                            if (i == j) {
+                                h += dgv[i];
+                                if (reg != 0.0) h += reg;
+                            }
+                            Guu[i * NU + j] = (e ? u1 : u0) + h;
+                        }
+                    }
+                }
+                __threadfence_block();
+                asm volatile("bar.arrive 1, %0;\n" ::"n"(32 * (NPROD + 1)) : "memory");
+            }
+            OCPQP_XTICK1(c, DBG_X1);
             double g[GROUNDS][2][2][2];
 #pragma unroll
             for (int r = 0; r < GROUNDS; ++r)
@@ -2215,8 +2256,8 @@ struct Kern {
                         for (int tj = 0; tj < 2; ++tj) dmma_acc(ga[ti][tj][0], ga[ti][tj][1], a[ti], b[tj]);
                 }
             };
-            // G = ([B A]' T1) + M~ (the reference's matmul_acc order) on the uu and xx blocks
-            auto addM = [&](double (&ga)[2][2][2], int task, bool uu) {
+            // G_xx = ([B A]' T1)_xx + M~_xx (the reference's matmul_acc order)
+            auto addM = [&](double (&ga)[2][2][2], int task) {
                 int rp, cp;
                 gtask(task, rp, cp);
 #pragma unroll
@@ -2226,69 +2267,40 @@ struct Kern {
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
                             const int i = 16 * rp + 8 * ti + gr, j = 16 * cp + 8 * tj + 2 * tg + e;
-                            double h;
-                            if (!uu && i >= NU && j >= NU)
-                                h = 0.5 * (Pc[(i - NU) * NX + (j - NU)] + Pc[(j - NU) * NX + (i - NU)]);
-                            else if (uu && i < NU && j < NU)
-                                h = 0.5 * (Rs[i * NU + j] + Rs[j * NU + i]);
-                            else
-                                continue;
-                            if (i == j) {
-                                h += dgv[i];
-                                if (reg != 0.0) h += reg;
+                            if (i >= NU && j >= NU) {
+                                double h = 0.5 * (Pc[(i - NU) * NX + (j - NU)] + Pc[(j - NU) * NX + (i - NU)]);
+                                if (i == j) {
+                                    h += dgv[i];
+                                    if (reg != 0.0) h += reg;
+                                }
+                                ga[ti][tj][e] += h;
                             }
-                            ga[ti][tj][e] += h;
                         }
             };
-            // ---- round 0, G_uu -> Guu, then warp 0: L_uu = chol(G_uu) | warps 1-7: the other tasks
-            kloop(g[0], warp);
-            OCPQP_XTICK(c, DBG_X0);
-            tm.wait(c.mbar, 2);
-            {
-                int rp, cp;
-                gtask(warp, rp, cp);
-                if (rp < NUR && cp <= rp) {
-                    addM(g[0], warp, true);
-#pragma unroll
-                    for (int ti = 0; ti < 2; ++ti)
-#pragma unroll
-                        for (int tj = 0; tj < 2; ++tj)
-#pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                const int i = 16 * rp + 8 * ti + gr, j = 16 * cp + 8 * tj + 2 * tg + e;
-                                if (i < NU && j <= i) Guu[i * NU + j] = g[0][ti][tj][e];
-                            }
-                    if constexpr (NPROD > 1) {
-                        if (warp != 0) {
-                            __threadfence_block();
-                            asm volatile("bar.arrive 1, %0;\n" ::"n"(32 * NPROD) : "memory");
-                        }
-                    }
-                }
-            }
-            OCPQP_XTICK(c, DBG_X1);
             double* Ln = Lst + n * NU * NU;
             double* Rinv_n = wsb<WS_RINV>(c, p) + n * NU;
             double* Kn = Kst + n * NU * NX;
+            // ---- warp 0: L_uu = chol(G_uu) | warps 1-7: G_ux, G_xx ----
             if (warp == 0) {
-                if constexpr (NPROD > 1) asm volatile("bar.sync 1, %0;\n" ::"n"(32 * NPROD) : "memory");
-                else __syncwarp();
+                asm volatile("bar.sync 1, %0;\n" ::"n"(32 * (NPROD + 1)) : "memory");
                 chol_uu(c, Guu, Ln, Rinv_n, rinv);
                 OCPQP_XTICK(c, DBG_X7);
                 tm.wait(c.mbar, 1);
-                addM(g[0], 0, false);
             } else {
-#pragma unroll
-                for (int r = 1; r < GROUNDS; ++r) {
-                    const int task = gtask_of(r);
-                    if (task >= 0) kloop(g[r], task);
-                }
-                tm.wait(c.mbar, 1);
 #pragma unroll
                 for (int r = 0; r < GROUNDS; ++r) {
                     const int task = gtask_of(r);
-                    if (task >= 0) addM(g[r], task, false);
+                    if (task >= 0) kloop(g[r], task);
                 }
+                OCPQP_XTICK1(c, DBG_X2);
+                tm.wait(c.mbar, 1);
+                OCPQP_XTICK1(c, DBG_X3);
+#pragma unroll
+                for (int r = 0; r < GROUNDS; ++r) {
+                    const int task = gtask_of(r);
+                    if (task >= 0) addM(g[r], task);
+                }
+                OCPQP_XTICK1(c, DBG_X4);
             }
             bar<TEAM>();   // every warp is done with T1' and [B A]'; L_uu is in Guu
             if (n > 0) tma_ba(c, tm, BAt, n - 1, 0);
@@ -2320,7 +2332,7 @@ struct Kern {
             }
             flops += 2ll * NX * NW * NX + 2ll * NW * NW * NX;
             flops += (long long)NU * NU * NU / 3;
-            OCPQP_XTICK(c, DBG_X4);
+            OCPQP_XTICK1(c, DBG_X5);
             bar<TEAM>();
             OCPQP_TICK(c, DBG_F_G);
             OCPQP_TICK(c, DBG_F_CHOL);
@@ -2331,7 +2343,7 @@ struct Kern {
             }
             // ---- K (kkt_ocp.py:238-243) ----
             tm.wait(c.mbar, 2);
-            OCPQP_XTICK(c, DBG_X6);
+            OCPQP_XTICK1(c, DBG_X6);
             kcols_big(Gu, Guu, rinv, Ss, Ks, Kn);
             flops += 2ll * NU * NU * NX;
             bar<TEAM>();
@@ -2395,7 +2407,6 @@ struct Kern {
                         }
             }
             flops += 2ll * NX * NX * NU;
-            OCPQP_XTICK(c, DBG_X5);
             bar<TEAM>();
         }
         OCPQP_TICK(c, DBG_F_P);

@@ -9,5 +9,4 @@ for s in "$@"; do
 done
 wait
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o paper_2003_02547_b200/_lib/libocpqp_b200.so build/obj/*.o
-touch build/obj/*.o paper_2003_02547_b200/_lib/libocpqp_b200.so
 echo linked
