@@ -397,7 +397,7 @@ __device__ ResNorms residuals(Ctx& c, const double* y, const double* pi, const d
 // In-place lower Cholesky of the n x n matrix at L (leading dim ld); the upper
 // triangle is zeroed.  Fails (returns false) on a pivot that is not > 0,
 // including NaN, like LAPACK potrf behind linalg.cholesky_factor (linalg.py:81-118).
-__device__ bool team_chol(double* L, int n, int ld, int* flag) {
+__device__ bool team_chol(double* L, int n, int ld, int* flag, bool keep_upper = false) {
     // Two barriers per column: every thread reads the pivot and takes the
     // (identical) square root itself; the diagonal is written back during the
     // trailing update, which reads only the scaled column.
@@ -421,19 +421,43 @@ __device__ bool team_chol(double* L, int n, int ld, int* flag) {
         if (tid == 0) L[k * ld + k] = dk;
         // rows round-robin over warps, columns j <= i over lanes
         const int lane = tid & 31, nwarp = (T + 31) >> 5;
-        const double* ck = L + k * ld;
-        for (int i = k + 1 + (tid >> 5); i < n; i += nwarp) {
-            double* Li = L + i * ld;
-            const double lik = Li[k];
-            for (int j = k + 1 + lane; j <= i; j += 32) Li[j] -= lik * ck[j];
+        const double* __restrict__ ck = L + k * ld;
+        if (n - k > 4 * nwarp) {
+            // four rows per warp pass: their loads are independent, so four
+            // L2 / L1 round trips overlap (same arithmetic per element)
+            for (int i0 = k + 1 + 4 * (tid >> 5); i0 < n; i0 += 4 * nwarp) {
+                double lik[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) lik[q] = i0 + q < n ? L[(i0 + q) * ld + k] : 0.0;
+                const int imax = min(i0 + 3, n - 1);
+                for (int j = k + 1 + lane; j <= imax; j += 32) {
+                    const double c = ck[j];
+                    double v[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v[q] = (i0 + q < n && j <= i0 + q) ? L[(i0 + q) * ld + j] : 0.0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (i0 + q < n && j <= i0 + q) L[(i0 + q) * ld + j] = v[q] - lik[q] * c;
+                }
+            }
+        } else {
+            for (int i = k + 1 + (tid >> 5); i < n; i += nwarp) {
+                double* Li = L + i * ld;
+                const double lik = Li[k];
+                for (int j = k + 1 + lane; j <= i; j += 32) Li[j] -= lik * ck[j];
+            }
         }
         tsync();
     }
-    for (int idx = tid; idx < n * n; idx += T) {
-        const int i = idx / n, j = idx - i * n;
-        if (j > i) L[i * ld + j] = 0.0;
+    // keep_upper: the caller still reads L' from the upper triangle (row k holds
+    // column k of L) and zeroes it itself
+    if (!keep_upper) {
+        for (int idx = tid; idx < n * n; idx += T) {
+            const int i = idx / n, j = idx - i * n;
+            if (j > i) L[i * ld + j] = 0.0;
+        }
+        tsync();
     }
-    tsync();
     return true;
 }
 
@@ -570,6 +594,7 @@ __device__ __noinline__ void rows_syrk(const Ctx& c, const StageInfo& s, const d
             const double* cb = jb < nu ? Dp + jb : Cp + (jb - nu);
             const int la = ia < nu ? nu : nx, lb = jb < nu ? nu : nx;
             double d0 = 0.0, d1 = 0.0;
+#pragma unroll 4   // the operand loads of four k steps in flight
             for (int r0 = 0; r0 < ng; r0 += 4) {
                 const int r = r0 + tg;
                 const bool rin = r < ng;
@@ -637,6 +662,46 @@ __device__ __noinline__ void rows_syrk(const Ctx& c, const StageInfo& s, const d
         }
     }
 }
+
+// ---------------------------------------------------------------------------
+// C(i, j) = sum_k a(k, i) b(k, j), i < M, j < N, k ascending with one fma chain
+// per output (the arithmetic of the one-output-per-thread loops it replaces),
+// over 4 x 4 register tiles: 8 operand loads per 16 FMAs, the loads of a k step
+// independent of each other.  epi(i, j, acc) stores.  Large stages only (the
+// condensed config-4 stage: 160 x 160 x 60).
+template <class FA, class FB, class FE>
+__device__ __forceinline__ void team_gemm_tn(int M, int N, int K, FA a, FB b, FE epi) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int tn = (N + 3) >> 2, nt = ((M + 3) >> 2) * tn;
+    for (int t = tid; t < nt; t += T) {
+        const int i0 = (t / tn) * 4, j0 = (t - (t / tn) * tn) * 4;
+        double acc[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[q][r] = 0.0;
+#pragma unroll 2
+        for (int k = 0; k < K; ++k) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                av[q] = i0 + q < M ? a(k, i0 + q) : 0.0;
+                bv[q] = j0 + q < N ? b(k, j0 + q) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) acc[q][r] = fma(av[q], bv[r], acc[q][r]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if (i0 + q < M && j0 + r < N) epi(i0 + q, j0 + r, acc[q][r]);
+    }
+}
+// stages large enough for the tiled paths (every thread gets several tiles)
+__device__ __forceinline__ bool big_stage(int nw) { return nw * nw >= 16 * (int)blockDim.x; }
 
 // ---------------------------------------------------------------------------
 // Householder QR of the m x n (m >= n) row-major stack S in place (LAPACK
@@ -744,6 +809,15 @@ __device__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops
         const double* Pn = Pall + c.st[n + 1].P_off;
         const double* An = fptr(c, OCPQP_F_A, s);
         const double* Bn = fptr(c, OCPQP_F_B, s);
+        const bool big = big_stage(nw);
+        auto BAat = [&](int k, int j) { return j < nu ? Bn[k * nu + j] : An[k * nx + (j - nu)]; };
+        if (big) {
+            team_gemm_tn(nxn, nw, nxn, [&](int k, int i) { return Pn[i * nxn + k]; }, BAat,
+                         [&](int i, int j, double v) { T1[i * nw + j] = v; });
+            tsync();
+            team_gemm_tn(nw, nw, nxn, BAat, [&](int k, int j) { return T1[k * nw + j]; },
+                         [&](int i, int j, double v) { G[i * nw + j] = v + Mb[i * nw + j]; });
+        } else {
         // T1 = P[n+1] [B A]  (nx' x nw): column j of [B A] read with stride
         for (int idx = tid; idx < nxn * nw; idx += T) {
             const int i = idx / nw, j = idx - i * nw;
@@ -763,6 +837,7 @@ __device__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops
             for (int k = 0; k < nxn; ++k) a = fma(col[k * ld], T1[k * nw + j], a);
             G[idx] = a + Mb[idx];
         }
+        }
         flops += 2ll * nxn * nw * nxn + 2ll * nw * nw * nxn;
         tsync();
     } else if (Mb != G) {
@@ -779,7 +854,71 @@ __device__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops
         }
         tsync();
         flops += (long long)nu * nu * nu / 3;
-        if (!team_chol(L, nu, nu, c.iflag)) return LINALG_NPD;
+        const bool bigk = nu >= 32 && (long long)nu * nx <= (long long)nxn * nw && n < N;
+        if (!team_chol(L, nu, nu, c.iflag, bigk)) return LINALG_NPD;
+        if (bigk) {
+            // K = -L'^{-1} L^{-1} G_ux (kkt_ocp.py:240-243), right-looking: the
+            // lane quad 4c..4c+3 owns column j, lane q its rows q, q + 4, ...;
+            // per pivot one division, the quad's FMAs on the rows still open
+            // (four rows per batch: loads first, then stores) and a quad-wide
+            // __syncwarp.  The column lives in T1 (free between G and the P
+            // update; shared memory when the plan placed it); both sweeps read
+            // row i of L, whose upper part still holds column i (team_chol).
+            const int q = tid & 3;
+            const unsigned qmask = 0xFu << (tid & 28);
+            double* __restrict__ Y = T1;
+            const double* __restrict__ Lr = L;
+            for (int j = tid >> 2; j < nx; j += T >> 2) {
+                for (int i = q; i < nu; i += 4) Y[i * nx + j] = G[i * nw + nu + j];
+                __syncwarp(qmask);
+                for (int i = 0; i < nu; ++i) {
+                    const double y = Y[i * nx + j] / Lr[i * nu + i];
+                    const double* Li = Lr + i * nu;
+                    for (int k = i + 1 + ((q - (i + 1)) & 3); k < nu; k += 16) {
+                        double l[4], v[4];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int kk = k + 4 * r;
+                            l[r] = kk < nu ? Li[kk] : 0.0;
+                            v[r] = kk < nu ? Y[kk * nx + j] : 0.0;
+                        }
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int kk = k + 4 * r;
+                            if (kk < nu) Y[kk * nx + j] = fma(-l[r], y, v[r]);
+                        }
+                    }
+                    __syncwarp(qmask);
+                    if (q == (i & 3)) Y[i * nx + j] = y;
+                }
+                __syncwarp(qmask);
+                for (int i = nu - 1; i >= 0; --i) {
+                    const double y = Y[i * nx + j] / Lr[i * nu + i];
+                    const double* Li = Lr + i * nu;
+                    for (int k = q; k < i; k += 16) {
+                        double l[4], v[4];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int kk = k + 4 * r;
+                            l[r] = kk < i ? Li[kk] : 0.0;
+                            v[r] = kk < i ? Y[kk * nx + j] : 0.0;
+                        }
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int kk = k + 4 * r;
+                            if (kk < i) Y[kk * nx + j] = fma(-l[r], y, v[r]);
+                        }
+                    }
+                    __syncwarp(qmask);
+                    if (q == (i & 3)) K[i * nx + j] = -y;
+                }
+            }
+            tsync();
+            for (int idx = tid; idx < nu * nu; idx += T) {
+                const int i = idx / nu, j = idx - i * nu;
+                if (j > i) L[idx] = 0.0;
+            }
+        } else
         // K = -L'^{-1} L^{-1} G_ux  (kkt_ocp.py:240-243), one column per thread
         for (int j = tid; j < nx; j += T) {
             for (int i = 0; i < nu; ++i) {
@@ -797,6 +936,11 @@ __device__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops
         flops += 2ll * nu * nu * nx;
         tsync();
         // P = G_xx + G_ux' K (kkt_ocp.py:244)
+        if (big_stage(nw)) {
+            team_gemm_tn(nx, nx, nu, [&](int k, int i) { return G[k * nw + nu + i]; },
+                         [&](int k, int j) { return K[k * nx + j]; },
+                         [&](int i, int j, double v) { T1[i * nx + j] = v + G[(nu + i) * nw + nu + j]; });
+        } else
         for (int idx = tid; idx < nx * nx; idx += T) {
             const int i = idx / nx, j = idx - i * nx;
             double a = 0.0;
