@@ -201,8 +201,10 @@ __device__ void rows_values(const Ctx& c, const double* y, double* rowv) {
                 const int g = i - s.nb, nu = s.nu, nx = s.nx;
                 const double* Dg = fptr(c, OCPQP_F_D, s) + g * nu;
                 const double* Cg = fptr(c, OCPQP_F_C, s) + g * nx;
-                v = 0.0;
+                v = 0.0;   // one fma chain; unrolled so that the loads of eight steps overlap
+#pragma unroll 8
                 for (int j = 0; j < nu; ++j) v = fma(Dg[j], w[j], v);
+#pragma unroll 8
                 for (int j = 0; j < nx; ++j) v = fma(Cg[j], w[nu + j], v);
             }
             rowv[s.m_off + i] = v;
@@ -221,6 +223,7 @@ __device__ __forceinline__ double rows_t(const Ctx& c, const StageInfo& s, int j
         const int ld = du ? s.nu : s.nx;
         const double* cg = coeff + s.nb;
         double g = 0.0;
+#pragma unroll 8
         for (int r = 0; r < s.ng; ++r) g = fma(col[r * ld], cg[r], g);
         out += g;
     }
@@ -571,7 +574,77 @@ __device__ void warp_cho_solve4(const double* L, int n, const double* xin, doubl
 __device__ __noinline__ void rows_syrk(const Ctx& c, const StageInfo& s, const double* cg,
                                        double* Mb, int nw, int ng, double reg) {
     const int tid = threadIdx.x, T = blockDim.x;
-    if (ng >= 32 && nw >= 24) {
+    if (ng >= 32 && nw >= 64) {
+        // Jg' diag(coef) Jg on the FP64 tensor cores (DMMA m8n8k4): one warp per
+        // 16 x 16 block (2 x 2 tiles) of the lower block triangle -- four
+        // operand loads feed four DMMAs (half the L2 traffic of one tile per
+        // warp) on four independent accumulator pairs; k = general rows in
+        // steps of 4, mirrored in the epilogue.  Fragment layout as below.
+        const int lane = tid & 31, warp = tid >> 5, nwarp = T >> 5;
+        const int gr = lane >> 2, tg = lane & 3;
+        const int nb16 = (nw + 15) >> 4, nblk = nb16 * (nb16 + 1) / 2;
+        const int nu = s.nu, nx = s.nx;
+        const double* Dp = fptr(c, OCPQP_F_D, s);
+        const double* Cp = fptr(c, OCPQP_F_C, s);
+        for (int t = warp; t < nblk; t += nwarp) {
+            int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+            while (bi * (bi + 1) / 2 > t) --bi;
+            while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+            const int bj = t - bi * (bi + 1) / 2;
+            const double* ca[2];
+            const double* cb[2];
+            int la[2], lb[2];
+            bool ina[2], inb[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int ia = bi * 16 + 8 * h + gr, jb = bj * 16 + 8 * h + gr;
+                ina[h] = ia < nw;
+                inb[h] = jb < nw;
+                ca[h] = ia < nu ? Dp + ia : Cp + (ia - nu);
+                cb[h] = jb < nu ? Dp + jb : Cp + (jb - nu);
+                la[h] = ia < nu ? nu : nx;
+                lb[h] = jb < nu ? nu : nx;
+            }
+            double d[2][2][2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int g = 0; g < 2; ++g) d[h][g][0] = d[h][g][1] = 0.0;
+#pragma unroll 2
+            for (int r0 = 0; r0 < ng; r0 += 4) {
+                const int r = r0 + tg;
+                const bool rin = r < ng;
+                const double w = rin ? cg[r] : 0.0;
+                double av[2], bv[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    av[h] = (rin && ina[h]) ? ca[h][r * la[h]] : 0.0;
+                    bv[h] = (rin && inb[h]) ? w * cb[h][r * lb[h]] : 0.0;
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int g = 0; g < 2; ++g)
+                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                                     : "+d"(d[h][g][0]), "+d"(d[h][g][1])
+                                     : "d"(av[h]), "d"(bv[g]));
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int i = bi * 16 + 8 * h + gr, j = bj * 16 + 8 * g + 2 * tg + e;
+                        if (i < nw && j <= i) {
+                            double hh = d[h][g][e] + Mb[i * nw + j];
+                            if (i == j && reg != 0.0) hh += reg;
+                            Mb[i * nw + j] = hh;
+                            Mb[j * nw + i] = hh;
+                        }
+                    }
+        }
+    } else if (ng >= 32 && nw >= 24) {
         // Jg' diag(coef) Jg on the FP64 tensor cores (DMMA m8n8k4): one warp
         // per 8x8 tile of the lower tile triangle, k = general rows in
         // steps of 4, mirrored in the epilogue.  Fragments: A row = lane/4,
@@ -872,6 +945,10 @@ __device__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops
                 for (int i = q; i < nu; i += 4) Y[i * nx + j] = G[i * nw + nu + j];
                 __syncwarp(qmask);
                 for (int i = 0; i < nu; ++i) {
+                    // row i + 1 of L -> L1 while this pivot runs (each row is touched
+                    // for the first time at its pivot: an L2 round trip per batch otherwise)
+                    if (i + 1 < nu && (tid & 31) * 16 < nu)
+                        asm volatile("prefetch.global.L1 [%0];\n" ::"l"(Lr + (i + 1) * nu + (tid & 31) * 16));
                     const double y = Y[i * nx + j] / Lr[i * nu + i];
                     const double* Li = Lr + i * nu;
                     for (int k = i + 1 + ((q - (i + 1)) & 3); k < nu; k += 16) {
@@ -893,6 +970,8 @@ __device__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops
                 }
                 __syncwarp(qmask);
                 for (int i = nu - 1; i >= 0; --i) {
+                    if (i > 0 && (tid & 31) * 16 < nu)
+                        asm volatile("prefetch.global.L1 [%0];\n" ::"l"(Lr + (i - 1) * nu + (tid & 31) * 16));
                     const double y = Y[i * nx + j] / Lr[i * nu + i];
                     const double* Li = Lr + i * nu;
                     for (int k = q; k < i; k += 16) {
