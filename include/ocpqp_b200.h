@@ -61,6 +61,8 @@ extern "C" {
 #define OCPQP_E_CUDA (-4)             /* CUDA runtime error */
 #define OCPQP_E_ARG (-5)              /* bad argument / NULL pointer */
 #define OCPQP_E_CONDENSE (-6)         /* CondenseError (errors.py; condensing.py:180-185) */
+#define OCPQP_E_NOT_PD (-7)           /* NotPositiveDefinite (linalg.py:110-113) */
+#define OCPQP_E_RANK (-8)             /* RankDeficient (linalg.py:181-184) */
 
 /* per-QP status words; values 0..4 mirror ipm_core.Status (ipm_core.py:56-63) */
 #define OCPQP_STATUS_SUCCESS 0
@@ -326,6 +328,14 @@ int ocpqp_pc_expand(OcpPcPlan* plan, int32_t B, const OcpQpDataC* in, const OcpI
  * _destroy take this plan too (N2 = 0; expansion = expand_solution). */
 int ocpqp_fc_create(const OcpQpDimC* dim, int32_t keep_x0, int32_t nfix, const int32_t* fix_row,
                     const int32_t* fix_comp, OcpPcPlan** out);
+
+/* Cost recursion of a full-condensing plan: 0 = classical (default), 1 = the
+ * square-root recursion of condense(variant="square_root") (condensing.py:
+ * 134-146: U_n = qr_cholesky([chol(Q_n)'; U_{n+1} A]), P_n = U_n' U_n,
+ * Y_n = (U A)' (U B) + S').  With it ocpqp_pc_condense reads one status word
+ * back per call and returns OCPQP_E_NOT_PD / OCPQP_E_RANK where the reference
+ * raises NotPositiveDefinite / RankDeficient. */
+int ocpqp_pc_set_variant(OcpPcPlan* plan, int32_t square_root);
 
 /* Soft rows of the condensed QP (partial or full plan): ns (N2+1 entries)
  * and the concatenated new idxs when non-NULL; returns sum(ns).  Slack data

@@ -227,10 +227,24 @@ def detect_fixed_x0(qp):
     return (not np.any(np.isnan(x0hat))) if nx0 else True, x0hat, fix
 
 
-def full_condense(qp, keep_x0=None):
+def _qr_cholesky(stack):
+    """R with R'R = stack'stack, nonnegative diagonal (linalg.py:152-187)."""
+    m, n = stack.shape
+    R = np.linalg.qr(stack, mode="r")
+    d = np.diag(R).copy()
+    tol = max(m, n) * np.finfo(float).eps * (np.max(np.abs(d)) if n else 0.0)
+    if np.any(np.abs(d) <= tol):
+        raise ArithmeticError("RankDeficient")
+    return np.where(d[:, None] < 0.0, -R, R)
+
+
+def full_condense(qp, keep_x0=None, variant="classical"):
     """Dense QP fields (H, g, idxb, lb, ub, C, lg, ug, maskl, masku) + map.
 
-    Classical cost recursion (condensing.py:148-157) with P[N] = sym(Q_N);
+    Classical cost recursion (condensing.py:148-157) with P[N] = sym(Q_N), or
+    the square-root recursion (condensing.py:134-146: U_n = qr_cholesky of
+    [chol(Q_n)'; U_{n+1} A], P_n = U_n' U_n, Y_n = (U A)'(U B) + S';
+    np.linalg.LinAlgError where the reference raises NotPositiveDefinite);
     z = [x0 (kept) | u_0 | ... | u_N]; x-box rows past stage 0 and all general
     rows become dense general rows in stage order; box rows sorted by z.
     """
@@ -262,12 +276,24 @@ def full_condense(qp, keep_x0=None):
     st = qp._stages
     P = [None] * (N + 1)
     Y = [None] * N
-    P[N] = 0.5 * (st[N]["Q"] + st[N]["Q"].T)
-    for n in range(N - 1, -1, -1):
-        A, B = qp._dyn[n]["A"], qp._dyn[n]["B"]
-        Y[n] = A.T @ (P[n + 1] @ B) + st[n]["S"].T
-        Pn = A.T @ (P[n + 1] @ A) + st[n]["Q"]
-        P[n] = 0.5 * (Pn + Pn.T)
+    if variant == "square_root":
+        def chol_lower(Q):   # scipy.linalg.cholesky(lower=True) reads the lower triangle
+            return np.linalg.cholesky(np.tril(Q) + np.tril(Q, -1).T)
+        U = chol_lower(st[N]["Q"]).T
+        P[N] = U.T @ U
+        for n in range(N - 1, -1, -1):
+            A, B = qp._dyn[n]["A"], qp._dyn[n]["B"]
+            UA, UB = U @ A, U @ B
+            Y[n] = UA.T @ UB + st[n]["S"].T
+            U = _qr_cholesky(np.vstack([chol_lower(st[n]["Q"]).T, UA]))
+            P[n] = U.T @ U
+    else:
+        P[N] = 0.5 * (st[N]["Q"] + st[N]["Q"].T)
+        for n in range(N - 1, -1, -1):
+            A, B = qp._dyn[n]["A"], qp._dyn[n]["B"]
+            Y[n] = A.T @ (P[n + 1] @ B) + st[n]["S"].T
+            Pn = A.T @ (P[n + 1] @ A) + st[n]["Q"]
+            P[n] = 0.5 * (Pn + Pn.T)
     beta = [None] * (N + 1)
     beta[N] = st[N]["q"] + st[N]["Q"] @ gamma[N]
     for n in range(N - 1, -1, -1):

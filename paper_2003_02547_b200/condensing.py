@@ -27,7 +27,8 @@ import numpy as np
 
 from . import _native as nat
 from .batch import OcpQpBatch, default_fill
-from .errors import CondenseError, DimensionMismatch, InvalidBlockSize, NativeLibraryError
+from .errors import (CondenseError, DimensionMismatch, InvalidBlockSize, NativeLibraryError,
+                     NotPositiveDefinite, RankDeficient)
 from .layout import FIELD_ORDER, QpSolution
 from .qp_data import OcpQp, OcpQpDim
 
@@ -51,6 +52,7 @@ def _lib():
                                       vp, vp, ctypes.POINTER(vp)]
         L.ocpqp_fc_create.restype = ctypes.c_int
         L.ocpqp_pc_soft.argtypes = [vp, vp, vp]
+        L.ocpqp_pc_set_variant.argtypes = [vp, ctypes.c_int32]
         L.ocpqp_pc_soft.restype = ctypes.c_int
         L.ocpqp_pc_last_error.restype = ctypes.c_char_p
         for f in ("ocpqp_pc_create", "ocpqp_pc_destroy", "ocpqp_pc_dims", "ocpqp_pc_condense",
@@ -72,6 +74,10 @@ def _check(rc):
         raise ValueError(msg)
     if rc == -6:
         raise CondenseError(msg)
+    if rc == -7:
+        raise NotPositiveDefinite(msg)
+    if rc == -8:
+        raise RankDeficient(msg)
     raise NativeLibraryError(f"partial condensing error {rc}: {msg}")
 
 
@@ -376,14 +382,22 @@ def _fmap_for(batch, keep_x0):
     return m
 
 
-def condense_batch(batch, keep_x0=None, device="cuda"):
-    """Fully condensed device batch (N = 0, nx = 0, nu = nv) and its map."""
+def condense_batch(batch, keep_x0=None, device="cuda", variant="classical"):
+    """Fully condensed device batch (N = 0, nx = 0, nu = nv) and its map.
+
+    ``variant``: the cost recursion of the reference's ``condense``
+    (condensing.py:128-157): "classical" (explicit P) or "square_root"
+    (Cholesky / QR factors of P; raises NotPositiveDefinite / RankDeficient
+    like the reference when a stage cost Q is not positive definite)."""
     import torch
 
     from .solver import _as_batch
 
+    if variant not in ("classical", "square_root"):
+        raise ValueError(f"unknown condensing variant '{variant}'")
     batch = _as_batch(batch, check=False)
     cmap = _fmap_for(batch, keep_x0)
+    _check(_lib().ocpqp_pc_set_variant(cmap.handle, 1 if variant == "square_root" else 0))
     src = _device_full(batch, device)
     out = OcpQpBatch(cmap.new_dim, batch.B, cmap.new_idxb, cmap.new_idxs)
     lay = out.layout
@@ -447,10 +461,8 @@ def condense(qp, keep_x0=None, variant="classical"):
 
     if not isinstance(qp, OcpQp):
         raise TypeError("condense expects an OcpQp")
-    if variant != "classical":
-        raise NotImplementedError("only the classical cost recursion is provided")
     b = OcpQpBatch.from_qps([qp])
-    cb, cmap = condense_batch(b, keep_x0)
+    cb, cmap = condense_batch(b, keep_x0, variant=variant)
     return ocp_to_dense(cb.numpy().qp(0)), cmap
 
 

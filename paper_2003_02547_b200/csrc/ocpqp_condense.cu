@@ -145,6 +145,9 @@ struct PcParams {
     double* fout[OCPQP_NUM_FIELDS]; long long bout[OCPQP_NUM_FIELDS];
     // workspace
     double* ws; long long ws_slot; int* counter;
+    // square-root cost recursion (condensing.py:134-146): per-slot extra workspace behind the
+    // classical one; *fail = 1 + 4 q (chol(Q) not positive definite) or 2 + 4 q (rank-deficient stack)
+    int sqrt_cost; int* fail;
     // solutions (expansion)
     const double* sy; const double* spi; const double* slam; const double* st;
     double* fy; double* fpi; double* flam; double* ft;
@@ -158,6 +161,87 @@ __device__ __forceinline__ const double* fin(const PcParams& p, int q, int f, in
 }
 __device__ __forceinline__ double* fout(const PcParams& p, int q, int f, int k) {
     return p.fout[f] + (long long)q * p.bout[f] + p.nfoff[(long long)k * OCPQP_NUM_FIELDS + f];
+}
+
+// In-place lower Cholesky of the n x n matrix at L (row-major, only the lower
+// triangle is read, as scipy.linalg.cholesky(lower=True) behind
+// linalg.cholesky_factor, linalg.py:81-118); the upper triangle is zeroed.
+// False on a pivot that is not > 0.
+__device__ bool pc_team_chol(double* L, int n) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    for (int k = 0; k < n; ++k) {
+        const double d = L[k * n + k];
+        if (!(d > 0.0)) {
+            __syncthreads();
+            return false;
+        }
+        const double dk = sqrt(d);
+        __syncthreads();
+        for (int i = k + tid; i < n; i += T) L[i * n + k] = i == k ? dk : L[i * n + k] / dk;
+        __syncthreads();
+        for (int e = tid; e < (n - k - 1) * (n - k - 1); e += T) {
+            const int i = k + 1 + e / (n - k - 1), j = k + 1 + e % (n - k - 1);
+            if (j <= i) L[i * n + j] -= L[i * n + k] * L[j * n + k];
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < n * n; e += T)
+        if (e % n > e / n) L[e] = 0.0;
+    __syncthreads();
+    return true;
+}
+
+// Householder QR of the m x n (m >= n) row-major stack S in place (LAPACK
+// dgeqr2 / dlarfg reflectors, the arithmetic of np.linalg.qr(mode="r")), then
+// qr_cholesky's rank test and row-sign normalisation (linalg.py:152-187): the
+// leading n x n block becomes R with a positive diagonal.  False when rank-deficient.
+__device__ bool pc_team_qr(double* S, int m, int n, double* red) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nwarp = (T + 31) >> 5;
+    for (int k = 0; k < n; ++k) {
+        double ss = 0.0;
+        for (int i = k + 1 + tid; i < m; i += T) ss = fma(S[i * n + k], S[i * n + k], ss);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        __syncthreads();
+        if (lane == 0) red[warp] = ss;
+        __syncthreads();
+        ss = 0.0;
+        for (int w = 0; w < nwarp; ++w) ss += red[w];
+        if (ss == 0.0) continue;    // H = I (tau = 0)
+        const double alpha = S[k * n + k];
+        const double beta = -copysign(hypot(alpha, sqrt(ss)), alpha);
+        const double tau = (beta - alpha) / beta;
+        const double sc = 1.0 / (alpha - beta);
+        __syncthreads();
+        for (int i = k + 1 + tid; i < m; i += T) S[i * n + k] *= sc;
+        __syncthreads();
+        for (int j = k + 1 + warp; j < n; j += nwarp) {
+            double w = 0.0;
+            for (int i = k + 1 + lane; i < m; i += 32) w = fma(S[i * n + k], S[i * n + j], w);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+            w = (S[k * n + j] + w) * tau;
+            for (int i = k + 1 + lane; i < m; i += 32) S[i * n + j] = fma(-w, S[i * n + k], S[i * n + j]);
+            if (lane == 0) S[k * n + j] -= w;
+        }
+        if (tid == 0) S[k * n + k] = beta;
+        __syncthreads();
+    }
+    double dmax = 0.0;
+    for (int i = 0; i < n; ++i) dmax = fmax(dmax, fabs(S[i * n + i]));
+    const double tol = (m > n ? m : n) * 2.220446049250313e-16 * dmax;
+    int bad = 0;
+    for (int i = 0; i < n; ++i)
+        if (!(fabs(S[i * n + i]) > tol)) bad = 1;
+    __syncthreads();
+    if (bad) return false;
+    for (int i = tid; i < n; i += T) {
+        const double sg = S[i * n + i] < 0.0 ? -1.0 : 1.0;
+        for (int j = 0; j < n; ++j) S[i * n + j] = j < i ? 0.0 : sg * S[i * n + j];
+    }
+    __syncthreads();
+    return true;
 }
 
 // One (QP, block) condensing work item; team = CTA.
@@ -178,6 +262,13 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
     double* pr1 = pr0 + (long long)XM * VM;            // XM * VM
     double* T1 = pr1 + (long long)XM * VM;             // XM * max(XM, UM)
     double* T2 = T1 + (long long)XM * (XM > UM ? XM : UM);  // XM * UM
+    // square-root cost recursion only (behind the classical workspace)
+    double* Uc = T2 + (long long)XM * UM + 64;         // XM * XM: U_{n+1} (upper triangular)
+    double* Stk = Uc + (long long)XM * XM;             // 2 XM * XM: [chol(Q_n)'; U_{n+1} A], then R
+    double* UBb = Stk + 2ll * XM * XM;                 // XM * UM: U_{n+1} B
+    double* Lq = UBb + (long long)XM * UM;             // XM * XM: chol(Q_n)
+    __shared__ double s_red[32];
+    const bool sq = p.sqrt_cost != 0;
     // gamma forward: gamma[0] = 0, gamma[i+1] = A gamma[i] + b  (condensing.py:199-207)
     // (full condensing without x0: gamma[0] = x0hat from the fixing rows, :97-118, :197)
     for (int a = tid; a < nx0; a += T) gam[a] = 0.0;
@@ -215,6 +306,23 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
             const double* R = fin(p, q, OCPQP_F_R, n0 + L);
             const double* qv = fin(p, q, OCPQP_F_q, n0 + L);
             const double* rv = fin(p, q, OCPQP_F_r, n0 + L);
+            if (sq) {
+                // U_N = chol(Q_N)', P_N = U_N' U_N (condensing.py:135-137)
+                for (int e = tid; e < nxL * nxL; e += T) Lq[e] = Q[e];
+                __syncthreads();
+                if (!pc_team_chol(Lq, nxL)) {
+                    if (tid == 0) atomicCAS(p.fail, 0, 1 + 4 * q);
+                    return;
+                }
+                for (int e = tid; e < nxL * nxL; e += T) {
+                    const int a = e / nxL, c = e - a * nxL;
+                    Uc[e] = Lq[c * nxL + a];
+                    const int km = a < c ? a : c;
+                    double v = 0.0;
+                    for (int k2 = 0; k2 <= km; ++k2) v = fma(Lq[a * nxL + k2], Lq[c * nxL + k2], v);
+                    PL[e] = v;
+                }
+            } else
             for (int e = tid; e < nxL * nxL; e += T) {
                 const int a = e / nxL, c = e - a * nxL;
                 PL[e] = 0.5 * (Q[e] + Q[c * nxL + a]);
@@ -274,6 +382,51 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
         // Y = A' PB + S'  (nx x nu) ; Pt = A' PA + Q (nx x nx) into P_i (unsymmetrised)
         double* Yi = Y + (long long)i * XM * UM;
         double* Pi = P + (long long)i * XM * XM;
+        if (sq) {
+            // UA = U_{n+1} A below chol(Q_n)' in the stack, UB = U_{n+1} B,
+            // Y = UA' UB + S', U_n = qr_cholesky([Uq; UA]), P_n = U_n' U_n
+            // (condensing.py:138-146)
+            for (int e = tid; e < nxn * nx; e += T) {
+                const int a = e / nx, c = e - a * nx;
+                double v = 0.0;
+                for (int k2 = a; k2 < nxn; ++k2) v = fma(Uc[a * nxn + k2], A[k2 * nx + c], v);
+                Stk[(nx + a) * nx + c] = v;
+            }
+            for (int e = tid; e < nxn * nu; e += T) {
+                const int a = e / nu, c = e - a * nu;
+                double v = 0.0;
+                for (int k2 = a; k2 < nxn; ++k2) v = fma(Uc[a * nxn + k2], Bm[k2 * nu + c], v);
+                UBb[e] = v;
+            }
+            for (int e = tid; e < nx * nx; e += T) Lq[e] = Q[e];
+            __syncthreads();
+            for (int e = tid; e < nx * nu; e += T) {
+                const int a = e / nu, c = e - a * nu;
+                double v = 0.0;
+                for (int k2 = 0; k2 < nxn; ++k2) v = fma(Stk[(nx + k2) * nx + a], UBb[k2 * nu + c], v);
+                Yi[e] = v + S[c * nx + a];
+            }
+            if (!pc_team_chol(Lq, nx)) {
+                if (tid == 0) atomicCAS(p.fail, 0, 1 + 4 * q);
+                return;
+            }
+            for (int e = tid; e < nx * nx; e += T) {
+                const int a = e / nx, c = e - a * nx;
+                Stk[e] = Lq[c * nx + a];
+            }
+            __syncthreads();
+            if (!pc_team_qr(Stk, nx + nxn, nx, s_red)) {
+                if (tid == 0) atomicCAS(p.fail, 0, 2 + 4 * q);
+                return;
+            }
+            for (int e = tid; e < nx * nx; e += T) {
+                const int a = e / nx, c = e - a * nx;
+                const int km = a < c ? a : c;
+                double v = 0.0;
+                for (int k2 = 0; k2 <= km; ++k2) v = fma(Stk[k2 * nx + a], Stk[k2 * nx + c], v);
+                Pi[e] = v;
+            }
+        } else {
         for (int e = tid; e < nx * nu; e += T) {
             const int a = e / nu, c = e - a * nu;
             double s = 0.0;
@@ -285,6 +438,7 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
             double s = 0.0;
             for (int k2 = 0; k2 < nxn; ++k2) s = fma(A[k2 * nx + a], T1[k2 * nx + c], s);
             Pi[e] = s + Q[e];
+        }
         }
         // condensed u_i block R + B' (P_{n+1} B) and gradient r + S gamma + B' beta
         // (condensing.py:229-237)
@@ -311,6 +465,11 @@ __device__ void condense_block(const PcParams& p, int q, int k, double* ws) {
             bet[i * XM + a] = (qv[a] + qg) + ab;
         }
         __syncthreads();
+        if (sq) {
+            for (int e = tid; e < nx * nx; e += T) Uc[e] = Stk[e];
+            __syncthreads();
+            continue;
+        }
         // symmetrise P_i in place (read pairs, then write)
         for (int e = tid; e < nx * nx; e += T) {
             const int a = e / nx, c = e - a * nx;
@@ -736,6 +895,8 @@ struct OcpPcPlan {
     std::vector<int> uoff, row_kind, row_stage, row_src, row_aux;
     int nxmax = 1, nvmax = 1, numax = 1, Lmax = 1;
     long long ws_slot = 1;
+    int sqrt_cost = 0;         // square-root cost recursion (full condensing)
+    int* d_fail = nullptr;
     // device copies of the tables
     bool uploaded = false;
     PcBlockDev* d_blk = nullptr;
@@ -791,6 +952,8 @@ void pc_size(OcpPcPlan* P) {
     P->nxmax = (int)XM;
     P->ws_slot = (P->Lmax + 1) * XM * XM + (long long)(P->Lmax + 1) * XM * UM + 2ll * (P->Lmax + 1) * XM +
                  VM * VM + VM + 2ll * XM * VM + XM * std::max(XM, UM) + XM * UM + 64;
+    // square-root cost recursion: U, the QR stack, U B, chol(Q)
+    if (P->sqrt_cost) P->ws_slot += 4ll * XM * XM + XM * UM + 64;
 }
 
 int pc_prepare(OcpPcPlan* P, int items) {
@@ -861,6 +1024,7 @@ void pc_fill(const OcpPcPlan* P, PcParams& k, int B) {
     k.n_u = P->d_nu; k.n_x = P->d_nx; k.n_pi = P->d_npi; k.n_c = P->d_nc;
     k.o_ib = P->d_oib; k.o_idxb = P->d_oidxb;
     k.ws = P->d_ws; k.ws_slot = P->ws_slot; k.counter = P->d_counter;
+    k.sqrt_cost = P->sqrt_cost; k.fail = P->d_fail;
     k.ny_s = P->nd.ny; k.ne_s = P->nd.ne; k.nc_s = P->nd.nc;
     k.ny_f = P->od.ny; k.ne_f = P->od.ne; k.nc_f = P->od.nc;
 }
@@ -1099,7 +1263,7 @@ int ocpqp_pc_destroy(OcpPcPlan* P) {
     cudaFree(P->d_onb); cudaFree(P->d_ong); cudaFree(P->d_ou); cudaFree(P->d_ox);
     cudaFree(P->d_opi); cudaFree(P->d_oc); cudaFree(P->d_nu); cudaFree(P->d_nx);
     cudaFree(P->d_npi); cudaFree(P->d_nc); cudaFree(P->d_oib); cudaFree(P->d_oidxb);
-    cudaFree(P->d_ofoff); cudaFree(P->d_nfoff); cudaFree(P->d_counter); cudaFree(P->d_ws);
+    cudaFree(P->d_ofoff); cudaFree(P->d_nfoff); cudaFree(P->d_counter); cudaFree(P->d_ws); cudaFree(P->d_fail);
     cudaFree(P->d_fix_row); cudaFree(P->d_fix_c);
     cudaFree(P->d_slk_stage); cudaFree(P->d_slk_j); cudaFree(P->d_os); cudaFree(P->d_ns);
     cudaFree(P->d_ons); cudaFree(P->d_nns);
@@ -1152,9 +1316,42 @@ int ocpqp_pc_condense(OcpPcPlan* P, int32_t B, const OcpQpDataC* in, OcpQpDataC*
     cudaStream_t st = (cudaStream_t)stream;
     if (cudaMemsetAsync(P->d_counter, 0, sizeof(int), st) != cudaSuccess)
         return pc_fail(OCPQP_E_CUDA, "memset");
+    if (P->sqrt_cost && cudaMemsetAsync(P->d_fail, 0, sizeof(int), st) != cudaSuccess)
+        return pc_fail(OCPQP_E_CUDA, "memset");
     k_pc_condense<<<std::min(P->slots, items), 256, 0, st>>>(k);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return pc_fail(OCPQP_E_CUDA, "k_pc_condense: %s", cudaGetErrorString(e));
+    if (P->sqrt_cost) {
+        // the square-root recursion can fail numerically (cholesky_factor / qr_cholesky raise
+        // in the reference, linalg.py:110-113, 181-184): one word back per call
+        int fail = 0;
+        if (cudaMemcpyAsync(&fail, P->d_fail, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return pc_fail(OCPQP_E_CUDA, "square-root condensing: status read failed");
+        if (fail) {
+            const int q = fail >> 2;
+            if ((fail & 3) == 1)
+                return pc_fail(OCPQP_E_NOT_PD, "NotPositiveDefinite: stage cost Q of QP %d is not positive definite", q);
+            return pc_fail(OCPQP_E_RANK, "RankDeficient: stacked cost factor of QP %d", q);
+        }
+    }
+    return OCPQP_OK;
+}
+
+// Cost recursion of full condensing (condense(variant=...), condensing.py:128-157):
+// 0 classical, 1 square-root.  Partial plans keep the classical recursion.
+int ocpqp_pc_set_variant(OcpPcPlan* P, int32_t square_root) {
+    if (!P) return pc_fail(OCPQP_E_ARG, "NULL plan");
+    if (square_root && !P->full)
+        return pc_fail(OCPQP_E_UNSUPPORTED, "the square-root cost recursion belongs to full condensing");
+    if ((square_root != 0) == (P->sqrt_cost != 0)) return OCPQP_OK;
+    P->sqrt_cost = square_root ? 1 : 0;
+    pc_size(P);
+    cudaFree(P->d_ws);       // the slot size changed: reallocated by the next call
+    P->d_ws = nullptr;
+    P->slots = 0;
+    if (P->sqrt_cost && !P->d_fail && cudaMalloc(&P->d_fail, sizeof(int)) != cudaSuccess)
+        return pc_fail(OCPQP_E_CUDA, "square-root condensing: allocation failed");
     return OCPQP_OK;
 }
 

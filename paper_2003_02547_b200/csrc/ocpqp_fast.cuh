@@ -1942,7 +1942,7 @@ struct Kern {
     // factor store.  G_ux = ([B A]' T1)_ux + S_n first (M~, kkt_common.py:100-115):
     // Ss is S_n in shared memory (TMA); the sum goes back to Gu for the P update.
     static constexpr int KW = 4, KCPW = (NX + KW - 1) / KW;   // warps, columns per warp
-    static_assert(KCPW <= 32 && KW * 32 <= TEAM, "kcols_big columns");
+    static_assert(!S::BIG || (KCPW <= 32 && KW * 32 <= TEAM), "kcols_big columns");
     __device__ __forceinline__ static int kcol_of(int tid) {
         const int w = tid >> 5, l = tid & 31;
         return (w < KW && l < KCPW && w * KCPW + l < NX) ? w * KCPW + l : -1;
@@ -1986,7 +1986,7 @@ struct Kern {
     // by thread PS_T0 + i.  The stores drain in the background; p_store_wait
     // before the rows in shared memory are overwritten.
     static constexpr int PS_T0 = 64;
-    static_assert(PS_T0 + NX <= TEAM, "store_p_big threads");
+    static_assert(!S::BIG || PS_T0 + NX <= TEAM, "store_p_big threads");
     __device__ __forceinline__ static void store_p_big(const double* Pc, double* Pn) {
 #ifdef OCPQP_NOPSTORE
         return;

@@ -306,6 +306,30 @@ def fcond():
     np.savez_compressed(HERE / "fcond.npz", **out)
 
 
+def fcond_sqrt():
+    """condense(variant="square_root") (condensing.py:134-146) of the fcond cases: the
+    Hessian and gradient of the dense QP (every other field does not depend on the
+    cost recursion), and the NotPositiveDefinite raise on a semidefinite stage cost."""
+    out = {}
+    for name, src, keep in FCOND_CASES:
+        qp = pcond_source(src)
+        dq, cmap = mpcqp.condense(qp, keep_x0=keep, variant="square_root")
+        dc, _ = mpcqp.condense(qp, keep_x0=keep)
+        out[f"{name}_H"] = dq.get_field("H")
+        out[f"{name}_g"] = dq.get_field("g")
+        out[f"{name}_H_vs_classical"] = np.max(np.abs(dq.get_field("H") - dc.get_field("H")))
+        print("fcond_sqrt", name, dq.nv, out[f"{name}_H_vs_classical"], flush=True)
+    qp = pcond_source(FCOND_CASES[0][1])
+    qp.set_field("Q", 2, np.zeros((3, 3)))
+    try:
+        mpcqp.condense(qp, variant="square_root")
+        out["npd_raises"] = np.array(0)
+    except mpcqp.errors.NotPositiveDefinite:
+        out["npd_raises"] = np.array(1)
+    print("fcond_sqrt npd", int(out["npd_raises"]), flush=True)
+    np.savez_compressed(HERE / "fcond_sqrt.npz", **out)
+
+
 # condensing with soft rows (condensing.py:289-334, 523-534, 592-601)
 SOFT_CASES = [
     ("s31", (31, dict(N=5, nx=3, nu=2, nb=4, ng=1, ns=2, fix_x0=True)), None, 2),
@@ -583,6 +607,6 @@ def qp_files():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["known", "residuals", "newton", "solve_random", "solve_cfg", "pcond",
                             "solve_modes", "closed_loop", "qp_files", "fcond", "soft_cond", "dense",
-                            "pcond_full", "dense_eq"]
+                            "pcond_full", "dense_eq", "fcond_sqrt"]
     for w in which:
         globals()[w]()

@@ -127,3 +127,23 @@ def test_detect_fixed_x0_batch_rules():
     with pytest.raises(CondenseError):
         detect_fixed_x0(OcpQpBatch.from_qps([qp, q2]))
     assert detect_fixed_x0(OcpQpBatch.from_qps([q2]))[0] is False
+
+
+@pytest.mark.parametrize("case", fcond_cases(), ids=lambda c: c[0])
+def test_oracle_square_root_condense_matches_reference(golden, case):
+    """condense(variant="square_root") (condensing.py:134-146): the oracle's restatement
+    against the reference's H and g (fcond_sqrt.npz)."""
+    name, src, keep = case
+    g = golden("fcond_sqrt")
+    dense, _ = co.full_condense(source_qp(src), keep, variant="square_root")
+    for f in ("H", "g"):
+        assert rel_err(dense[f].reshape(-1), g[f"{name}_{f}"].reshape(-1)) <= 1e-12, f
+
+
+def test_oracle_square_root_condense_needs_definite_q(golden):
+    assert int(golden("fcond_sqrt")["npd_raises"]) == 1
+    qp = source_qp(fcond_cases()[0][1])
+    qp.set_field("Q", 2, np.zeros((3, 3)))
+    with pytest.raises(np.linalg.LinAlgError):
+        co.full_condense(qp, variant="square_root")
+    co.full_condense(qp)   # the classical recursion tolerates it

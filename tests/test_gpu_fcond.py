@@ -114,3 +114,38 @@ def test_gpu_condensed_config_batch_vs_oracle(cuda, oracle, speed_arg, cfg, B):
                                            rep.t.cpu().numpy()[i])
         for k, v, r in (("y", y, fy), ("pi", pi, fpi), ("lam", lam, flam), ("t", t, ft)):
             assert rel_err(v.cpu().numpy()[i], r) <= 1e-10, (i, k)
+
+
+@pytest.mark.parametrize("case", fcond_cases(), ids=lambda c: c[0])
+def test_gpu_square_root_condense_matches_reference(cuda, golden, case):
+    """condense(variant="square_root") on the GPU (U_n = qr_cholesky([chol(Q_n)'; U_{n+1} A]),
+    condensing.py:134-146) against the reference's dense H and g; the other
+    fields do not depend on the cost recursion and must equal the classical ones."""
+    name, src, keep = case
+    g, gc = golden("fcond_sqrt"), golden("fcond")
+    batch = OcpQpBatch.from_qps([source_qp(src)])
+    cb, cmap = condense_batch(batch, keep, variant="square_root")
+    q = cb.numpy().qp(0)
+    assert rel_err(q.get_field("R", 0).reshape(-1), g[f"{name}_H"].reshape(-1)) <= 1e-12
+    assert rel_err(q.get_field("r", 0).reshape(-1), g[f"{name}_g"].reshape(-1)) <= 1e-12
+    for f, o in DMAP.items():
+        if f not in ("H", "g"):
+            assert rel_err(finite(q.get_field(o, 0)).reshape(-1),
+                           finite(gc[f"{name}_{f}"]).reshape(-1)) <= 1e-12, f
+    # the same plan goes back to the classical recursion
+    cb2, _ = condense_batch(batch, keep)
+    assert rel_err(cb2.numpy().qp(0).get_field("R", 0).reshape(-1), gc[f"{name}_H"].reshape(-1)) <= 1e-12
+
+
+def test_gpu_square_root_condense_raises_like_the_reference(cuda, golden):
+    from paper_2003_02547_b200.errors import NotPositiveDefinite
+
+    assert int(golden("fcond_sqrt")["npd_raises"]) == 1
+    qp = source_qp(fcond_cases()[0][1])
+    qp.set_field("Q", 2, np.zeros((3, 3)))
+    with pytest.raises(NotPositiveDefinite):
+        pkg.condense(qp, variant="square_root")
+    pkg.condense(qp)   # the classical recursion tolerates a semidefinite stage cost
+    batch = OcpQpBatch.from_qps([source_qp(fcond_cases()[0][1]), qp])
+    with pytest.raises(NotPositiveDefinite, match="QP 1"):
+        condense_batch(batch, variant="square_root")
