@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = (
     "ocpqp_plan_info", "ocpqp_fp64_peak", "ocpqp_abi_version", "ocpqp_last_error",
     "ocpqp_pc_create", "ocpqp_pc_destroy", "ocpqp_pc_dims", "ocpqp_pc_condense",
     "ocpqp_pc_expand", "ocpqp_pc_last_error", "ocpqp_shift_guess", "ocpqp_fc_create",
-    "ocpqp_pc_soft", "ocpqp_dense_plan_create", "ocpqp_dense_plan_destroy", "ocpqp_dense_solve",
+    "ocpqp_pc_soft", "ocpqp_pc_set_variant", "ocpqp_dense_plan_create", "ocpqp_dense_plan_destroy", "ocpqp_dense_solve",
 )
 
 _i32p = ctypes.POINTER(ctypes.c_int32)
