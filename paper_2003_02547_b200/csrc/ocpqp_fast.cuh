@@ -409,8 +409,10 @@ struct FCtx {
     int flag;
     int q;
     double n_act;
-    long long ph[DBG_NUM];  // clock64 phase accumulators (KParams::dbg)
-    long long tk1;          // OCPQP_XTICK1: previous tick of thread 32
+    long long ph[DBG_KEPT];  // clock64 phase accumulators (KParams::dbg)
+#ifdef OCPQP_XDIAG
+    long long tk1;           // OCPQP_XTICK1: previous tick of thread 32
+#endif
     long long tk;
 };
 
@@ -3372,7 +3374,7 @@ struct Kern {
         const double reg2 = arg.reg_prim > 0.0 ? 2.0 * arg.reg_prim : 1e-8;
         const long long t_start = clock64();
         if (p.dbg && tid == 0) {
-            for (int i = 0; i < DBG_NUM; ++i) c.ph[i] = 0;
+            for (int i = 0; i < DBG_KEPT; ++i) c.ph[i] = 0;
             c.tk = t_start;
         }
         long long flops_top = 0;   // flops before this iteration (escape resume point)
@@ -3603,7 +3605,7 @@ struct Kern {
             if (p.dbg) {
                 c.ph[DBG_TOTAL] = clock64() - t_start;
                 c.ph[DBG_ITERS] = it;
-                for (int i = 0; i < DBG_NUM; ++i) p.dbg[(long long)q * DBG_NUM + i] = c.ph[i];
+                for (int i = 0; i < DBG_KEPT; ++i) p.dbg[(long long)q * DBG_NUM + i] = c.ph[i];
             }
         }
     }

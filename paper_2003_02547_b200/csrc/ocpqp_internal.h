@@ -119,6 +119,13 @@ enum DbgPhase { DBG_RES = 0, DBG_FACTOR, DBG_SOLVE_AFF, DBG_SOLVE_DIR, DBG_STEP,
                 // free slots for finer diagnostics (OCPQP_XTICK, -DOCPQP_XDIAG builds)
                 DBG_X0, DBG_X1, DBG_X2, DBG_X3, DBG_X4, DBG_X5, DBG_X6, DBG_X7,
                 DBG_NUM = 24 };
+// phase slots a kernel keeps per QP: the diagnostic slots only in -DOCPQP_XDIAG builds (the
+// accumulators live in the CTA's static shared memory; the buffer stride stays DBG_NUM)
+#ifdef OCPQP_XDIAG
+constexpr int DBG_KEPT = DBG_NUM;
+#else
+constexpr int DBG_KEPT = DBG_X0;
+#endif
 
 struct SolveParams {
     OcpIpmArgC arg;

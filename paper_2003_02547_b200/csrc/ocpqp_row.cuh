@@ -889,7 +889,7 @@ struct RKern {
         int it = 0, status = -1;
         Res res;
         const double reg2 = arg.reg_prim > 0.0 ? 2.0 * arg.reg_prim : 1e-8;
-        long long ph[DBG_NUM] = {0, 0, 0, 0, 0, 0, 0, 0};
+        long long ph[DBG_KEPT] = {0, 0, 0, 0, 0, 0, 0, 0};
         const long long t_start = clock64();
         long long tc = t_start;
         while (true) {
@@ -971,7 +971,7 @@ struct RKern {
             if (p.dbg) {
                 ph[DBG_TOTAL] = clock64() - t_start;
                 ph[DBG_ITERS] = it;
-                for (int i = 0; i < DBG_NUM; ++i) p.dbg[(long long)q * DBG_NUM + i] = ph[i];
+                for (int i = 0; i < DBG_KEPT; ++i) p.dbg[(long long)q * DBG_NUM + i] = ph[i];
             }
         }
     }
