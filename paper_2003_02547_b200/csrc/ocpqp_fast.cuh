@@ -251,6 +251,34 @@ struct MVo {
     }
 };
 
+// warp-tiled mat-vec on the warps W0 .. W0 + NWP - 1 of the CTA (only they may
+// call it): 8 rows per warp task (lane / 4), 4 lanes per row (lane % 4 takes
+// k = tg, tg + 4, ...), butterfly over the 4 lanes.  For a row-major operand
+// with a row stride of 4 or 12 mod 16 doubles (60, 84: the DMMA fragment
+// pattern) -- or its transpose read with the roles of i and k swapped -- a
+// half-warp's loads hit 16 different banks (the lane-pair split of MV has
+// two-way conflicts on every load of a 60-double row stride).
+template <int R, int KD, int NWP, int W0>
+struct MVw {
+    template <class FA, class FX, class FO>
+    __device__ __forceinline__ static void run(FA a, FX x, FO out) {
+        const int lane = threadIdx.x & 31, w = (int)(threadIdx.x >> 5) - W0;
+        const int gr = lane >> 2, tg = lane & 3;
+#pragma unroll
+        for (int i0 = 0; i0 < R; i0 += 8 * NWP) {
+            const int i = i0 + 8 * w + gr;
+            double acc = 0.0;
+            if (i < R) {
+#pragma unroll 5
+                for (int k = tg; k < KD; k += 4) acc = fma(a(i, k), x(k), acc);
+            }
+            acc += __shfl_xor_sync(FULL, acc, 1);
+            acc += __shfl_xor_sync(FULL, acc, 2);
+            if (i < R && tg == 0) out(i, acc);
+        }
+    }
+};
+
 // Cholesky of an NN x NN (NN <= 32) matrix held row-wise by the lanes of one
 // warp (lane i: row[j] = A[i][j], j <= i).  Pivot test as LAPACK potrf: a
 // pivot that is not > 0 (or NaN) fails (linalg.py:81-118).
@@ -2599,9 +2627,9 @@ struct Kern {
             // A: rr, rq = rhat + [B A]' (P_{n+1} r_b + p_{n+1})
             tm.wait(c.mbar, s);
             const double* BAn = sBA[s];
-            MV<NW, NX, TEAM>::run([&](int j, int k) { return BAn[j * NX + k]; },
-                                  [&](int k) { return qv[k] + pvs[k]; },
-                                  [&](int j, double v) { win[j] = rhs[j] + v; });
+            MVw<NW, NX, TEAM / 32, 0>::run([&](int j, int k) { return BAn[j * NX + k]; },
+                                           [&](int k) { return qv[k] + pvs[k]; },
+                                           [&](int j, double v) { win[j] = rhs[j] + v; });
             bar<TEAM>();
             if (n > 1) tma_ba(c, tm, sBA[s], n - 2, s);
             // B: p_n, k_n, and q_{n-1} for the next stage
@@ -2670,7 +2698,7 @@ struct Kern {
             const double* Pn = blk + FP;
             const double* pvn = blk + FV;
             if (n > 0) {
-                MV<NU + NX, NX, TEAM>::run(
+                MVw<NU + NX, NX, TEAM / 32, 0>::run(
                     [&](int i, int k) { return i < NU ? Kn[i * NX + k] : Pget(Pn, i - NU, k); },
                     [&](int k) { return xa[k]; },
                     [&](int i, double v) {
@@ -2685,7 +2713,7 @@ struct Kern {
                         }
                     });
             } else {
-                MV<NU, NX, TEAM>::run([&](int i, int k) { return Kn[i * NX + k]; },
+                MVw<NU, NX, TEAM / 32, 0>::run([&](int i, int k) { return Kn[i * NX + k]; },
                                       [&](int k) { return xa[k]; },
                                       [&](int i, double v) {
                                           const double u = v + kf[i];
@@ -2700,7 +2728,7 @@ struct Kern {
             tm.wait(c.mbar, s);
             const double* BAn = sBA[s];
             double* xd = dy + (n + 1) * NW + (n + 1 < N ? NU : 0);
-            MV<NX, NW, TEAM>::run(
+            MVw<NX, NW, TEAM / 32, 0>::run(
                 [&](int i, int k) { return k < NX ? BAn[(NU + k) * NX + i] : BAn[(k - NX) * NX + i]; },
                 [&](int k) { return k < NX ? xa[k] : uv[k - NX]; },
                 [&](int i, double v) {
