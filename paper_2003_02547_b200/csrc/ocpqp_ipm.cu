@@ -197,6 +197,8 @@ __device__ void rows_values(const Ctx& c, const double* y, double* rowv) {
             double v;
             if (i < s.nb) {
                 v = w[p.idxb[s.ib_off + i]];
+            } else if (s.ng >= 32) {
+                continue;   // large stages: one warp per general row, below
             } else {
                 const int g = i - s.nb, nu = s.nu, nx = s.nx;
                 const double* Dg = fptr(c, OCPQP_F_D, s) + g * nu;
@@ -210,6 +212,41 @@ __device__ void rows_values(const Ctx& c, const double* y, double* rowv) {
             rowv[s.m_off + i] = v;
         }
     END_FOR_STAGE_ITEMS
+    // general rows of large stages (the condensed config-4 stage: 240 rows of
+    // 160 columns): one warp per row, the lanes across the columns (coalesced
+    // loads, one butterfly) instead of one thread walking a 160-term chain
+    const int lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    for (int n = 0; n <= c.N; ++n) {
+        const StageInfo& s = c.st[n];
+        if (s.ng < 32) continue;
+        const int nu = s.nu, nx = s.nx;
+        const double* w = y + s.u_off;
+        const double* D = fptr(c, OCPQP_F_D, s);
+        const double* C = fptr(c, OCPQP_F_C, s);
+        for (int g0 = 2 * (threadIdx.x >> 5); g0 < s.ng; g0 += 2 * nwarp) {
+            double v0 = 0.0, v1 = 0.0;
+            const bool two = g0 + 1 < s.ng;
+            for (int j = lane; j < nu; j += 32) {
+                const double wj = w[j];
+                v0 = fma(D[g0 * nu + j], wj, v0);
+                if (two) v1 = fma(D[(g0 + 1) * nu + j], wj, v1);
+            }
+            for (int j = lane; j < nx; j += 32) {
+                const double wj = w[nu + j];
+                v0 = fma(C[g0 * nx + j], wj, v0);
+                if (two) v1 = fma(C[(g0 + 1) * nx + j], wj, v1);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+                v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+            }
+            if (lane == 0) {
+                rowv[s.m_off + s.nb + g0] = v0;
+                if (two) rowv[s.m_off + s.nb + g0 + 1] = v1;
+            }
+        }
+    }
 }
 
 __device__ __forceinline__ double rows_t(const Ctx& c, const StageInfo& s, int j,
@@ -223,8 +260,23 @@ __device__ __forceinline__ double rows_t(const Ctx& c, const StageInfo& s, int j
         const int ld = du ? s.nu : s.nx;
         const double* cg = coeff + s.nb;
         double g = 0.0;
+        if (s.ng >= 32) {
+            // large stages: four interleaved partial sums (the chain is the cost)
+            double g1 = 0.0, g2 = 0.0, g3 = 0.0;
+            int r = 0;
+#pragma unroll 2
+            for (; r + 3 < s.ng; r += 4) {
+                g = fma(col[r * ld], cg[r], g);
+                g1 = fma(col[(r + 1) * ld], cg[r + 1], g1);
+                g2 = fma(col[(r + 2) * ld], cg[r + 2], g2);
+                g3 = fma(col[(r + 3) * ld], cg[r + 3], g3);
+            }
+            for (; r < s.ng; ++r) g = fma(col[r * ld], cg[r], g);
+            g = (g + g1) + (g2 + g3);
+        } else {
 #pragma unroll 8
-        for (int r = 0; r < s.ng; ++r) g = fma(col[r * ld], cg[r], g);
+            for (int r = 0; r < s.ng; ++r) g = fma(col[r * ld], cg[r], g);
+        }
         out += g;
     }
     return out;
