@@ -992,7 +992,13 @@ __device__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops
             const int q = tid & 3;
             const unsigned qmask = 0xFu << (tid & 28);
             double* __restrict__ Y = T1;
+            double* __restrict__ rinv = T1 + nu * nx;   // 1 / L_ii (behind the columns)
             const double* __restrict__ Lr = L;
+            const bool have_rinv = (long long)nu * nx + nu <= (long long)nxn * nw;
+            if (have_rinv) {
+                for (int i = tid; i < nu; i += T) rinv[i] = 1.0 / Lr[i * nu + i];
+                tsync();
+            }
             for (int j = tid >> 2; j < nx; j += T >> 2) {
                 for (int i = q; i < nu; i += 4) Y[i * nx + j] = G[i * nw + nu + j];
                 __syncwarp(qmask);
@@ -1001,18 +1007,18 @@ __device__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops
                     // for the first time at its pivot: an L2 round trip per batch otherwise)
                     if (i + 1 < nu && (tid & 31) * 16 < nu)
                         asm volatile("prefetch.global.L1 [%0];\n" ::"l"(Lr + (i + 1) * nu + (tid & 31) * 16));
-                    const double y = Y[i * nx + j] / Lr[i * nu + i];
+                    const double y = have_rinv ? Y[i * nx + j] * rinv[i] : Y[i * nx + j] / Lr[i * nu + i];
                     const double* Li = Lr + i * nu;
-                    for (int k = i + 1 + ((q - (i + 1)) & 3); k < nu; k += 16) {
-                        double l[4], v[4];
+                    for (int k = i + 1 + ((q - (i + 1)) & 3); k < nu; k += 32) {
+                        double l[8], v[8];
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) {
+                        for (int r = 0; r < 8; ++r) {
                             const int kk = k + 4 * r;
                             l[r] = kk < nu ? Li[kk] : 0.0;
                             v[r] = kk < nu ? Y[kk * nx + j] : 0.0;
                         }
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) {
+                        for (int r = 0; r < 8; ++r) {
                             const int kk = k + 4 * r;
                             if (kk < nu) Y[kk * nx + j] = fma(-l[r], y, v[r]);
                         }
@@ -1024,18 +1030,18 @@ __device__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops
                 for (int i = nu - 1; i >= 0; --i) {
                     if (i > 0 && (tid & 31) * 16 < nu)
                         asm volatile("prefetch.global.L1 [%0];\n" ::"l"(Lr + (i - 1) * nu + (tid & 31) * 16));
-                    const double y = Y[i * nx + j] / Lr[i * nu + i];
+                    const double y = have_rinv ? Y[i * nx + j] * rinv[i] : Y[i * nx + j] / Lr[i * nu + i];
                     const double* Li = Lr + i * nu;
-                    for (int k = q; k < i; k += 16) {
-                        double l[4], v[4];
+                    for (int k = q; k < i; k += 32) {
+                        double l[8], v[8];
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) {
+                        for (int r = 0; r < 8; ++r) {
                             const int kk = k + 4 * r;
                             l[r] = kk < i ? Li[kk] : 0.0;
                             v[r] = kk < i ? Y[kk * nx + j] : 0.0;
                         }
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) {
+                        for (int r = 0; r < 8; ++r) {
                             const int kk = k + 4 * r;
                             if (kk < i) Y[kk * nx + j] = fma(-l[r], y, v[r]);
                         }
