@@ -2621,44 +2621,70 @@ struct Kern {
             for (int i = tid; i < NW; i += TEAM) rhs[i] = rhat[(N - 1) * NW + i];
         }
         bar<TEAM>();
+        // The k_n = -G_uu^{-1} rr solve (forty dependent shuffle steps, the longest
+        // piece of a stage) feeds only the forward sweep (kkt_ocp.py:296), so the last
+        // warp runs it one stage behind, off the recursion's critical path: at stage n
+        // it copies L_n, 1 / L_ii and rr_n to a private area and solves while the other
+        // warps do phase B of stage n and phase A of stage n - 1.  Named barriers: 2 =
+        // phase A done (all warps), 3 = phase B done (the solver warp only arrives).
+        constexpr int LW = TEAM / 32 - 1;
+        double* Lp = rvs + NU;         // NU x NU
+        double* rip = Lp + NU * NU;    // NU
+        double* rrp = rip + NU;        // NU
+        static_assert(NW + 4 * NX + NU + NW + NU + NU * NU + 2 * NU <= S::VECB, "sweeps_big k-solve copies");
+        int kpend = -1;
         for (int n = N - 1; n >= 0; --n) {
             const int s = n & 1;
             l2pf(n - 3);
-            // A: rr, rq = rhat + [B A]' (P_{n+1} r_b + p_{n+1})
+            // A: rr, rq = rhat + [B A]' (P_{n+1} r_b + p_{n+1})  |  the pending k solve
             tm.wait(c.mbar, s);
             const double* BAn = sBA[s];
-            MVw<NW, NX, TEAM / 32, 0>::run([&](int j, int k) { return BAn[j * NX + k]; },
-                                           [&](int k) { return qv[k] + pvs[k]; },
-                                           [&](int j, double v) { win[j] = rhs[j] + v; });
-            bar<TEAM>();
+            if (warp != LW) {
+                MVw<NW, NX, LW, 0>::run([&](int j, int k) { return BAn[j * NX + k]; },
+                                        [&](int k) { return qv[k] + pvs[k]; },
+                                        [&](int j, double v) { win[j] = rhs[j] + v; });
+            } else if (kpend >= 0) {
+                warp_cho_solve<NU>(Lp, rip, rrp, kff + kpend * NU, -1.0);
+            }
+            asm volatile("bar.sync 2, %0;\n" ::"n"(TEAM) : "memory");
             if (n > 1) tma_ba(c, tm, sBA[s], n - 2, s);
-            // B: p_n, k_n, and q_{n-1} for the next stage
+            // B: p_n = rq + K' rr (warps 4-6) | q_{n-1} = P_n r_b,n-1 for the next stage
+            // (warps 0-3: independent of p_n, kkt_ocp.py:282 split as P r_b + p)
             tm.wait(c.mbar, 2);
             const double* Kn = blk + YK;
-            const double* Ln = blk + YL;
-            const double* Rn = rvs;
             double* pvc = pv + n * NX;
-            if (warp == TEAM / 32 - 1) {
-                warp_cho_solve<NU>(Ln, Rn, win, kff + n * NU, -1.0);
-            } else if (warp >= 4) {
-                MVo<NX, NU, TEAM - 160, 128>::run([&](int i, int k) { return Kn[k * NX + i]; },
-                                                  [&](int k) { return win[k]; },
-                                                  [&](int i, double v) {
-                                                      const double r = win[NU + i] + v;
-                                                      pvc[i] = r;
-                                                      pvs[i] = r;
-                                                  });
-            } else if (n > 0) {
-                const double* Pn = blk + YP;
-                const double* rbm = blk + YB;
-                MVo<NX, NX, 128, 0>::run([&](int i, int k) { return Pget(Pn, i, k); },
-                                         [&](int k) { return rbm[k]; }, [&](int i, double v) { qv[i] = v; });
-                for (int i = tid; i < NW; i += 128) rhs[i] = blk[YH + i];
+            if (warp == LW) {
+                const int lane = tid & 31;
+                for (int i = lane; i < NU * NU; i += 32) Lp[i] = blk[YL + i];
+                if (lane < NU) {
+                    rip[lane] = rvs[lane];
+                    rrp[lane] = win[lane];
+                }
+                __syncwarp();
+                kpend = n;
+                asm volatile("bar.arrive 3, %0;\n" ::"n"(TEAM) : "memory");
+            } else {
+                if (warp >= 4) {
+                    MVo<NX, NU, TEAM - 160, 128>::run([&](int i, int k) { return Kn[k * NX + i]; },
+                                                      [&](int k) { return win[k]; },
+                                                      [&](int i, double v) {
+                                                          const double r = win[NU + i] + v;
+                                                          pvc[i] = r;
+                                                          pvs[i] = r;
+                                                      });
+                } else if (n > 0) {
+                    const double* Pn = blk + YP;
+                    const double* rbm = blk + YB;
+                    MVo<NX, NX, 128, 0>::run([&](int i, int k) { return Pget(Pn, i, k); },
+                                             [&](int k) { return rbm[k]; }, [&](int i, double v) { qv[i] = v; });
+                    for (int i = tid; i < NW; i += 128) rhs[i] = blk[YH + i];
+                }
+                asm volatile("bar.sync 3, %0;\n" ::"n"(TEAM) : "memory");
             }
             flops += 2ll * NU * NU;
-            bar<TEAM>();
             if (n > 0) issue_Y(n - 1);
         }
+        if (warp == LW && kpend >= 0) warp_cho_solve<NU>(Lp, rip, rrp, kff + kpend * NU, -1.0);
         OCPQP_TICK(c, DBG_S_BWD);
         // x0 step: dx_0 = -P_0^{-1} p_0
         if (warp == 0) warp_cho_solve<NX>(wsb<WS_LP0>(c, p), Rst + N * NU, pvs, xa, -1.0);
