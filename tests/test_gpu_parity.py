@@ -275,6 +275,24 @@ def test_gpu_full_batch_properties(cuda, oracle, speed_arg, cfg):
     assert np.array_equal(rep.iterations.cpu().numpy()[idx], ref["iters"])
 
 
+def test_gpu_config4_full_batch_matches_oracle(cuda, oracle, speed_arg):
+    """The headline workload at full size (BASELINE config 4: 256 QPs, N = 100,
+    nx = 60, nu = 20) on the BIG team kernel: every QP converges to tol, and a
+    64-QP sample spread over the batch matches the oracle -- status, iteration
+    count, counted flops identical; y / pi / lam / t and the final norms within
+    1e-8 (assert_parity)."""
+    batch = make_batch(4)
+    rep = solve_ocp_qp_batch(batch, speed_arg, trace=False)
+    st = rep.status_code.cpu().numpy()
+    assert np.all(st == 0)
+    res = rep.res.cpu().numpy()
+    assert np.all(res <= 1e-8)
+    idx = np.linspace(0, batch.B - 1, 64).astype(int)
+    ref = oracle.solve(batch.select(idx), speed_arg, trace=False)
+    got = {k: v[idx] for k, v in host(rep).items() if v is not None}
+    assert_parity(got, ref, tol=1e-8)
+
+
 def test_gpu_config3_lambda_distribution(cuda, oracle, speed_arg):
     """Known-hard row: the lam parity distribution on config 3.
 
