@@ -516,6 +516,46 @@ __device__ bool team_chol(double* L, int n, int ld, int* flag, bool keep_upper =
     return true;
 }
 
+// The same factorization with the matrix held as a packed lower triangle in the
+// scratch buffer `sm` (the stage's T1 buffer, shared memory when the plan placed
+// it): every column step then costs shared-memory round trips instead of L2
+// ones.  Same operations and order per element as team_chol.  keep_upper as there.
+__device__ bool team_chol_packed(double* L, int n, double* sm, bool keep_upper) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int lane = tid & 31, nwarp = (T + 31) >> 5;
+    auto at = [&](int i, int j) -> double& { return sm[i * (i + 1) / 2 + j]; };
+    for (int e = tid; e < n * n; e += T) {
+        const int i = e / n, j = e - i * n;
+        if (j <= i) at(i, j) = L[e];
+    }
+    tsync();
+    bool ok = true;
+    for (int k = 0; k < n; ++k) {
+        const double d = at(k, k);
+        if (!(d > 0.0)) {
+            ok = false;
+            break;
+        }
+        const double dk = sqrt(d);
+        for (int i = k + 1 + tid; i < n; i += T) at(i, k) = at(i, k) / dk;
+        tsync();
+        if (tid == 0) at(k, k) = dk;   // read by nobody in this column step
+        for (int i = k + 1 + (tid >> 5); i < n; i += nwarp) {
+            const double lik = at(i, k);
+            for (int j = k + 1 + lane; j <= i; j += 32) at(i, j) -= lik * at(j, k);
+        }
+        tsync();
+    }
+    tsync();
+    if (!ok) return false;
+    for (int e = tid; e < n * n; e += T) {
+        const int i = e / n, j = e - i * n;
+        L[e] = j <= i ? at(i, j) : (keep_upper ? at(j, i) : 0.0);
+    }
+    tsync();
+    return true;
+}
+
 // serial cho_solve x = (L L')^{-1} b for one thread (kkt_ocp.py:66-67)
 __device__ __forceinline__ void cho_solve_serial(const double* L, int n, double* x) {
     for (int i = 0; i < n; ++i) {
@@ -1013,7 +1053,11 @@ __device__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops
         tsync();
         flops += (long long)nu * nu * nu / 3;
         const bool bigk = nu >= 32 && (long long)nu * nx <= (long long)nxn * nw && n < N;
-        if (!team_chol(L, nu, nu, c.iflag, bigk)) return LINALG_NPD;
+        // large stages: factor in the T1 buffer (free between G and the K solve)
+        const bool packed = nu >= 32 && n < N && (long long)nu * (nu + 1) / 2 <= (long long)nxn * nw &&
+                            __isShared(T1);   // only pays when the plan placed T1 in shared memory
+        if (!(packed ? team_chol_packed(L, nu, T1, bigk) : team_chol(L, nu, nu, c.iflag, bigk)))
+            return LINALG_NPD;
         if (bigk) {
             // K = -L'^{-1} L^{-1} G_ux (kkt_ocp.py:240-243), right-looking: the
             // lane quad 4c..4c+3 owns column j, lane q its rows q, q + 4, ...;
