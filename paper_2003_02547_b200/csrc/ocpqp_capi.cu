@@ -296,7 +296,7 @@ void place_workspace(OcpPlan* P) {
         budget = (228ll * 1024) / tgt - 2048;
         budget = std::min(budget, 227ll * 1024 - 1024);
     }
-    const int prio[] = {WS_G, WS_T1, WS_VEC, WS_ACT, WS_DVEC, WS_GAM, WS_WALL, WS_COEF,
+    const int prio[] = {WS_T1, WS_G, WS_VEC, WS_ACT, WS_DVEC, WS_GAM, WS_WALL, WS_COEF,
                         WS_CROW, WS_ROWV, WS_RHAT, WS_P, WS_K, WS_L, WS_LP0, WS_PV, WS_KFF,
                         WS_RG, WS_RB, WS_RD, WS_DIR_LAM, WS_DIR_T, WS_AFF_LAM, WS_AFF_T,
                         WS_DIR_Y, WS_DIR_PI, WS_AFF_Y, WS_AFF_PI, WS_DL, WS_DU, WS_RTSL, WS_RTSU};
@@ -548,7 +548,7 @@ void place_generic_on_fast(OcpPlan* P) {
     const Layout& L = P->L;
     const int per_sm = std::max(1, (P->slots + P->num_sms - 1) / std::max(1, P->num_sms));
     long long budget = std::min((228ll * 1024) / per_sm - 2048, 227ll * 1024 - 1024);
-    const int prio[] = {WS_G, WS_T1, WS_VEC, WS_ACT, WS_DVEC, WS_GAM, WS_WALL, WS_COEF,
+    const int prio[] = {WS_T1, WS_G, WS_VEC, WS_ACT, WS_DVEC, WS_GAM, WS_WALL, WS_COEF,
                         WS_CROW, WS_ROWV, WS_RHAT, WS_P, WS_K, WS_L, WS_LP0, WS_PV, WS_KFF,
                         WS_RG, WS_RB, WS_RD, WS_DIR_LAM, WS_DIR_T, WS_AFF_LAM, WS_AFF_T,
                         WS_DIR_Y, WS_DIR_PI, WS_AFF_Y, WS_AFF_PI, WS_DL, WS_DU, WS_RTSL, WS_RTSU};
