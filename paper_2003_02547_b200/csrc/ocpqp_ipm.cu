@@ -865,14 +865,28 @@ __device__ __noinline__ void rows_syrk(const Ctx& c, const StageInfo& s, const d
 // C(i, j) = sum_k a(k, i) b(k, j), i < M, j < N, k ascending with one fma chain
 // per output (the arithmetic of the one-output-per-thread loops it replaces),
 // over 4 x 4 register tiles: 8 operand loads per 16 FMAs, the loads of a k step
-// independent of each other.  epi(i, j, acc) stores.  Large stages only (the
+// independent of each other.  Operand columns are given as (pointer, stride):
+// ca(i) / cb(j) return the address of element (0, i) / (0, j) and the stride
+// between consecutive k, so the k loop carries no index arithmetic beyond two
+// multiply-adds per operand.  epi(i, j, acc) stores.  Large stages only (the
 // condensed config-4 stage: 160 x 160 x 60).
+struct ColRef {
+    const double* p;
+    int ld;
+};
 template <class FA, class FB, class FE>
-__device__ __forceinline__ void team_gemm_tn(int M, int N, int K, FA a, FB b, FE epi) {
+__device__ __forceinline__ void team_gemm_tn(int M, int N, int K, FA ca, FB cb, FE epi) {
     const int tid = threadIdx.x, T = blockDim.x;
     const int tn = (N + 3) >> 2, nt = ((M + 3) >> 2) * tn;
     for (int t = tid; t < nt; t += T) {
         const int i0 = (t / tn) * 4, j0 = (t - (t / tn) * tn) * 4;
+        ColRef ra[4], rb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            // out-of-range columns re-read the tile's first one (finite data; never stored)
+            ra[q] = ca(i0 + q < M ? i0 + q : i0);
+            rb[q] = cb(j0 + q < N ? j0 + q : j0);
+        }
         double acc[4][4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
@@ -883,8 +897,8 @@ __device__ __forceinline__ void team_gemm_tn(int M, int N, int K, FA a, FB b, FE
             double av[4], bv[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                av[q] = i0 + q < M ? a(k, i0 + q) : 0.0;
-                bv[q] = j0 + q < N ? b(k, j0 + q) : 0.0;
+                av[q] = ra[q].p[k * ra[q].ld];
+                bv[q] = rb[q].p[k * rb[q].ld];
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
@@ -1008,12 +1022,12 @@ __device__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops
         const double* An = fptr(c, OCPQP_F_A, s);
         const double* Bn = fptr(c, OCPQP_F_B, s);
         const bool big = big_stage(nw);
-        auto BAat = [&](int k, int j) { return j < nu ? Bn[k * nu + j] : An[k * nx + (j - nu)]; };
+        auto BAcol = [&](int j) { return j < nu ? ColRef{Bn + j, nu} : ColRef{An + (j - nu), nx}; };
         if (big) {
-            team_gemm_tn(nxn, nw, nxn, [&](int k, int i) { return Pn[i * nxn + k]; }, BAat,
+            team_gemm_tn(nxn, nw, nxn, [&](int i) { return ColRef{Pn + i * nxn, 1}; }, BAcol,
                          [&](int i, int j, double v) { T1[i * nw + j] = v; });
             tsync();
-            team_gemm_tn(nw, nw, nxn, BAat, [&](int k, int j) { return T1[k * nw + j]; },
+            team_gemm_tn(nw, nw, nxn, BAcol, [&](int j) { return ColRef{T1 + j, nw}; },
                          [&](int i, int j, double v) { G[i * nw + j] = v + Mb[i * nw + j]; });
         } else {
         // T1 = P[n+1] [B A]  (nx' x nw): column j of [B A] read with stride
@@ -1151,8 +1165,8 @@ __device__ int stage_classical(Ctx& c, int n, const double* Mb, long long& flops
         tsync();
         // P = G_xx + G_ux' K (kkt_ocp.py:244)
         if (big_stage(nw)) {
-            team_gemm_tn(nx, nx, nu, [&](int k, int i) { return G[k * nw + nu + i]; },
-                         [&](int k, int j) { return K[k * nx + j]; },
+            team_gemm_tn(nx, nx, nu, [&](int i) { return ColRef{G + nu + i, nw}; },
+                         [&](int j) { return ColRef{K + j, nx}; },
                          [&](int i, int j, double v) { T1[i * nx + j] = v + G[(nu + i) * nw + nu + j]; });
         } else
         for (int idx = tid; idx < nx * nx; idx += T) {
