@@ -402,6 +402,36 @@ def bench_ocp(cx, cfg, B, arg, steps, warmup, *, e2e=True, cpu=True, cpu_seconds
                        "max": float(times.max())}}
     if clk is not None:
         res["clocks"] = clk
+    if plan_info.get("kernel") == "team" and cx.world == 1 and cfg == 4:
+        # Not part of `value`: the same batch with the plan's opt-in dispatch hint
+        # (ocpqp_plan_dispatch_hint: QPs handed out by the PREVIOUS solve's iteration
+        # counts, the slowest to the CTAs alone on their SM).  It needs a previous solve
+        # of a similar batch (closed-loop MPC); here that is the identical batch, so the
+        # number shows what the launch's tail costs, not the one-shot throughput.
+        plan = get_plan(dev)
+        plan.dispatch_hint(True)
+        try:
+            for _ in range(3):
+                step()
+            hev = cx.events(5)
+            for e0, e1 in hev:
+                cx.flush.zero_()
+                e0.record(stream)
+                step()
+                e1.record(stream)
+            torch.cuda.synchronize()
+            th = float(np.mean([e0.elapsed_time(e1) for e0, e1 in hev]))
+            same = bool(np.array_equal(out["iters"].cpu().numpy(), o["iters"])) and all(
+                bool(np.array_equal(out[k].cpu().numpy(), o[k])) for k in ("y", "pi", "lam", "t"))
+            res["dispatch_hint"] = {
+                "value": B / (th * 1e-3), "unit": "solves/s", "ms_per_step": th, "steps": 5,
+                "identical_results": same,
+                "note": "opt-in, off in `value`: QP order from the plan's previous solve of the "
+                        "same batch (slowest QPs to the CTAs alone on their SM)"}
+        finally:
+            plan.dispatch_hint(False)
+            step()
+            torch.cuda.synchronize()
     if e2e:
         hb = batch.pin_memory()
         hout = dict(y=torch.empty((B, lay.ny), dtype=torch.float64).pin_memory(),

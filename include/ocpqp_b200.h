@@ -251,6 +251,16 @@ int ocpqp_factor_export(OcpPlan* plan, int32_t qp, double* P_out, double* K_out)
 int ocpqp_shift_guess(OcpPlan* plan, const OcpQpDataC* data, const OcpIterC* sol,
                       OcpIterC* guess, void* stream);
 
+/* Dispatch hint of the team kernel (off by default; OCPQP_DISPATCH_HINT=1 turns
+ * it on at plan creation).  With it a solve hands out its QPs in the order of
+ * the plan's PREVIOUS solve's iteration counts, slowest first, and the CTAs
+ * that find themselves alone on their SM take the slowest ones: a QP alone on
+ * an SM runs ~20 % faster per iteration, and a launch ends with its slowest
+ * QP.  Meant for repeated solves of similar batches (closed-loop MPC, where
+ * consecutive iteration counts correlate); the first solve after enabling
+ * runs unhinted; results are identical with and without it. */
+int ocpqp_plan_dispatch_hint(OcpPlan* plan, int32_t on);
+
 /* Plan introspection: out[0..4] = threads per CTA, resident CTA slots,
  * dynamic shared memory bytes per CTA, shared-memory buffer mask, workspace
  * doubles per slot; out[5] kernel kind (0 generic, 1 team, 2 row), out[6]

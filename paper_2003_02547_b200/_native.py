@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = (
     "ocpqp_plan_info", "ocpqp_fp64_peak", "ocpqp_abi_version", "ocpqp_last_error",
     "ocpqp_pc_create", "ocpqp_pc_destroy", "ocpqp_pc_dims", "ocpqp_pc_condense",
     "ocpqp_pc_expand", "ocpqp_pc_last_error", "ocpqp_shift_guess", "ocpqp_fc_create",
-    "ocpqp_pc_soft", "ocpqp_pc_set_variant", "ocpqp_dense_plan_create", "ocpqp_dense_plan_destroy", "ocpqp_dense_solve",
+    "ocpqp_pc_soft", "ocpqp_pc_set_variant", "ocpqp_plan_dispatch_hint", "ocpqp_dense_plan_create", "ocpqp_dense_plan_destroy", "ocpqp_dense_solve",
 )
 
 _i32p = ctypes.POINTER(ctypes.c_int32)
@@ -234,6 +234,13 @@ class Plan:
         return dict(kernel=kind, threads_per_cta=out[0], slots=out[1], smem_bytes=out[2],
                     smem_mask=out[3], ws_doubles_per_slot=out[4], lanes_per_qp=out[6],
                     grid=out[7], store_in_smem=bool(out[8]))
+
+    def dispatch_hint(self, on=True):
+        """Hand out the next solves' QPs by this plan's previous iteration counts
+        (ocpqp_plan_dispatch_hint; team kernel, repeated solves of similar batches)."""
+        L = lib()
+        L.ocpqp_plan_dispatch_hint.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+        check(L.ocpqp_plan_dispatch_hint(self.handle, 1 if on else 0))
 
     def close(self):
         if getattr(self, "handle", None):

@@ -94,6 +94,11 @@ struct KParams {
     unsigned long long smem_mask;  // bit b set: buffer b lives in shared memory
     int smem_off[WS_NUM];     // offsets within dynamic smem (doubles)
     int* counter;             // dynamic QP scheduler
+    // dispatch hint (team kernel, opt-in): `order` lists the QPs by the previous solve's
+    // iteration count, slowest first; its first n_first entries go to the CTAs that find
+    // themselves alone on their SM (hint_ctr: [0] / [1] list cursors, [2 + smid] CTAs per SM),
+    // prev_iters receives this solve's counts for the next one (nullptr = off)
+    const int* order; int n_first; int* hint_ctr; int* prev_iters;
     // shaped-kernel structure (uniform stages 0..N-1, terminal stage N)
     int NB, NBN, NGN;         // box rows (n < N), box / general rows at N
     int box_ident;            // 1: every stage's idxb is 0..nb-1 (box row i bounds variable i)

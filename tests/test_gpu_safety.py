@@ -72,3 +72,36 @@ def test_gpu_outputs_stay_inside_guard_bands(cuda, cfg, B, N):
             assert np.all(h[:G] == -7) and np.all(h[-G:] == -7), k
     assert np.array_equal(rep.y.cpu().numpy(), ref["y"])
     assert np.array_equal(rep.iterations.cpu().numpy(), ref["iters"])
+
+
+def test_dispatch_hint_changes_nothing_but_the_order(cuda):
+    """ocpqp_plan_dispatch_hint (opt-in): the QPs of a solve are handed out in
+    the order of the plan's previous solve's iteration counts, the slowest to
+    the CTAs alone on their SM.  Results, iteration counts, statuses and flop
+    counts must be bit-identical with and without it, on the full config-4
+    batch (256 CTAs, two per SM: the case the hint is for) and on a batch that
+    runs in several waves."""
+    import torch
+
+    from paper_2003_02547_b200 import mode_preset, solve_ocp_qp_batch
+    from paper_2003_02547_b200.generators import make_batch
+    from paper_2003_02547_b200.solver import get_plan
+
+    arg = mode_preset("speed").with_tol(1e-8)
+    for cfg, B in ((4, 256), (3, 512)):
+        dev = make_batch(cfg, batch=B).to("cuda")
+        base = solve_ocp_qp_batch(dev, arg, trace=False)
+        ref = {k: getattr(base, k).clone() for k in ("y", "pi", "lam", "t", "iterations", "status_code", "flops")}
+        plan = get_plan(dev)
+        plan.dispatch_hint(True)
+        try:
+            for _ in range(3):   # the first hinted solve only records the counts
+                rep = solve_ocp_qp_batch(dev, arg, trace=False)
+                torch.cuda.synchronize()
+                for k, v in ref.items():
+                    assert torch.equal(getattr(rep, k), v), (cfg, k)
+        finally:
+            plan.dispatch_hint(False)
+        rep = solve_ocp_qp_batch(dev, arg, trace=False)
+        for k, v in ref.items():
+            assert torch.equal(getattr(rep, k), v), (cfg, k)
