@@ -362,7 +362,7 @@ def test_gpu_warm_start_not_slower(cuda, speed_arg):
 
 
 # ------------------------------------------- shaped kernel on random structure
-FAST_SHAPES = [(8, 3, 0), (24, 4, 0), (30, 10, 10)]
+FAST_SHAPES = [(8, 3, 0), (24, 4, 0), (30, 10, 10), (60, 20, 0)]
 
 
 @pytest.mark.parametrize("nx,nu,ng", FAST_SHAPES)
@@ -384,7 +384,12 @@ def test_gpu_shaped_kernel_random_structure(cuda, oracle, speed_arg, nx, nu, ng,
     batch = OcpQpBatch.from_qps([qpgen.build_qp(pkg, dims, stages, dyn)])
     use_kind("auto")
     assert S.get_plan(batch).info()["kernel"] == "team"
-    arg = pkg.mode_preset("speed").with_tol(1e-6)
+    # the BIG shape (60, 20: TMA-staged factor and sweeps, config 4's kernel): these random
+    # stages have entries of O(1e3), so the rounding floor of res_g is ~1e-6 (the oracle's own
+    # res_g hovers at 1.0e-6 .. 1.3e-6 for two iterations on seed 17) -- an exit tolerance of
+    # 1e-6 would compare two noise-driven exits; 1e-5 keeps the exit unambiguous
+    tol = 1e-5 if nx >= 48 else 1e-6
+    arg = pkg.mode_preset("speed").with_tol(tol)
     got = host(solve_ocp_qp_batch(batch, arg))
     ref = oracle.solve(batch, arg)
     if ref["status"][0] == 4:
@@ -396,8 +401,8 @@ def test_gpu_shaped_kernel_random_structure(cuda, oracle, speed_arg, nx, nu, ng,
         return
     # general rows: lam (and with it res_g of a tol-1e-6 exit, whose norms are
     # up to 1e-6 themselves) is the known-hard row: norms within 0.25 tol
-    assert_parity(got, ref, allow_lam_frac=1.0 if ng else 0.0, tol=1e-6,
-                  res_bar=2.5e-7 if ng else 1e-8)
+    assert_parity(got, ref, allow_lam_frac=1.0 if ng else 0.0, tol=tol,
+                  res_bar=0.25 * tol if (ng or nx >= 48) else 1e-8)
     if ng:  # lam: bounded like the config-3 known-hard row
         assert rel_err(got["lam"][0], ref["lam"][0]) <= 1e-6
 
