@@ -322,7 +322,7 @@ def bench_ocp(cx, cfg, B, arg, steps, warmup, *, e2e=True, cpu=True, cpu_seconds
     torch.cuda.synchronize()
     plan_info = get_plan(dev).info()
     if plan_info.get("kernel") == "team" and not team_supports(
-            arg, int(batch.dim.nx[0]) + int(batch.dim.nu[0])):
+            arg, int(batch.dim.nx[0]) + int(batch.dim.nu[0]), int(batch.dim.nx[0])):
         plan_info["kernel"] = "generic"   # square-root / robust run on k_ipm_solve
     evs = cx.events(steps)
     sampler = ClockSampler(index=cx.device.index or 0) if clocks else None

@@ -582,7 +582,7 @@ void place_generic_on_fast(OcpPlan* P) {
 // The team kernel runs the classical-Riccati delta-form loop with optional
 // refinement of the combined direction (speed, balance); the QR rungs of the
 // balance ladder are left to the generic kernel per QP (escape list).
-bool team_supports(const OcpIpmArgC* a, int nw) {
+bool team_supports(const OcpIpmArgC* a, int nw, int nx) {
     // delta form with residuals every iteration, or the speed_abs combination
     // (absolute form, residuals only at exit, no refinement / QR)
     const bool delta = !a->abs_form && a->comp_res_pred;
@@ -590,7 +590,10 @@ bool team_supports(const OcpIpmArgC* a, int nw) {
                            !a->use_qr_fallback;
     // square-root variant: warp Cholesky of the whole stage block (nw <= 32)
     const bool variant_ok = a->riccati_variant == 0 || (a->riccati_variant == 1 && nw <= 32);
-    return (delta || abs_speed) && !a->use_qr_always && variant_ok && a->itref_pred_max <= 0;
+    // robust mode's QR stage: the stacked factor (nw + nx rows) by one warp; soft-iterate
+    // refinement of the ladder as in balance
+    const bool qr_ok = !a->use_qr_always || (delta && nw + nx <= 32 && a->riccati_variant == 0);
+    return (delta || abs_speed) && qr_ok && variant_ok && a->itref_pred_max <= 0;
 }
 
 // modes beyond the classical speed loop need the extended workspace
@@ -841,7 +844,7 @@ int ocpqp_solve(OcpPlan* P, const OcpQpDataC* data, const OcpIpmArgC* arg, OcpIt
     const bool ext = needs_ext(arg);
     if (ext && (rc = ensure_ext(P))) return rc;
     const bool team = P->fast && P->shape.kind == 0 &&
-                      team_supports(arg, P->shape.nx + P->shape.nu) && !getenv("OCPQP_EXT_GENERIC");
+                      team_supports(arg, P->shape.nx + P->shape.nu, P->shape.nx) && !getenv("OCPQP_EXT_GENERIC");
     KParams k;
     fill_kparams(P, k, data, !(ext && P->fast) || team);
     size_t gen_smem = P->smem_bytes;

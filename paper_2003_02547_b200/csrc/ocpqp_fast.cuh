@@ -279,6 +279,60 @@ struct MVw {
     }
 };
 
+// Householder QR of an m x NN stack (m <= 32) held row-wise by the lanes of one
+// warp (lane r: srow[j] = S[r][j]), in registers: LAPACK dgeqr2 / dlarfg
+// reflectors (the arithmetic of np.linalg.qr(mode="r") behind
+// linalg.qr_cholesky, linalg.py:152-187, and of the generic kernel's
+// warp_qr_reflectors), then qr_cholesky's rank test and row-sign
+// normalisation.  On return lanes k < NN hold row k of R (zero below the
+// diagonal, positive diagonal).  False when rank deficient.
+template <int NN>
+__device__ __forceinline__ bool warp_qr_rows(double (&srow)[NN], int lane, int m) {
+#pragma unroll
+    for (int k = 0; k < NN; ++k) {
+        const bool below = lane > k && lane < m;
+        const double sk = below ? srow[k] : 0.0;
+        double ss = sk * sk;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
+        const double alpha = __shfl_sync(FULL, srow[k], k);
+        if (ss != 0.0) {   // else H = I (tau = 0); uniform across the warp
+            const double beta = -copysign(hypot(alpha, sqrt(ss)), alpha);
+            const double tau = (beta - alpha) / beta;
+            const double sc = 1.0 / (alpha - beta);
+            const double vk = below ? sk * sc : 0.0;
+#pragma unroll
+            for (int j = k + 1; j < NN; ++j) {
+                double w = below ? vk * srow[j] : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(FULL, w, o);
+                const double skj = __shfl_sync(FULL, srow[j], k);
+                w = (skj + w) * tau;
+                if (below) srow[j] = fma(-w, vk, srow[j]);
+                if (lane == k) srow[j] -= w;
+            }
+            if (lane == k) srow[k] = beta;
+        }
+        if (below) srow[k] = 0.0;
+    }
+    double dmax = 0.0;
+#pragma unroll
+    for (int k = 0; k < NN; ++k) dmax = fmax(dmax, fabs(__shfl_sync(FULL, srow[k], k)));
+    const double tol = (m > NN ? m : NN) * 2.220446049250313e-16 * dmax;
+    bool bad = false;
+    double sg = 1.0;
+#pragma unroll
+    for (int k = 0; k < NN; ++k) {
+        const double dk = __shfl_sync(FULL, srow[k], k);
+        if (!(fabs(dk) > tol)) bad = true;
+        if (lane == k && dk < 0.0) sg = -1.0;
+    }
+    if (bad) return false;
+#pragma unroll
+    for (int j = 0; j < NN; ++j) srow[j] = (lane < NN && j >= lane) ? sg * srow[j] : 0.0;
+    return true;
+}
+
 // Cholesky of an NN x NN (NN <= 32) matrix held row-wise by the lanes of one
 // warp (lane i: row[j] = A[i][j], j <= i).  Pivot test as LAPACK potrf: a
 // pivot that is not > 0 (or NaN) fails (linalg.py:81-118).
@@ -1409,10 +1463,16 @@ struct Kern {
         int fs;
         long long flops;
     };
+    // use_qr (robust mode, use_qr_always; NW + NX <= 32): L_G = qr_cholesky of the stack
+    // [chol(M~)'; W] instead of chol(W'W + M~) (kkt_ocp.py:221-224), by warp 0 with the
+    // stack rows in registers (warp_qr_rows); fs = -4: rank-deficient stack
+    static constexpr bool QR_OK = NW + NX <= 32;
     __device__ __noinline__ static FacOut factor_sqrt(FCtx& c, const RD& d, const KParams& p,
                                                       double* stg, const double* lam,
-                                                      const double* t, double reg) {
+                                                      const double* t, double reg, bool use_qr = false) {
         long long flops = 0;
+        if (!QR_OK) use_qr = false;
+        int rank_bad = 0;
         const int tid = threadIdx.x;
         const double* act = c.w[WS_DVEC];
         double* gam = c.w[WS_GAM];
@@ -1510,6 +1570,9 @@ struct Kern {
             }
             if (NG > 0 && ng > 0) flops += 2ll * NX * NX * ng;
             flops += (long long)NX * NX * NX / 3;
+            // terminal stack = chol(M~_N)' alone: its QR is the identity (every sub-column is
+            // zero), only the count of qr_cholesky is added (linalg.py:174)
+            if (use_qr) flops += 2ll * NX * NX * NX - (2ll * NX * NX * NX) / 3;
             bar<TEAM>();
             if (!c.flag) return FacOut{n, flops};
             // ---- stages N-1 .. 0 ----
@@ -1520,7 +1583,8 @@ struct Kern {
                     [&](int i, int k) { return k >= i ? Lc[k * NX + i] : 0.0; },
                     [&](int k, int j) { return BAn[k * BK + j * BJ]; }, NoPre(),
                     [&](int i, int j, double v, double) { W[i * NW + j] = v; });
-                flops += 2ll * NX * NW * NX + 2ll * NW * NW * NX;
+                flops += 2ll * NX * NW * NX;
+                if (!use_qr) flops += 2ll * NW * NW * NX;
                 bar<TEAM>();
                 const double* Qn = Q(c, n);
                 const double* Rn = R(c, n);
@@ -1529,6 +1593,7 @@ struct Kern {
                 const bool full_box = p.box_ident && d.NB == NW;
                 if (warp_id_uniform() == 0) {
                     // lane i: row i of G = W'W + M~ (j <= i), then the warp Cholesky
+                    // (use_qr: row i of M~ alone)
                     const int i = tid;
                     double row[NW];
 #pragma unroll
@@ -1536,7 +1601,8 @@ struct Kern {
                         double h = 0.0;
                         if (i < NW && j <= i) {
                             double a = 0.0;
-                            for (int k = 0; k < NX; ++k) a = fma(W[k * NW + i], W[k * NW + j], a);
+                            if (!use_qr)
+                                for (int k = 0; k < NX; ++k) a = fma(W[k * NW + i], W[k * NW + j], a);
                             double mij, mji;
                             if (i < NU && j < NU) { mij = Rn[i * NU + j]; mji = Rn[j * NU + i]; }
                             else if (i < NU) { mij = Sn[i * NX + (j - NU)]; mji = mij; }
@@ -1554,12 +1620,53 @@ struct Kern {
                                 m = sg + m;
                             }
                             if (i == j && reg != 0.0) m += reg;
-                            h = a + m;
+                            h = use_qr ? m : a + m;
                         }
                         row[j] = h;
                     }
                     double rin = 0.0;
-                    const bool ok = warp_chol<NW>(row, i, rin);
+                    bool ok = warp_chol<NW>(row, i, rin);
+                    if constexpr (QR_OK) {
+                        if (use_qr && ok) {
+                            // stack rows: r < NW: chol(M~)' (row r = column r of L_M), then W
+                            double* sc = W;   // NW x NW scratch = the W and L_xu tiles (W is consumed first)
+                            double srow[NW];
+#pragma unroll
+                            for (int j = 0; j < NW; ++j)
+                                srow[j] = (i >= NW && i < NW + NX) ? W[(i - NW) * NW + j] : 0.0;
+                            __syncwarp();
+                            if (i < NW) {
+#pragma unroll
+                                for (int j = 0; j < NW; ++j) sc[i * NW + j] = j <= i ? row[j] : 0.0;
+                            }
+                            __syncwarp();
+                            if (i < NW) {
+#pragma unroll
+                                for (int j = 0; j < NW; ++j) srow[j] = sc[j * NW + i];
+                            }
+                            __syncwarp();
+                            const bool full = warp_qr_rows<NW>(srow, i, NW + NX);
+                            if (!full) {
+                                if (tid == 0) c.flag = 0;
+                                rank_bad = 1;
+                            }
+                            // L_G = R': through the scratch again
+                            if (i < NW) {
+#pragma unroll
+                                for (int j = 0; j < NW; ++j) sc[i * NW + j] = srow[j];
+                            }
+                            __syncwarp();
+#pragma unroll
+                            for (int j = 0; j < NW; ++j) row[j] = (i < NW && j <= i) ? sc[j * NW + i] : 0.0;
+                            __syncwarp();
+                            // 1 / L_ii of this lane's row
+                            rin = 0.0;
+#pragma unroll
+                            for (int j = 0; j < NW; ++j)
+                                if (j == i) rin = 1.0 / row[j];
+                            ok = full;
+                        }
+                    }
                     if (tid == 0) c.flag = ok;
                     if (ok) {
                         if (i < NU) {
@@ -1576,8 +1683,9 @@ struct Kern {
                 }
                 if (NG > 0) flops += 2ll * NW * NW * NG;
                 flops += (long long)NW * NW * NW / 3;
+                if (use_qr) flops += 2ll * (NW + NX) * NW * NW - (2ll * NW * NW * NW) / 3;
                 bar<TEAM>();
-                if (!c.flag) return FacOut{n, flops};
+                if (!c.flag) return FacOut{any_of<TEAM>(rank_bad) ? -4 : n, flops};
                 // K = -L_uu^{-T} L_xu' : column j from row j of L_xu (back substitution)
                 const double* Ln = Lst + n * NU * NU;
                 const double* rv = Rst + n * NU;
@@ -3487,11 +3595,13 @@ struct Kern {
             if (status >= 0) break;
             bar<TEAM>();
             // square-root variant (REF instantiation, NW <= 32): factor_sqrt
-            const bool sqv = REF && arg.riccati_variant != 0;
+            // ... and robust mode's QR stage (use_qr_always) where the stack fits one warp
+            const bool qrv = REF && arg.use_qr_always && QR_OK;
+            const bool sqv = REF && (arg.riccati_variant != 0 || qrv);
             auto do_factor = [&](double rg) -> int {
                 if constexpr (REF && NW <= 32) {
                     if (sqv) {
-                        const FacOut fo = factor_sqrt(c, d, p, stg, lam, t, rg);
+                        const FacOut fo = factor_sqrt(c, d, p, stg, lam, t, rg, qrv);
                         flops += fo.flops;
                         return fo.fs;
                     }
@@ -3503,6 +3613,8 @@ struct Kern {
             // the balance-mode ladder continues with the QR array algorithm
             // (solver.py:145-164): the generic kernel re-solves this QP
             if (REF && fs >= 0 && arg.use_qr_fallback) { status = STATUS_ESCAPE; break; }
+            // rank-deficient QR stack: the generic kernel raises it (status RankDeficient)
+            if (REF && fs == -4) { status = STATUS_ESCAPE; break; }
             if (fs >= 0) { bar<TEAM>(); fs = do_factor(reg2); }
             if (fs == -2) { status = OCPQP_STATUS_NONPOSITIVE_ITERATE; break; }
             if (fs >= 0) { status = OCPQP_STATUS_FAILURE; break; }
@@ -3580,7 +3692,7 @@ struct Kern {
                 const RefOut ro = refine(c, d, p, stg, lam, t, dy, dpi, dlam, dt,
                                          arg.itref_corr_max, arg.itref_stop_ratio, sqv, &tm);
                 flops += ro.flops;
-                if (arg.use_qr_fallback && ro.best > arg.qr_fallback_ratio * ro.rhs) {
+                if (arg.use_qr_fallback && !arg.use_qr_always && ro.best > arg.qr_fallback_ratio * ro.rhs) {
                     status = STATUS_ESCAPE;   // QR refactorization: generic kernel
                     break;
                 }

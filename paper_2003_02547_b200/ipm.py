@@ -164,14 +164,18 @@ def is_speed_classical(arg):
             and arg.riccati_variant == "classical")
 
 
-def team_supports(arg, nw=None):
+def team_supports(arg, nw=None, nx=None):
     """The settings the shaped team kernel runs (ocpqp_capi.cu team_supports):
     the delta form with per-iteration residuals (speed, balance -- QR rungs
-    escape per QP to the generic kernel) or the speed_abs combination."""
+    escape per QP to the generic kernel; robust where the stacked factor of
+    nw + nx rows fits one warp) or the speed_abs combination."""
     delta = not arg.abs_form and arg.comp_res_pred
     abs_speed = (arg.abs_form and not arg.comp_res_pred and arg.itref_corr_max <= 0
                  and not arg.use_qr_fallback)
     variant_ok = arg.riccati_variant == "classical" or (
         arg.riccati_variant == "square_root" and nw is not None and nw <= 32)
-    return ((delta or abs_speed) and not arg.use_qr_always and variant_ok
+    qr_ok = (not arg.use_qr_always) or (
+        delta and nw is not None and nx is not None and nw + nx <= 32
+        and arg.riccati_variant == "classical")
+    return ((delta or abs_speed) and qr_ok and variant_ok
             and arg.itref_pred_max <= 0)
